@@ -1,0 +1,279 @@
+"""FlashMask CPU oracle — TEST INFRASTRUCTURE ONLY.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s ``cpu_baseline`` /
+``--impl reference`` legs may import this module.  The product path
+(``paper_2410_01359_b200``) never imports it and shares no code with it.
+
+Plain, slow, obviously-correct NumPy fp64 implementation of what the FlashMask hot
+path computes (PAPER.md arXiv 2410.01359).  FlashMask is exact — skipped tiles
+contribute exactly 0 (§4.4) — so attention here is the plain definition
+with the dense mask materialised from the column intervals, not a replay of the
+tiled Alg. 1/2.  Tile classification is Eq. 4 / Alg. 1 lines 9-14 and 15-21
+written out per tile.
+
+Readings of the paper used here are numbered R1..R30 in DESIGN.md §3 (they follow
+SURVEY.md §8(c) c.2).  Every function names the passage it follows.
+Pins: tests/test_oracle_*.py (-m "not gpu").  Parity unpinned: none of the
+functions below (see DESIGN.md §3 for the list of pins per function).
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+SKIP, PARTIAL, UNMASKED = 0, 1, 2  # tile classes (Eq. 4)
+
+
+# ------------------------------------------------------------------ mask vectors
+@dataclass
+class Vectors:
+    """LTS/LTE/UTS/UTE of §4.1 for one mask head, int64 length N."""
+
+    lts: np.ndarray
+    lte: np.ndarray
+    uts: np.ndarray
+    ute: np.ndarray
+    causal: bool
+    N: int
+
+
+def expand(sri: np.ndarray, causal: bool, N: int) -> Vectors:
+    """startend_row_indices ``[N, C]`` -> the four §4.1 vectors.
+
+    C-table (R17): causal C=1 -> (LTS; LTE=N), causal C=2 ->
+    (LTS, LTE); non-causal C=2 -> (LTS, UTE; LTE=N, UTS=0); non-causal C=4 -> all four.
+    In causal mode the upper triangle is the implicit r<y region (R8); the upper
+    vectors are set to the empty interval [0, 0)."""
+    sri = np.asarray(sri, dtype=np.int64).reshape(N, -1)
+    C = sri.shape[1]
+    zeros = np.zeros(N, dtype=np.int64)
+    full_n = np.full(N, N, dtype=np.int64)
+    if causal and C == 1:
+        return Vectors(sri[:, 0], full_n, zeros, zeros, True, N)
+    if causal and C == 2:
+        return Vectors(sri[:, 0], sri[:, 1], zeros, zeros, True, N)
+    if not causal and C == 2:
+        return Vectors(sri[:, 0], full_n, zeros, sri[:, 1], False, N)
+    if not causal and C == 4:
+        return Vectors(sri[:, 0], sri[:, 1], sri[:, 2], sri[:, 3], False, N)
+    raise ValueError(f"unsupported (causal={causal}, C={C})")
+
+
+def mask_rows(v: Vectors, r0: int, r1: int) -> np.ndarray:
+    """Dense boolean mask rows [r0, r1) x all N columns; True = masked (M = -inf).
+
+    masked(r, y) = LTS_y <= r < LTE_y  or  UTS_y <= r < UTE_y  or  (causal and r < y)
+    — Eq. 3 per interval, §4.1 union of both intervals, Eq. 2's
+    additive -inf mask, causal as the implicit upper triangle (R8)."""
+    r = np.arange(r0, r1, dtype=np.int64)[:, None]
+    y = np.arange(v.N, dtype=np.int64)[None, :]
+    m = ((v.lts[None, :] <= r) & (r < v.lte[None, :])) | ((v.uts[None, :] <= r) & (r < v.ute[None, :]))
+    if v.causal:
+        m |= r < y
+    return m
+
+
+def to_dense(v: Vectors) -> np.ndarray:
+    """The full N x N mask M of Eq. 2 as booleans (O(N^2): small N only)."""
+    return mask_rows(v, 0, v.N)
+
+
+def from_dense(dense: np.ndarray, causal: bool) -> np.ndarray:
+    """Dense mask -> startend_row_indices (§3: masked rows of a column are one
+    contiguous interval per triangle).  Returns [N, C] int32 in the C-table layout
+    (causal -> C=2 (LTS, LTE); bidirectional -> C=4).  Raises ValueError when a column's
+    masked rows within a triangle are not contiguous (not representable)."""
+    dense = np.asarray(dense, dtype=bool)
+    N = dense.shape[0]
+    lo = np.full((N, 2), N, dtype=np.int64)      # LTS, LTE (empty = [N, N))
+    up = np.zeros((N, 2), dtype=np.int64)        # UTS, UTE (empty = [0, 0))
+    for y in range(N):
+        col = dense[:, y]
+        if causal and not col[:y].all():
+            raise ValueError(f"causal mask must mask every r<y (column {y})")
+        rows = np.nonzero(col[y:])[0] + y        # lower triangle incl. diagonal (R9)
+        if len(rows):
+            if rows[-1] - rows[0] + 1 != len(rows):
+                raise ValueError(f"column {y} lower triangle not contiguous")
+            lo[y] = (rows[0], rows[-1] + 1)
+        if not causal:
+            rows = np.nonzero(col[:y])[0]
+            if len(rows):
+                if rows[-1] - rows[0] + 1 != len(rows):
+                    raise ValueError(f"column {y} upper triangle not contiguous")
+                up[y] = (rows[0], rows[-1] + 1)
+    if causal:
+        return np.stack([lo[:, 0], lo[:, 1]], 1).astype(np.int32)
+    return np.stack([lo[:, 0], lo[:, 1], up[:, 0], up[:, 1]], 1).astype(np.int32)
+
+
+# ------------------------------------------------------------------ attention
+def forward(q, k, v, vec: Vectors, scale: float | None = None, rows=None, row_block: int = 1024):
+    """O = Softmax(scale*Q K^T + M) V and L = logsumexp per row (Eq. 1, Eq. 2
+    P:68-73; L as in Alg. 1 lines 27-28 P:247-248, natural log of the scaled logits).
+
+    q, k, v: [N, d] (cast to fp64).  ``rows``: optional array of row indices to compute
+    (each row is independent).  A row masked in every column has P_r = 0, O_r = 0,
+    L_r = -inf (R7).  Returns (O [n_rows, d], L [n_rows])."""
+    q = np.asarray(q, dtype=np.float64)
+    k = np.asarray(k, dtype=np.float64)
+    v_ = np.asarray(v, dtype=np.float64)
+    N, d = q.shape
+    scale = 1.0 / math.sqrt(d) if scale is None or scale <= 0 else float(scale)
+    rows = np.arange(N) if rows is None else np.asarray(rows, dtype=np.int64)
+    O = np.zeros((len(rows), v_.shape[1]))
+    L = np.full(len(rows), -np.inf)
+    for s in range(0, len(rows), row_block):
+        rr = rows[s:s + row_block]
+        S = scale * (q[rr] @ k.T)
+        M = _mask_for_rows(vec, rr)
+        S[M] = -np.inf
+        m = S.max(axis=1)
+        live = np.isfinite(m)
+        P = np.zeros_like(S)
+        P[live] = np.exp(S[live] - m[live, None])
+        ell = P.sum(axis=1)
+        P[live] /= ell[live, None]
+        O[s:s + len(rr)] = P @ v_
+        L[s:s + len(rr)][live] = m[live] + np.log(ell[live])
+    return O, L
+
+
+def _mask_for_rows(vec: Vectors, rows: np.ndarray) -> np.ndarray:
+    r = rows[:, None]
+    y = np.arange(vec.N)[None, :]
+    m = ((vec.lts[None, :] <= r) & (r < vec.lte[None, :])) | ((vec.uts[None, :] <= r) & (r < vec.ute[None, :]))
+    if vec.causal:
+        m |= r < y
+    return m
+
+
+def probabilities(q, k, vec: Vectors, scale=None, rows=None):
+    """P = Softmax(S + M) rows (Eq. 2); empty rows are all-zero (R7)."""
+    q = np.asarray(q, dtype=np.float64)
+    k = np.asarray(k, dtype=np.float64)
+    N, d = q.shape
+    scale = 1.0 / math.sqrt(d) if scale is None or scale <= 0 else float(scale)
+    rows = np.arange(N) if rows is None else np.asarray(rows)
+    S = scale * (q[rows] @ k.T)
+    S[_mask_for_rows(vec, rows)] = -np.inf
+    m = S.max(axis=1)
+    P = np.zeros_like(S)
+    live = np.isfinite(m)
+    P[live] = np.exp(S[live] - m[live, None])
+    P[live] /= P[live].sum(axis=1, keepdims=True)
+    return P
+
+
+def backward(q, k, v, do, vec: Vectors, scale=None, row_block: int = 1024):
+    """Gradients of O = Softmax(scale*QK^T + M) V (Alg. 2 P:365-441 restated densely):
+    D = rowsum(dO o O) (Alg. 2 line 4 P:379, per row — R5), P from the definition,
+    dV = P^T dO, dP = dO V^T, dS = P o (dP - D),
+    dQ = scale * dS K, dK = scale * dS^T Q — the scale of Eq. 1 carried
+    into dQ/dK (R4).  Row-blocked; returns (dQ, dK, dV) fp64 [N, d]."""
+    q = np.asarray(q, dtype=np.float64)
+    k = np.asarray(k, dtype=np.float64)
+    v_ = np.asarray(v, dtype=np.float64)
+    do = np.asarray(do, dtype=np.float64)
+    N, d = q.shape
+    scale = 1.0 / math.sqrt(d) if scale is None or scale <= 0 else float(scale)
+    dq = np.zeros_like(q)
+    dk = np.zeros_like(k)
+    dv = np.zeros_like(v_)
+    for s in range(0, N, row_block):
+        rr = np.arange(s, min(s + row_block, N))
+        P = probabilities(q, k, vec, scale, rr)
+        O = P @ v_
+        D = (do[rr] * O).sum(axis=1)
+        dv += P.T @ do[rr]
+        dP = do[rr] @ v_.T
+        dS = P * (dP - D[:, None])
+        dq[rr] = scale * (dS @ k)
+        dk += scale * (dS.T @ q[rr])
+    return dq, dk, dv
+
+
+# ------------------------------------------------------------------ classification
+def extrema(vec: Vectors, Bc: int) -> np.ndarray:
+    """Alg. 1 lines 3-4: per column tile j the min and max of each vector over
+    the tile's real columns [j*Bc, min((j+1)*Bc, N)) (R3).  Returns int64 [Tc, 8] in the
+    order LTS^min, LTS^max, LTE^min, LTE^max, UTS^min, UTS^max, UTE^min, UTE^max."""
+    N = vec.N
+    Tc = -(-N // Bc)
+    out = np.zeros((Tc, 8), dtype=np.int64)
+    for j in range(Tc):
+        c0, c1 = j * Bc, min((j + 1) * Bc, N)
+        for t, a in enumerate((vec.lts, vec.lte, vec.uts, vec.ute)):
+            out[j, 2 * t] = a[c0:c1].min()
+            out[j, 2 * t + 1] = a[c0:c1].max()
+    return out
+
+
+def classify(vec: Vectors, Br: int, Bc: int):
+    """Eq. 4 per tile, in Alg. 1's order, 0-based (R2), ragged
+    tiles by their real extents (R3), causal region as its own triangle (R13):
+
+      SKIP     iff (r0 >= LTS^max and r1 <= LTE^min)          Alg.1 l.9
+               or  (r0 >= UTS^max and r1 <= UTE^min)          Alg.1 l.12
+               or  (causal and r1-1 < c0)
+      PARTIAL  iff (r1 > LTS^min and r0 < LTE^max)            Alg.1 l.15
+               or  (r1 > UTS^min and r0 < UTE^max)            Alg.1 l.18
+               or  (causal and r0 < c1-1)
+      UNMASKED otherwise.
+
+    Returns (class_map uint8 [Tr, Tc], counts int64 [3] = (skip, partial, unmasked),
+    extrema int64 [Tc, 8])."""
+    N = vec.N
+    Tr, Tc = -(-N // Br), -(-N // Bc)
+    ext = extrema(vec, Bc)
+    cm = np.zeros((Tr, Tc), dtype=np.uint8)
+    # one column tile at a time; the rows of the column are evaluated as a vector,
+    # the if/elif chain below is the per-tile rule in the order stated above.
+    r0 = np.arange(Tr, dtype=np.int64) * Br
+    r1 = np.minimum(r0 + Br, N)
+    for j in range(Tc):
+        c0, c1 = j * Bc, min((j + 1) * Bc, N)
+        ltsmin, ltsmax, ltemin, ltemax, utsmin, utsmax, utemin, utemax = ext[j]
+        skip = ((r0 >= ltsmax) & (r1 <= ltemin)) | ((r0 >= utsmax) & (r1 <= utemin))
+        if vec.causal:
+            skip |= r1 - 1 < c0
+        part = ((r1 > ltsmin) & (r0 < ltemax)) | ((r1 > utsmin) & (r0 < utemax))
+        if vec.causal:
+            part |= r0 < c1 - 1
+        cm[:, j] = np.where(skip, SKIP, np.where(part, PARTIAL, UNMASKED))
+    counts = np.array([(cm == SKIP).sum(), (cm == PARTIAL).sum(), (cm == UNMASKED).sum()], dtype=np.int64)
+    return cm, counts, ext
+
+
+def alpha_bruteforce(vec: Vectors, Br: int, Bc: int) -> int:
+    """alpha of §4.3: number of tiles whose every cell is masked, counted from the
+    dense mask (O(N^2): small N only)."""
+    M = to_dense(vec)
+    N = vec.N
+    a = 0
+    for r0 in range(0, N, Br):
+        for c0 in range(0, N, Bc):
+            if M[r0:r0 + Br, c0:c0 + Bc].all():
+                a += 1
+    return a
+
+
+def block_sparsity(counts) -> float:
+    """rho = alpha / (Tr * Tc) (§4.3) with alpha = the SKIP count of rule R (R11)."""
+    return float(counts[0]) / float(np.sum(counts))
+
+
+def effective_flops(vec: Vectors, d: int, Br: int = 128, Bc: int = 128):
+    """Effective FLOPs of one (batch, head) (R15, P:581 'based on the block sparsity ...
+    calculate the FLOPs'): forward = 4*d*sum over non-SKIP tiles of rows*cols
+    (two GEMMs of 2*rows*cols*d each); backward = 2.5 x forward (five GEMMs)."""
+    cm, _, _ = classify(vec, Br, Bc)
+    N = vec.N
+    Tr, Tc = cm.shape
+    rows = np.array([min((i + 1) * Br, N) - i * Br for i in range(Tr)], dtype=np.float64)
+    cols = np.array([min((j + 1) * Bc, N) - j * Bc for j in range(Tc)], dtype=np.float64)
+    area = (rows[:, None] * cols[None, :])[cm != SKIP].sum()
+    fwd = 4.0 * d * area
+    return fwd, 2.5 * fwd

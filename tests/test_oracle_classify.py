@@ -1,0 +1,209 @@
+"""Pins for the oracle's preprocessing (Alg. 1 lines 3-4) and tile classification (Eq. 4).
+
+* SPEC worked examples (S:166-168 extrema, S:176-178 classes, S:186-188 rho).
+* Soundness against brute force on the dense mask: SKIP => every cell masked,
+  UNMASKED => no cell masked, #SKIP <= alpha.
+* Closed-form class counts — exact integers.
+* The paper's own tables: FW/BW TFLOPs of the closed-form masks are reproduced from the
+  oracle's SKIP counts at 128x128 tiles and FLOPs = 4 N^2 d B H (1 - rho)
+  (tests/golden/paper_kernel_tables_d128.txt).
+"""
+import os
+
+import numpy as np
+import pytest
+
+from oracle import flashmask_oracle as fo
+from workloads import masks as wm
+
+
+def vec(m):
+    return fo.expand(m.sri, m.causal, m.N)
+
+
+def test_spec_extrema_examples():
+    v = fo.Vectors(np.array([3, 3, 3, 7, 7, 7, 7, 8]), np.full(8, 8), np.zeros(8, int), np.zeros(8, int), True, 8)
+    e = fo.extrema(v, 4)
+    assert list(e[:, 0]) == [3, 7] and list(e[:, 1]) == [7, 8]
+    assert list(e[:, 2]) == [8, 8] and list(e[:, 3]) == [8, 8]
+    e = fo.extrema(vec(wm.causal_document([3, 4, 3])), 5)
+    assert list(e[:, 0]) == [3, 7] and list(e[:, 1]) == [7, 10]
+    v = fo.Vectors(np.full(8, 8), np.full(8, 8), np.zeros(8, int), np.zeros(8, int), True, 8)
+    e = fo.extrema(v, 4)
+    assert list(e[:, 0]) == [8, 8] and list(e[:, 1]) == [8, 8]
+
+
+def _one_col_tile(lts, lte, N=16, causal=False):
+    z = np.zeros(N, dtype=np.int64)
+    return fo.Vectors(np.asarray(lts, dtype=np.int64), np.asarray(lte, dtype=np.int64), z, z, causal, N)
+
+
+def test_spec_classification_examples():
+    # Rows [4,8) with LTS=4, LTE=8 over the column tile -> SKIP
+    v = _one_col_tile(np.full(8, 4), np.full(8, 8), N=8)
+    cm, _, _ = fo.classify(v, 4, 8)
+    assert cm[1, 0] == fo.SKIP
+    # Rows [4,8), LTS min/max 3/7, LTE 10 -> PARTIAL
+    lts = np.array([3, 4, 5, 6, 7, 7, 7, 7, 7, 7])
+    v = _one_col_tile(lts, np.full(10, 10), N=10)
+    cm, _, _ = fo.classify(v, 4, 10)
+    assert cm[1, 0] == fo.PARTIAL
+    # Rows [0,4), all-empty lower intervals -> UNMASKED
+    v = _one_col_tile(np.full(8, 8), np.full(8, 8), N=8)
+    cm, _, _ = fo.classify(v, 4, 4)
+    assert cm[0, 0] == fo.UNMASKED and cm[0, 1] == fo.UNMASKED
+
+
+def test_spec_sparsity_examples():
+    # S:186 empty bidirectional -> rho 0 ; S:187 causal N=128, 64x64 -> alpha=1, rho=0.25
+    _, c, _ = fo.classify(vec(wm.full(64)), 16, 16)
+    assert fo.block_sparsity(c) == 0.0
+    v = vec(wm.causal(128))
+    _, c, _ = fo.classify(v, 64, 64)
+    assert c[0] == 1 and fo.block_sparsity(c) == 0.25 and fo.alpha_bruteforce(v, 64, 64) == 1
+    # S:188 causal N=8192 at 128x128 -> 0.4922
+    _, c, _ = fo.classify(vec(wm.causal(8192)), 128, 128)
+    assert round(fo.block_sparsity(c), 4) == 0.4922
+
+
+def _random_vectors(rng, N, causal):
+    """Arbitrary int32-ish vectors, including invalid / inverted intervals (R10)."""
+    lo, hi = -3, N + 3
+    a = rng.integers(lo, hi, size=(4, N))
+    if causal:
+        z = np.zeros(N, dtype=np.int64)
+        return fo.Vectors(a[0], a[1], z, z, True, N)
+    return fo.Vectors(a[0], a[1], a[2], a[3], False, N)
+
+
+@pytest.mark.parametrize("seed", range(60))
+def test_classification_soundness_bruteforce(seed):
+    rng = np.random.default_rng(seed)
+    N = int(rng.integers(1, 40))
+    causal = bool(seed % 2)
+    fam = seed % 3
+    if fam == 0:
+        v = _random_vectors(rng, N, causal)
+    else:
+        m = wm.sample_family(wm.FAMILIES[seed % len(wm.FAMILIES)], max(N, 4), rng, (1, 4))
+        v = vec(m)
+        N = v.N
+    M = fo.to_dense(v)
+    for Br in (1, 2, 3, 4, 8, 16):
+        for Bc in (1, 2, 4, 5, 16):
+            cm, counts, _ = fo.classify(v, Br, Bc)
+            for i in range(cm.shape[0]):
+                for j in range(cm.shape[1]):
+                    blk = M[i * Br:(i + 1) * Br, j * Bc:(j + 1) * Bc]
+                    if cm[i, j] == fo.SKIP:
+                        assert blk.all()
+                    elif cm[i, j] == fo.UNMASKED:
+                        assert not blk.any()
+            assert counts[0] <= fo.alpha_bruteforce(v, Br, Bc)
+            assert counts.sum() == cm.size
+
+
+def _closed_form_counts(kind, N, **kw):
+    T = N // 128
+    if kind == "full":
+        return 0, 0, T * T
+    if kind == "causal":
+        return T * (T - 1) // 2, T, T * (T - 1) // 2
+    if kind == "sliding_window":
+        W = kw["w"] // 128
+        skip = T * (T - 1) // 2 + (T - W - 1) * (T - W) // 2
+        part = T + (T - W)
+        return skip, part, sum(T - k for k in range(1, W))
+    if kind == "prefix_lm_causal":
+        P = kw["p"] // 128
+        skip = sum(range(P, T))
+        part = T - P
+        return skip, part, T * T - skip - part
+    if kind == "global_sliding":
+        W, G = kw["w"] // 128, kw["g"] // 128
+        n = T - G
+        skip = n * (n - 1) // 2 + (n - W - 1) * (n - W) // 2
+        part = n + (n - W)
+        return skip, part, T * G + G * n + sum(n - k for k in range(1, W))
+    raise KeyError(kind)
+
+
+def _build(kind, N, rng=None):
+    if kind == "full":
+        return wm.full(N), {}
+    if kind == "causal":
+        return wm.causal(N), {}
+    if kind == "sliding_window":
+        return wm.sliding_window(N, N // 16), {"w": N // 16}
+    if kind == "prefix_lm_causal":
+        return wm.prefix_lm_causal(N, N // 2), {"p": N // 2}
+    if kind == "global_sliding":
+        return wm.global_sliding_window(N, N // 16, 256), {"g": N // 16, "w": 256}
+    if kind == "random_eviction":
+        return wm.random_eviction(N, N // 16, rng), {}
+    raise KeyError(kind)
+
+
+@pytest.mark.parametrize("N", [4096, 8192, 32768])
+@pytest.mark.parametrize("kind", ["full", "causal", "sliding_window", "prefix_lm_causal", "global_sliding"])
+def test_closed_form_class_counts(kind, N):
+    m, kw = _build(kind, N)
+    _, counts, _ = fo.classify(vec(m), 128, 128)
+    assert tuple(int(x) for x in counts) == _closed_form_counts(kind, N, **kw)
+
+
+def _table_rows(golden_dir):
+    rows = []
+    for line in open(os.path.join(golden_dir, "paper_kernel_tables_d128.txt")):
+        if line.startswith("#") or not line.strip():
+            continue
+        name, N, fw, bw, sp, src = line.split()
+        rows.append((name, int(N), float(fw), float(bw), float(sp), src))
+    return rows
+
+
+def test_paper_table_flops_reproduced(golden_dir):
+    rng = np.random.default_rng(7)
+    for name, N, fw, bw, sp, src in _table_rows(golden_dir):
+        if N > 32768 and name == "random_eviction":
+            continue  # O(N) python loop in the generator; 8K/32K rows cover it
+        m, _ = _build(name, N, rng)
+        v = vec(m)
+        _, counts, _ = fo.classify(v, 128, 128)
+        rho = fo.block_sparsity(counts)
+        d, H, B = 128, 32, 131072 // N
+        F = 4.0 * N * N * d * B * H * (1 - rho) / 1e12
+        # FW is printed to 2 decimals; at 128K the paper's FW cells sit one unit in the
+        # last place above round(F) (281.48 vs 281.475) while BW/TOTAL (703.69, 985.16)
+        # round exactly, so FW is checked to +-0.011 and BW to the rounding of 2.5 F.
+        assert round(F, 2) == pytest.approx(fw, abs=0.011), (name, N, src, F)
+        assert round(2.5 * F, 2) == pytest.approx(bw, abs=0.011), (name, N, src)
+        assert round(rho, 2) == pytest.approx(sp, abs=0.006), (name, N, src, rho)
+        ef, eb = fo.effective_flops(v, d)
+        assert ef * B * H / 1e12 == pytest.approx(F, rel=1e-12)
+
+
+def test_random_eviction_skip_equals_causal():
+    """R22: the bounded-span construction skips exactly the causal tiles (P:613 vs P:623)."""
+    rng = np.random.default_rng(3)
+    for N in (1024, 8192):
+        _, c, _ = fo.classify(vec(wm.random_eviction(N, N // 16, rng)), 128, 128)
+        T = N // 128
+        assert c[0] == T * (T - 1) // 2
+
+
+def test_ragged_tiles():
+    """R3: ragged last tiles are classified by their real extents (no padding)."""
+    for N in (127, 129, 257, 300):
+        v = vec(wm.causal_document([N // 3, N // 3, N - 2 * (N // 3)]))
+        cm, c, _ = fo.classify(v, 128, 128)
+        T = -(-N // 128)
+        assert cm.shape == (T, T) and c.sum() == T * T
+        M = fo.to_dense(v)
+        for i in range(T):
+            for j in range(T):
+                blk = M[i * 128:(i + 1) * 128, j * 128:(j + 1) * 128]
+                if cm[i, j] == fo.SKIP:
+                    assert blk.all()
+                if cm[i, j] == fo.UNMASKED:
+                    assert not blk.any()
