@@ -1,0 +1,144 @@
+/*
+ * flashmask.h — C ABI of the B200 (sm_100a) FlashMask hot path.
+ *
+ * FlashMask (arXiv 2410.01359, /root/reference/PAPER.md) computes exact masked
+ * attention  O = Softmax(scale * Q K^T + M) V  (Eq. 1, Eq. 2) and its
+ * gradients, where M is never materialised: every key column y carries at most two
+ * masked row intervals [LTS_y, LTE_y) and [UTS_y, UTE_y) (Eq. 3, §4.1
+ * P:118-127).  A per-column-tile min/max preprocessing (Alg. 1 lines 3-4)
+ * classifies every tile as fully masked (skipped before any load), partially masked
+ * (masked element-wise) or unmasked (Eq. 4, Alg. 1).
+ *
+ * Conventions shared by every entry point
+ * ---------------------------------------
+ *  - All tensor pointers are DEVICE pointers owned by the caller; nothing is
+ *    allocated inside the library.  `stream` is a cudaStream_t passed as void*
+ *    (NULL = legacy default stream).  Every call is asynchronous on `stream`;
+ *    no device synchronisation happens inside; asynchronous faults surface at the
+ *    caller's next synchronisation.
+ *  - Argument errors are detected on the host before anything is launched and are
+ *    returned as FM_ERR_INVALID_ARGUMENT / FM_ERR_UNSUPPORTED /
+ *    FM_ERR_WORKSPACE_TOO_SMALL; launch failures return FM_ERR_CUDA.  The detail
+ *    of the last non-OK status of the calling thread is in flashmask_last_error().
+ *    No C++ exception crosses the ABI.  There is no fallback path.
+ *  - The library is stateless and re-entrant (a call_once device-attribute and
+ *    driver-entry-point cache is its only global state).
+ *  - q, k, v, o, dout, dq, dk, dv: [batch, seqlen, num_heads, head_dim] contiguous,
+ *    16-byte aligned.  lse: [batch, num_heads, seqlen] fp32, natural log of the
+ *    scaled logits (Alg. 1 line 28); -inf for a row masked in every column
+ *    (then its O row is 0 and it contributes nothing to the gradients; R7).
+ *  - startend_row_indices: int32 [batch, mask_heads, seqlen, C], 16-byte aligned.
+ *    Column y = key token y.  Columns by (causal, C), missing vectors defaulted:
+ *
+ *        causal  C   col0  col1  col2  col3   implicit
+ *        1       1   LTS   -     -     -      LTE = N, plus the r < y triangle
+ *        1       2   LTS   LTE   -     -      plus the r < y triangle
+ *        0       2   LTS   UTE   -     -      LTE = N, UTS = 0
+ *        0       4   LTS   LTE   UTS   UTE    -
+ *
+ *    masked(r, y) = LTS_y <= r < LTE_y  or  UTS_y <= r < UTE_y  or  (causal and r < y).
+ *    Any int32 value is accepted (start >= end is an empty interval); values are only
+ *    compared, never used as addresses.  Self-attention only (query length = key
+ *    length = seqlen).
+ */
+#ifndef FLASHMASK_H_
+#define FLASHMASK_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define FM_API __attribute__((visibility("default")))
+#else
+#define FM_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  FM_OK = 0,
+  FM_ERR_INVALID_ARGUMENT = 1,   /* null / misaligned pointer, bad shape or combination */
+  FM_ERR_UNSUPPORTED = 2,        /* valid request this build does not implement          */
+  FM_ERR_WORKSPACE_TOO_SMALL = 3,
+  FM_ERR_CUDA = 4                /* a CUDA runtime/driver call or launch failed          */
+} fm_status;
+
+typedef enum { FM_BF16 = 0, FM_FP32 = 1 } fm_dtype;
+
+/* Tile classes of Eq. 4, as written to class maps. */
+typedef enum { FM_TILE_SKIP = 0, FM_TILE_PARTIAL = 1, FM_TILE_UNMASKED = 2 } fm_tile_class;
+
+/* fm_params.flags bits. */
+enum {
+  /* Debug: visit SKIP tiles as PARTIAL (masked element-wise).  The outputs must be
+   * bitwise identical to the default run — the exactness claim of §4.4. */
+  FM_FLAG_NO_SKIP = 1
+};
+
+typedef struct {
+  int64_t batch;       /* B >= 1                                                    */
+  int64_t seqlen;      /* N >= 1 (queries = keys)                                  */
+  int64_t num_heads;   /* H >= 1                                                    */
+  int64_t head_dim;    /* d in {64, 128}                                            */
+  int64_t mask_heads;  /* 1 (one mask per batch entry, broadcast) or num_heads      */
+  int64_t mask_cols;   /* C in {1, 2, 4}; must match `causal` per the table above   */
+  int32_t causal;      /* 0 or 1                                                    */
+  float   scale;       /* softmax scale; <= 0 means 1/sqrt(head_dim) (Eq. 1)        */
+  int32_t in_dtype;    /* fm_dtype of q, k, v, dout: FM_BF16 only in this build    */
+  int32_t out_dtype;   /* fm_dtype of o, dq, dk, dv: FM_BF16 or FM_FP32            */
+  int32_t flags;       /* FM_FLAG_*                                                 */
+} fm_params;
+
+enum { FM_PASS_FWD = 0, FM_PASS_BWD = 1 };
+
+/* Bytes of device workspace flashmask_fwd (pass = FM_PASS_FWD) or flashmask_bwd
+ * (FM_PASS_BWD) needs for these params: the expanded mask vectors and their per-tile
+ * extrema (Alg. 1 line 4), the kernels' tile-class maps, and for the backward the
+ * per-row D = rowsum(dO o O) (Alg. 2 line 4), a log2-scaled copy of lse and the
+ * fp32 dQ accumulator (Alg. 2 line 3).  O(N * (1 + H * d) + T_r * T_c) per batch
+ * entry.  Returns 0 for invalid params (see flashmask_last_error()). */
+FM_API size_t flashmask_workspace_size(const fm_params* p, int pass);
+
+/* Preprocessing + tile classification (Alg. 1 lines 3-4 P:210-211; Eq. 4 P:143-150 with
+ * Alg. 1's skip tests P:220-226 and partial tests P:232-240, 0-based, causal region as a
+ * third triangle).  Tiles are br x bc (br, bc >= 1); ragged last tiles use their real
+ * extents.  Outputs (device pointers):
+ *   minmax     int32 [B, Hm, Tc, 8], required: per column tile the min and max over its
+ *              real columns of LTS, LTE, UTS, UTE (order LTSmin, LTSmax, LTEmin, LTEmax,
+ *              UTSmin, UTSmax, UTEmin, UTEmax), with the table's defaults filled in.
+ *   class_map  uint8 [B, Hm, Tr, Tc] fm_tile_class, or NULL.
+ *   counts     int64 [B, Hm, 3] = (#SKIP, #PARTIAL, #UNMASKED), or NULL.
+ * Tr = ceil(N / br), Tc = ceil(N / bc).  The class map ignores FM_FLAG_NO_SKIP. */
+FM_API fm_status flashmask_classify(const fm_params* p, const int32_t* startend_row_indices, int32_t br, int32_t bc,
+                             int32_t* minmax, uint8_t* class_map, int64_t* counts, void* stream);
+
+/* Forward pass (Alg. 1): o = Softmax(scale*q k^T + M) v, lse = logsumexp.
+ *   q, k, v  [B, N, H, d] in_dtype;  o [B, N, H, d] out_dtype;  lse fp32 [B, H, N].
+ * Fully masked tiles issue no load and no MMA; partially masked tiles are masked
+ * element-wise; unmasked tiles do no mask work. */
+FM_API fm_status flashmask_fwd(const fm_params* p, const void* q, const void* k, const void* v,
+                        const int32_t* startend_row_indices, void* o, float* lse,
+                        void* workspace, size_t workspace_bytes, void* stream);
+
+/* Backward pass (Alg. 2): given dout = dL/do, writes dq, dk, dv
+ * ([B, N, H, d], out_dtype).  o and lse must come from flashmask_fwd on the same inputs
+ * (o in out_dtype).  dK/dV are accumulated per key tile on chip and written once
+ * (column-parallel); dQ is reduced in fp32 in the workspace and
+ * converted at the end.  Skipping and masking rules are those of the forward. */
+FM_API fm_status flashmask_bwd(const fm_params* p, const void* q, const void* k, const void* v, const void* o,
+                        const void* dout, const float* lse, const int32_t* startend_row_indices,
+                        void* dq, void* dk, void* dv, void* workspace, size_t workspace_bytes, void* stream);
+
+/* Static description of a status code. */
+FM_API const char* flashmask_status_string(fm_status s);
+
+/* Thread-local detail message for the calling thread's last non-OK status ("" if none). */
+FM_API const char* flashmask_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FLASHMASK_H_ */

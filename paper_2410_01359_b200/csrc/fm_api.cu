@@ -1,0 +1,267 @@
+// fm_api.cu — the C ABI of include/flashmask.h: argument validation, workspace layout,
+// TMA descriptor encoding and the launch sequence K1 -> K2 (forward) and
+// K1 -> K3 -> K4 -> K5 (backward).
+#include <cudaTypedefs.h>
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "../../include/flashmask.h"
+#include "fm_internal.h"
+
+namespace {
+
+thread_local std::string g_last_error;
+
+fm_status fail(fm_status s, const std::string& msg) {
+  g_last_error = msg;
+  return s;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+std::once_flag g_once;
+cudaError_t g_encode_err = cudaSuccess;
+
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  std::call_once(g_once, [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    g_encode_err = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
+    if (g_encode_err == cudaSuccess && q == cudaDriverEntryPointSuccess)
+      g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  });
+  return g_encode;
+}
+
+// [B, N, H, D] bf16 tensor viewed as the 4-D box grid (D, H, N, B); box = 64 x 1 x rows x 1,
+// 128-byte swizzle, out-of-bounds rows zero-filled.
+bool make_map(CUtensorMap* m, const void* ptr, const fm::Dims& d, int box_rows, std::string* err) {
+  auto enc = get_encode();
+  if (!enc) {
+    *err = "cuTensorMapEncodeTiled unavailable";
+    return false;
+  }
+  cuuint64_t dims[4] = {static_cast<cuuint64_t>(d.D), static_cast<cuuint64_t>(d.H), static_cast<cuuint64_t>(d.N),
+                        static_cast<cuuint64_t>(d.B)};
+  cuuint64_t strides[3] = {static_cast<cuuint64_t>(d.D) * 2, static_cast<cuuint64_t>(d.H) * d.D * 2,
+                           static_cast<cuuint64_t>(d.N) * d.H * d.D * 2};
+  cuuint32_t box[4] = {64, 1, static_cast<cuuint32_t>(box_rows), 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(ptr), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    *err = "cuTensorMapEncodeTiled failed with CUresult " + std::to_string(static_cast<int>(r));
+    return false;
+  }
+  return true;
+}
+
+fm_status check_params(const fm_params* p, fm::Dims* d, bool need_attention) {
+  if (!p) return fail(FM_ERR_INVALID_ARGUMENT, "params is NULL");
+  if (p->batch < 1 || p->seqlen < 1 || p->num_heads < 1)
+    return fail(FM_ERR_INVALID_ARGUMENT, "batch, seqlen and num_heads must be >= 1");
+  if (p->batch > 65535 || p->num_heads > 65535 || p->seqlen > (1LL << 30))
+    return fail(FM_ERR_UNSUPPORTED, "batch/num_heads > 65535 or seqlen > 2^30");
+  if (p->mask_heads != 1 && p->mask_heads != p->num_heads)
+    return fail(FM_ERR_INVALID_ARGUMENT, "mask_heads must be 1 or num_heads");
+  const int C = static_cast<int>(p->mask_cols);
+  const bool ok_c = p->causal ? (C == 1 || C == 2) : (C == 2 || C == 4);
+  if ((p->causal != 0 && p->causal != 1) || !ok_c)
+    return fail(FM_ERR_INVALID_ARGUMENT, "invalid (causal, mask_cols) combination; see the C-table in flashmask.h");
+  if (p->out_dtype != FM_BF16 && p->out_dtype != FM_FP32) return fail(FM_ERR_INVALID_ARGUMENT, "bad out_dtype");
+  if (p->in_dtype != FM_BF16 && p->in_dtype != FM_FP32) return fail(FM_ERR_INVALID_ARGUMENT, "bad in_dtype");
+  if (need_attention) {
+    if (p->head_dim != 64 && p->head_dim != 128) return fail(FM_ERR_INVALID_ARGUMENT, "head_dim must be 64 or 128");
+    if (p->in_dtype != FM_BF16) return fail(FM_ERR_UNSUPPORTED, "in_dtype FM_FP32 (tf32) is not implemented");
+  }
+  d->B = static_cast<int>(p->batch);
+  d->N = static_cast<int>(p->seqlen);
+  d->H = static_cast<int>(p->num_heads);
+  d->D = static_cast<int>(p->head_dim);
+  d->Hm = static_cast<int>(p->mask_heads);
+  d->C = C;
+  d->causal = p->causal;
+  d->Tr = (d->N + fm::kTile - 1) / fm::kTile;
+  d->Tc = d->Tr;
+  d->Brb = (d->D == 128) ? 64 : 128;
+  d->Trb = (d->N + d->Brb - 1) / d->Brb;
+  d->Npb = d->Trb * d->Brb;
+  d->scale = (p->scale > 0.f) ? p->scale : 1.0f / std::sqrt(static_cast<float>(p->head_dim > 0 ? p->head_dim : 1));
+  d->out_f32 = p->out_dtype == FM_FP32;
+  d->flags = p->flags;
+  if (need_attention && d->Tc > fm::kMaxTc) return fail(FM_ERR_UNSUPPORTED, "seqlen > 262144");
+  return FM_OK;
+}
+
+// Carve the workspace.  Returns the total size; pointers valid only when base != nullptr.
+size_t carve(const fm::Dims& d, int pass, void* base, fm::Workspace* w) {
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    const size_t o = off;
+    off = align_up(off + bytes, 256);
+    return base ? static_cast<uint8_t*>(base) + o : nullptr;
+  };
+  const size_t bhm = static_cast<size_t>(d.B) * d.Hm;
+  const size_t bh = static_cast<size_t>(d.B) * d.H;
+  w->ext8 = reinterpret_cast<int32_t*>(take(bhm * d.Tc * 8 * sizeof(int32_t)));
+  w->vec4 = reinterpret_cast<int4*>(take(bhm * d.Tc * 128 * sizeof(int4)));
+  w->fmap = nullptr;
+  w->bmap = nullptr;
+  w->dvec = w->l2 = w->dqacc = nullptr;
+  if (pass == FM_PASS_FWD) {
+    w->fmap = take(bhm * d.Tr * d.Tc);
+  } else {
+    w->bmap = take(bhm * d.Tc * d.Trb);
+    w->dvec = reinterpret_cast<float*>(take(bh * d.Npb * sizeof(float)));
+    w->l2 = reinterpret_cast<float*>(take(bh * d.Npb * sizeof(float)));
+    w->dqacc = reinterpret_cast<float*>(take(bh * d.Npb * d.D * sizeof(float)));
+  }
+  w->bytes = off;
+  return off;
+}
+
+fm_status cuda_fail(cudaError_t e, const char* where) {
+  return fail(FM_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* flashmask_status_string(fm_status s) {
+  switch (s) {
+    case FM_OK: return "FM_OK";
+    case FM_ERR_INVALID_ARGUMENT: return "FM_ERR_INVALID_ARGUMENT";
+    case FM_ERR_UNSUPPORTED: return "FM_ERR_UNSUPPORTED";
+    case FM_ERR_WORKSPACE_TOO_SMALL: return "FM_ERR_WORKSPACE_TOO_SMALL";
+    case FM_ERR_CUDA: return "FM_ERR_CUDA";
+  }
+  return "FM_UNKNOWN_STATUS";
+}
+
+const char* flashmask_last_error(void) { return g_last_error.c_str(); }
+
+size_t flashmask_workspace_size(const fm_params* p, int pass) {
+  fm::Dims d{};
+  if (check_params(p, &d, true) != FM_OK) return 0;
+  if (pass != FM_PASS_FWD && pass != FM_PASS_BWD) {
+    fail(FM_ERR_INVALID_ARGUMENT, "pass must be FM_PASS_FWD or FM_PASS_BWD");
+    return 0;
+  }
+  fm::Workspace w{};
+  return carve(d, pass, nullptr, &w);
+}
+
+fm_status flashmask_classify(const fm_params* p, const int32_t* sri, int32_t br, int32_t bc, int32_t* minmax,
+                             uint8_t* class_map, int64_t* counts, void* stream) {
+  g_last_error.clear();
+  fm::Dims d{};
+  fm_status s = check_params(p, &d, false);
+  if (s != FM_OK) return s;
+  if (!sri || !minmax) return fail(FM_ERR_INVALID_ARGUMENT, "startend_row_indices and minmax are required");
+  if (br < 1 || bc < 1) return fail(FM_ERR_INVALID_ARGUMENT, "br and bc must be >= 1");
+  if (!aligned16(minmax)) return fail(FM_ERR_INVALID_ARGUMENT, "minmax must be 16-byte aligned");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  cudaError_t e = fm::launch_expand(sri, d, bc, minmax, nullptr, st);
+  if (e != cudaSuccess) return cuda_fail(e, "expand");
+  if (class_map || counts) {
+    fm::Dims d0 = d;
+    d0.flags = 0;
+    e = fm::launch_classify(minmax, d0, br, bc, class_map, 0, 0, counts, st);
+    if (e != cudaSuccess) return cuda_fail(e, "classify");
+  }
+  return FM_OK;
+}
+
+fm_status flashmask_fwd(const fm_params* p, const void* q, const void* k, const void* v, const int32_t* sri, void* o,
+                        float* lse, void* workspace, size_t workspace_bytes, void* stream) {
+  g_last_error.clear();
+  fm::Dims d{};
+  fm_status s = check_params(p, &d, true);
+  if (s != FM_OK) return s;
+  if (!q || !k || !v || !sri || !o || !lse || !workspace) return fail(FM_ERR_INVALID_ARGUMENT, "NULL pointer argument");
+  if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(o) || !aligned16(sri) || !aligned16(workspace))
+    return fail(FM_ERR_INVALID_ARGUMENT, "q, k, v, o, startend_row_indices and workspace must be 16-byte aligned");
+  fm::Workspace w{};
+  if (carve(d, FM_PASS_FWD, nullptr, &w) > workspace_bytes)
+    return fail(FM_ERR_WORKSPACE_TOO_SMALL, "workspace smaller than flashmask_workspace_size(FM_PASS_FWD)");
+  carve(d, FM_PASS_FWD, workspace, &w);
+  std::string err;
+  CUtensorMap tq, tk, tv;
+  if (!make_map(&tq, q, d, 128, &err) || !make_map(&tk, k, d, 128, &err) || !make_map(&tv, v, d, 128, &err))
+    return fail(FM_ERR_CUDA, err);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  cudaError_t e = fm::launch_expand(sri, d, fm::kTile, w.ext8, w.vec4, st);
+  if (e != cudaSuccess) return cuda_fail(e, "expand");
+  e = fm::launch_classify(w.ext8, d, fm::kTile, fm::kTile, w.fmap, 0, 1, nullptr, st);
+  if (e != cudaSuccess) return cuda_fail(e, "classify");
+  fm::FwdArgs a{};
+  a.B = d.B; a.N = d.N; a.H = d.H; a.Hm = d.Hm; a.Tr = d.Tr; a.Tc = d.Tc;
+  a.scale_log2 = d.scale * 1.4426950408889634f;
+  a.fmap = w.fmap;
+  a.vec4 = w.vec4;
+  a.o = o;
+  a.lse = lse;
+  e = fm::launch_fwd(d, tq, tk, tv, a, st);
+  if (e != cudaSuccess) return cuda_fail(e, "forward kernel");
+  return FM_OK;
+}
+
+fm_status flashmask_bwd(const fm_params* p, const void* q, const void* k, const void* v, const void* o,
+                        const void* dout, const float* lse, const int32_t* sri, void* dq, void* dk, void* dv,
+                        void* workspace, size_t workspace_bytes, void* stream) {
+  g_last_error.clear();
+  fm::Dims d{};
+  fm_status s = check_params(p, &d, true);
+  if (s != FM_OK) return s;
+  if (!q || !k || !v || !o || !dout || !lse || !sri || !dq || !dk || !dv || !workspace)
+    return fail(FM_ERR_INVALID_ARGUMENT, "NULL pointer argument");
+  if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(o) || !aligned16(dout) || !aligned16(sri) ||
+      !aligned16(dq) || !aligned16(dk) || !aligned16(dv) || !aligned16(workspace))
+    return fail(FM_ERR_INVALID_ARGUMENT, "tensor pointers and workspace must be 16-byte aligned");
+  if (d.Trb > 4096) return fail(FM_ERR_UNSUPPORTED, "seqlen too large for the backward visit list");
+  fm::Workspace w{};
+  if (carve(d, FM_PASS_BWD, nullptr, &w) > workspace_bytes)
+    return fail(FM_ERR_WORKSPACE_TOO_SMALL, "workspace smaller than flashmask_workspace_size(FM_PASS_BWD)");
+  carve(d, FM_PASS_BWD, workspace, &w);
+  std::string err;
+  CUtensorMap tq, tk, tv, tdo;
+  if (!make_map(&tq, q, d, d.Brb, &err) || !make_map(&tk, k, d, 128, &err) || !make_map(&tv, v, d, 128, &err) ||
+      !make_map(&tdo, dout, d, d.Brb, &err))
+    return fail(FM_ERR_CUDA, err);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  cudaError_t e = fm::launch_expand(sri, d, fm::kTile, w.ext8, w.vec4, st);
+  if (e != cudaSuccess) return cuda_fail(e, "expand");
+  e = fm::launch_classify(w.ext8, d, d.Brb, fm::kTile, w.bmap, 1, 1, nullptr, st);
+  if (e != cudaSuccess) return cuda_fail(e, "classify");
+  e = fm::launch_bwd_pre(d, o, dout, lse, w.dvec, w.l2, w.dqacc, st);
+  if (e != cudaSuccess) return cuda_fail(e, "bwd preprocess");
+  fm::BwdArgs a{};
+  a.B = d.B; a.N = d.N; a.H = d.H; a.Hm = d.Hm; a.Tc = d.Tc; a.Trb = d.Trb; a.Npb = d.Npb;
+  a.scale_log2 = d.scale * 1.4426950408889634f;
+  a.scale = d.scale;
+  a.bmap = w.bmap;
+  a.vec4 = w.vec4;
+  a.dvec = w.dvec;
+  a.l2 = w.l2;
+  a.dqacc = w.dqacc;
+  a.dk = dk;
+  a.dv = dv;
+  e = fm::launch_bwd(d, tq, tk, tv, tdo, a, st);
+  if (e != cudaSuccess) return cuda_fail(e, "backward kernel");
+  e = fm::launch_dq_convert(d, w.dqacc, dq, st);
+  if (e != cudaSuccess) return cuda_fail(e, "dq convert");
+  return FM_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,389 @@
+// fm_bwd.cu — K4: FlashMask backward main kernel (Alg. 2) for sm_100a.
+//
+// Column-parallel: one CTA owns key tile j (128 keys) of one (batch, head),
+// keeps dK_j and dV_j as fp32 accumulators in TMEM for the whole row loop and writes them
+// once at the end (atomic-free).  The four mask values of its 128 keys are loaded once into
+// registers — thread = key = TMEM lane in the transposed S^T layout (Alg. 2 lines 10-11,
+// P:394-395 "loaded once per column tile").  Row tiles that are SKIP for this column tile
+// are never loaded (Alg. 2 lines 13-18).
+//
+// Row tile Br = 64 for d = 128, 128 for d = 64.  Per visited row tile i:
+//   S^T  = K_j Q_i^T          (tcgen05, M=128 keys, N=Br, K=d)
+//   dP^T = V_j dO_i^T         (tcgen05)
+//   P^T  = exp2(S^T*scale*log2e - L2_i), masked on PARTIAL tiles
+//   dS^T = P^T o (dP^T - D_i)
+//   dV  += P^T dO_i           (A = P^T from TMEM)
+//   dK  += dS^T Q_i           (A = dS^T from TMEM)
+//   d=128: dQ_i^T = K_j^T dS^T (M = d); d=64: dQ_i = dS K_j (M = queries)
+// and the dQ tile is added into the fp32 workspace with one bulk reduce-add
+// (cp.reduce.async.bulk .add.f32) instead of a read-modify-write.
+// Warp roles: 0-3 compute WG (keys), 4-7 dQ WG (TMEM -> smem -> bulk reduce),
+// 8 TMA producer, 9 TMEM allocator + MMA issuer.
+#include <cuda_bf16.h>
+#include <cmath>
+
+#include "fm_internal.h"
+#include "fm_ptx.cuh"
+
+namespace fm {
+
+namespace bwd {
+
+constexpr int NT = 320;
+constexpr int QST = 2;
+constexpr int kMaxTrb = 4096;
+
+template <int D>
+struct Cfg {
+  static constexpr int BR = (D == 128) ? 64 : 128;
+  static constexpr bool DQT = (D == 128);          // dQ computed transposed (M = d)
+  static constexpr int KV_TILE = 128 * D * 2;      // bytes
+  static constexpr int Q_TILE = BR * D * 2;
+  static constexpr int DS_BYTES = 128 * BR * 2;
+  static constexpr int STG_BYTES = BR * D * 4;
+  static constexpr int S_COL = 0, DP_COL = BR, DQ_COL = 2 * BR;
+  static constexpr int DV_COL = (D == 128) ? 256 : 320;
+  static constexpr int DK_COL = DV_COL + D;
+};
+
+template <int D>
+struct Smem {
+  using C = Cfg<D>;
+  uint8_t k[C::KV_TILE];
+  uint8_t v[C::KV_TILE];
+  uint8_t q[QST][C::Q_TILE];
+  uint8_t dO[QST][C::Q_TILE];
+  uint8_t ds[C::DS_BYTES];
+  float stg[C::BR * D];
+  float lvec[QST][C::BR];
+  float dvec[QST][C::BR];
+  uint32_t list[kMaxTrb];
+  uint64_t kv_full;
+  uint64_t q_full[QST], q_empty[QST];
+  uint64_t s_full, p_full, dq_full, dq_empty, ds_empty, done;
+  uint32_t tmem_base;
+  int n_entries;
+  int warp_cnt[NT / 32];
+};
+
+}  // namespace bwd
+
+template <int D, bool CAUSAL, bool OUT_F32>
+__global__ void __launch_bounds__(bwd::NT, 1)
+    fm_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                  const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO,
+                  const BwdArgs a) {
+  using namespace bwd;
+  using C = Cfg<D>;
+  using S = Smem<D>;
+  constexpr int BR = C::BR;
+  extern __shared__ uint8_t smem_raw[];
+  S& sm = *reinterpret_cast<S*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int j = static_cast<int>(blockIdx.x);
+  const int h = blockIdx.y, b = blockIdx.z;
+  const int hm = (a.Hm == 1) ? 0 : h;
+  const size_t bhm = static_cast<size_t>(b) * a.Hm + hm;
+  const size_t bh = static_cast<size_t>(b) * a.H + h;
+
+  if (warp == 8 && lane == 0) {
+    mbar_init(&sm.kv_full, 1);
+    for (int s = 0; s < QST; ++s) { mbar_init(&sm.q_full[s], 1); mbar_init(&sm.q_empty[s], 1); }
+    mbar_init(&sm.s_full, 1);
+    mbar_init(&sm.p_full, 128);
+    mbar_init(&sm.dq_full, 1);
+    mbar_init(&sm.dq_empty, 128);
+    mbar_init(&sm.ds_empty, 1);
+    mbar_init(&sm.done, 1);
+    fence_barrier_init();
+  }
+  if (warp == 9) tmem_alloc<512>(&sm.tmem_base);
+
+  // ---- visit list: row tiles i that are not SKIP for column tile j (K1 transposed map) ----
+  {
+    const uint8_t* col = a.bmap + (bhm * a.Tc + j) * a.Trb;
+    int base = 0;
+    for (int i0 = 0; i0 < a.Trb; i0 += NT) {
+      const int i = i0 + tid;
+      const uint32_t c = (i < a.Trb) ? col[i] : 0u;
+      const bool vis = c != 0u;
+      const unsigned bal = __ballot_sync(0xffffffffu, vis);
+      if (lane == 0) sm.warp_cnt[warp] = __popc(bal);
+      __syncthreads();
+      int off = base, tot = 0;
+      for (int w = 0; w < NT / 32; ++w) {
+        const int cw = sm.warp_cnt[w];
+        if (w < warp) off += cw;
+        tot += cw;
+      }
+      off += __popc(bal & ((1u << lane) - 1u));
+      if (vis) sm.list[off] = static_cast<uint32_t>(i) | (c << 24);
+      base += tot;
+      __syncthreads();
+    }
+    if (tid == 0) sm.n_entries = base;
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const int nE = sm.n_entries;
+  const uint32_t tbase = sm.tmem_base;
+
+  if (warp == 8) {
+    // ================================ TMA producer ================================
+    if (lane == 0 && nE > 0) {
+      tma_prefetch_desc(&tmQ);
+      tma_prefetch_desc(&tmK);
+      tma_prefetch_desc(&tmV);
+      tma_prefetch_desc(&tmdO);
+      mbar_expect_tx(&sm.kv_full, 2 * C::KV_TILE);
+#pragma unroll
+      for (int c = 0; c < D / 64; ++c) {
+        tma_load_4d(sm.k + c * 16384, &tmK, &sm.kv_full, c * 64, h, j * 128, b);
+        tma_load_4d(sm.v + c * 16384, &tmV, &sm.kv_full, c * 64, h, j * 128, b);
+      }
+      for (int t = 0; t < nE; ++t) {
+        const int i = static_cast<int>(sm.list[t] & 0xFFFFFFu);
+        const int st = t % QST;
+        mbar_wait(&sm.q_empty[st], ((t / QST) & 1) ^ 1);
+        mbar_expect_tx(&sm.q_full[st], 2 * C::Q_TILE + 2 * BR * 4);
+#pragma unroll
+        for (int c = 0; c < D / 64; ++c) {
+          tma_load_4d(sm.q[st] + c * (BR * 128), &tmQ, &sm.q_full[st], c * 64, h, i * BR, b);
+          tma_load_4d(sm.dO[st] + c * (BR * 128), &tmdO, &sm.q_full[st], c * 64, h, i * BR, b);
+        }
+        bulk_g2s(sm.lvec[st], a.l2 + bh * a.Npb + static_cast<size_t>(i) * BR, BR * 4, &sm.q_full[st]);
+        bulk_g2s(sm.dvec[st], a.dvec + bh * a.Npb + static_cast<size_t>(i) * BR, BR * 4, &sm.q_full[st]);
+      }
+    }
+  } else if (warp == 9) {
+    // ================================ MMA issuer ================================
+    if (lane == 0 && nE > 0) {
+      constexpr uint32_t ID_S = idesc_bf16(128, BR, 0, 0);   // S^T, dP^T: A, B K-major
+      constexpr uint32_t ID_G = idesc_bf16(128, D, 0, 1);    // dV, dK: A in TMEM, B MN-major
+      constexpr uint32_t ID_Q = idesc_bf16(128, 64, 1, 1);   // dQ^T (d=128) / dQ (d=64)
+      const uint32_t k_addr = smem_u32(sm.k), v_addr = smem_u32(sm.v), ds_addr = smem_u32(sm.ds);
+      mbar_wait(&sm.kv_full, 0);
+      for (int t = 0; t < nE; ++t) {
+        const int st = t % QST;
+        mbar_wait(&sm.q_full[st], (t / QST) & 1);
+        tc_fence_after();
+        const uint32_t q_addr = smem_u32(sm.q[st]), do_addr = smem_u32(sm.dO[st]);
+        // S^T = K Q^T ; dP^T = V dO^T
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint32_t ao = (kk >> 2) * 16384 + (kk & 3) * 32;
+          const uint32_t bo = (kk >> 2) * (BR * 128) + (kk & 3) * 32;
+          mma_ss(tbase + C::S_COL, sdesc_sw128(k_addr + ao, 16, 1024), sdesc_sw128(q_addr + bo, 16, 1024), ID_S,
+                 kk > 0 ? 1u : 0u);
+        }
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint32_t ao = (kk >> 2) * 16384 + (kk & 3) * 32;
+          const uint32_t bo = (kk >> 2) * (BR * 128) + (kk & 3) * 32;
+          mma_ss(tbase + C::DP_COL, sdesc_sw128(v_addr + ao, 16, 1024), sdesc_sw128(do_addr + bo, 16, 1024), ID_S,
+                 kk > 0 ? 1u : 0u);
+        }
+        mma_commit(&sm.s_full);
+        mbar_wait(&sm.p_full, t & 1);
+        tc_fence_after();
+        // dV += P^T dO ; dK += dS^T Q   (K = BR queries)
+#pragma unroll
+        for (int kk = 0; kk < BR / 16; ++kk) {
+          const uint32_t acc = (t > 0 || kk > 0) ? 1u : 0u;
+          mma_ts(tbase + C::DV_COL, tbase + C::S_COL + kk * 8, sdesc_sw128(do_addr + kk * 2048, BR * 128, 1024), ID_G,
+                 acc);
+          mma_ts(tbase + C::DK_COL, tbase + C::DP_COL + kk * 8, sdesc_sw128(q_addr + kk * 2048, BR * 128, 1024), ID_G,
+                 acc);
+        }
+        // dQ (K = 128 keys)
+        mbar_wait(&sm.dq_empty, (t & 1) ^ 1);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          if constexpr (C::DQT)
+            mma_ss(tbase + C::DQ_COL, sdesc_sw128(k_addr + kk * 2048, 16384, 1024),
+                   sdesc_sw128(ds_addr + kk * 2048, 16384, 1024), ID_Q, kk > 0 ? 1u : 0u);
+          else
+            mma_ss(tbase + C::DQ_COL, sdesc_sw128(ds_addr + kk * 2048, 16384, 1024),
+                   sdesc_sw128(k_addr + kk * 2048, 16384, 1024), ID_Q, kk > 0 ? 1u : 0u);
+        }
+        mma_commit(&sm.dq_full);
+        mma_commit(&sm.ds_empty);
+        mma_commit(&sm.q_empty[st]);
+      }
+      mma_commit(&sm.done);
+    }
+  } else if (warp < 4) {
+    // ============================ compute WG (thread = key) ============================
+    const int key_t = warp * 32 + lane;
+    const int key = j * 128 + key_t;
+    const uint32_t lane_off = static_cast<uint32_t>(warp * 32) << 16;
+    const int4 mv = a.vec4[(bhm * a.Tc) * 128 + key];  // this key's (LTS, LTE, UTS, UTE), normalised
+    const float sl2 = a.scale_log2;
+    for (int t = 0; t < nE; ++t) {
+      const uint32_t ent = sm.list[t];
+      const int i = static_cast<int>(ent & 0xFFFFFFu);
+      const bool partial = ((ent >> 24) & 3u) == 1u;
+      const int st = t % QST;
+      mbar_wait(&sm.q_full[st], (t / QST) & 1);
+      mbar_wait(&sm.s_full, t & 1);
+      tc_fence_after();
+      mbar_wait(&sm.ds_empty, (t & 1) ^ 1);  // dQ GEMM of the previous row tile has read dS
+      const float* lv = sm.lvec[st];
+      const float* dv = sm.dvec[st];
+#pragma unroll 1
+      for (int ch = 0; ch < BR / 32; ++ch) {
+        uint32_t sr[32], dr[32];
+        tmem_ld32(tbase + lane_off + C::S_COL + ch * 32, sr);
+        tmem_ld32(tbase + lane_off + C::DP_COL + ch * 32, dr);
+        tmem_wait_ld();
+        uint32_t pp[16], dp[16];
+#pragma unroll
+        for (int c = 0; c < 32; c += 2) {
+          float pv[2], dsv[2];
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            const int qc = ch * 32 + c + u;
+            float p = ex2(fmaf(__uint_as_float(sr[c + u]), sl2, -lv[qc]));
+            if (partial) {
+              const int r = i * BR + qc;
+              bool msk = static_cast<unsigned>(r - mv.x) < static_cast<unsigned>(mv.y - mv.x);
+              if constexpr (CAUSAL)
+                msk |= r < key;
+              else
+                msk |= static_cast<unsigned>(r - mv.z) < static_cast<unsigned>(mv.w - mv.z);
+              p = msk ? 0.f : p;
+            }
+            pv[u] = p;
+            dsv[u] = p * (__uint_as_float(dr[c + u]) - dv[qc]);
+          }
+          pp[c >> 1] = pack_bf16(pv[0], pv[1]);
+          dp[c >> 1] = pack_bf16(dsv[0], dsv[1]);
+        }
+        tmem_st16(tbase + lane_off + C::S_COL + ch * 16, pp);
+        tmem_st16(tbase + lane_off + C::DP_COL + ch * 16, dp);
+        // dS^T row of this key into the SW128 MN-major smem operand of the dQ GEMM
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int g = ch * 4 + u;  // 8-query group
+          const int sub = g >> 3, gg = g & 7;
+          uint8_t* dst = sm.ds + sub * 16384 + key_t * 128 + ((gg ^ (key_t & 7)) << 4);
+          *reinterpret_cast<uint4*>(dst) = make_uint4(dp[4 * u], dp[4 * u + 1], dp[4 * u + 2], dp[4 * u + 3]);
+        }
+      }
+      fence_proxy_async_smem();
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(&sm.p_full);
+    }
+    // ---- epilogue: dK_j = scale * dK, dV_j written once (Alg. 2 line 30) ----
+    if (nE > 0) {
+      mbar_wait(&sm.done, 0);
+      tc_fence_after();
+    }
+    const size_t orow = ((static_cast<size_t>(b) * a.N + key) * a.H + h) * D;
+#pragma unroll 1
+    for (int which = 0; which < 2; ++which) {
+      const uint32_t col = which == 0 ? C::DV_COL : C::DK_COL;
+      const float mul = which == 0 ? 1.0f : a.scale;
+      void* outp = which == 0 ? a.dv : a.dk;
+#pragma unroll 1
+      for (int c = 0; c < D / 32; ++c) {
+        uint32_t r[32];
+        if (nE > 0) {
+          tmem_ld32(tbase + lane_off + col + c * 32, r);
+          tmem_wait_ld();
+        }
+        float f[32];
+#pragma unroll
+        for (int t = 0; t < 32; ++t) f[t] = nE > 0 ? __uint_as_float(r[t]) * mul : 0.f;
+        if (key < a.N) {
+          if constexpr (OUT_F32) {
+            float4* dst = reinterpret_cast<float4*>(static_cast<float*>(outp) + orow + c * 32);
+#pragma unroll
+            for (int t = 0; t < 8; ++t) dst[t] = make_float4(f[4 * t], f[4 * t + 1], f[4 * t + 2], f[4 * t + 3]);
+          } else {
+            uint4* dst = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(outp) + orow + c * 32);
+#pragma unroll
+            for (int t = 0; t < 4; ++t)
+              dst[t] = make_uint4(pack_bf16(f[8 * t], f[8 * t + 1]), pack_bf16(f[8 * t + 2], f[8 * t + 3]),
+                                  pack_bf16(f[8 * t + 4], f[8 * t + 5]), pack_bf16(f[8 * t + 6], f[8 * t + 7]));
+          }
+        }
+      }
+    }
+  } else {
+    // ============================ dQ WG: TMEM -> smem -> bulk reduce-add ============================
+    const int wl = warp - 4;
+    const int t_id = wl * 32 + lane;  // TMEM lane: d index (d=128) or query (d=64)
+    const uint32_t lane_off = static_cast<uint32_t>(wl * 32) << 16;
+    for (int t = 0; t < nE; ++t) {
+      const int i = static_cast<int>(sm.list[t] & 0xFFFFFFu);
+      mbar_wait(&sm.dq_full, t & 1);
+      tc_fence_after();
+      uint32_t r[64];
+      tmem_ld32(tbase + lane_off + C::DQ_COL, r);
+      tmem_ld32(tbase + lane_off + C::DQ_COL + 32, r + 32);
+      tmem_wait_ld();
+      tc_fence_before();
+      mbar_arrive(&sm.dq_empty);
+      if (t_id == 0) bulk_wait_read0();  // previous reduce finished reading the staging tile
+      named_bar_sync(1, 128);
+      if constexpr (C::DQT) {
+        // r[q] = dQ^T[d = t_id][q] -> stg[q][d]
+#pragma unroll
+        for (int q = 0; q < 64; ++q) sm.stg[q * D + t_id] = __uint_as_float(r[q]);
+      } else {
+        // r[c] = dQ[query = t_id][c] -> stg[query][c]
+#pragma unroll
+        for (int c4 = 0; c4 < 16; ++c4)
+          reinterpret_cast<float4*>(sm.stg + t_id * D)[c4] =
+              make_float4(__uint_as_float(r[c4 * 4]), __uint_as_float(r[c4 * 4 + 1]), __uint_as_float(r[c4 * 4 + 2]),
+                          __uint_as_float(r[c4 * 4 + 3]));
+      }
+      fence_proxy_async_smem();
+      named_bar_sync(1, 128);
+      if (t_id == 0) {
+        bulk_reduce_add_f32(a.dqacc + (bh * a.Npb + static_cast<size_t>(i) * BR) * D, sm.stg, C::STG_BYTES);
+        bulk_commit();
+      }
+    }
+    if (t_id == 0) bulk_wait0();
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 9) {
+    tc_fence_after();
+    tmem_dealloc<512>(tbase);
+  }
+}
+
+template <int D, bool CAUSAL, bool OUT_F32>
+static cudaError_t launch_bwd_t(const Dims& d, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
+                                const CUtensorMap& tdo, const BwdArgs& a, cudaStream_t st) {
+  auto kern = fm_bwd_kernel<D, CAUSAL, OUT_F32>;
+  const size_t smem = sizeof(bwd::Smem<D>) + 1024;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  dim3 grid(d.Tc, d.H, d.B);
+  kern<<<grid, bwd::NT, smem, st>>>(tq, tk, tv, tdo, a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_bwd(const Dims& d, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
+                       const CUtensorMap& tdo, const BwdArgs& a, cudaStream_t st) {
+#define FM_B(DD, CC, FF) return launch_bwd_t<DD, CC, FF>(d, tq, tk, tv, tdo, a, st)
+  if (d.D == 128) {
+    if (d.causal) { if (d.out_f32) FM_B(128, true, true); else FM_B(128, true, false); }
+    else { if (d.out_f32) FM_B(128, false, true); else FM_B(128, false, false); }
+  } else {
+    if (d.causal) { if (d.out_f32) FM_B(64, true, true); else FM_B(64, true, false); }
+    else { if (d.out_f32) FM_B(64, false, true); else FM_B(64, false, false); }
+  }
+#undef FM_B
+}
+
+}  // namespace fm

@@ -1,0 +1,378 @@
+// fm_fwd.cu — K2: FlashMask forward (Alg. 1) for sm_100a.
+//
+// One CTA owns a pair of 128-row query tiles (Q0, Q1) of one (batch, head).  Warp roles:
+//   warps 0-3  softmax WG0  (thread = one row of Q0 = one TMEM lane)
+//   warps 4-7  softmax WG1  (rows of Q1)
+//   warp  8    TMA producer (lane 0): Q once, then K_j, V_j and the mask slice of tile j
+//   warp  9    TMEM allocator + tcgen05 MMA issuer (lane 0)
+// The visit list — the column tiles j that are not SKIP for Q0 or Q1 — is built from the
+// K1 class map before the roles split, so fully masked tiles issue no load and no MMA
+// (Alg. 1 lines 9-14).  S_q = Q_q K_j^T (tcgen05, fp32 in TMEM), softmax in
+// registers with the element-wise interval mask applied only on PARTIAL tiles (Alg. 1
+// lines 15-21), P_q written back to TMEM as bf16 (aliasing S_q) and
+// O_q += P_q V_j issued with P as the TMEM A operand.  The two query tiles ping-pong: while
+// one WG runs its softmax the tensor core computes the other tile's S / PV.
+// TMEM columns: S0 [0,128)  S1 [128,256)  O0 [256,256+D)  O1 [256+D, 256+2D).
+#include <cuda_bf16.h>
+#include <cmath>
+
+#include "fm_internal.h"
+#include "fm_ptx.cuh"
+
+namespace fm {
+
+namespace fwd {
+
+constexpr int NT = 320;
+constexpr int KST = 2, VST = 2, MST = 4;
+
+template <int D>
+struct Smem {
+  static constexpr int TILE = 128 * D * 2;
+  uint8_t q[2][TILE];
+  uint8_t k[KST][TILE];
+  uint8_t v[VST][TILE];
+  int4 mask[MST][128];
+  uint32_t list[kMaxTc];
+  uint64_t bar_q;
+  uint64_t k_full[KST], k_empty[KST], v_full[VST], v_empty[VST];
+  uint64_t m_full[MST], m_empty[MST];
+  uint64_t s_full[2], p_full[2], o_full[2];
+  uint32_t tmem_base;
+  int n_entries;
+  int warp_cnt[NT / 32];
+};
+
+__device__ __forceinline__ int ent_cls(uint32_t ent, int q) { return (ent >> (24 + 2 * q)) & 3; }
+
+}  // namespace fwd
+
+template <int D, bool CAUSAL, bool OUT_F32>
+__global__ void __launch_bounds__(fwd::NT, 1)
+    fm_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                  const __grid_constant__ CUtensorMap tmV, const FwdArgs a) {
+  using namespace fwd;
+  using S = Smem<D>;
+  extern __shared__ uint8_t smem_raw[];
+  S& sm = *reinterpret_cast<S*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int npairs = (a.Tr + 1) >> 1;
+  const int pair = npairs - 1 - static_cast<int>(blockIdx.x);  // heaviest (last) row tiles first
+  const int h = blockIdx.y, b = blockIdx.z;
+  const int hm = (a.Hm == 1) ? 0 : h;
+  const int i0 = 2 * pair, i1 = 2 * pair + 1;
+  const bool has_q1 = i1 < a.Tr;
+  const size_t bhm = static_cast<size_t>(b) * a.Hm + hm;
+
+  // ---- setup: barriers (warp 8), TMEM (warp 9) ----
+  if (warp == 8 && lane == 0) {
+    mbar_init(&sm.bar_q, 1);
+    for (int s = 0; s < KST; ++s) { mbar_init(&sm.k_full[s], 1); mbar_init(&sm.k_empty[s], 1); }
+    for (int s = 0; s < VST; ++s) { mbar_init(&sm.v_full[s], 1); mbar_init(&sm.v_empty[s], 1); }
+    for (int s = 0; s < MST; ++s) { mbar_init(&sm.m_full[s], 1); mbar_init(&sm.m_empty[s], 8); }
+    for (int q = 0; q < 2; ++q) {
+      mbar_init(&sm.s_full[q], 1);
+      mbar_init(&sm.p_full[q], 128);
+      mbar_init(&sm.o_full[q], 1);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 9) tmem_alloc<512>(&sm.tmem_base);
+
+  // ---- visit list: union of the non-SKIP column tiles of Q0 and Q1 (K1 class map) ----
+  {
+    const uint8_t* row0 = a.fmap + (bhm * a.Tr + i0) * a.Tc;
+    const uint8_t* row1 = row0 + a.Tc;
+    int base = 0;
+    for (int j0 = 0; j0 < a.Tc; j0 += NT) {
+      const int j = j0 + tid;
+      uint32_t c0 = 0, c1 = 0;
+      if (j < a.Tc) {
+        c0 = row0[j];
+        c1 = has_q1 ? row1[j] : 0u;
+      }
+      const bool vis = (c0 | c1) != 0u;
+      const unsigned bal = __ballot_sync(0xffffffffu, vis);
+      if (lane == 0) sm.warp_cnt[warp] = __popc(bal);
+      __syncthreads();
+      int off = base;
+      int tot = 0;
+      for (int w = 0; w < NT / 32; ++w) {
+        const int c = sm.warp_cnt[w];
+        if (w < warp) off += c;
+        tot += c;
+      }
+      off += __popc(bal & ((1u << lane) - 1u));
+      if (vis) sm.list[off] = static_cast<uint32_t>(j) | (c0 << 24) | (c1 << 26);
+      base += tot;
+      __syncthreads();
+    }
+    if (tid == 0) sm.n_entries = base;
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const int nE = sm.n_entries;
+  const uint32_t tbase = sm.tmem_base;
+
+  if (warp == 8) {
+    // ================================ TMA producer ================================
+    if (lane == 0) {
+      tma_prefetch_desc(&tmQ);
+      tma_prefetch_desc(&tmK);
+      tma_prefetch_desc(&tmV);
+      constexpr uint32_t TB = S::TILE;
+      if (nE > 0) {
+        mbar_expect_tx(&sm.bar_q, has_q1 ? 2 * TB : TB);
+#pragma unroll
+        for (int c = 0; c < D / 64; ++c) {
+          tma_load_4d(sm.q[0] + c * 16384, &tmQ, &sm.bar_q, c * 64, h, i0 * 128, b);
+          if (has_q1) tma_load_4d(sm.q[1] + c * 16384, &tmQ, &sm.bar_q, c * 64, h, i1 * 128, b);
+        }
+      }
+      const int4* vec_bh = a.vec4 + bhm * static_cast<size_t>(a.Tc) * 128;
+      for (int e = 0; e < nE; ++e) {
+        const uint32_t ent = sm.list[e];
+        const int j = static_cast<int>(ent & 0xFFFFFFu);
+        const int ks = e % KST, vs = e % VST, ms = e % MST;
+        mbar_wait(&sm.k_empty[ks], ((e / KST) & 1) ^ 1);
+        mbar_expect_tx(&sm.k_full[ks], TB);
+#pragma unroll
+        for (int c = 0; c < D / 64; ++c) tma_load_4d(sm.k[ks] + c * 16384, &tmK, &sm.k_full[ks], c * 64, h, j * 128, b);
+        mbar_wait(&sm.m_empty[ms], ((e / MST) & 1) ^ 1);
+        if (ent_cls(ent, 0) == 1 || ent_cls(ent, 1) == 1) {
+          mbar_expect_tx(&sm.m_full[ms], 128 * 16);
+          bulk_g2s(sm.mask[ms], vec_bh + static_cast<size_t>(j) * 128, 128 * 16, &sm.m_full[ms]);
+        } else {
+          mbar_arrive(&sm.m_full[ms]);
+        }
+        mbar_wait(&sm.v_empty[vs], ((e / VST) & 1) ^ 1);
+        mbar_expect_tx(&sm.v_full[vs], TB);
+#pragma unroll
+        for (int c = 0; c < D / 64; ++c) tma_load_4d(sm.v[vs] + c * 16384, &tmV, &sm.v_full[vs], c * 64, h, j * 128, b);
+      }
+    }
+  } else if (warp == 9) {
+    // ================================ MMA issuer ================================
+    if (lane == 0) {
+      constexpr uint32_t ID_S = idesc_bf16(128, 128, 0, 0);  // S = Q K^T, both K-major
+      constexpr uint32_t ID_PV = idesc_bf16(128, D, 0, 1);   // O += P V, V is MN-major
+      const uint32_t tS[2] = {tbase + 0, tbase + 128};
+      const uint32_t tO[2] = {tbase + 256, tbase + 256 + D};
+      const uint32_t q_addr[2] = {smem_u32(sm.q[0]), smem_u32(sm.q[1])};
+      int pend[2] = {-1, -1};
+      uint32_t pv_cnt[2] = {0, 0};
+      auto issue_pv = [&](int q) {
+        const int pe = pend[q];
+        mbar_wait(&sm.p_full[q], pv_cnt[q] & 1);
+        const int vs = pe % VST;
+        mbar_wait(&sm.v_full[vs], (pe / VST) & 1);
+        tc_fence_after();
+        const uint32_t v_addr = smem_u32(sm.v[vs]);
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          const uint64_t bd = sdesc_sw128(v_addr + kk * 2048, 16384, 1024);
+          mma_ts(tO[q], tS[q] + kk * 8, bd, ID_PV, (pv_cnt[q] > 0 || kk > 0) ? 1u : 0u);
+        }
+        pv_cnt[q]++;
+        const uint32_t ent = sm.list[pe];
+        const int last = (ent_cls(ent, 1) != 0) ? 1 : 0;
+        if (q == last) mma_commit(&sm.v_empty[vs]);
+        pend[q] = -1;
+      };
+      if (nE > 0) {
+        mbar_wait(&sm.bar_q, 0);
+        tc_fence_after();
+      }
+      for (int e = 0; e < nE; ++e) {
+        const uint32_t ent = sm.list[e];
+        const int ks = e % KST;
+        mbar_wait(&sm.k_full[ks], (e / KST) & 1);
+        tc_fence_after();
+        const uint32_t k_addr = smem_u32(sm.k[ks]);
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          if (pend[q] >= 0) issue_pv(q);
+          if (ent_cls(ent, q) != 0) {
+#pragma unroll
+            for (int kk = 0; kk < D / 16; ++kk) {
+              const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
+              mma_ss(tS[q], sdesc_sw128(q_addr[q] + off, 16, 1024), sdesc_sw128(k_addr + off, 16, 1024), ID_S,
+                     kk > 0 ? 1u : 0u);
+            }
+            mma_commit(&sm.s_full[q]);
+            pend[q] = e;
+          }
+        }
+        mma_commit(&sm.k_empty[ks]);
+      }
+      for (int q = 0; q < 2; ++q)
+        if (pend[q] >= 0) issue_pv(q);
+      mma_commit(&sm.o_full[0]);
+      mma_commit(&sm.o_full[1]);
+    }
+  } else {
+    // ================================ softmax WGs ================================
+    const int q = warp >> 2;
+    const int wl = warp & 3;
+    const int row_t = wl * 32 + lane;
+    const int row = (q == 0 ? i0 : i1) * 128 + row_t;
+    const uint32_t lane_off = static_cast<uint32_t>(wl * 32) << 16;
+    const uint32_t tS = tbase + lane_off + (q == 0 ? 0u : 128u);
+    const uint32_t tO = tbase + lane_off + 256u + (q == 0 ? 0u : static_cast<uint32_t>(D));
+    const float sl2 = a.scale_log2;
+    float m_used = -INFINITY;  // running max of the scaled logits, log2 units (threshold-updated)
+    float l = 0.f;
+    uint32_t cnt = 0;
+    for (int e = 0; e < nE; ++e) {
+      const uint32_t ent = sm.list[e];
+      const int cls = ent_cls(ent, q);
+      const int ms = e % MST;
+      mbar_wait(&sm.m_full[ms], (e / MST) & 1);
+      if (cls != 0) {
+        const int j = static_cast<int>(ent & 0xFFFFFFu);
+        mbar_wait(&sm.s_full[q], cnt & 1);
+        tc_fence_after();
+        uint32_t sr[128];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) tmem_ld32(tS + c * 32, sr + c * 32);
+        tmem_wait_ld();
+        float* s = reinterpret_cast<float*>(sr);
+        if (cls == 1) {
+          const int4* mk = sm.mask[ms];
+          const int y0 = j * 128;
+#pragma unroll
+          for (int c = 0; c < 128; ++c) {
+            const int4 mv = mk[c];
+            bool msk = static_cast<unsigned>(row - mv.x) < static_cast<unsigned>(mv.y - mv.x);
+            if constexpr (CAUSAL)
+              msk |= row < y0 + c;
+            else
+              msk |= static_cast<unsigned>(row - mv.z) < static_cast<unsigned>(mv.w - mv.z);
+            s[c] = msk ? -INFINITY : s[c];
+          }
+        }
+        float mx0 = s[0], mx1 = s[1], mx2 = s[2], mx3 = s[3];
+#pragma unroll
+        for (int c = 4; c < 128; c += 4) {
+          mx0 = fmaxf(mx0, s[c]);
+          mx1 = fmaxf(mx1, s[c + 1]);
+          mx2 = fmaxf(mx2, s[c + 2]);
+          mx3 = fmaxf(mx3, s[c + 3]);
+        }
+        const float m_tile = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3)) * sl2;
+        // Conditional rescale: the running max only moves when it grows by more than 2^8
+        // (exact: P is computed against the same m that scales l and O).  The decision is
+        // made per warp so the TMEM accesses stay warp-collective.
+        const bool need = m_tile > m_used + 8.0f;
+        float alpha = 1.0f;
+        if (need) {
+          alpha = ex2(m_used - m_tile);  // Alg. 1 line 25 factor e^{m_old - m_new}
+          l *= alpha;
+          m_used = m_tile;
+        }
+        if (__any_sync(0xffffffffu, need) && cnt > 0) {
+#pragma unroll 1
+          for (int c = 0; c < D / 32; ++c) {
+            uint32_t ov[32];
+            tmem_ld32(tO + c * 32, ov);
+            tmem_wait_ld();
+#pragma unroll
+            for (int t = 0; t < 32; ++t) ov[t] = __float_as_uint(__uint_as_float(ov[t]) * alpha);
+            tmem_st32(tO + c * 32, ov);
+          }
+        }
+        const float m_use = (m_used == -INFINITY) ? 0.f : m_used;
+        float ls0 = 0.f, ls1 = 0.f;
+        uint32_t pk[64];
+#pragma unroll
+        for (int c = 0; c < 128; c += 2) {
+          const float p0 = ex2(fmaf(s[c], sl2, -m_use));
+          const float p1 = ex2(fmaf(s[c + 1], sl2, -m_use));
+          ls0 += p0;
+          ls1 += p1;
+          pk[c >> 1] = pack_bf16(p0, p1);
+        }
+        l += ls0 + ls1;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) tmem_st16(tS + c * 16, pk + c * 16);
+        tmem_wait_st();
+        tc_fence_before();
+        mbar_arrive(&sm.p_full[q]);
+        ++cnt;
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sm.m_empty[ms]);
+    }
+    // ---- epilogue: O = O / l, L = m + ln(l) (Alg. 1 lines 27-28) ----
+    const bool live = (cnt > 0) && (l > 0.f);
+    if (cnt > 0) {
+      mbar_wait(&sm.o_full[q], 0);
+      tc_fence_after();
+    }
+    const float inv = live ? 1.0f / l : 0.f;
+    const size_t orow = ((static_cast<size_t>(b) * a.N + row) * a.H + h) * D;
+#pragma unroll 1
+    for (int c = 0; c < D / 32; ++c) {
+      uint32_t ov[32];
+      if (cnt > 0) {  // WG-uniform: the tcgen05.ld stays warp-collective
+        tmem_ld32(tO + c * 32, ov);
+        tmem_wait_ld();
+      }
+      float f[32];
+#pragma unroll
+      for (int t = 0; t < 32; ++t) f[t] = live ? __uint_as_float(ov[t]) * inv : 0.f;
+      if (row < a.N) {
+        if constexpr (OUT_F32) {
+          float4* dst = reinterpret_cast<float4*>(static_cast<float*>(a.o) + orow + c * 32);
+#pragma unroll
+          for (int t = 0; t < 8; ++t) dst[t] = make_float4(f[4 * t], f[4 * t + 1], f[4 * t + 2], f[4 * t + 3]);
+        } else {
+          uint4* dst = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(a.o) + orow + c * 32);
+#pragma unroll
+          for (int t = 0; t < 4; ++t)
+            dst[t] = make_uint4(pack_bf16(f[8 * t], f[8 * t + 1]), pack_bf16(f[8 * t + 2], f[8 * t + 3]),
+                                pack_bf16(f[8 * t + 4], f[8 * t + 5]), pack_bf16(f[8 * t + 6], f[8 * t + 7]));
+        }
+      }
+    }
+    if (row < a.N)
+      a.lse[(static_cast<size_t>(b) * a.H + h) * a.N + row] =
+          live ? (m_used + __log2f(l)) * 0.6931471805599453f : -INFINITY;
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 9) {
+    tc_fence_after();
+    tmem_dealloc<512>(tbase);
+  }
+}
+
+template <int D, bool CAUSAL, bool OUT_F32>
+static cudaError_t launch_fwd_t(const Dims& d, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
+                                const FwdArgs& a, cudaStream_t st) {
+  auto kern = fm_fwd_kernel<D, CAUSAL, OUT_F32>;
+  const size_t smem = sizeof(fwd::Smem<D>) + 1024;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  dim3 grid((d.Tr + 1) / 2, d.H, d.B);
+  kern<<<grid, fwd::NT, smem, st>>>(tq, tk, tv, a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fwd(const Dims& d, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
+                       const FwdArgs& a, cudaStream_t st) {
+#define FM_F(DD, CC, FF) return launch_fwd_t<DD, CC, FF>(d, tq, tk, tv, a, st)
+  if (d.D == 128) {
+    if (d.causal) { if (d.out_f32) FM_F(128, true, true); else FM_F(128, true, false); }
+    else { if (d.out_f32) FM_F(128, false, true); else FM_F(128, false, false); }
+  } else {
+    if (d.causal) { if (d.out_f32) FM_F(64, true, true); else FM_F(64, true, false); }
+    else { if (d.out_f32) FM_F(64, false, true); else FM_F(64, false, false); }
+  }
+#undef FM_F
+}
+
+}  // namespace fm

@@ -1,0 +1,68 @@
+// fm_internal.h — host/device structures shared by the FlashMask kernels and the C-ABI layer.
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+namespace fm {
+
+constexpr int kTile = 128;      // column (key) tile Bc, forward row (query) tile Br
+constexpr int kMaxTc = 2048;    // forward visit-list capacity -> N <= 262144
+
+// Workspace layout (all offsets 256-byte aligned), produced by flashmask_fwd/bwd.
+struct Workspace {
+  int32_t* ext8;    // [B, Hm, Tc, 8] raw extrema (Alg. 1 line 4)
+  int4* vec4;       // [B, Hm, Tc*128] normalised (LTS, LTE, UTS, UTE) per column, padded columns masked
+  uint8_t* fmap;    // [B, Hm, Tr, Tc] forward kernel map (128 x 128)
+  uint8_t* bmap;    // [B, Hm, Tc, Trb] backward kernel map, transposed (Brb x 128)
+  float* dvec;      // [B, H, Npb] D = rowsum(dO o O)
+  float* l2;        // [B, H, Npb] lse * log2(e) (+inf for empty / padded rows)
+  float* dqacc;     // [B, H, Npb, d] fp32 dQ accumulator
+  size_t bytes;
+};
+
+struct Dims {
+  int B, N, H, D, Hm, C, causal;
+  int Tr, Tc;       // 128-row / 128-column tile counts
+  int Brb, Trb, Npb;  // backward row tile, its count, padded rows
+  float scale;
+  int out_f32;
+  int flags;
+};
+
+struct FwdArgs {
+  int B, N, H, Hm, Tr, Tc;
+  float scale_log2;
+  const uint8_t* fmap;
+  const int4* vec4;
+  void* o;
+  float* lse;
+};
+
+struct BwdArgs {
+  int B, N, H, Hm, Tc, Trb, Npb;
+  float scale_log2;
+  float scale;
+  const uint8_t* bmap;
+  const int4* vec4;
+  const float* dvec;
+  const float* l2;
+  float* dqacc;
+  void* dk;
+  void* dv;
+};
+
+// launchers (return cudaError_t of the launch)
+cudaError_t launch_expand(const int32_t* sri, const Dims& d, int bc, int32_t* ext8, int4* vec4, cudaStream_t st);
+cudaError_t launch_classify(const int32_t* ext8, const Dims& d, int br, int bc, uint8_t* map, int transposed,
+                            int kernel_map, int64_t* counts, cudaStream_t st);
+cudaError_t launch_fwd(const Dims& d, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
+                       const FwdArgs& a, cudaStream_t st);
+cudaError_t launch_bwd_pre(const Dims& d, const void* o, const void* dout, const float* lse, float* dvec, float* l2,
+                           float* dqacc, cudaStream_t st);
+cudaError_t launch_bwd(const Dims& d, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
+                       const CUtensorMap& tdo, const BwdArgs& a, cudaStream_t st);
+cudaError_t launch_dq_convert(const Dims& d, const float* dqacc, void* dq, cudaStream_t st);
+
+}  // namespace fm

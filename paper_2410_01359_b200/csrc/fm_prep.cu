@@ -1,0 +1,275 @@
+// fm_prep.cu — K1 (preprocessing + tile classification), K3 (backward preprocess) and
+// K5 (dQ convert).  All three are integer / HBM-bound passes.
+#include <cuda_bf16.h>
+#include <climits>
+
+#include "fm_internal.h"
+
+namespace fm {
+
+// ---------------------------------------------------------------------------------------
+// K1a: expand startend_row_indices with the C-table defaults (flashmask.h) and reduce the
+// per-column-tile min/max of LTS, LTE, UTS, UTE (Alg. 1 lines 3-4).  Optionally
+// also writes the per-column normalised interval vector used by the attention kernels:
+// (LTS, LTE, UTS, UTE) clamped to [0, N] with empty intervals as [0, 0); padded columns
+// y >= N get the lower interval [0, INT_MAX) so that they are masked for every row.
+// Grid (Tc, B*Hm), 128 threads; one CTA reduces one column tile.
+// ---------------------------------------------------------------------------------------
+__device__ __forceinline__ void expand_col(const int32_t* s, int C, int causal, int N, int& lts, int& lte, int& uts,
+                                           int& ute) {
+  if (causal) {
+    lts = s[0];
+    lte = (C >= 2) ? s[1] : N;
+    uts = 0;
+    ute = 0;
+  } else if (C == 2) {
+    lts = s[0];
+    lte = N;
+    uts = 0;
+    ute = s[1];
+  } else {
+    lts = s[0];
+    lte = s[1];
+    uts = s[2];
+    ute = s[3];
+  }
+}
+
+__device__ __forceinline__ int clampi(int x, int lo, int hi) { return x < lo ? lo : (x > hi ? hi : x); }
+
+__global__ void __launch_bounds__(128) k1_expand(const int32_t* __restrict__ sri, int N, int C, int causal, int bc,
+                                                 int Tc, int32_t* __restrict__ ext8, int4* __restrict__ vec4) {
+  const int j = blockIdx.x;
+  const int bh = blockIdx.y;
+  const int32_t* base = sri + static_cast<size_t>(bh) * N * C;
+  int mn[4] = {INT_MAX, INT_MAX, INT_MAX, INT_MAX};
+  int mx[4] = {INT_MIN, INT_MIN, INT_MIN, INT_MIN};
+  for (int c = threadIdx.x; c < bc; c += blockDim.x) {
+    const long y = static_cast<long>(j) * bc + c;
+    int4 nv;
+    if (y < N) {
+      int v[4];
+      expand_col(base + y * C, C, causal, N, v[0], v[1], v[2], v[3]);
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        mn[t] = min(mn[t], v[t]);
+        mx[t] = max(mx[t], v[t]);
+      }
+      int a = clampi(v[0], 0, N), b = clampi(v[1], 0, N), u = clampi(v[2], 0, N), w = clampi(v[3], 0, N);
+      if (a >= b) a = b = 0;
+      if (u >= w) u = w = 0;
+      nv = make_int4(a, b, u, w);
+    } else {
+      nv = make_int4(0, INT_MAX, 0, 0);
+    }
+    if (vec4) vec4[static_cast<size_t>(bh) * Tc * bc + y] = nv;
+  }
+  // block reduce (128 threads = 4 warps)
+  __shared__ int red[4][8];
+#pragma unroll
+  for (int t = 0; t < 4; ++t) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      mn[t] = min(mn[t], __shfl_xor_sync(0xffffffffu, mn[t], o));
+      mx[t] = max(mx[t], __shfl_xor_sync(0xffffffffu, mx[t], o));
+    }
+  }
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) {
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      red[w][2 * t] = mn[t];
+      red[w][2 * t + 1] = mx[t];
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < 8) {
+    const int t = threadIdx.x;
+    int r = red[0][t];
+    const int nw = blockDim.x >> 5;
+    for (int k = 1; k < nw; ++k) r = (t & 1) ? max(r, red[k][t]) : min(r, red[k][t]);
+    ext8[(static_cast<size_t>(bh) * Tc + j) * 8 + t] = r;
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// K1b: Eq. 4 per tile with Alg. 1's tests, 0-based, real extents,
+// causal region as a third triangle:
+//   SKIP     iff (r0>=LTSmax && r1<=LTEmin) || (r0>=UTSmax && r1<=UTEmin) || (causal && r1-1<c0)
+//   PARTIAL  iff (r1>LTSmin && r0<LTEmax)   || (r1>UTSmin && r0<UTEmax)   || (causal && r0<c1-1)
+//   UNMASKED otherwise.
+// kernel_map = 1 writes the map the attention kernels consume: SKIP -> PARTIAL under
+// FM_FLAG_NO_SKIP, and a non-SKIP ragged last column tile -> PARTIAL (bounds mask).
+// Counts always use the true classes.  Grid (ceil(Tc/128), Tr, B*Hm), 128 threads.
+// ---------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(128) k1_classify(const int32_t* __restrict__ ext8, int N, int causal, int br, int bc,
+                                                   int Tr, int Tc, uint8_t* __restrict__ map, int transposed,
+                                                   int kernel_map, int no_skip,
+                                                   unsigned long long* __restrict__ counts) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  const int i = blockIdx.y;
+  const int bh = blockIdx.z;
+  int cls = -1;
+  if (j < Tc) {
+    const int4* e = reinterpret_cast<const int4*>(ext8 + (static_cast<size_t>(bh) * Tc + j) * 8);
+    const int4 a = e[0], b = e[1];  // (LTSmin, LTSmax, LTEmin, LTEmax), (UTSmin, UTSmax, UTEmin, UTEmax)
+    const long r0 = static_cast<long>(i) * br, r1 = min(static_cast<long>(N), r0 + br);
+    const long c0 = static_cast<long>(j) * bc, c1 = min(static_cast<long>(N), c0 + bc);
+    if ((r0 >= a.y && r1 <= a.z) || (r0 >= b.y && r1 <= b.z) || (causal && r1 - 1 < c0))
+      cls = 0;
+    else if ((r1 > a.x && r0 < a.w) || (r1 > b.x && r0 < b.w) || (causal && r0 < c1 - 1))
+      cls = 1;
+    else
+      cls = 2;
+    int out = cls;
+    if (kernel_map) {
+      if (out == 0 && no_skip) out = 1;
+      if (out == 2 && (N % bc) != 0 && j == Tc - 1) out = 1;
+    }
+    if (map) {
+      const size_t idx = transposed ? (static_cast<size_t>(bh) * Tc + j) * Tr + i
+                                    : (static_cast<size_t>(bh) * Tr + i) * Tc + j;
+      map[idx] = static_cast<uint8_t>(out);
+    }
+  }
+  if (counts) {
+    __shared__ unsigned int cnt[3];
+    if (threadIdx.x < 3) cnt[threadIdx.x] = 0;
+    __syncthreads();
+    const unsigned m0 = __ballot_sync(0xffffffffu, cls == 0);
+    const unsigned m1 = __ballot_sync(0xffffffffu, cls == 1);
+    const unsigned m2 = __ballot_sync(0xffffffffu, cls == 2);
+    if ((threadIdx.x & 31) == 0) {
+      atomicAdd(&cnt[0], __popc(m0));
+      atomicAdd(&cnt[1], __popc(m1));
+      atomicAdd(&cnt[2], __popc(m2));
+    }
+    __syncthreads();
+    if (threadIdx.x < 3 && cnt[threadIdx.x])
+      atomicAdd(&counts[static_cast<size_t>(bh) * 3 + threadIdx.x], static_cast<unsigned long long>(cnt[threadIdx.x]));
+  }
+}
+
+cudaError_t launch_expand(const int32_t* sri, const Dims& d, int bc, int32_t* ext8, int4* vec4, cudaStream_t st) {
+  const int Tc = (d.N + bc - 1) / bc;
+  dim3 grid(Tc, d.B * d.Hm);
+  k1_expand<<<grid, 128, 0, st>>>(sri, d.N, d.C, d.causal, bc, Tc, ext8, vec4);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_classify(const int32_t* ext8, const Dims& d, int br, int bc, uint8_t* map, int transposed,
+                            int kernel_map, int64_t* counts, cudaStream_t st) {
+  const int Tr = (d.N + br - 1) / br, Tc = (d.N + bc - 1) / bc;
+  if (counts) {
+    cudaError_t e = cudaMemsetAsync(counts, 0, sizeof(int64_t) * 3 * d.B * d.Hm, st);
+    if (e != cudaSuccess) return e;
+  }
+  dim3 grid((Tc + 127) / 128, Tr, d.B * d.Hm);
+  k1_classify<<<grid, 128, 0, st>>>(ext8, d.N, d.causal, br, bc, Tr, Tc, map, transposed, kernel_map,
+                                    (d.flags & 1) ? 1 : 0, reinterpret_cast<unsigned long long*>(counts));
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------------------
+// K3: backward preprocess (Alg. 2 line 4, D per row — DESIGN.md R5).  One warp per
+// (b, h, r), r < Npb: D = sum_c dO[r,c] * O[r,c]; l2 = lse * log2(e), or +inf when the row
+// is empty (lse = -inf) or padded (r >= N) so that exp2(S - l2) = 0 exactly; zero dQacc.
+// ---------------------------------------------------------------------------------------
+template <int D, bool OUT_F32>
+__global__ void __launch_bounds__(256) k3_bwd_pre(const void* __restrict__ o, const __nv_bfloat16* __restrict__ dout,
+                                                  const float* __restrict__ lse, int B, int N, int H, int Npb,
+                                                  float* __restrict__ dvec, float* __restrict__ l2,
+                                                  float* __restrict__ dqacc) {
+  const long gw = (static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const long total = static_cast<long>(B) * H * Npb;
+  if (gw >= total) return;
+  const int r = static_cast<int>(gw % Npb);
+  const long bh = gw / Npb;
+  const int h = static_cast<int>(bh % H), b = static_cast<int>(bh / H);
+  constexpr int PER = D / 32;
+  float acc = 0.f;
+  if (r < N) {
+    const size_t off = ((static_cast<size_t>(b) * N + r) * H + h) * D + lane * PER;
+#pragma unroll
+    for (int t = 0; t < PER; ++t) {
+      float ov;
+      if constexpr (OUT_F32)
+        ov = static_cast<const float*>(o)[off + t];
+      else
+        ov = __bfloat162float(static_cast<const __nv_bfloat16*>(o)[off + t]);
+      acc += ov * __bfloat162float(dout[off + t]);
+    }
+#pragma unroll
+    for (int s = 16; s > 0; s >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, s);
+  }
+  if (lane == 0) {
+    const size_t ri = static_cast<size_t>(bh) * Npb + r;
+    dvec[ri] = (r < N) ? acc : 0.f;
+    float lv = (r < N) ? lse[static_cast<size_t>(bh) * N + r] : -INFINITY;
+    l2[ri] = (lv == -INFINITY) ? INFINITY : lv * 1.4426950408889634f;
+  }
+  float* dq = dqacc + (static_cast<size_t>(bh) * Npb + r) * D + lane * PER;
+#pragma unroll
+  for (int t = 0; t < PER; ++t) dq[t] = 0.f;
+}
+
+cudaError_t launch_bwd_pre(const Dims& d, const void* o, const void* dout, const float* lse, float* dvec, float* l2,
+                           float* dqacc, cudaStream_t st) {
+  const long warps = static_cast<long>(d.B) * d.H * d.Npb;
+  const long blocks = (warps * 32 + 255) / 256;
+  const __nv_bfloat16* dob = static_cast<const __nv_bfloat16*>(dout);
+#define FM_PRE(DD, F32) \
+  k3_bwd_pre<DD, F32><<<blocks, 256, 0, st>>>(o, dob, lse, d.B, d.N, d.H, d.Npb, dvec, l2, dqacc)
+  if (d.D == 128) {
+    if (d.out_f32) FM_PRE(128, true); else FM_PRE(128, false);
+  } else {
+    if (d.out_f32) FM_PRE(64, true); else FM_PRE(64, false);
+  }
+#undef FM_PRE
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------------------
+// K5: dQ = scale * dQacc (the scale of Eq. 1 carried into dQ, R4) -> out dtype,
+// [B,H,Npb,D] -> [B,N,H,D].  One thread per 4 elements.
+// ---------------------------------------------------------------------------------------
+template <int D, bool OUT_F32>
+__global__ void __launch_bounds__(256) k5_dq_convert(const float* __restrict__ dqacc, int B, int N, int H, int Npb,
+                                                     float scale, void* __restrict__ dq) {
+  const long idx4 = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const long total4 = static_cast<long>(B) * N * H * D / 4;
+  if (idx4 >= total4) return;
+  const long e = idx4 * 4;
+  const int c = static_cast<int>(e % D);
+  const long row = e / D;  // (b, r, h)
+  const int h = static_cast<int>(row % H);
+  const long br = row / H;
+  const int r = static_cast<int>(br % N), b = static_cast<int>(br / N);
+  const float4 v = *reinterpret_cast<const float4*>(dqacc + ((static_cast<size_t>(b) * H + h) * Npb + r) * D + c);
+  if constexpr (OUT_F32) {
+    reinterpret_cast<float4*>(dq)[idx4] = make_float4(v.x * scale, v.y * scale, v.z * scale, v.w * scale);
+  } else {
+    __nv_bfloat162 lo = __floats2bfloat162_rn(v.x * scale, v.y * scale);
+    __nv_bfloat162 hi = __floats2bfloat162_rn(v.z * scale, v.w * scale);
+    uint2 pk;
+    pk.x = *reinterpret_cast<uint32_t*>(&lo);
+    pk.y = *reinterpret_cast<uint32_t*>(&hi);
+    reinterpret_cast<uint2*>(dq)[idx4] = pk;
+  }
+}
+
+cudaError_t launch_dq_convert(const Dims& d, const float* dqacc, void* dq, cudaStream_t st) {
+  const long total4 = static_cast<long>(d.B) * d.N * d.H * d.D / 4;
+  const long blocks = (total4 + 255) / 256;
+#define FM_CV(DD, F32) k5_dq_convert<DD, F32><<<blocks, 256, 0, st>>>(dqacc, d.B, d.N, d.H, d.Npb, d.scale, dq)
+  if (d.D == 128) {
+    if (d.out_f32) FM_CV(128, true); else FM_CV(128, false);
+  } else {
+    if (d.out_f32) FM_CV(64, true); else FM_CV(64, false);
+  }
+#undef FM_CV
+  return cudaGetLastError();
+}
+
+}  // namespace fm

@@ -1,0 +1,147 @@
+"""Thin ctypes binding over libflashmask.so (include/flashmask.h).
+
+Argument marshalling only: every step of the path runs in the library's CUDA kernels.
+PyTorch provides device memory and the current stream.  There is no CPU or eager
+fallback: if the shared library is missing, importing this module raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+import os
+
+import torch
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libflashmask.so")
+
+FM_OK, FM_ERR_INVALID_ARGUMENT, FM_ERR_UNSUPPORTED, FM_ERR_WORKSPACE_TOO_SMALL, FM_ERR_CUDA = range(5)
+FM_BF16, FM_FP32 = 0, 1
+FM_TILE_SKIP, FM_TILE_PARTIAL, FM_TILE_UNMASKED = 0, 1, 2
+FM_FLAG_NO_SKIP = 1
+FM_PASS_FWD, FM_PASS_BWD = 0, 1
+
+EXPORTED = ["flashmask_workspace_size", "flashmask_classify", "flashmask_fwd", "flashmask_bwd",
+            "flashmask_status_string", "flashmask_last_error"]
+
+
+class FmParams(ctypes.Structure):
+    _fields_ = [("batch", ctypes.c_int64), ("seqlen", ctypes.c_int64), ("num_heads", ctypes.c_int64),
+                ("head_dim", ctypes.c_int64), ("mask_heads", ctypes.c_int64), ("mask_cols", ctypes.c_int64),
+                ("causal", ctypes.c_int32), ("scale", ctypes.c_float), ("in_dtype", ctypes.c_int32),
+                ("out_dtype", ctypes.c_int32), ("flags", ctypes.c_int32)]
+
+
+class FlashMaskError(RuntimeError):
+    def __init__(self, status: int, what: str, detail: str):
+        super().__init__(f"{what}: {detail}")
+        self.status = status
+
+
+def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
+    if not os.path.exists(path):
+        raise ImportError(f"{path} not built; run `python -m paper_2410_01359_b200.build` (no fallback path exists)")
+    lib = ctypes.CDLL(path)
+    P = ctypes.POINTER(FmParams)
+    vp, sz, i32 = ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int32
+    lib.flashmask_workspace_size.argtypes = [P, ctypes.c_int]
+    lib.flashmask_workspace_size.restype = sz
+    lib.flashmask_classify.argtypes = [P, vp, i32, i32, vp, vp, vp, vp]
+    lib.flashmask_classify.restype = ctypes.c_int
+    lib.flashmask_fwd.argtypes = [P, vp, vp, vp, vp, vp, vp, vp, sz, vp]
+    lib.flashmask_fwd.restype = ctypes.c_int
+    lib.flashmask_bwd.argtypes = [P, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp]
+    lib.flashmask_bwd.restype = ctypes.c_int
+    lib.flashmask_status_string.argtypes = [ctypes.c_int]
+    lib.flashmask_status_string.restype = ctypes.c_char_p
+    lib.flashmask_last_error.argtypes = []
+    lib.flashmask_last_error.restype = ctypes.c_char_p
+    return lib
+
+
+_lib = load_library()
+
+
+def _check(status: int, what: str):
+    if status != FM_OK:
+        raise FlashMaskError(status, what, f"{_lib.flashmask_status_string(status).decode()}: "
+                                           f"{_lib.flashmask_last_error().decode()}")
+
+
+def _ptr(t):
+    return ctypes.c_void_p(0 if t is None else t.data_ptr())
+
+
+def _stream(stream):
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+def make_params(B, N, H, d, sri: torch.Tensor, causal: bool, scale=None, out_dtype=torch.bfloat16,
+                flags: int = 0) -> FmParams:
+    assert sri.dim() == 4 and sri.shape[0] == B and sri.shape[2] == N, sri.shape
+    return FmParams(batch=B, seqlen=N, num_heads=H, head_dim=d, mask_heads=sri.shape[1], mask_cols=sri.shape[3],
+                    causal=int(bool(causal)), scale=float(scale) if scale else 0.0, in_dtype=FM_BF16,
+                    out_dtype=FM_FP32 if out_dtype == torch.float32 else FM_BF16, flags=int(flags))
+
+
+def flashmask_workspace_size(params: FmParams, pass_: int) -> int:
+    n = _lib.flashmask_workspace_size(ctypes.byref(params), pass_)
+    if n == 0:
+        _check(FM_ERR_INVALID_ARGUMENT, "flashmask_workspace_size")
+    return int(n)
+
+
+def flashmask_classify(sri: torch.Tensor, causal: bool, br: int = 128, bc: int = 128, num_heads: int | None = None,
+                       class_map: bool = True, stream=None):
+    """Tile classification (K1).  sri: int32 cuda [B, Hm, N, C].  Returns
+    (minmax int32 [B,Hm,Tc,8], class_map uint8 [B,Hm,Tr,Tc] or None, counts int64 [B,Hm,3])."""
+    B, Hm, N, C = sri.shape
+    p = FmParams(batch=B, seqlen=N, num_heads=num_heads or Hm, head_dim=128, mask_heads=Hm, mask_cols=C,
+                 causal=int(bool(causal)), scale=0.0, in_dtype=FM_BF16, out_dtype=FM_BF16, flags=0)
+    Tr, Tc = -(-N // br), -(-N // bc)
+    dev = sri.device
+    minmax = torch.empty(B, Hm, Tc, 8, dtype=torch.int32, device=dev)
+    cmap = torch.empty(B, Hm, Tr, Tc, dtype=torch.uint8, device=dev) if class_map else None
+    counts = torch.empty(B, Hm, 3, dtype=torch.int64, device=dev)
+    _check(_lib.flashmask_classify(ctypes.byref(p), _ptr(sri), br, bc, _ptr(minmax), _ptr(cmap), _ptr(counts),
+                                   _stream(stream)), "flashmask_classify")
+    return minmax, cmap, counts
+
+
+def _workspace(params, pass_, workspace, dev):
+    need = flashmask_workspace_size(params, pass_)
+    if workspace is None or workspace.numel() < need:
+        workspace = torch.empty(max(need, 256), dtype=torch.uint8, device=dev)
+    return workspace, need
+
+
+def flashmask_fwd(q, k, v, sri, causal: bool, scale=None, out_dtype=torch.bfloat16, flags: int = 0,
+                  out=None, lse=None, workspace=None, stream=None):
+    """o, lse = FlashMask forward.  q/k/v: bf16 cuda [B, N, H, d]; sri: int32 [B, Hm, N, C]."""
+    B, N, H, d = q.shape
+    p = make_params(B, N, H, d, sri, causal, scale, out_dtype, flags)
+    o = out if out is not None else torch.empty(B, N, H, d, dtype=out_dtype, device=q.device)
+    lse = lse if lse is not None else torch.empty(B, H, N, dtype=torch.float32, device=q.device)
+    ws, need = _workspace(p, FM_PASS_FWD, workspace, q.device)
+    _check(_lib.flashmask_fwd(ctypes.byref(p), _ptr(q), _ptr(k), _ptr(v), _ptr(sri), _ptr(o), _ptr(lse), _ptr(ws),
+                              ws.numel(), _stream(stream)), "flashmask_fwd")
+    return o, lse
+
+
+def flashmask_bwd(q, k, v, o, do, lse, sri, causal: bool, scale=None, out_dtype=torch.bfloat16, flags: int = 0,
+                  dq=None, dk=None, dv=None, workspace=None, stream=None):
+    """dq, dk, dv = FlashMask backward (o in out_dtype, lse from flashmask_fwd)."""
+    B, N, H, d = q.shape
+    p = make_params(B, N, H, d, sri, causal, scale, out_dtype, flags)
+    mk = lambda t: t if t is not None else torch.empty(B, N, H, d, dtype=out_dtype, device=q.device)
+    dq, dk, dv = mk(dq), mk(dk), mk(dv)
+    ws, need = _workspace(p, FM_PASS_BWD, workspace, q.device)
+    _check(_lib.flashmask_bwd(ctypes.byref(p), _ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(do), _ptr(lse), _ptr(sri),
+                              _ptr(dq), _ptr(dk), _ptr(dv), _ptr(ws), ws.numel(), _stream(stream)), "flashmask_bwd")
+    return dq, dk, dv
+
+
+def default_scale(d: int) -> float:
+    return 1.0 / math.sqrt(d)

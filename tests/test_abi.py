@@ -1,0 +1,83 @@
+"""CPU checks of the C-ABI library: it builds for sm_100a, exports every symbol that
+include/flashmask.h declares, and validates arguments on the host (no GPU needed —
+argument errors return before any CUDA call)."""
+import ctypes
+import os
+import re
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def lib_path():
+    from paper_2410_01359_b200 import build
+    return build.build()
+
+
+def declared_symbols():
+    src = open(os.path.join(ROOT, "include", "flashmask.h")).read()
+    return sorted(set(re.findall(r"FM_API\s+[\w\s\*]+?\b(flashmask_\w+)\s*\(", src)))
+
+
+def test_header_declares_the_north_star_calls():
+    syms = declared_symbols()
+    for s in ("flashmask_fwd", "flashmask_bwd", "flashmask_classify", "flashmask_workspace_size",
+              "flashmask_status_string", "flashmask_last_error"):
+        assert s in syms
+
+
+def test_library_exports_every_declared_symbol(lib_path):
+    out = subprocess.run(["nm", "-D", "--defined-only", lib_path], capture_output=True, text=True).stdout
+    exported = set(re.findall(r"\sT\s(\w+)", out))
+    missing = [s for s in declared_symbols() if s not in exported]
+    assert not missing, missing
+    lib = ctypes.CDLL(lib_path)
+    for s in declared_symbols():
+        assert hasattr(lib, s)
+
+
+def test_sass_contains_tcgen05_and_tma(lib_path):
+    """The kernels are sm_100a tcgen05/TMA code (B200_PROFILING.md SASS mnemonics)."""
+    sass = subprocess.run(["cuobjdump", "-sass", lib_path], capture_output=True, text=True).stdout
+    assert "UTCHMMA" in sass or "UTCMMA" in sass, "no tcgen05.mma in SASS"
+    assert "UTMALDG" in sass, "no TMA tensor loads in SASS"
+    assert "LDTM" in sass and "STTM" in sass, "no tcgen05.ld/st in SASS"
+    assert "HMMA" not in re.sub(r"UTC\w*HMMA", "", sass), "legacy mma.sync path present"
+
+
+def test_host_validation_without_gpu(lib_path):
+    from paper_2410_01359_b200 import flashmask as fm
+    lib = fm._lib
+    p = fm.FmParams(batch=1, seqlen=128, num_heads=1, head_dim=96, mask_heads=1, mask_cols=1, causal=1, scale=0.0,
+                    in_dtype=0, out_dtype=0, flags=0)
+    st = lib.flashmask_fwd(ctypes.byref(p), None, None, None, None, None, None, None, 0, None)
+    assert st == fm.FM_ERR_INVALID_ARGUMENT
+    assert b"head_dim" in lib.flashmask_last_error()
+    p.head_dim = 128
+    p.mask_cols = 4   # causal with C=4 is not in the C-table
+    assert lib.flashmask_fwd(ctypes.byref(p), None, None, None, None, None, None, None, 0, None) == \
+        fm.FM_ERR_INVALID_ARGUMENT
+    p.mask_cols = 1
+    assert lib.flashmask_fwd(ctypes.byref(p), None, None, None, None, None, None, None, 0, None) == \
+        fm.FM_ERR_INVALID_ARGUMENT  # NULL pointers
+    p.in_dtype = 1
+    assert lib.flashmask_fwd(ctypes.byref(p), None, None, None, None, None, None, None, 0, None) == \
+        fm.FM_ERR_UNSUPPORTED
+    p.in_dtype = 0
+    assert lib.flashmask_status_string(fm.FM_ERR_WORKSPACE_TOO_SMALL) == b"FM_ERR_WORKSPACE_TOO_SMALL"
+
+
+def test_workspace_size_is_linear_in_n(lib_path):
+    from paper_2410_01359_b200 import flashmask as fm
+    sizes = {}
+    for N in (8192, 16384):
+        p = fm.FmParams(batch=1, seqlen=N, num_heads=32, head_dim=128, mask_heads=1, mask_cols=1, causal=1,
+                        scale=0.0, in_dtype=0, out_dtype=0, flags=0)
+        sizes[N] = (fm.flashmask_workspace_size(p, fm.FM_PASS_FWD), fm.flashmask_workspace_size(p, fm.FM_PASS_BWD))
+    # forward: O(N) vectors + O(T^2) bytes of class map; backward dominated by the O(N H d) dQ accumulator
+    assert sizes[8192][0] < 2 * 1024 * 1024
+    assert 1.9 < sizes[16384][1] / sizes[8192][1] < 2.1
+    assert sizes[8192][1] >= 8192 * 32 * 128 * 4

@@ -1,0 +1,185 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the fp64 oracle on the same seeded inputs.
+
+Bars (BASELINE.json north_star): tile classification bit-exact; O, dQ, dK, dV (bf16 in,
+fp32 accumulate, fp32 out — DESIGN.md R27) max abs <= 2e-2 and mean abs <= 2e-3; lse abs
+<= 1e-3 with -inf matching exactly.  Exactness: SKIP-as-PARTIAL gives bitwise equal
+O / lse / dK / dV.
+"""
+import numpy as np
+import pytest
+import torch
+
+from oracle import flashmask_oracle as fo
+from workloads import masks as wm
+
+from gpu_util import assert_close, assert_lse, build_case, oracle_head, to_cuda
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def fmlib():
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device (no CPU fallback exists)"
+    from paper_2410_01359_b200 import flashmask
+    return flashmask
+
+
+# ------------------------------------------------------------------------- classification
+CLS_CASES = [(fam, N) for fam in wm.FAMILIES for N in (1, 127, 128, 129, 300, 1000)] + \
+            [(fam, 8192) for fam in wm.FAMILIES if fam != "random_eviction"] + [("random_eviction", 4096)]
+
+
+@pytest.mark.parametrize("fam,N", CLS_CASES)
+def test_classify_bit_exact(fmlib, fam, N):
+    rng = np.random.default_rng(N * 31 + len(fam))
+    masks = [wm.sample_family(fam, N, rng, (1, 5)) for _ in range(2)]
+    m0 = masks[0]
+    sri = torch.from_numpy(wm.stack(masks, 1)).cuda()
+    for br, bc in ((128, 128), (64, 128), (3, 5), (128, 64)):
+        minmax, cmap, counts = fmlib.flashmask_classify(sri, m0.causal, br, bc)
+        torch.cuda.synchronize()
+        for b, m in enumerate(masks):
+            vec = fo.expand(m.sri, m.causal, N)
+            cm_ref, cnt_ref, ext_ref = fo.classify(vec, br, bc)
+            assert np.array_equal(minmax[b, 0].cpu().numpy().astype(np.int64), ext_ref), (br, bc)
+            assert np.array_equal(cmap[b, 0].cpu().numpy(), cm_ref), (br, bc)
+            assert np.array_equal(counts[b, 0].cpu().numpy(), cnt_ref), (br, bc)
+
+
+def test_classify_arbitrary_int32_vectors(fmlib):
+    """R10: any int32 values (inverted / out-of-range intervals) classify like the oracle."""
+    rng = np.random.default_rng(0)
+    for causal, C in ((True, 1), (True, 2), (False, 2), (False, 4)):
+        N = 777
+        raw = rng.integers(-1000, N + 1000, size=(1, 1, N, C)).astype(np.int32)
+        raw[0, 0, :5] = np.iinfo(np.int32).max
+        raw[0, 0, 5:9] = np.iinfo(np.int32).min
+        _, cmap, counts = fmlib.flashmask_classify(torch.from_numpy(raw).cuda(), causal, 128, 128)
+        vec = fo.expand(raw[0, 0], causal, N)
+        cm_ref, cnt_ref, _ = fo.classify(vec, 128, 128)
+        assert np.array_equal(cmap[0, 0].cpu().numpy(), cm_ref)
+        assert np.array_equal(counts[0, 0].cpu().numpy(), cnt_ref)
+
+
+# ------------------------------------------------------------------------- forward / backward
+ATTN_CASES = [
+    # (family, N, d, B, H)
+    ("causal_document", 128, 64, 1, 1),       # config C1 shape (R26: bf16 inputs)
+    ("causal", 256, 128, 1, 2),
+    ("full", 384, 128, 2, 1),
+    ("causal_document", 1000, 128, 2, 2),
+    ("document", 640, 128, 1, 2),
+    ("share_question", 896, 128, 1, 2),
+    ("sliding_window", 1024, 128, 1, 1),
+    ("global_sliding_window", 768, 128, 1, 2),
+    ("causal_blockwise", 700, 128, 1, 1),
+    ("prefix_lm_document", 512, 128, 1, 1),
+    ("prefix_lm_causal", 640, 128, 1, 1),
+    ("qk_sparse", 513, 128, 1, 1),
+    ("hash_sparse", 600, 128, 1, 1),
+    ("random_eviction", 512, 128, 1, 1),
+    ("causal_document", 1000, 64, 2, 2),
+    ("document", 257, 64, 1, 2),
+    ("global_sliding_window", 700, 64, 1, 1),
+    ("random_eviction", 384, 64, 1, 1),
+    ("causal", 129, 128, 1, 1),
+    ("full", 1, 128, 1, 1),
+    ("full", 127, 64, 1, 1),
+]
+
+
+def _run(fmlib, fam, N, d, B, H, seed=0, flags=0, out_dtype=torch.float32):
+    rng = np.random.default_rng(seed + N + d)
+    masks = [wm.sample_family(fam, N, rng, (2, 5)) for _ in range(B)]
+    sri, t = build_case(masks, H, d, base=seed)
+    sri_c, tc = to_cuda(sri, t)
+    causal = masks[0].causal
+    o, lse = fmlib.flashmask_fwd(tc["q"], tc["k"], tc["v"], sri_c, causal, out_dtype=out_dtype, flags=flags)
+    dq, dk, dv = fmlib.flashmask_bwd(tc["q"], tc["k"], tc["v"], o, tc["do"], lse, sri_c, causal,
+                                     out_dtype=out_dtype, flags=flags)
+    torch.cuda.synchronize()
+    return masks, sri, t, (o, lse, dq, dk, dv)
+
+
+@pytest.mark.parametrize("fam,N,d,B,H", ATTN_CASES)
+def test_fwd_bwd_parity(fmlib, fam, N, d, B, H):
+    masks, sri, t, (o, lse, dq, dk, dv) = _run(fmlib, fam, N, d, B, H)
+    sri_np = sri.numpy()
+    for b in range(B):
+        for h in range(H):
+            O, L, (gq, gk, gv) = oracle_head(t, masks, sri_np, b, h, 1, masks[0].causal)
+            assert_close(f"O[{b},{h}]", o[b, :, h].cpu().numpy(), O)
+            assert_lse(lse[b, h].cpu().numpy(), L)
+            assert_close(f"dQ[{b},{h}]", dq[b, :, h].cpu().numpy(), gq)
+            assert_close(f"dK[{b},{h}]", dk[b, :, h].cpu().numpy(), gk)
+            assert_close(f"dV[{b},{h}]", dv[b, :, h].cpu().numpy(), gv)
+
+
+@pytest.mark.parametrize("fam,N,d", [("causal_document", 1000, 128), ("global_sliding_window", 768, 128),
+                                     ("document", 640, 64), ("random_eviction", 512, 128)])
+def test_skip_equivalence_bitwise(fmlib, fam, N, d):
+    """§4.4: skipping fully masked tiles changes nothing, bit for bit."""
+    _, _, _, r0 = _run(fmlib, fam, N, d, 1, 2, seed=3)
+    _, _, _, r1 = _run(fmlib, fam, N, d, 1, 2, seed=3, flags=fmlib.FM_FLAG_NO_SKIP)
+    for name, a, b in zip(("O", "lse", "dK", "dV"), (r0[0], r0[1], r0[3], r0[4]), (r1[0], r1[1], r1[3], r1[4])):
+        assert torch.equal(a, b), name
+
+
+def test_bf16_outputs_close(fmlib):
+    """bf16 outputs (the timing configuration) agree with fp32 outputs to bf16 rounding."""
+    _, _, _, r32 = _run(fmlib, "causal_document", 1000, 128, 1, 2, seed=5)
+    _, _, _, r16 = _run(fmlib, "causal_document", 1000, 128, 1, 2, seed=5, out_dtype=torch.bfloat16)
+    for a, b in zip(r32, r16):
+        if a.dtype == torch.float32 and b.dtype == torch.bfloat16:
+            err = (a - b.float()).abs().max().item()
+            assert err <= 0.02 * max(1.0, a.abs().max().item()), err
+    assert torch.equal(r32[1], r16[1])
+
+
+def test_empty_rows(fmlib):
+    """Rows masked in every column: O = 0, lse = -inf, zero dQ; padding keys get zero dK/dV."""
+    m = wm.empty_rows_padding([100, 150], 50)
+    sri, t = build_case([m], 2, 128)
+    sri_c, tc = to_cuda(sri, t)
+    o, lse = fmlib.flashmask_fwd(tc["q"], tc["k"], tc["v"], sri_c, True, out_dtype=torch.float32)
+    dq, dk, dv = fmlib.flashmask_bwd(tc["q"], tc["k"], tc["v"], o, tc["do"], lse, sri_c, True, out_dtype=torch.float32)
+    torch.cuda.synchronize()
+    assert torch.isneginf(lse[:, :, 250:]).all() and (o[:, 250:] == 0).all() and (dq[:, 250:] == 0).all()
+    for h in range(2):
+        O, L, (gq, gk, gv) = oracle_head(t, [m], sri.numpy(), 0, h, 1, True)
+        assert_close("O", o[0, :, h].cpu().numpy(), O)
+        assert_lse(lse[0, h].cpu().numpy(), L)
+        assert_close("dK", dk[0, :, h].cpu().numpy(), gk)
+        assert_close("dV", dv[0, :, h].cpu().numpy(), gv)
+
+
+def test_masked_key_null_influence(fmlib):
+    """perturbing K/V of keys masked for every row leaves every output bitwise unchanged."""
+    m = wm.qk_sparse(512, [3, 200, 201, 450], (300, 310))
+    sri, t = build_case([m], 2, 128)
+    sri_c, tc = to_cuda(sri, t)
+    run = lambda tt: (lambda o, l: (o, l, *fmlib.flashmask_bwd(tt["q"], tt["k"], tt["v"], o, tt["do"], l, sri_c, True)))(
+        *fmlib.flashmask_fwd(tt["q"], tt["k"], tt["v"], sri_c, True))
+    r0 = run(tc)
+    tc2 = {k: v.clone() for k, v in tc.items()}
+    tc2["k"][:, [3, 200, 201, 450]] += 1.5
+    tc2["v"][:, [3, 200, 201, 450]] -= 2.0
+    r1 = run(tc2)
+    torch.cuda.synchronize()
+    for a, b in zip(r0[:3], r1[:3]):
+        assert torch.equal(a, b)
+    keep = [i for i in range(512) if i not in (3, 200, 201, 450)]
+    assert torch.equal(r0[3][:, keep], r1[3][:, keep]) and torch.equal(r0[4][:, keep], r1[4][:, keep])
+
+
+def test_abi_errors(fmlib):
+    q = torch.zeros(1, 128, 1, 96, dtype=torch.bfloat16, device="cuda")
+    sri = torch.zeros(1, 1, 128, 1, dtype=torch.int32, device="cuda")
+    with pytest.raises(fmlib.FlashMaskError) as e:
+        fmlib.flashmask_fwd(q, q, q, sri, True)
+    assert e.value.status == fmlib.FM_ERR_INVALID_ARGUMENT
+    q = torch.zeros(1, 128, 1, 128, dtype=torch.bfloat16, device="cuda")
+    sri4 = torch.zeros(1, 1, 128, 4, dtype=torch.int32, device="cuda")
+    with pytest.raises(fmlib.FlashMaskError) as e:
+        fmlib.flashmask_fwd(q, q, q, sri4, True)   # causal with C=4 is not in the C-table
+    assert e.value.status == fmlib.FM_ERR_INVALID_ARGUMENT

@@ -215,7 +215,8 @@ def sample_doc_lens(N: int, n_docs: int, rng: np.random.Generator, min_len: int 
     """Document lengths summing to N (App. A.5.2 P:588 'sampled the length of each document
     such that the total length equaled').  Normalised-uniform weights with a minimum length;
     the last document takes the remainder (reading R21)."""
-    n_docs = max(1, min(n_docs, N // max(min_len, 1)))
+    n_docs = max(1, min(n_docs, N // max(min_len, 1), N))
+    min_len = max(1, min(min_len, N // n_docs))
     w = rng.uniform(0.0, 1.0, n_docs) + 1e-9
     spare = N - n_docs * min_len
     lens = np.floor(w / w.sum() * spare).astype(np.int64) + min_len
