@@ -131,6 +131,26 @@ FM_API fm_status flashmask_bwd(const fm_params* p, const void* q, const void* k,
                         const void* dout, const float* lse, const int32_t* startend_row_indices,
                         void* dq, void* dk, void* dv, void* workspace, size_t workspace_bytes, void* stream);
 
+/* Kernel ids of the optional per-launch timing below. */
+enum {
+  FM_KERNEL_EXPAND = 0,      /* K1a  preprocessing: expand + per-tile min/max (Alg. 1 l.3-4) */
+  FM_KERNEL_CLASSIFY = 1,    /* K1b  tile classification (Eq. 4)                             */
+  FM_KERNEL_FWD = 2,         /* K2   forward (Alg. 1)                                        */
+  FM_KERNEL_BWD_PRE = 3,     /* K3   D = rowsum(dO o O), zero dQ accumulator (Alg. 2 l.3-4)  */
+  FM_KERNEL_BWD = 4,         /* K4   backward main loop (Alg. 2)                             */
+  FM_KERNEL_DQ_CONVERT = 5,  /* K5   dQ = scale * dQacc -> out dtype                         */
+  FM_NUM_KERNELS = 6
+};
+
+/* Optional per-kernel timing for roofline reporting (off by default).  While enabled,
+ * every kernel this thread launches through the calls above is bracketed by two CUDA
+ * events recorded on the caller's stream (no extra synchronisation, same stream order).
+ * flashmask_timing_collect() waits for the recorded events, ADDS the elapsed
+ * milliseconds and the launch counts per kernel id into ms[FM_NUM_KERNELS] and
+ * launches[FM_NUM_KERNELS] (caller-owned host arrays), and clears the record. */
+FM_API fm_status flashmask_timing_enable(int enable);
+FM_API fm_status flashmask_timing_collect(double* ms, int64_t* launches);
+
 /* Static description of a status code. */
 FM_API const char* flashmask_status_string(fm_status s);
 

@@ -195,6 +195,26 @@ def backward(q, k, v, do, vec: Vectors, scale=None, row_block: int = 1024):
     return dq, dk, dv
 
 
+def backward_rows(q, k, v, do, vec: Vectors, rows, scale=None):
+    """One row block of ``backward`` (the same statements, for a given set of query rows):
+    returns (dQ[rows], dK contribution, dV contribution).  Summing the contributions over
+    a partition of the rows gives ``backward``'s dK, dV.  Used to time the oracle on a
+    bounded sample (bench.py cpu_baseline)."""
+    q = np.asarray(q, dtype=np.float64)
+    k = np.asarray(k, dtype=np.float64)
+    v_ = np.asarray(v, dtype=np.float64)
+    do = np.asarray(do, dtype=np.float64)
+    d = q.shape[1]
+    scale = 1.0 / math.sqrt(d) if scale is None or scale <= 0 else float(scale)
+    rr = np.asarray(rows, dtype=np.int64)
+    P = probabilities(q, k, vec, scale, rr)
+    O = P @ v_
+    D = (do[rr] * O).sum(axis=1)
+    dv = P.T @ do[rr]
+    dS = P * (do[rr] @ v_.T - D[:, None])
+    return scale * (dS @ k), scale * (dS.T @ q[rr]), dv
+
+
 # ------------------------------------------------------------------ classification
 def extrema(vec: Vectors, Bc: int) -> np.ndarray:
     """Alg. 1 lines 3-4: per column tile j the min and max of each vector over

@@ -10,6 +10,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <vector>
 
 #include "../../include/flashmask.h"
 #include "fm_internal.h"
@@ -134,6 +135,40 @@ fm_status cuda_fail(cudaError_t e, const char* where) {
   return fail(FM_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
 }
 
+// ---- optional per-launch timing (flashmask_timing_enable / _collect) ----
+struct TimingRec {
+  int kid;
+  cudaEvent_t a, b;
+};
+struct Timing {
+  bool on = false;
+  std::vector<TimingRec> recs;
+  std::vector<cudaEvent_t> pool;
+  cudaEvent_t get() {
+    if (!pool.empty()) {
+      cudaEvent_t e = pool.back();
+      pool.pop_back();
+      return e;
+    }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+  }
+};
+thread_local Timing g_timing;
+
+// Launch `fn` (returns cudaError_t) bracketed by events when timing is on.
+template <class F>
+cudaError_t timed(int kid, cudaStream_t st, F&& fn) {
+  if (!g_timing.on) return fn();
+  TimingRec r{kid, g_timing.get(), g_timing.get()};
+  cudaEventRecord(r.a, st);
+  cudaError_t e = fn();
+  cudaEventRecord(r.b, st);
+  g_timing.recs.push_back(r);
+  return e;
+}
+
 }  // namespace
 
 extern "C" {
@@ -172,12 +207,12 @@ fm_status flashmask_classify(const fm_params* p, const int32_t* sri, int32_t br,
   if (br < 1 || bc < 1) return fail(FM_ERR_INVALID_ARGUMENT, "br and bc must be >= 1");
   if (!aligned16(minmax)) return fail(FM_ERR_INVALID_ARGUMENT, "minmax must be 16-byte aligned");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  cudaError_t e = fm::launch_expand(sri, d, bc, minmax, nullptr, st);
+  cudaError_t e = timed(FM_KERNEL_EXPAND, st, [&] { return fm::launch_expand(sri, d, bc, minmax, nullptr, st); });
   if (e != cudaSuccess) return cuda_fail(e, "expand");
   if (class_map || counts) {
     fm::Dims d0 = d;
     d0.flags = 0;
-    e = fm::launch_classify(minmax, d0, br, bc, class_map, 0, 0, counts, st);
+    e = timed(FM_KERNEL_CLASSIFY, st, [&] { return fm::launch_classify(minmax, d0, br, bc, class_map, 0, 0, counts, st); });
     if (e != cudaSuccess) return cuda_fail(e, "classify");
   }
   return FM_OK;
@@ -201,9 +236,9 @@ fm_status flashmask_fwd(const fm_params* p, const void* q, const void* k, const 
   if (!make_map(&tq, q, d, 128, &err) || !make_map(&tk, k, d, 128, &err) || !make_map(&tv, v, d, 128, &err))
     return fail(FM_ERR_CUDA, err);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  cudaError_t e = fm::launch_expand(sri, d, fm::kTile, w.ext8, w.vec4, st);
+  cudaError_t e = timed(FM_KERNEL_EXPAND, st, [&] { return fm::launch_expand(sri, d, fm::kTile, w.ext8, w.vec4, st); });
   if (e != cudaSuccess) return cuda_fail(e, "expand");
-  e = fm::launch_classify(w.ext8, d, fm::kTile, fm::kTile, w.fmap, 0, 1, nullptr, st);
+  e = timed(FM_KERNEL_CLASSIFY, st, [&] { return fm::launch_classify(w.ext8, d, fm::kTile, fm::kTile, w.fmap, 0, 1, nullptr, st); });
   if (e != cudaSuccess) return cuda_fail(e, "classify");
   fm::FwdArgs a{};
   a.B = d.B; a.N = d.N; a.H = d.H; a.Hm = d.Hm; a.Tr = d.Tr; a.Tc = d.Tc;
@@ -212,7 +247,7 @@ fm_status flashmask_fwd(const fm_params* p, const void* q, const void* k, const 
   a.vec4 = w.vec4;
   a.o = o;
   a.lse = lse;
-  e = fm::launch_fwd(d, tq, tk, tv, a, st);
+  e = timed(FM_KERNEL_FWD, st, [&] { return fm::launch_fwd(d, tq, tk, tv, a, st); });
   if (e != cudaSuccess) return cuda_fail(e, "forward kernel");
   return FM_OK;
 }
@@ -240,11 +275,11 @@ fm_status flashmask_bwd(const fm_params* p, const void* q, const void* k, const 
       !make_map(&tdo, dout, d, d.Brb, &err))
     return fail(FM_ERR_CUDA, err);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  cudaError_t e = fm::launch_expand(sri, d, fm::kTile, w.ext8, w.vec4, st);
+  cudaError_t e = timed(FM_KERNEL_EXPAND, st, [&] { return fm::launch_expand(sri, d, fm::kTile, w.ext8, w.vec4, st); });
   if (e != cudaSuccess) return cuda_fail(e, "expand");
-  e = fm::launch_classify(w.ext8, d, d.Brb, fm::kTile, w.bmap, 1, 1, nullptr, st);
+  e = timed(FM_KERNEL_CLASSIFY, st, [&] { return fm::launch_classify(w.ext8, d, d.Brb, fm::kTile, w.bmap, 1, 1, nullptr, st); });
   if (e != cudaSuccess) return cuda_fail(e, "classify");
-  e = fm::launch_bwd_pre(d, o, dout, lse, w.dvec, w.l2, w.dqacc, st);
+  e = timed(FM_KERNEL_BWD_PRE, st, [&] { return fm::launch_bwd_pre(d, o, dout, lse, w.dvec, w.l2, w.dqacc, st); });
   if (e != cudaSuccess) return cuda_fail(e, "bwd preprocess");
   fm::BwdArgs a{};
   a.B = d.B; a.N = d.N; a.H = d.H; a.Hm = d.Hm; a.Tc = d.Tc; a.Trb = d.Trb; a.Npb = d.Npb;
@@ -257,11 +292,36 @@ fm_status flashmask_bwd(const fm_params* p, const void* q, const void* k, const 
   a.dqacc = w.dqacc;
   a.dk = dk;
   a.dv = dv;
-  e = fm::launch_bwd(d, tq, tk, tv, tdo, a, st);
+  e = timed(FM_KERNEL_BWD, st, [&] { return fm::launch_bwd(d, tq, tk, tv, tdo, a, st); });
   if (e != cudaSuccess) return cuda_fail(e, "backward kernel");
-  e = fm::launch_dq_convert(d, w.dqacc, dq, st);
+  e = timed(FM_KERNEL_DQ_CONVERT, st, [&] { return fm::launch_dq_convert(d, w.dqacc, dq, st); });
   if (e != cudaSuccess) return cuda_fail(e, "dq convert");
   return FM_OK;
+}
+
+fm_status flashmask_timing_enable(int enable) {
+  g_timing.on = enable != 0;
+  return FM_OK;
+}
+
+fm_status flashmask_timing_collect(double* ms, int64_t* launches) {
+  g_last_error.clear();
+  if (!ms || !launches) return fail(FM_ERR_INVALID_ARGUMENT, "ms and launches are required");
+  fm_status s = FM_OK;
+  for (TimingRec& r : g_timing.recs) {
+    float t = 0.f;
+    cudaError_t e = cudaEventSynchronize(r.b);
+    if (e == cudaSuccess) e = cudaEventElapsedTime(&t, r.a, r.b);
+    if (e != cudaSuccess && s == FM_OK) s = cuda_fail(e, "timing");
+    if (r.kid >= 0 && r.kid < FM_NUM_KERNELS) {
+      ms[r.kid] += t;
+      launches[r.kid] += 1;
+    }
+    g_timing.pool.push_back(r.a);
+    g_timing.pool.push_back(r.b);
+  }
+  g_timing.recs.clear();
+  return s;
 }
 
 }  // extern "C"

@@ -22,7 +22,8 @@ FM_FLAG_NO_SKIP = 1
 FM_PASS_FWD, FM_PASS_BWD = 0, 1
 
 EXPORTED = ["flashmask_workspace_size", "flashmask_classify", "flashmask_fwd", "flashmask_bwd",
-            "flashmask_status_string", "flashmask_last_error"]
+            "flashmask_status_string", "flashmask_last_error", "flashmask_timing_enable", "flashmask_timing_collect"]
+KERNEL_NAMES = ["expand", "classify", "fwd", "bwd_pre", "bwd", "dq_convert"]
 
 
 class FmParams(ctypes.Structure):
@@ -56,6 +57,10 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.flashmask_status_string.restype = ctypes.c_char_p
     lib.flashmask_last_error.argtypes = []
     lib.flashmask_last_error.restype = ctypes.c_char_p
+    lib.flashmask_timing_enable.argtypes = [ctypes.c_int]
+    lib.flashmask_timing_enable.restype = ctypes.c_int
+    lib.flashmask_timing_collect.argtypes = [ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int64)]
+    lib.flashmask_timing_collect.restype = ctypes.c_int
     return lib
 
 
@@ -141,6 +146,19 @@ def flashmask_bwd(q, k, v, o, do, lse, sri, causal: bool, scale=None, out_dtype=
     _check(_lib.flashmask_bwd(ctypes.byref(p), _ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(do), _ptr(lse), _ptr(sri),
                               _ptr(dq), _ptr(dk), _ptr(dv), _ptr(ws), ws.numel(), _stream(stream)), "flashmask_bwd")
     return dq, dk, dv
+
+
+def flashmask_timing_enable(enable: bool = True):
+    _check(_lib.flashmask_timing_enable(int(bool(enable))), "flashmask_timing_enable")
+
+
+def flashmask_timing_collect():
+    """{kernel name: (total ms, launches)} of the launches recorded since the last collect."""
+    n = len(KERNEL_NAMES)
+    ms = (ctypes.c_double * n)()
+    cnt = (ctypes.c_int64 * n)()
+    _check(_lib.flashmask_timing_collect(ms, cnt), "flashmask_timing_collect")
+    return {KERNEL_NAMES[i]: (ms[i], cnt[i]) for i in range(n)}
 
 
 def default_scale(d: int) -> float:

@@ -205,3 +205,18 @@ def test_row_subset_matches_full():
     rows = np.array([0, 7, 199, 100])
     Os, Ls = fo.forward(q, k, v_, vv, rows=rows)
     assert np.array_equal(Os, O[rows]) and np.array_equal(Ls, L[rows])
+
+
+def test_backward_rows_partition_sums_to_backward():
+    rng = np.random.default_rng(21)
+    m = wm.sample_family("document", 90, rng)
+    vv = vec(m)
+    q, k, v_, do = (rnd(rng, 90, 5) for _ in range(4))
+    dq, dk, dv = fo.backward(q, k, v_, do, vv)
+    acc_k, acc_v = np.zeros_like(dk), np.zeros_like(dv)
+    for s in (range(0, 40), range(40, 90)):
+        gq, gk, gv = fo.backward_rows(q, k, v_, do, vv, np.array(list(s)))
+        assert np.abs(gq - dq[list(s)]).max() < 1e-13
+        acc_k += gk
+        acc_v += gv
+    assert np.abs(acc_k - dk).max() < 1e-12 and np.abs(acc_v - dv).max() < 1e-12
