@@ -4,21 +4,24 @@
 // keeps dK_j and dV_j as fp32 accumulators in TMEM for the whole row loop and writes them
 // once at the end (atomic-free).  The four mask values of its 128 keys are loaded once into
 // registers — thread = key = TMEM lane in the transposed S^T layout (Alg. 2 lines 10-11,
-// P:394-395 "loaded once per column tile").  Row tiles that are SKIP for this column tile
-// are never loaded (Alg. 2 lines 13-18).
+// P:394-395).  Row tiles that are SKIP for this column tile are never loaded (Alg. 2 lines
+// 13-18).
 //
-// Row tile Br = 64 for d = 128, 128 for d = 64.  Per visited row tile i:
-//   S^T  = K_j Q_i^T          (tcgen05, M=128 keys, N=Br, K=d)
-//   dP^T = V_j dO_i^T         (tcgen05)
-//   P^T  = exp2(S^T*scale*log2e - L2_i), masked on PARTIAL tiles
-//   dS^T = P^T o (dP^T - D_i)                                             P:430
-//   dV  += P^T dO_i           (A = P^T from TMEM)
-//   dK  += dS^T Q_i           (A = dS^T from TMEM)
-//   d=128: dQ_i^T = K_j^T dS^T (M = d); d=64: dQ_i = dS K_j (M = queries)
-// and the dQ tile is added into the fp32 workspace with one bulk reduce-add
-// (cp.reduce.async.bulk .add.f32) instead of a read-modify-write.
-// Warp roles: 0-3 compute WG (keys), 4-7 dQ WG (TMEM -> smem -> bulk reduce),
-// 8 TMA producer, 9 TMEM allocator + MMA issuer.
+// Row tile Br = 64 (d = 128) or 128 (d = 64).  Per visited row tile i:
+//   S^T  = K_j Q_i^T,  dP^T = V_j dO_i^T      (tcgen05, M = 128 keys)
+//   P^T  = exp2(S^T*scale*log2e - L2_i), interval mask on PARTIAL tiles only
+//   dS^T = P^T o (dP^T - D_i)                                                  P:430
+//   dV  += P^T dO_i,  dK += dS^T Q_i         (A operands bf16 from TMEM)
+//   d=128: dQ_i^T = K_j^T dS^T (M = d);  d=64: dQ_i = dS K_j (M = queries)
+// dQ tiles are added into the fp32 workspace by TMA tensor reduce-add (no read-modify-write).
+//
+// Pipelining: the compute WGs copy S^T/dP^T of row tile t into registers and release them at
+// once, so the MMA warp issues S^T/dP^T of tile t+1 while P/dS of tile t are being computed;
+// P and dS live in their own TMEM columns.  TMEM columns:
+//   d=128: S [0,64) dP [64,128) P [128,160) dS [160,192) dQ^T [192,256) dV [256,384) dK [384,512)
+//   d=64 : S [0,128) dP [128,256) P [256,320) dS [320,384) dQ = P cols (aliased) dV [384,448) dK [448,512)
+// Warp roles: 0-7 two compute WGs (query halves), 8-11 dQ WG (TMEM -> smem -> reduce),
+// 12 TMA producer, 13 TMEM allocator + MMA issuer.
 #include <cuda_bf16.h>
 #include <cmath>
 
@@ -29,7 +32,7 @@ namespace fm {
 
 namespace bwd {
 
-constexpr int NT = 320;
+constexpr int NT = 448;
 constexpr int QST = 2;
 constexpr int kMaxTrb = 4096;
 
@@ -37,12 +40,15 @@ template <int D>
 struct Cfg {
   static constexpr int BR = (D == 128) ? 64 : 128;
   static constexpr bool DQT = (D == 128);          // dQ computed transposed (M = d)
+  static constexpr bool DQ_ALIAS = (D == 64);      // dQ accumulator aliases the P columns
   static constexpr int KV_TILE = 128 * D * 2;      // bytes
   static constexpr int Q_TILE = BR * D * 2;
   static constexpr int DS_BYTES = 128 * BR * 2;
   static constexpr int STG_BYTES = BR * D * 4;
-  static constexpr int S_COL = 0, DP_COL = BR, DQ_COL = 2 * BR;
-  static constexpr int DV_COL = (D == 128) ? 256 : 320;
+  static constexpr int CH_PER_WG = BR / 64;        // 32-query chunks per compute WG
+  static constexpr int S_COL = 0, DP_COL = BR, P_COL = 2 * BR, DS_COL = 2 * BR + BR / 2;
+  static constexpr int DQ_COL = DQ_ALIAS ? P_COL : 192;
+  static constexpr int DV_COL = (D == 128) ? 256 : 384;
   static constexpr int DK_COL = DV_COL + D;
 };
 
@@ -54,13 +60,14 @@ struct Smem {
   uint8_t q[QST][C::Q_TILE];
   uint8_t dO[QST][C::Q_TILE];
   uint8_t ds[C::DS_BYTES];
-  float stg[C::BR * D];
+  uint8_t stg[2][C::STG_BYTES];
   float lvec[QST][C::BR];
   float dvec[QST][C::BR];
-  uint32_t list[kMaxTrb];
+  uint16_t list[kMaxTrb];
+  uint32_t part_bits[kMaxTrb / 32];
   uint64_t kv_full;
   uint64_t q_full[QST], q_empty[QST];
-  uint64_t s_full, p_full, dq_full, dq_empty, ds_empty, done;
+  uint64_t s_full, sdp_free, p_full, pds_free, dq_full, dq_empty, ds_empty, done;
   uint32_t tmem_base;
   int n_entries;
   int warp_cnt[NT / 32];
@@ -72,7 +79,7 @@ template <int D, bool CAUSAL, bool OUT_F32>
 __global__ void __launch_bounds__(bwd::NT, 1)
     fm_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                   const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO,
-                  const BwdArgs a) {
+                  const __grid_constant__ CUtensorMap tmdQ, const BwdArgs a) {
   using namespace bwd;
   using C = Cfg<D>;
   using S = Smem<D>;
@@ -87,18 +94,20 @@ __global__ void __launch_bounds__(bwd::NT, 1)
   const size_t bhm = static_cast<size_t>(b) * a.Hm + hm;
   const size_t bh = static_cast<size_t>(b) * a.H + h;
 
-  if (warp == 8 && lane == 0) {
+  if (warp == 12 && lane == 0) {
     mbar_init(&sm.kv_full, 1);
     for (int s = 0; s < QST; ++s) { mbar_init(&sm.q_full[s], 1); mbar_init(&sm.q_empty[s], 1); }
     mbar_init(&sm.s_full, 1);
-    mbar_init(&sm.p_full, 128);
+    mbar_init(&sm.sdp_free, 256);
+    mbar_init(&sm.p_full, 256);
+    mbar_init(&sm.pds_free, 1);
     mbar_init(&sm.dq_full, 1);
     mbar_init(&sm.dq_empty, 128);
     mbar_init(&sm.ds_empty, 1);
     mbar_init(&sm.done, 1);
     fence_barrier_init();
   }
-  if (warp == 9) tmem_alloc<512>(&sm.tmem_base);
+  if (warp == 13) tmem_alloc<512>(&sm.tmem_base);
 
   // ---- visit list: row tiles i that are not SKIP for column tile j (K1 transposed map) ----
   {
@@ -118,7 +127,11 @@ __global__ void __launch_bounds__(bwd::NT, 1)
         tot += cw;
       }
       off += __popc(bal & ((1u << lane) - 1u));
-      if (vis) sm.list[off] = static_cast<uint32_t>(i) | (c << 24);
+      if (vis) {
+        sm.list[off] = static_cast<uint16_t>(i);
+        if (c == 1u) atomicOr(&sm.part_bits[off >> 5], 1u << (off & 31));
+        else atomicAnd(&sm.part_bits[off >> 5], ~(1u << (off & 31)));
+      }
       base += tot;
       __syncthreads();
     }
@@ -130,7 +143,7 @@ __global__ void __launch_bounds__(bwd::NT, 1)
   const int nE = sm.n_entries;
   const uint32_t tbase = sm.tmem_base;
 
-  if (warp == 8) {
+  if (warp == 12) {
     // ================================ TMA producer ================================
     if (lane == 0 && nE > 0) {
       tma_prefetch_desc(&tmQ);
@@ -144,7 +157,7 @@ __global__ void __launch_bounds__(bwd::NT, 1)
         tma_load_4d(sm.v + c * 16384, &tmV, &sm.kv_full, c * 64, h, j * 128, b);
       }
       for (int t = 0; t < nE; ++t) {
-        const int i = static_cast<int>(sm.list[t] & 0xFFFFFFu);
+        const int i = sm.list[t];
         const int st = t % QST;
         mbar_wait(&sm.q_empty[st], ((t / QST) & 1) ^ 1);
         mbar_expect_tx(&sm.q_full[st], 2 * C::Q_TILE + 2 * BR * 4);
@@ -157,47 +170,50 @@ __global__ void __launch_bounds__(bwd::NT, 1)
         bulk_g2s(sm.dvec[st], a.dvec + bh * a.Npb + static_cast<size_t>(i) * BR, BR * 4, &sm.q_full[st]);
       }
     }
-  } else if (warp == 9) {
+  } else if (warp == 13) {
     // ================================ MMA issuer ================================
     if (lane == 0 && nE > 0) {
       constexpr uint32_t ID_S = idesc_bf16(128, BR, 0, 0);   // S^T, dP^T: A, B K-major
       constexpr uint32_t ID_G = idesc_bf16(128, D, 0, 1);    // dV, dK: A in TMEM, B MN-major
-      constexpr uint32_t ID_Q = idesc_bf16(128, 64, 1, 1);   // dQ^T (d=128) / dQ (d=64)
+      constexpr uint32_t ID_Q = idesc_bf16(128, 64, 1, 1);   // dQ^T (d=128) / dQ (d=64), both MN-major
       const uint32_t k_addr = smem_u32(sm.k), v_addr = smem_u32(sm.v), ds_addr = smem_u32(sm.ds);
-      mbar_wait(&sm.kv_full, 0);
-      for (int t = 0; t < nE; ++t) {
+      auto issue_sdp = [&](int t) {
         const int st = t % QST;
         mbar_wait(&sm.q_full[st], (t / QST) & 1);
         tc_fence_after();
         const uint32_t q_addr = smem_u32(sm.q[st]), do_addr = smem_u32(sm.dO[st]);
-        // S^T = K Q^T ; dP^T = V dO^T
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
           const uint32_t ao = (kk >> 2) * 16384 + (kk & 3) * 32;
           const uint32_t bo = (kk >> 2) * (BR * 128) + (kk & 3) * 32;
           mma_ss(tbase + C::S_COL, sdesc_sw128(k_addr + ao, 16, 1024), sdesc_sw128(q_addr + bo, 16, 1024), ID_S,
                  kk > 0 ? 1u : 0u);
-        }
-#pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk) {
-          const uint32_t ao = (kk >> 2) * 16384 + (kk & 3) * 32;
-          const uint32_t bo = (kk >> 2) * (BR * 128) + (kk & 3) * 32;
           mma_ss(tbase + C::DP_COL, sdesc_sw128(v_addr + ao, 16, 1024), sdesc_sw128(do_addr + bo, 16, 1024), ID_S,
                  kk > 0 ? 1u : 0u);
         }
         mma_commit(&sm.s_full);
+      };
+      mbar_wait(&sm.kv_full, 0);
+      issue_sdp(0);
+      for (int t = 0; t < nE; ++t) {
+        const int st = t % QST;
+        if (t + 1 < nE) {
+          mbar_wait(&sm.sdp_free, t & 1);  // compute WGs hold S^T/dP^T(t) in registers
+          issue_sdp(t + 1);
+        }
         mbar_wait(&sm.p_full, t & 1);
         tc_fence_after();
-        // dV += P^T dO ; dK += dS^T Q   (K = BR queries)
+        const uint32_t q_addr = smem_u32(sm.q[st]), do_addr = smem_u32(sm.dO[st]);
 #pragma unroll
         for (int kk = 0; kk < BR / 16; ++kk) {
           const uint32_t acc = (t > 0 || kk > 0) ? 1u : 0u;
-          mma_ts(tbase + C::DV_COL, tbase + C::S_COL + kk * 8, sdesc_sw128(do_addr + kk * 2048, BR * 128, 1024), ID_G,
+          mma_ts(tbase + C::DV_COL, tbase + C::P_COL + kk * 8, sdesc_sw128(do_addr + kk * 2048, BR * 128, 1024), ID_G,
                  acc);
-          mma_ts(tbase + C::DK_COL, tbase + C::DP_COL + kk * 8, sdesc_sw128(q_addr + kk * 2048, BR * 128, 1024), ID_G,
+          mma_ts(tbase + C::DK_COL, tbase + C::DS_COL + kk * 8, sdesc_sw128(q_addr + kk * 2048, BR * 128, 1024), ID_G,
                  acc);
         }
-        // dQ (K = 128 keys)
+        mma_commit(&sm.pds_free);
+        mma_commit(&sm.q_empty[st]);
         mbar_wait(&sm.dq_empty, (t & 1) ^ 1);
         tc_fence_after();
 #pragma unroll
@@ -211,41 +227,45 @@ __global__ void __launch_bounds__(bwd::NT, 1)
         }
         mma_commit(&sm.dq_full);
         mma_commit(&sm.ds_empty);
-        mma_commit(&sm.q_empty[st]);
       }
       mma_commit(&sm.done);
     }
-  } else if (warp < 4) {
-    // ============================ compute WG (thread = key) ============================
-    const int key_t = warp * 32 + lane;
+  } else if (warp < 8) {
+    // ====================== compute WGs (thread = key, WG = query half) ======================
+    const int wg = warp >> 2, wl = warp & 3;
+    const int key_t = wl * 32 + lane;
     const int key = j * 128 + key_t;
-    const uint32_t lane_off = static_cast<uint32_t>(warp * 32) << 16;
+    const uint32_t lane_off = static_cast<uint32_t>(wl * 32) << 16;
     const int4 mv = a.vec4[(bhm * a.Tc) * 128 + key];  // this key's (LTS, LTE, UTS, UTE), normalised
     const float sl2 = a.scale_log2;
+    constexpr int CH = C::CH_PER_WG;
     for (int t = 0; t < nE; ++t) {
-      const uint32_t ent = sm.list[t];
-      const int i = static_cast<int>(ent & 0xFFFFFFu);
-      const bool partial = ((ent >> 24) & 3u) == 1u;
+      const int i = sm.list[t];
+      const bool partial = (sm.part_bits[t >> 5] >> (t & 31)) & 1u;
       const int st = t % QST;
       mbar_wait(&sm.q_full[st], (t / QST) & 1);
       mbar_wait(&sm.s_full, t & 1);
       tc_fence_after();
-      mbar_wait(&sm.ds_empty, (t & 1) ^ 1);  // dQ GEMM of the previous row tile has read dS
       const float* lv = sm.lvec[st];
       const float* dv = sm.dvec[st];
-#pragma unroll 1
-      for (int ch = 0; ch < BR / 32; ++ch) {
+      uint32_t pp[CH][16], dp[CH][16];
+#pragma unroll
+      for (int ch = 0; ch < CH; ++ch) {
+        const int q0 = (wg * CH + ch) * 32;  // first query of this chunk within the row tile
         uint32_t sr[32], dr[32];
-        tmem_ld32(tbase + lane_off + C::S_COL + ch * 32, sr);
-        tmem_ld32(tbase + lane_off + C::DP_COL + ch * 32, dr);
+        tmem_ld32(tbase + lane_off + C::S_COL + q0, sr);
+        tmem_ld32(tbase + lane_off + C::DP_COL + q0, dr);
         tmem_wait_ld();
-        uint32_t pp[16], dp[16];
+        if (ch == CH - 1) {
+          tc_fence_before();
+          mbar_arrive(&sm.sdp_free);
+        }
 #pragma unroll
         for (int c = 0; c < 32; c += 2) {
           float pv[2], dsv[2];
 #pragma unroll
           for (int u = 0; u < 2; ++u) {
-            const int qc = ch * 32 + c + u;
+            const int qc = q0 + c + u;
             float p = ex2(fmaf(__uint_as_float(sr[c + u]), sl2, -lv[qc]));
             if (partial) {
               const int r = i * BR + qc;
@@ -259,18 +279,34 @@ __global__ void __launch_bounds__(bwd::NT, 1)
             pv[u] = p;
             dsv[u] = p * (__uint_as_float(dr[c + u]) - dv[qc]);
           }
-          pp[c >> 1] = pack_bf16(pv[0], pv[1]);
-          dp[c >> 1] = pack_bf16(dsv[0], dsv[1]);
+          pp[ch][c >> 1] = pack_bf16(pv[0], pv[1]);
+          dp[ch][c >> 1] = pack_bf16(dsv[0], dsv[1]);
         }
-        tmem_st16(tbase + lane_off + C::S_COL + ch * 16, pp);
-        tmem_st16(tbase + lane_off + C::DP_COL + ch * 16, dp);
-        // dS^T row of this key into the SW128 MN-major smem operand of the dQ GEMM
+      }
+      // P / dS TMEM columns free: dV/dK(t-1) done (and, when aliased, dQ(t-1) read out)
+      if constexpr (C::DQ_ALIAS)
+        mbar_wait(&sm.dq_empty, (t & 1) ^ 1);
+      else
+        mbar_wait(&sm.pds_free, (t & 1) ^ 1);
+      tc_fence_after();
+#pragma unroll
+      for (int ch = 0; ch < CH; ++ch) {
+        const int q0 = (wg * CH + ch) * 32;
+        tmem_st16(tbase + lane_off + C::P_COL + q0 / 2, pp[ch]);
+        tmem_st16(tbase + lane_off + C::DS_COL + q0 / 2, dp[ch]);
+      }
+      // dS^T row of this key into the SW128 MN-major smem operand of the dQ GEMM
+      mbar_wait(&sm.ds_empty, (t & 1) ^ 1);
+#pragma unroll
+      for (int ch = 0; ch < CH; ++ch) {
+        const int q0 = (wg * CH + ch) * 32;
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          const int g = ch * 4 + u;  // 8-query group
+          const int g = (q0 >> 3) + u;  // 8-query group
           const int sub = g >> 3, gg = g & 7;
           uint8_t* dst = sm.ds + sub * 16384 + key_t * 128 + ((gg ^ (key_t & 7)) << 4);
-          *reinterpret_cast<uint4*>(dst) = make_uint4(dp[4 * u], dp[4 * u + 1], dp[4 * u + 2], dp[4 * u + 3]);
+          *reinterpret_cast<uint4*>(dst) =
+              make_uint4(dp[ch][4 * u], dp[ch][4 * u + 1], dp[ch][4 * u + 2], dp[ch][4 * u + 3]);
         }
       }
       fence_proxy_async_smem();
@@ -284,43 +320,42 @@ __global__ void __launch_bounds__(bwd::NT, 1)
       tc_fence_after();
     }
     const size_t orow = ((static_cast<size_t>(b) * a.N + key) * a.H + h) * D;
+    // WG0 writes dV, WG1 writes dK
+    const uint32_t col = wg == 0 ? C::DV_COL : C::DK_COL;
+    const float mul = wg == 0 ? 1.0f : a.scale;
+    void* outp = wg == 0 ? a.dv : a.dk;
 #pragma unroll 1
-    for (int which = 0; which < 2; ++which) {
-      const uint32_t col = which == 0 ? C::DV_COL : C::DK_COL;
-      const float mul = which == 0 ? 1.0f : a.scale;
-      void* outp = which == 0 ? a.dv : a.dk;
-#pragma unroll 1
-      for (int c = 0; c < D / 32; ++c) {
-        uint32_t r[32];
-        if (nE > 0) {
-          tmem_ld32(tbase + lane_off + col + c * 32, r);
-          tmem_wait_ld();
-        }
-        float f[32];
+    for (int c = 0; c < D / 32; ++c) {
+      uint32_t r[32];
+      if (nE > 0) {
+        tmem_ld32(tbase + lane_off + col + c * 32, r);
+        tmem_wait_ld();
+      }
+      float f[32];
 #pragma unroll
-        for (int t = 0; t < 32; ++t) f[t] = nE > 0 ? __uint_as_float(r[t]) * mul : 0.f;
-        if (key < a.N) {
-          if constexpr (OUT_F32) {
-            float4* dst = reinterpret_cast<float4*>(static_cast<float*>(outp) + orow + c * 32);
+      for (int t = 0; t < 32; ++t) f[t] = nE > 0 ? __uint_as_float(r[t]) * mul : 0.f;
+      if (key < a.N) {
+        if constexpr (OUT_F32) {
+          float4* dst = reinterpret_cast<float4*>(static_cast<float*>(outp) + orow + c * 32);
 #pragma unroll
-            for (int t = 0; t < 8; ++t) dst[t] = make_float4(f[4 * t], f[4 * t + 1], f[4 * t + 2], f[4 * t + 3]);
-          } else {
-            uint4* dst = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(outp) + orow + c * 32);
+          for (int t = 0; t < 8; ++t) dst[t] = make_float4(f[4 * t], f[4 * t + 1], f[4 * t + 2], f[4 * t + 3]);
+        } else {
+          uint4* dst = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(outp) + orow + c * 32);
 #pragma unroll
-            for (int t = 0; t < 4; ++t)
-              dst[t] = make_uint4(pack_bf16(f[8 * t], f[8 * t + 1]), pack_bf16(f[8 * t + 2], f[8 * t + 3]),
-                                  pack_bf16(f[8 * t + 4], f[8 * t + 5]), pack_bf16(f[8 * t + 6], f[8 * t + 7]));
-          }
+          for (int t = 0; t < 4; ++t)
+            dst[t] = make_uint4(pack_bf16(f[8 * t], f[8 * t + 1]), pack_bf16(f[8 * t + 2], f[8 * t + 3]),
+                                pack_bf16(f[8 * t + 4], f[8 * t + 5]), pack_bf16(f[8 * t + 6], f[8 * t + 7]));
         }
       }
     }
   } else {
-    // ============================ dQ WG: TMEM -> smem -> bulk reduce-add ============================
-    const int wl = warp - 4;
+    // ============= dQ WG: TMEM -> swizzled smem staging -> TMA tensor reduce-add =============
+    const int wl = warp - 8;
     const int t_id = wl * 32 + lane;  // TMEM lane: d index (d=128) or query (d=64)
     const uint32_t lane_off = static_cast<uint32_t>(wl * 32) << 16;
+    if (t_id == 0) tma_prefetch_desc(&tmdQ);
     for (int t = 0; t < nE; ++t) {
-      const int i = static_cast<int>(sm.list[t] & 0xFFFFFFu);
+      const int i = sm.list[t];
       mbar_wait(&sm.dq_full, t & 1);
       tc_fence_after();
       uint32_t r[64];
@@ -329,24 +364,34 @@ __global__ void __launch_bounds__(bwd::NT, 1)
       tmem_wait_ld();
       tc_fence_before();
       mbar_arrive(&sm.dq_empty);
-      if (t_id == 0) bulk_wait_read0();  // previous reduce finished reading the staging tile
+      const int sb = t & 1;
+      if (t_id == 0) bulk_wait_read1();  // the reduce that last used stg[sb] has read it
       named_bar_sync(1, 128);
+      uint8_t* stg = sm.stg[sb];
+      // staging = D/32 boxes of [BR rows][32 fp32], 128-byte swizzled (chunk ^= row & 7)
       if constexpr (C::DQT) {
-        // r[q] = dQ^T[d = t_id][q] -> stg[q][d]
+        // r[q] = dQ^T[d = t_id][q]
+        const int box = t_id >> 5, chunk = (t_id & 31) >> 2, e4 = (t_id & 3) * 4;
 #pragma unroll
-        for (int q = 0; q < 64; ++q) sm.stg[q * D + t_id] = __uint_as_float(r[q]);
+        for (int q = 0; q < 64; ++q)
+          *reinterpret_cast<float*>(stg + box * (BR * 128) + q * 128 + ((chunk ^ (q & 7)) << 4) + e4) =
+              __uint_as_float(r[q]);
       } else {
-        // r[c] = dQ[query = t_id][c] -> stg[query][c]
+        // r[c] = dQ[query = t_id][c]
 #pragma unroll
-        for (int c4 = 0; c4 < 16; ++c4)
-          reinterpret_cast<float4*>(sm.stg + t_id * D)[c4] =
-              make_float4(__uint_as_float(r[c4 * 4]), __uint_as_float(r[c4 * 4 + 1]), __uint_as_float(r[c4 * 4 + 2]),
-                          __uint_as_float(r[c4 * 4 + 3]));
+        for (int c4 = 0; c4 < 16; ++c4) {
+          const int box = c4 >> 3, chunk = c4 & 7;
+          *reinterpret_cast<float4*>(stg + box * (BR * 128) + t_id * 128 + ((chunk ^ (t_id & 7)) << 4)) =
+              make_float4(__uint_as_float(r[c4 * 4]), __uint_as_float(r[c4 * 4 + 1]),
+                          __uint_as_float(r[c4 * 4 + 2]), __uint_as_float(r[c4 * 4 + 3]));
+        }
       }
       fence_proxy_async_smem();
       named_bar_sync(1, 128);
       if (t_id == 0) {
-        bulk_reduce_add_f32(a.dqacc + (bh * a.Npb + static_cast<size_t>(i) * BR) * D, sm.stg, C::STG_BYTES);
+#pragma unroll
+        for (int bx = 0; bx < D / 32; ++bx)
+          tma_reduce_add_3d(&tmdQ, stg + bx * (BR * 128), bx * 32, i * BR, static_cast<int>(bh));
         bulk_commit();
       }
     }
@@ -355,7 +400,7 @@ __global__ void __launch_bounds__(bwd::NT, 1)
 
   tc_fence_before();
   __syncthreads();
-  if (warp == 9) {
+  if (warp == 13) {
     tc_fence_after();
     tmem_dealloc<512>(tbase);
   }
@@ -363,19 +408,19 @@ __global__ void __launch_bounds__(bwd::NT, 1)
 
 template <int D, bool CAUSAL, bool OUT_F32>
 static cudaError_t launch_bwd_t(const Dims& d, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
-                                const CUtensorMap& tdo, const BwdArgs& a, cudaStream_t st) {
+                                const CUtensorMap& tdo, const CUtensorMap& tdq, const BwdArgs& a, cudaStream_t st) {
   auto kern = fm_bwd_kernel<D, CAUSAL, OUT_F32>;
   const size_t smem = sizeof(bwd::Smem<D>) + 1024;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (e != cudaSuccess) return e;
   dim3 grid(d.Tc, d.H, d.B);
-  kern<<<grid, bwd::NT, smem, st>>>(tq, tk, tv, tdo, a);
+  kern<<<grid, bwd::NT, smem, st>>>(tq, tk, tv, tdo, tdq, a);
   return cudaGetLastError();
 }
 
 cudaError_t launch_bwd(const Dims& d, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
-                       const CUtensorMap& tdo, const BwdArgs& a, cudaStream_t st) {
-#define FM_B(DD, CC, FF) return launch_bwd_t<DD, CC, FF>(d, tq, tk, tv, tdo, a, st)
+                       const CUtensorMap& tdo, const CUtensorMap& tdq, const BwdArgs& a, cudaStream_t st) {
+#define FM_B(DD, CC, FF) return launch_bwd_t<DD, CC, FF>(d, tq, tk, tv, tdo, tdq, a, st)
   if (d.D == 128) {
     if (d.causal) { if (d.out_f32) FM_B(128, true, true); else FM_B(128, true, false); }
     else { if (d.out_f32) FM_B(128, false, true); else FM_B(128, false, false); }
