@@ -67,28 +67,6 @@ bool make_map(CUtensorMap* m, const void* ptr, const fm::Dims& d, int box_rows, 
   return true;
 }
 
-// fp32 dQ accumulator [B*H, Npb, D] viewed as (D, Npb, B*H); box = 32 x Br x 1, 128-byte
-// swizzle — the layout the backward kernel stages dQ tiles in before the TMA reduce-add.
-bool make_dq_map(CUtensorMap* m, float* ptr, const fm::Dims& d, std::string* err) {
-  auto enc = get_encode();
-  if (!enc) {
-    *err = "cuTensorMapEncodeTiled unavailable";
-    return false;
-  }
-  cuuint64_t dims[3] = {static_cast<cuuint64_t>(d.D), static_cast<cuuint64_t>(d.Npb),
-                        static_cast<cuuint64_t>(d.B) * d.H};
-  cuuint64_t strides[2] = {static_cast<cuuint64_t>(d.D) * 4, static_cast<cuuint64_t>(d.Npb) * d.D * 4};
-  cuuint32_t box[3] = {32, static_cast<cuuint32_t>(d.Brb), 1};
-  cuuint32_t estr[3] = {1, 1, 1};
-  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, ptr, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) {
-    *err = "cuTensorMapEncodeTiled (dQ accumulator) failed with CUresult " + std::to_string(static_cast<int>(r));
-    return false;
-  }
-  return true;
-}
-
 fm_status check_params(const fm_params* p, fm::Dims* d, bool need_attention) {
   if (!p) return fail(FM_ERR_INVALID_ARGUMENT, "params is NULL");
   if (p->batch < 1 || p->seqlen < 1 || p->num_heads < 1)
@@ -292,9 +270,9 @@ fm_status flashmask_bwd(const fm_params* p, const void* q, const void* k, const 
     return fail(FM_ERR_WORKSPACE_TOO_SMALL, "workspace smaller than flashmask_workspace_size(FM_PASS_BWD)");
   carve(d, FM_PASS_BWD, workspace, &w);
   std::string err;
-  CUtensorMap tq, tk, tv, tdo, tdq;
+  CUtensorMap tq, tk, tv, tdo;
   if (!make_map(&tq, q, d, d.Brb, &err) || !make_map(&tk, k, d, 128, &err) || !make_map(&tv, v, d, 128, &err) ||
-      !make_map(&tdo, dout, d, d.Brb, &err) || !make_dq_map(&tdq, w.dqacc, d, &err))
+      !make_map(&tdo, dout, d, d.Brb, &err))
     return fail(FM_ERR_CUDA, err);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   cudaError_t e = timed(FM_KERNEL_EXPAND, st, [&] { return fm::launch_expand(sri, d, fm::kTile, w.ext8, w.vec4, st); });
@@ -314,7 +292,7 @@ fm_status flashmask_bwd(const fm_params* p, const void* q, const void* k, const 
   a.dqacc = w.dqacc;
   a.dk = dk;
   a.dv = dv;
-  e = timed(FM_KERNEL_BWD, st, [&] { return fm::launch_bwd(d, tq, tk, tv, tdo, tdq, a, st); });
+  e = timed(FM_KERNEL_BWD, st, [&] { return fm::launch_bwd(d, tq, tk, tv, tdo, a, st); });
   if (e != cudaSuccess) return cuda_fail(e, "backward kernel");
   e = timed(FM_KERNEL_DQ_CONVERT, st, [&] { return fm::launch_dq_convert(d, w.dqacc, dq, st); });
   if (e != cudaSuccess) return cuda_fail(e, "dq convert");
@@ -347,3 +325,4 @@ fm_status flashmask_timing_collect(double* ms, int64_t* launches) {
 }
 
 }  // extern "C"
+

@@ -13,14 +13,20 @@
 //   dS^T = P^T o (dP^T - D_i)
 //   dV  += P^T dO_i,  dK += dS^T Q_i         (A operands bf16 from TMEM)
 //   d=128: dQ_i^T = K_j^T dS^T (M = d);  d=64: dQ_i = dS K_j (M = queries)
-// dQ tiles are added into the fp32 workspace by TMA tensor reduce-add (no read-modify-write).
+// dQ tiles are added into the fp32 workspace with red.global.add straight from registers
+// (no read-modify-write, no shared-memory staging).
 //
 // Pipelining: the compute WGs copy S^T/dP^T of row tile t into registers and release them at
 // once, so the MMA warp issues S^T/dP^T of tile t+1 while P/dS of tile t are being computed;
-// P and dS live in their own TMEM columns.  TMEM columns:
-//   d=128: S [0,64) dP [64,128) P [128,160) dS [160,192) dQ^T [192,256) dV [256,384) dK [384,512)
-//   d=64 : S [0,128) dP [128,256) P [256,320) dS [320,384) dQ = P cols (aliased) dV [384,448) dK [448,512)
-// Warp roles: 0-7 two compute WGs (query halves), 8-11 dQ WG (TMEM -> smem -> reduce),
+// P and dS live in their own TMEM columns, which the dQ GEMM of the same tile then reuses.
+// Shared-memory bandwidth is the scarce resource here (every SS MMA re-reads its operands),
+// so for d=128 K_j is copied once into TMEM and S^T = K_j Q_i^T runs with A from TMEM.
+// TMEM columns:
+//   d=128: S [0,64) dP [64,128) P [128,160) dS [160,192) (dQ^T aliases [128,192)) K_j [192,256)
+//          dV [256,384) dK [384,512)
+//   d=64 : S [0,128) dP [128,256) P [256,320) dS [320,384) (dQ aliases [256,320))
+//          dV [384,448) dK [448,512)
+// Warp roles: 0-7 two compute WGs (query halves), 8-11 dQ WG (TMEM -> red.global.add),
 // 12 TMA producer, 13 TMEM allocator + MMA issuer.
 #include <cuda_bf16.h>
 #include <cmath>
@@ -28,26 +34,42 @@
 #include "fm_internal.h"
 #include "fm_ptx.cuh"
 
+#ifdef FM_TRACE
+namespace fm { __device__ long long g_fm_trace[64 * 16]; }
+#define FM_T(slot, t)                                                                        \
+  do {                                                                                        \
+    if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && (t) < 64) fm::g_fm_trace[(t) * 16 + (slot)] = clock64(); \
+  } while (0)
+#else
+#define FM_T(slot, t) \
+  do {                \
+  } while (0)
+#endif
+
+#ifndef FM_DQ_MODE
+#define FM_DQ_MODE 0  // experiments only: nonzero = skip the dQ global reduction
+#endif
+
 namespace fm {
 
 namespace bwd {
 
 constexpr int NT = 448;
-constexpr int QST = 2;
+constexpr int QST = 4;
 constexpr int kMaxTrb = 4096;
 
 template <int D>
 struct Cfg {
   static constexpr int BR = (D == 128) ? 64 : 128;
   static constexpr bool DQT = (D == 128);          // dQ computed transposed (M = d)
-  static constexpr bool DQ_ALIAS = (D == 64);      // dQ accumulator aliases the P columns
+  static constexpr bool KA_TMEM = (D == 128);      // K_j held in TMEM as the A operand of S^T
   static constexpr int KV_TILE = 128 * D * 2;      // bytes
   static constexpr int Q_TILE = BR * D * 2;
   static constexpr int DS_BYTES = 128 * BR * 2;
-  static constexpr int STG_BYTES = BR * D * 4;
   static constexpr int CH_PER_WG = BR / 64;        // 32-query chunks per compute WG
   static constexpr int S_COL = 0, DP_COL = BR, P_COL = 2 * BR, DS_COL = 2 * BR + BR / 2;
-  static constexpr int DQ_COL = DQ_ALIAS ? P_COL : 192;
+  static constexpr int DQ_COL = P_COL;             // dQ(t) overwrites P/dS(t) after dV/dK(t) read them
+  static constexpr int KA_COL = 192;
   static constexpr int DV_COL = (D == 128) ? 256 : 384;
   static constexpr int DK_COL = DV_COL + D;
 };
@@ -60,18 +82,51 @@ struct Smem {
   uint8_t q[QST][C::Q_TILE];
   uint8_t dO[QST][C::Q_TILE];
   uint8_t ds[C::DS_BYTES];
-  uint8_t stg[2][C::STG_BYTES];
   float lvec[QST][C::BR];
   float dvec[QST][C::BR];
   uint16_t list[kMaxTrb];
   uint32_t part_bits[kMaxTrb / 32];
   uint64_t kv_full;
   uint64_t q_full[QST], q_empty[QST];
-  uint64_t s_full, sdp_free, p_full, pds_free, dq_full, dq_empty, ds_empty, done;
+  uint64_t s_full, sdp_free, p_full, dq_full, dq_empty, ds_empty, ka_full, done;
   uint32_t tmem_base;
   int n_entries;
   int warp_cnt[NT / 32];
 };
+
+// P^T / dS^T for one 32-query chunk of one key (Alg. 2 lines 20-25):
+//   p = exp2(S*scale*log2e - L2_r) (masked to 0 on PARTIAL tiles), ds = p * (dP - D_r)
+// Branch-free per template so the compiler can overlap the shared loads, FMAs and MUFU ops.
+template <bool PART, bool CAUSAL>
+__device__ __forceinline__ void pds_chunk(const uint32_t* sr, const uint32_t* dr, const float* lq, const float* dq,
+                                          float sl2, int r0, int key, int4 mv, uint32_t* pp, uint32_t* dp) {
+#pragma unroll
+  for (int c = 0; c < 32; c += 4) {
+    const float4 L4 = *reinterpret_cast<const float4*>(lq + c);
+    const float4 D4 = *reinterpret_cast<const float4*>(dq + c);
+    const float l4[4] = {L4.x, L4.y, L4.z, L4.w};
+    const float d4[4] = {D4.x, D4.y, D4.z, D4.w};
+    float p[4], ds[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      p[u] = ex2(fmaf(__uint_as_float(sr[c + u]), sl2, -l4[u]));
+      if constexpr (PART) {
+        const int r = r0 + c + u;
+        bool msk = static_cast<unsigned>(r - mv.x) < static_cast<unsigned>(mv.y - mv.x);
+        if constexpr (CAUSAL)
+          msk |= r < key;
+        else
+          msk |= static_cast<unsigned>(r - mv.z) < static_cast<unsigned>(mv.w - mv.z);
+        p[u] = msk ? 0.f : p[u];
+      }
+      ds[u] = p[u] * (__uint_as_float(dr[c + u]) - d4[u]);
+    }
+    pp[c / 2] = pack_bf16(p[0], p[1]);
+    pp[c / 2 + 1] = pack_bf16(p[2], p[3]);
+    dp[c / 2] = pack_bf16(ds[0], ds[1]);
+    dp[c / 2 + 1] = pack_bf16(ds[2], ds[3]);
+  }
+}
 
 }  // namespace bwd
 
@@ -79,13 +134,13 @@ template <int D, bool CAUSAL, bool OUT_F32>
 __global__ void __launch_bounds__(bwd::NT, 1)
     fm_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                   const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO,
-                  const __grid_constant__ CUtensorMap tmdQ, const BwdArgs a) {
+                  const BwdArgs a) {
   using namespace bwd;
   using C = Cfg<D>;
   using S = Smem<D>;
   constexpr int BR = C::BR;
   extern __shared__ uint8_t smem_raw[];
-  S& sm = *reinterpret_cast<S*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  S& sm = *smem_align1024<S>(smem_raw);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int j = static_cast<int>(blockIdx.x);
@@ -100,7 +155,7 @@ __global__ void __launch_bounds__(bwd::NT, 1)
     mbar_init(&sm.s_full, 1);
     mbar_init(&sm.sdp_free, 256);
     mbar_init(&sm.p_full, 256);
-    mbar_init(&sm.pds_free, 1);
+    mbar_init(&sm.ka_full, 128);
     mbar_init(&sm.dq_full, 1);
     mbar_init(&sm.dq_empty, 128);
     mbar_init(&sm.ds_empty, 1);
@@ -180,28 +235,38 @@ __global__ void __launch_bounds__(bwd::NT, 1)
       auto issue_sdp = [&](int t) {
         const int st = t % QST;
         mbar_wait(&sm.q_full[st], (t / QST) & 1);
+        FM_T(14, t - 1);
         tc_fence_after();
         const uint32_t q_addr = smem_u32(sm.q[st]), do_addr = smem_u32(sm.dO[st]);
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
           const uint32_t ao = (kk >> 2) * 16384 + (kk & 3) * 32;
           const uint32_t bo = (kk >> 2) * (BR * 128) + (kk & 3) * 32;
-          mma_ss(tbase + C::S_COL, sdesc_sw128(k_addr + ao, 16, 1024), sdesc_sw128(q_addr + bo, 16, 1024), ID_S,
-                 kk > 0 ? 1u : 0u);
+          if constexpr (C::KA_TMEM)
+            mma_ts(tbase + C::S_COL, tbase + C::KA_COL + kk * 8, sdesc_sw128(q_addr + bo, 16, 1024), ID_S,
+                   kk > 0 ? 1u : 0u);
+          else
+            mma_ss(tbase + C::S_COL, sdesc_sw128(k_addr + ao, 16, 1024), sdesc_sw128(q_addr + bo, 16, 1024), ID_S,
+                   kk > 0 ? 1u : 0u);
           mma_ss(tbase + C::DP_COL, sdesc_sw128(v_addr + ao, 16, 1024), sdesc_sw128(do_addr + bo, 16, 1024), ID_S,
                  kk > 0 ? 1u : 0u);
         }
         mma_commit(&sm.s_full);
       };
       mbar_wait(&sm.kv_full, 0);
+      if constexpr (C::KA_TMEM) mbar_wait(&sm.ka_full, 0);  // K_j copied into TMEM
       issue_sdp(0);
       for (int t = 0; t < nE; ++t) {
         const int st = t % QST;
+        FM_T(0, t);
         if (t + 1 < nE) {
           mbar_wait(&sm.sdp_free, t & 1);  // compute WGs hold S^T/dP^T(t) in registers
+          FM_T(1, t);
           issue_sdp(t + 1);
+          FM_T(11, t);
         }
         mbar_wait(&sm.p_full, t & 1);
+        FM_T(2, t);
         tc_fence_after();
         const uint32_t q_addr = smem_u32(sm.q[st]), do_addr = smem_u32(sm.dO[st]);
 #pragma unroll
@@ -212,10 +277,10 @@ __global__ void __launch_bounds__(bwd::NT, 1)
           mma_ts(tbase + C::DK_COL, tbase + C::DS_COL + kk * 8, sdesc_sw128(q_addr + kk * 2048, BR * 128, 1024), ID_G,
                  acc);
         }
-        mma_commit(&sm.pds_free);
         mma_commit(&sm.q_empty[st]);
-        mbar_wait(&sm.dq_empty, (t & 1) ^ 1);
-        tc_fence_after();
+        FM_T(12, t);
+        // dQ(t) overwrites the P/dS columns: issued after dV/dK(t) (in-order), and the dQ WG has
+        // read dQ(t-1) before the compute WGs stored P/dS(t) (they waited dq_empty(t-1)).
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
           if constexpr (C::DQT)
@@ -227,6 +292,7 @@ __global__ void __launch_bounds__(bwd::NT, 1)
         }
         mma_commit(&sm.dq_full);
         mma_commit(&sm.ds_empty);
+        FM_T(13, t);
       }
       mma_commit(&sm.done);
     }
@@ -239,12 +305,35 @@ __global__ void __launch_bounds__(bwd::NT, 1)
     const int4 mv = a.vec4[(bhm * a.Tc) * 128 + key];  // this key's (LTS, LTE, UTS, UTE), normalised
     const float sl2 = a.scale_log2;
     constexpr int CH = C::CH_PER_WG;
+    if constexpr (C::KA_TMEM) {
+      // copy row key_t of K_j (SW128 smem, two 64-column boxes) into TMEM as the A operand of S^T
+      if (wg == 0 && nE > 0) {
+        mbar_wait(&sm.kv_full, 0);
+#pragma unroll
+        for (int bx = 0; bx < 2; ++bx) {
+          uint32_t kr[32];
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            const uint4 v4 = *reinterpret_cast<const uint4*>(sm.k + bx * 16384 + key_t * 128 + ((c ^ (key_t & 7)) << 4));
+            kr[4 * c] = v4.x;
+            kr[4 * c + 1] = v4.y;
+            kr[4 * c + 2] = v4.z;
+            kr[4 * c + 3] = v4.w;
+          }
+          tmem_st32(tbase + lane_off + C::KA_COL + bx * 32, kr);
+        }
+        tmem_wait_st();
+        tc_fence_before();
+        mbar_arrive(&sm.ka_full);
+      }
+    }
     for (int t = 0; t < nE; ++t) {
       const int i = sm.list[t];
       const bool partial = (sm.part_bits[t >> 5] >> (t & 31)) & 1u;
       const int st = t % QST;
       mbar_wait(&sm.q_full[st], (t / QST) & 1);
       mbar_wait(&sm.s_full, t & 1);
+      if (tid == 0) FM_T(4, t);
       tc_fence_after();
       const float* lv = sm.lvec[st];
       const float* dv = sm.dvec[st];
@@ -260,34 +349,15 @@ __global__ void __launch_bounds__(bwd::NT, 1)
           tc_fence_before();
           mbar_arrive(&sm.sdp_free);
         }
-#pragma unroll
-        for (int c = 0; c < 32; c += 2) {
-          float pv[2], dsv[2];
-#pragma unroll
-          for (int u = 0; u < 2; ++u) {
-            const int qc = q0 + c + u;
-            float p = ex2(fmaf(__uint_as_float(sr[c + u]), sl2, -lv[qc]));
-            if (partial) {
-              const int r = i * BR + qc;
-              bool msk = static_cast<unsigned>(r - mv.x) < static_cast<unsigned>(mv.y - mv.x);
-              if constexpr (CAUSAL)
-                msk |= r < key;
-              else
-                msk |= static_cast<unsigned>(r - mv.z) < static_cast<unsigned>(mv.w - mv.z);
-              p = msk ? 0.f : p;
-            }
-            pv[u] = p;
-            dsv[u] = p * (__uint_as_float(dr[c + u]) - dv[qc]);
-          }
-          pp[ch][c >> 1] = pack_bf16(pv[0], pv[1]);
-          dp[ch][c >> 1] = pack_bf16(dsv[0], dsv[1]);
-        }
+        if (partial)
+          pds_chunk<true, CAUSAL>(sr, dr, lv + q0, dv + q0, sl2, i * BR + q0, key, mv, pp[ch], dp[ch]);
+        else
+          pds_chunk<false, CAUSAL>(sr, dr, lv + q0, dv + q0, sl2, i * BR + q0, key, mv, pp[ch], dp[ch]);
       }
-      // P / dS TMEM columns free: dV/dK(t-1) done (and, when aliased, dQ(t-1) read out)
-      if constexpr (C::DQ_ALIAS)
-        mbar_wait(&sm.dq_empty, (t & 1) ^ 1);
-      else
-        mbar_wait(&sm.pds_free, (t & 1) ^ 1);
+      if (tid == 0) FM_T(5, t);
+      // P / dS TMEM columns free: dQ(t-1), which reuses them, has been read out
+      mbar_wait(&sm.dq_empty, (t & 1) ^ 1);
+      if (tid == 0) FM_T(6, t);
       tc_fence_after();
 #pragma unroll
       for (int ch = 0; ch < CH; ++ch) {
@@ -297,6 +367,7 @@ __global__ void __launch_bounds__(bwd::NT, 1)
       }
       // dS^T row of this key into the SW128 MN-major smem operand of the dQ GEMM
       mbar_wait(&sm.ds_empty, (t & 1) ^ 1);
+      if (tid == 0) FM_T(7, t);
 #pragma unroll
       for (int ch = 0; ch < CH; ++ch) {
         const int q0 = (wg * CH + ch) * 32;
@@ -313,6 +384,7 @@ __global__ void __launch_bounds__(bwd::NT, 1)
       tmem_wait_st();
       tc_fence_before();
       mbar_arrive(&sm.p_full);
+      if (tid == 0) FM_T(8, t);
     }
     // ---- epilogue: dK_j = scale * dK, dV_j written once (Alg. 2 line 30) ----
     if (nE > 0) {
@@ -349,14 +421,14 @@ __global__ void __launch_bounds__(bwd::NT, 1)
       }
     }
   } else {
-    // ============= dQ WG: TMEM -> swizzled smem staging -> TMA tensor reduce-add =============
+    // ================= dQ WG: TMEM -> registers -> red.global.add.f32 =================
     const int wl = warp - 8;
     const int t_id = wl * 32 + lane;  // TMEM lane: d index (d=128) or query (d=64)
     const uint32_t lane_off = static_cast<uint32_t>(wl * 32) << 16;
-    if (t_id == 0) tma_prefetch_desc(&tmdQ);
     for (int t = 0; t < nE; ++t) {
       const int i = sm.list[t];
       mbar_wait(&sm.dq_full, t & 1);
+      if (t_id == 0) FM_T(9, t);
       tc_fence_after();
       uint32_t r[64];
       tmem_ld32(tbase + lane_off + C::DQ_COL, r);
@@ -364,38 +436,21 @@ __global__ void __launch_bounds__(bwd::NT, 1)
       tmem_wait_ld();
       tc_fence_before();
       mbar_arrive(&sm.dq_empty);
-      const int sb = t & 1;
-      if (t_id == 0) bulk_wait_read1();  // the reduce that last used stg[sb] has read it
-      named_bar_sync(1, 128);
-      uint8_t* stg = sm.stg[sb];
-      // staging = D/32 boxes of [BR rows][32 fp32], 128-byte swizzled (chunk ^= row & 7)
+      if (FM_DQ_MODE != 0) continue;
+      float* base = a.dqacc + (bh * a.Npb + static_cast<size_t>(i) * BR) * D;
       if constexpr (C::DQT) {
-        // r[q] = dQ^T[d = t_id][q]
-        const int box = t_id >> 5, chunk = (t_id & 31) >> 2, e4 = (t_id & 3) * 4;
+        // r[q] = dQ^T[d = t_id][q]: a warp adds 32 consecutive floats of one query row
 #pragma unroll
-        for (int q = 0; q < 64; ++q)
-          *reinterpret_cast<float*>(stg + box * (BR * 128) + q * 128 + ((chunk ^ (q & 7)) << 4) + e4) =
-              __uint_as_float(r[q]);
+        for (int q = 0; q < 64; ++q) red_add_f32(base + q * D + t_id, __uint_as_float(r[q]));
       } else {
-        // r[c] = dQ[query = t_id][c]
+        // r[c] = dQ[query = t_id][c]: 16-byte vector adds along the row
 #pragma unroll
-        for (int c4 = 0; c4 < 16; ++c4) {
-          const int box = c4 >> 3, chunk = c4 & 7;
-          *reinterpret_cast<float4*>(stg + box * (BR * 128) + t_id * 128 + ((chunk ^ (t_id & 7)) << 4)) =
-              make_float4(__uint_as_float(r[c4 * 4]), __uint_as_float(r[c4 * 4 + 1]),
-                          __uint_as_float(r[c4 * 4 + 2]), __uint_as_float(r[c4 * 4 + 3]));
-        }
+        for (int c4 = 0; c4 < 16; ++c4)
+          red_add_v4_f32(base + t_id * D + c4 * 4, __uint_as_float(r[4 * c4]), __uint_as_float(r[4 * c4 + 1]),
+                         __uint_as_float(r[4 * c4 + 2]), __uint_as_float(r[4 * c4 + 3]));
       }
-      fence_proxy_async_smem();
-      named_bar_sync(1, 128);
-      if (t_id == 0) {
-#pragma unroll
-        for (int bx = 0; bx < D / 32; ++bx)
-          tma_reduce_add_3d(&tmdQ, stg + bx * (BR * 128), bx * 32, i * BR, static_cast<int>(bh));
-        bulk_commit();
-      }
+      if (t_id == 0) FM_T(10, t);
     }
-    if (t_id == 0) bulk_wait0();
   }
 
   tc_fence_before();
@@ -408,19 +463,19 @@ __global__ void __launch_bounds__(bwd::NT, 1)
 
 template <int D, bool CAUSAL, bool OUT_F32>
 static cudaError_t launch_bwd_t(const Dims& d, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
-                                const CUtensorMap& tdo, const CUtensorMap& tdq, const BwdArgs& a, cudaStream_t st) {
+                                const CUtensorMap& tdo, const BwdArgs& a, cudaStream_t st) {
   auto kern = fm_bwd_kernel<D, CAUSAL, OUT_F32>;
   const size_t smem = sizeof(bwd::Smem<D>) + 1024;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (e != cudaSuccess) return e;
   dim3 grid(d.Tc, d.H, d.B);
-  kern<<<grid, bwd::NT, smem, st>>>(tq, tk, tv, tdo, tdq, a);
+  kern<<<grid, bwd::NT, smem, st>>>(tq, tk, tv, tdo, a);
   return cudaGetLastError();
 }
 
 cudaError_t launch_bwd(const Dims& d, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
-                       const CUtensorMap& tdo, const CUtensorMap& tdq, const BwdArgs& a, cudaStream_t st) {
-#define FM_B(DD, CC, FF) return launch_bwd_t<DD, CC, FF>(d, tq, tk, tv, tdo, tdq, a, st)
+                       const CUtensorMap& tdo, const BwdArgs& a, cudaStream_t st) {
+#define FM_B(DD, CC, FF) return launch_bwd_t<DD, CC, FF>(d, tq, tk, tv, tdo, a, st)
   if (d.D == 128) {
     if (d.causal) { if (d.out_f32) FM_B(128, true, true); else FM_B(128, true, false); }
     else { if (d.out_f32) FM_B(128, false, true); else FM_B(128, false, false); }
@@ -432,3 +487,9 @@ cudaError_t launch_bwd(const Dims& d, const CUtensorMap& tq, const CUtensorMap& 
 }
 
 }  // namespace fm
+
+#ifdef FM_TRACE
+extern "C" __attribute__((visibility("default"))) int flashmask_debug_trace(long long* host) {
+  return cudaMemcpyFromSymbol(host, fm::g_fm_trace, sizeof(long long) * 64 * 16) == cudaSuccess ? 0 : 1;
+}
+#endif

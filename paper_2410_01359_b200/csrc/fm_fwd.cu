@@ -54,7 +54,7 @@ __global__ void __launch_bounds__(fwd::NT, 1)
   using namespace fwd;
   using S = Smem<D>;
   extern __shared__ uint8_t smem_raw[];
-  S& sm = *reinterpret_cast<S*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  S& sm = *smem_align1024<S>(smem_raw);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int npairs = (a.Tr + 1) >> 1;

@@ -12,6 +12,13 @@ namespace fm {
 
 FM_DEV uint32_t smem_u32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
 
+// Align the dynamic shared-memory base to 1024 B (SW128 atoms) with pointer arithmetic only,
+// so the compiler keeps the shared address space (LDS/STS, not generic LD/ST).
+template <class T>
+FM_DEV T* smem_align1024(uint8_t* raw) {
+  return reinterpret_cast<T*>(raw + ((1024u - (smem_u32(raw) & 1023u)) & 1023u));
+}
+
 FM_DEV uint32_t lane_id() { uint32_t r; asm volatile("mov.u32 %0, %%laneid;" : "=r"(r)); return r; }
 
 // ------------------------------------------------------------------ mbarrier
@@ -85,6 +92,11 @@ FM_DEV void tma_reduce_add_3d(const CUtensorMap* m, const void* smem_src, int c0
       : "memory");
 }
 FM_DEV void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
+// fp32 reductions into global memory (no return value)
+FM_DEV void red_add_f32(float* p, float v) { asm volatile("red.global.add.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory"); }
+FM_DEV void red_add_v4_f32(float* p, float a, float b, float c, float d) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(a), "f"(b), "f"(c), "f"(d) : "memory");
+}
 FM_DEV void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 FM_DEV void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 FM_DEV void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }

@@ -13,7 +13,7 @@ import os
 import torch
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libflashmask.so")
+LIB_PATH = os.environ.get("FLASHMASK_LIB", os.path.join(_PKG, "libflashmask.so"))
 
 FM_OK, FM_ERR_INVALID_ARGUMENT, FM_ERR_UNSUPPORTED, FM_ERR_WORKSPACE_TOO_SMALL, FM_ERR_CUDA = range(5)
 FM_BF16, FM_FP32 = 0, 1

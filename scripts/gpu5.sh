@@ -1,0 +1,5 @@
+cd $GRAFT_REPO_ROOT
+export PYTHONUNBUFFERED=1
+timeout -s KILL 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -4
+timeout -s KILL 300 python scripts/time_kernels.py C3 3 2>&1 | tail -3
+timeout -s KILL 300 python scripts/time_kernels.py C2 5 2>&1 | tail -4

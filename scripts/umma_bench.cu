@@ -1,0 +1,90 @@
+// Microbenchmark: cycles per tcgen05.mma (kind::f16, bf16 -> fp32, K = 16) by shape and
+// operand source.  One CTA per SM; one thread issues REPS back-to-back MMAs.
+// nvcc -gencode arch=compute_100a,code=sm_100a -std=c++17 -O3 -o umma_bench scripts/umma_bench.cu
+#include <cstdio>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../paper_2410_01359_b200/csrc/fm_ptx.cuh"
+
+using namespace fm;
+
+constexpr int REPS = 4096;
+
+template <int M, int N, bool A_TMEM, int A_MN, int B_MN>
+__global__ void __launch_bounds__(128, 1) bench(unsigned long long* out) {
+  extern __shared__ uint8_t raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tbase_s;
+  const int warp = threadIdx.x / 32;
+  for (int i = threadIdx.x; i < 65536 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(sm)[i] = 0;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    fence_barrier_init();
+  }
+  if (warp == 0) tmem_alloc<512>(&tbase_s);
+  fence_proxy_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tb = tbase_s;
+  if (threadIdx.x == 0) {
+    const uint32_t id = idesc_bf16(M, N, A_MN, B_MN);
+    const uint32_t a = smem_u32(sm), b = smem_u32(sm + 32768);
+    const long long t0 = clock64();
+    for (int r = 0; r < REPS; ++r) {
+      const uint32_t off = (r & 3) * 32;
+      if constexpr (A_TMEM)
+        mma_ts(tb + 256, tb + (r & 3) * 8, sdesc_sw128(b + off, 16384, 1024), id, 1);
+      else
+        mma_ss(tb + 256, sdesc_sw128(a + off, 16384, 1024), sdesc_sw128(b + off, 16384, 1024), id, 1);
+    }
+    mma_commit(&bar);
+    mbar_wait(&bar, 0);
+    const long long t1 = clock64();
+    out[blockIdx.x] = static_cast<unsigned long long>(t1 - t0);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_dealloc<512>(tb);
+  }
+}
+
+template <int M, int N, bool AT, int AMN, int BMN>
+void run(const char* name) {
+  unsigned long long* d;
+  cudaMalloc(&d, 148 * 8);
+  auto k = bench<M, N, AT, AMN, BMN>;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536 + 1024);
+  k<<<148, 128, 65536 + 1024>>>(d);
+  k<<<148, 128, 65536 + 1024>>>(d);
+  cudaError_t e = cudaDeviceSynchronize();
+  unsigned long long h[148];
+  cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
+  double avg = 0;
+  for (int i = 0; i < 148; ++i) avg += h[i];
+  avg /= 148;
+  const double per = avg / REPS;
+  const double macs = double(M) * N * 16;
+  printf("%-34s %s  %7.1f clk/MMA  %7.0f MAC/clk/SM (%.0f%% of 4096)\n", name, cudaGetErrorString(e), per, macs / per,
+         100.0 * macs / per / 4096);
+  cudaFree(d);
+}
+
+int main() {
+  run<128, 64, false, 0, 0>("SS M128 N64  A K  B K");
+  run<128, 128, false, 0, 0>("SS M128 N128 A K  B K");
+  run<128, 256, false, 0, 0>("SS M128 N256 A K  B K");
+  run<128, 64, false, 1, 1>("SS M128 N64  A MN B MN");
+  run<128, 128, false, 0, 1>("SS M128 N128 A K  B MN");
+  run<128, 64, true, 0, 1>("TS M128 N64  B MN");
+  run<128, 128, true, 0, 1>("TS M128 N128 B MN");
+  run<128, 256, true, 0, 1>("TS M128 N256 B MN");
+  run<128, 128, true, 0, 0>("TS M128 N128 B K");
+  run<128, 32, false, 0, 0>("SS M128 N32  A K  B K");
+  run<128, 16, false, 0, 0>("SS M128 N16  A K  B K");
+  return 0;
+}
