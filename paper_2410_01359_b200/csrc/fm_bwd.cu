@@ -18,16 +18,13 @@
 //
 // Pipelining: the compute WGs copy S^T/dP^T of row tile t into registers and release them at
 // once, so the MMA warp issues S^T/dP^T of tile t+1 while P/dS of tile t are being computed;
-// P and dS live in their own TMEM columns, which the dQ GEMM of the same tile then reuses.
-// Shared-memory bandwidth is the scarce resource here (every SS MMA re-reads its operands),
-// so for d=128 K_j is copied once into TMEM and S^T = K_j Q_i^T runs with A from TMEM.
+// P and dS live in their own TMEM columns (at d=64 the dQ GEMM of the same tile reuses them).
 // TMEM columns:
-//   d=128: S [0,64) dP [64,128) P [128,160) dS [160,192) (dQ^T aliases [128,192)) K_j [192,256)
-//          dV [256,384) dK [384,512)
+//   d=128: S [0,64) dP [64,128) P [128,160) dS [160,192) dQ^T [192,256) dV [256,384) dK [384,512)
 //   d=64 : S [0,128) dP [128,256) P [256,320) dS [320,384) (dQ aliases [256,320))
 //          dV [384,448) dK [448,512)
 // Warp roles: 0-7 two compute WGs (query halves), 8-11 dQ WG (TMEM -> red.global.add),
-// 12 TMA producer, 13 TMEM allocator + MMA issuer.
+// 12 TMA producer, 13 TMEM allocator + S/dP MMA issuer, 14 dV/dK/dQ MMA issuer.
 #include <cuda_bf16.h>
 #include <cmath>
 
@@ -46,6 +43,10 @@ namespace fm { __device__ long long g_fm_trace[64 * 16]; }
   } while (0)
 #endif
 
+#ifndef FM_EXP
+#define FM_EXP 0  // experiments only: 1 = compute WGs skip TMEM/math/smem work
+#endif
+
 #ifndef FM_DQ_MODE
 #define FM_DQ_MODE 0  // experiments only: nonzero = skip the dQ global reduction
 #endif
@@ -54,21 +55,22 @@ namespace fm {
 
 namespace bwd {
 
-constexpr int NT = 448;
-constexpr int QST = 4;
+constexpr int NT = 480;
+constexpr int QST = 3;
 constexpr int kMaxTrb = 4096;
 
 template <int D>
 struct Cfg {
   static constexpr int BR = (D == 128) ? 64 : 128;
   static constexpr bool DQT = (D == 128);          // dQ computed transposed (M = d)
-  static constexpr bool KA_TMEM = (D == 128);      // K_j held in TMEM as the A operand of S^T
+  static constexpr bool KA_TMEM = false;           // K_j in TMEM as S^T's A operand (measured: no gain)
+  static constexpr bool DQ_ALIAS = (D == 64);      // dQ shares the P/dS columns (TMEM is full at d=64)
   static constexpr int KV_TILE = 128 * D * 2;      // bytes
   static constexpr int Q_TILE = BR * D * 2;
   static constexpr int DS_BYTES = 128 * BR * 2;
   static constexpr int CH_PER_WG = BR / 64;        // 32-query chunks per compute WG
   static constexpr int S_COL = 0, DP_COL = BR, P_COL = 2 * BR, DS_COL = 2 * BR + BR / 2;
-  static constexpr int DQ_COL = P_COL;             // dQ(t) overwrites P/dS(t) after dV/dK(t) read them
+  static constexpr int DQ_COL = DQ_ALIAS ? P_COL : 192;
   static constexpr int KA_COL = 192;
   static constexpr int DV_COL = (D == 128) ? 256 : 384;
   static constexpr int DK_COL = DV_COL + D;
@@ -81,14 +83,14 @@ struct Smem {
   uint8_t v[C::KV_TILE];
   uint8_t q[QST][C::Q_TILE];
   uint8_t dO[QST][C::Q_TILE];
-  uint8_t ds[C::DS_BYTES];
+  uint8_t ds[2][C::DS_BYTES];  // double-buffered: dS(t+1) is written while dQ(t) reads dS(t)
   float lvec[QST][C::BR];
   float dvec[QST][C::BR];
   uint16_t list[kMaxTrb];
   uint32_t part_bits[kMaxTrb / 32];
   uint64_t kv_full;
   uint64_t q_full[QST], q_empty[QST];
-  uint64_t s_full, sdp_free, p_full, dq_full, dq_empty, ds_empty, ka_full, done;
+  uint64_t s_full, sdp_free, p_full, pds_free, dq_full, dq_empty, ds_empty[2], ka_full, done;
   uint32_t tmem_base;
   int n_entries;
   int warp_cnt[NT / 32];
@@ -156,9 +158,11 @@ __global__ void __launch_bounds__(bwd::NT, 1)
     mbar_init(&sm.sdp_free, 256);
     mbar_init(&sm.p_full, 256);
     mbar_init(&sm.ka_full, 128);
+    mbar_init(&sm.pds_free, 1);
     mbar_init(&sm.dq_full, 1);
     mbar_init(&sm.dq_empty, 128);
-    mbar_init(&sm.ds_empty, 1);
+    mbar_init(&sm.ds_empty[0], 1);
+    mbar_init(&sm.ds_empty[1], 1);
     mbar_init(&sm.done, 1);
     fence_barrier_init();
   }
@@ -225,76 +229,85 @@ __global__ void __launch_bounds__(bwd::NT, 1)
         bulk_g2s(sm.dvec[st], a.dvec + bh * a.Npb + static_cast<size_t>(i) * BR, BR * 4, &sm.q_full[st]);
       }
     }
-  } else if (warp == 13) {
-    // ================================ MMA issuer ================================
+  } else if (warp == 13 || warp == 14) {
+    // ============================ two MMA issuers ============================
+    // The tensor core accepts only a few queued MMAs before an issuing thread blocks, so any
+    // dependency wait in a single issuer starves it.  Warp 13 issues S^T/dP^T(t) as soon as the
+    // compute WGs have released tile t-1; warp 14 issues dV/dK/dQ(t) once P/dS(t) are ready.
+    // Each warp commits only to barriers that track its own MMAs.
     if (lane == 0 && nE > 0) {
       constexpr uint32_t ID_S = idesc_bf16(128, BR, 0, 0);   // S^T, dP^T: A, B K-major
       constexpr uint32_t ID_G = idesc_bf16(128, D, 0, 1);    // dV, dK: A in TMEM, B MN-major
       constexpr uint32_t ID_Q = idesc_bf16(128, 64, 1, 1);   // dQ^T (d=128) / dQ (d=64), both MN-major
-      const uint32_t k_addr = smem_u32(sm.k), v_addr = smem_u32(sm.v), ds_addr = smem_u32(sm.ds);
-      auto issue_sdp = [&](int t) {
-        const int st = t % QST;
-        mbar_wait(&sm.q_full[st], (t / QST) & 1);
-        FM_T(14, t - 1);
-        tc_fence_after();
-        const uint32_t q_addr = smem_u32(sm.q[st]), do_addr = smem_u32(sm.dO[st]);
-#pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk) {
-          const uint32_t ao = (kk >> 2) * 16384 + (kk & 3) * 32;
-          const uint32_t bo = (kk >> 2) * (BR * 128) + (kk & 3) * 32;
-          if constexpr (C::KA_TMEM)
-            mma_ts(tbase + C::S_COL, tbase + C::KA_COL + kk * 8, sdesc_sw128(q_addr + bo, 16, 1024), ID_S,
-                   kk > 0 ? 1u : 0u);
-          else
-            mma_ss(tbase + C::S_COL, sdesc_sw128(k_addr + ao, 16, 1024), sdesc_sw128(q_addr + bo, 16, 1024), ID_S,
-                   kk > 0 ? 1u : 0u);
-          mma_ss(tbase + C::DP_COL, sdesc_sw128(v_addr + ao, 16, 1024), sdesc_sw128(do_addr + bo, 16, 1024), ID_S,
-                 kk > 0 ? 1u : 0u);
-        }
-        mma_commit(&sm.s_full);
-      };
+      const uint32_t k_addr = smem_u32(sm.k), v_addr = smem_u32(sm.v);
       mbar_wait(&sm.kv_full, 0);
-      if constexpr (C::KA_TMEM) mbar_wait(&sm.ka_full, 0);  // K_j copied into TMEM
-      issue_sdp(0);
-      for (int t = 0; t < nE; ++t) {
-        const int st = t % QST;
-        FM_T(0, t);
-        if (t + 1 < nE) {
-          mbar_wait(&sm.sdp_free, t & 1);  // compute WGs hold S^T/dP^T(t) in registers
+      if (warp == 13) {
+        if constexpr (C::KA_TMEM) mbar_wait(&sm.ka_full, 0);  // K_j copied into TMEM
+        for (int t = 0; t < nE; ++t) {
+          const int st = t % QST;
+          if (t > 0) mbar_wait(&sm.sdp_free, (t - 1) & 1);  // compute WGs hold S^T/dP^T(t-1) in registers
           FM_T(1, t);
-          issue_sdp(t + 1);
+          mbar_wait(&sm.q_full[st], (t / QST) & 1);
+          FM_T(14, t);
+          tc_fence_after();
+          const uint32_t q_addr = smem_u32(sm.q[st]), do_addr = smem_u32(sm.dO[st]);
+#pragma unroll
+          for (int kk = 0; kk < D / 16; ++kk) {
+            const uint32_t ao = (kk >> 2) * 16384 + (kk & 3) * 32;
+            const uint32_t bo = (kk >> 2) * (BR * 128) + (kk & 3) * 32;
+            if constexpr (C::KA_TMEM)
+              mma_ts(tbase + C::S_COL, tbase + C::KA_COL + kk * 8, sdesc_sw128(q_addr + bo, 16, 1024), ID_S,
+                     kk > 0 ? 1u : 0u);
+            else
+              mma_ss(tbase + C::S_COL, sdesc_sw128(k_addr + ao, 16, 1024), sdesc_sw128(q_addr + bo, 16, 1024), ID_S,
+                     kk > 0 ? 1u : 0u);
+            mma_ss(tbase + C::DP_COL, sdesc_sw128(v_addr + ao, 16, 1024), sdesc_sw128(do_addr + bo, 16, 1024), ID_S,
+                   kk > 0 ? 1u : 0u);
+          }
+          mma_commit(&sm.s_full);
           FM_T(11, t);
         }
-        mbar_wait(&sm.p_full, t & 1);
-        FM_T(2, t);
-        tc_fence_after();
-        const uint32_t q_addr = smem_u32(sm.q[st]), do_addr = smem_u32(sm.dO[st]);
+      } else {
+        for (int t = 0; t < nE; ++t) {
+          const int st = t % QST;
+          FM_T(0, t);
+          mbar_wait(&sm.p_full, t & 1);
+          FM_T(2, t);
+          tc_fence_after();
+          const uint32_t q_addr = smem_u32(sm.q[st]), do_addr = smem_u32(sm.dO[st]);
 #pragma unroll
-        for (int kk = 0; kk < BR / 16; ++kk) {
-          const uint32_t acc = (t > 0 || kk > 0) ? 1u : 0u;
-          mma_ts(tbase + C::DV_COL, tbase + C::P_COL + kk * 8, sdesc_sw128(do_addr + kk * 2048, BR * 128, 1024), ID_G,
-                 acc);
-          mma_ts(tbase + C::DK_COL, tbase + C::DS_COL + kk * 8, sdesc_sw128(q_addr + kk * 2048, BR * 128, 1024), ID_G,
-                 acc);
-        }
-        mma_commit(&sm.q_empty[st]);
-        FM_T(12, t);
-        // dQ(t) overwrites the P/dS columns: issued after dV/dK(t) (in-order), and the dQ WG has
-        // read dQ(t-1) before the compute WGs stored P/dS(t) (they waited dq_empty(t-1)).
+          for (int kk = 0; kk < BR / 16; ++kk) {
+            const uint32_t acc = (t > 0 || kk > 0) ? 1u : 0u;
+            mma_ts(tbase + C::DV_COL, tbase + C::P_COL + kk * 8, sdesc_sw128(do_addr + kk * 2048, BR * 128, 1024),
+                   ID_G, acc);
+            mma_ts(tbase + C::DK_COL, tbase + C::DS_COL + kk * 8, sdesc_sw128(q_addr + kk * 2048, BR * 128, 1024),
+                   ID_G, acc);
+          }
+          // S^T/dP^T(t) (warp 13) completed before the compute WGs produced P/dS(t)
+          mma_commit(&sm.q_empty[st]);
+          mma_commit(&sm.pds_free);
+          FM_T(12, t);
+          // d=64: dQ(t) overwrites the P/dS columns — issued after dV/dK(t) by this thread (in
+          // order), and the compute WGs stored P/dS(t) only after dQ(t-1) was read (dq_empty).
+          // d=128: dQ^T has its own columns; wait until the dQ WG has read dQ^T(t-1).
+          if constexpr (!C::DQ_ALIAS) mbar_wait(&sm.dq_empty, (t & 1) ^ 1);
+          tc_fence_after();
+          const uint32_t ds_addr = smem_u32(sm.ds[t & 1]);
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {
-          if constexpr (C::DQT)
-            mma_ss(tbase + C::DQ_COL, sdesc_sw128(k_addr + kk * 2048, 16384, 1024),
-                   sdesc_sw128(ds_addr + kk * 2048, 16384, 1024), ID_Q, kk > 0 ? 1u : 0u);
-          else
-            mma_ss(tbase + C::DQ_COL, sdesc_sw128(ds_addr + kk * 2048, 16384, 1024),
-                   sdesc_sw128(k_addr + kk * 2048, 16384, 1024), ID_Q, kk > 0 ? 1u : 0u);
+          for (int kk = 0; kk < 8; ++kk) {
+            if constexpr (C::DQT)
+              mma_ss(tbase + C::DQ_COL, sdesc_sw128(k_addr + kk * 2048, 16384, 1024),
+                     sdesc_sw128(ds_addr + kk * 2048, 16384, 1024), ID_Q, kk > 0 ? 1u : 0u);
+            else
+              mma_ss(tbase + C::DQ_COL, sdesc_sw128(ds_addr + kk * 2048, 16384, 1024),
+                     sdesc_sw128(k_addr + kk * 2048, 16384, 1024), ID_Q, kk > 0 ? 1u : 0u);
+          }
+          mma_commit(&sm.dq_full);
+          mma_commit(&sm.ds_empty[t & 1]);
+          FM_T(13, t);
         }
-        mma_commit(&sm.dq_full);
-        mma_commit(&sm.ds_empty);
-        FM_T(13, t);
+        mma_commit(&sm.done);  // all S^T/dP^T completed earlier (they precede every p_full)
       }
-      mma_commit(&sm.done);
     }
   } else if (warp < 8) {
     // ====================== compute WGs (thread = key, WG = query half) ======================
@@ -338,6 +351,15 @@ __global__ void __launch_bounds__(bwd::NT, 1)
       const float* lv = sm.lvec[st];
       const float* dv = sm.dvec[st];
       uint32_t pp[CH][16], dp[CH][16];
+      if (FM_EXP == 1) {
+        tc_fence_before();
+        mbar_arrive(&sm.sdp_free);
+        mbar_wait(&sm.ds_empty[t & 1], ((t >> 1) & 1) ^ 1);
+        mbar_wait(&sm.dq_empty, (t & 1) ^ 1);
+        tc_fence_before();
+        mbar_arrive(&sm.p_full);
+        continue;
+      }
 #pragma unroll
       for (int ch = 0; ch < CH; ++ch) {
         const int q0 = (wg * CH + ch) * 32;  // first query of this chunk within the row tile
@@ -355,18 +377,9 @@ __global__ void __launch_bounds__(bwd::NT, 1)
           pds_chunk<false, CAUSAL>(sr, dr, lv + q0, dv + q0, sl2, i * BR + q0, key, mv, pp[ch], dp[ch]);
       }
       if (tid == 0) FM_T(5, t);
-      // P / dS TMEM columns free: dQ(t-1), which reuses them, has been read out
-      mbar_wait(&sm.dq_empty, (t & 1) ^ 1);
-      if (tid == 0) FM_T(6, t);
-      tc_fence_after();
-#pragma unroll
-      for (int ch = 0; ch < CH; ++ch) {
-        const int q0 = (wg * CH + ch) * 32;
-        tmem_st16(tbase + lane_off + C::P_COL + q0 / 2, pp[ch]);
-        tmem_st16(tbase + lane_off + C::DS_COL + q0 / 2, dp[ch]);
-      }
       // dS^T row of this key into the SW128 MN-major smem operand of the dQ GEMM
-      mbar_wait(&sm.ds_empty, (t & 1) ^ 1);
+      // (first: it only needs dQ(t-1) to have finished reading the buffer)
+      mbar_wait(&sm.ds_empty[t & 1], ((t >> 1) & 1) ^ 1);  // dQ(t-2) has read this buffer
       if (tid == 0) FM_T(7, t);
 #pragma unroll
       for (int ch = 0; ch < CH; ++ch) {
@@ -375,10 +388,23 @@ __global__ void __launch_bounds__(bwd::NT, 1)
         for (int u = 0; u < 4; ++u) {
           const int g = (q0 >> 3) + u;  // 8-query group
           const int sub = g >> 3, gg = g & 7;
-          uint8_t* dst = sm.ds + sub * 16384 + key_t * 128 + ((gg ^ (key_t & 7)) << 4);
+          uint8_t* dst = sm.ds[t & 1] + sub * 16384 + key_t * 128 + ((gg ^ (key_t & 7)) << 4);
           *reinterpret_cast<uint4*>(dst) =
               make_uint4(dp[ch][4 * u], dp[ch][4 * u + 1], dp[ch][4 * u + 2], dp[ch][4 * u + 3]);
         }
+      }
+      // P / dS TMEM columns free: dV/dK(t-1) done (d=64: dQ(t-1), which reuses them, read out)
+      if constexpr (C::DQ_ALIAS)
+        mbar_wait(&sm.dq_empty, (t & 1) ^ 1);
+      else
+        mbar_wait(&sm.pds_free, (t & 1) ^ 1);
+      if (tid == 0) FM_T(6, t);
+      tc_fence_after();
+#pragma unroll
+      for (int ch = 0; ch < CH; ++ch) {
+        const int q0 = (wg * CH + ch) * 32;
+        tmem_st16(tbase + lane_off + C::P_COL + q0 / 2, pp[ch]);
+        tmem_st16(tbase + lane_off + C::DS_COL + q0 / 2, dp[ch]);
       }
       fence_proxy_async_smem();
       tmem_wait_st();
