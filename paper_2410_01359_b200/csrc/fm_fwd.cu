@@ -15,9 +15,26 @@
 // TMEM columns: S0 [0,128)  S1 [128,256)  O0 [256,256+D)  O1 [256+D, 256+2D).
 #include <cuda_bf16.h>
 #include <cmath>
+#include <type_traits>
 
 #include "fm_internal.h"
 #include "fm_ptx.cuh"
+
+#ifdef FM_TRACE
+namespace fm { __device__ long long g_fm_trace_fwd[64 * 16]; }
+#define FT(slot, e)                                                                                   \
+  do {                                                                                                 \
+    if (blockIdx.x == 64 && blockIdx.y == 0 && blockIdx.z == 0 && (e) < 64) fm::g_fm_trace_fwd[(e) * 16 + (slot)] = clock64(); \
+  } while (0)
+#else
+#define FT(slot, e) \
+  do {              \
+  } while (0)
+#endif
+
+#ifndef FM_POLY_PAIRS
+#define FM_POLY_PAIRS 3  // of every 8 column pairs, how many use the FMA-pipe exp2 (rest: MUFU)
+#endif
 
 namespace fm {
 
@@ -166,6 +183,7 @@ __global__ void __launch_bounds__(fwd::NT, 1)
       auto issue_pv = [&](int q) {
         const int pe = pend[q];
         mbar_wait(&sm.p_full[q], pv_cnt[q] & 1);
+        FT(4 + q, pe);
         const int vs = pe % VST;
         mbar_wait(&sm.v_full[vs], (pe / VST) & 1);
         tc_fence_after();
@@ -189,6 +207,7 @@ __global__ void __launch_bounds__(fwd::NT, 1)
         const uint32_t ent = sm.list[e];
         const int ks = e % KST;
         mbar_wait(&sm.k_full[ks], (e / KST) & 1);
+        FT(8, e);
         tc_fence_after();
         const uint32_t k_addr = smem_u32(sm.k[ks]);
 #pragma unroll
@@ -202,6 +221,7 @@ __global__ void __launch_bounds__(fwd::NT, 1)
                      kk > 0 ? 1u : 0u);
             }
             mma_commit(&sm.s_full[q]);
+            FT(6 + q, e);
             pend[q] = e;
           }
         }
@@ -233,35 +253,48 @@ __global__ void __launch_bounds__(fwd::NT, 1)
       if (cls != 0) {
         const int j = static_cast<int>(ent & 0xFFFFFFu);
         mbar_wait(&sm.s_full[q], cnt & 1);
+        if (row_t == 0) FT(0 + q, e);
         tc_fence_after();
-        uint32_t sr[128];
+        // Pass 1: row max over the 128 columns, 32 at a time from TMEM (S stays in TMEM and is
+        // re-read in pass 2, which keeps register pressure low).  On PARTIAL tiles the element
+        // mask (Alg. 1 lines 15-21) is evaluated here once and kept as 4 x 32 bits.
+        uint32_t mbits[4] = {0u, 0u, 0u, 0u};
+        float mx0 = -INFINITY, mx1 = -INFINITY, mx2 = -INFINITY, mx3 = -INFINITY;
+        uint32_t sr[2][32];
+        tmem_ld32(tS, sr[0]);
 #pragma unroll
-        for (int c = 0; c < 4; ++c) tmem_ld32(tS + c * 32, sr + c * 32);
-        tmem_wait_ld();
-        float* s = reinterpret_cast<float*>(sr);
-        if (cls == 1) {
-          const int4* mk = sm.mask[ms];
-          const int y0 = j * 128;
+        for (int c = 0; c < 4; ++c) {
+          tmem_wait_ld();
+          if (c + 1 < 4) tmem_ld32(tS + (c + 1) * 32, sr[(c + 1) & 1]);
+          float* sv = reinterpret_cast<float*>(sr[c & 1]);
+          if (cls == 1) {
+            const int4* mk = sm.mask[ms] + c * 32;
+            const int y0 = j * 128 + c * 32;
+            uint32_t bits = 0u;
 #pragma unroll
-          for (int c = 0; c < 128; ++c) {
-            const int4 mv = mk[c];
-            bool msk = static_cast<unsigned>(row - mv.x) < static_cast<unsigned>(mv.y - mv.x);
-            if constexpr (CAUSAL)
-              msk |= row < y0 + c;
-            else
-              msk |= static_cast<unsigned>(row - mv.z) < static_cast<unsigned>(mv.w - mv.z);
-            s[c] = msk ? -INFINITY : s[c];
+            for (int t = 0; t < 32; ++t) {
+              const int4 mv = mk[t];
+              bool msk = static_cast<unsigned>(row - mv.x) < static_cast<unsigned>(mv.y - mv.x);
+              if constexpr (CAUSAL)
+                msk |= row < y0 + t;
+              else
+                msk |= static_cast<unsigned>(row - mv.z) < static_cast<unsigned>(mv.w - mv.z);
+              bits |= (msk ? 1u : 0u) << t;
+              sv[t] = msk ? -INFINITY : sv[t];
+            }
+            mbits[c] = bits;
+          }
+#pragma unroll
+          for (int t = 0; t < 32; t += 8) {
+            mx0 = fmax3(mx0, sv[t], sv[t + 1]);
+            mx1 = fmax3(mx1, sv[t + 2], sv[t + 3]);
+            mx2 = fmax3(mx2, sv[t + 4], sv[t + 5]);
+            mx3 = fmax3(mx3, sv[t + 6], sv[t + 7]);
           }
         }
-        float mx0 = s[0], mx1 = s[1], mx2 = s[2], mx3 = s[3];
-#pragma unroll
-        for (int c = 4; c < 128; c += 4) {
-          mx0 = fmaxf(mx0, s[c]);
-          mx1 = fmaxf(mx1, s[c + 1]);
-          mx2 = fmaxf(mx2, s[c + 2]);
-          mx3 = fmaxf(mx3, s[c + 3]);
-        }
+        if (row_t == 0 && q == 0) FT(9, e);
         const float m_tile = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3)) * sl2;
+        if (row_t == 0 && q == 0) FT(10, e);
         // Conditional rescale: the running max only moves when it grows by more than 2^8
         // (exact: P is computed against the same m that scales l and O).  The decision is
         // made per warp so the TMEM accesses stay warp-collective.
@@ -283,23 +316,65 @@ __global__ void __launch_bounds__(fwd::NT, 1)
             tmem_st32(tO + c * 32, ov);
           }
         }
+        if (row_t == 0 && q == 0) FT(11, e);
         const float m_use = (m_used == -INFINITY) ? 0.f : m_used;
-        float ls0 = 0.f, ls1 = 0.f;
-        uint32_t pk[64];
+        // P = exp2(S*scale*log2e - m): packed FFMA2 for the argument; 5 of every 8 pairs on the
+        // MUFU (ex2.approx), 3 of 8 on the FMA pipe (exp2_poly2) so that neither unit alone
+        // bounds the tile; row sums with packed FADD2.
+        const uint64_t sl2x2 = f2pack(sl2, sl2), negm2 = f2pack(-m_use, -m_use);
+        uint64_t acc[4] = {0ull, 0ull, 0ull, 0ull};
+        // Pass 2: re-read S in 32-column chunks (prefetching the next), apply the kept mask bits,
+        // exponentiate and write the packed bf16 P of each chunk straight back to TMEM (it lands
+        // on S columns already consumed by this pass).
+        auto pass2 = [&](auto partial_tag) {
+          constexpr bool PART = decltype(partial_tag)::value;
+          tmem_ld32(tS, sr[0]);
 #pragma unroll
-        for (int c = 0; c < 128; c += 2) {
-          const float p0 = ex2(fmaf(s[c], sl2, -m_use));
-          const float p1 = ex2(fmaf(s[c + 1], sl2, -m_use));
-          ls0 += p0;
-          ls1 += p1;
-          pk[c >> 1] = pack_bf16(p0, p1);
+          for (int ch = 0; ch < 4; ++ch) {
+            tmem_wait_ld();
+            if (ch + 1 < 4) tmem_ld32(tS + (ch + 1) * 32, sr[(ch + 1) & 1]);
+            const float* sv = reinterpret_cast<const float*>(sr[ch & 1]);
+            uint32_t pk[16];
+#pragma unroll
+            for (int kk = 0; kk < 16; ++kk) {
+              const int k = ch * 16 + kk;
+              float a0 = sv[2 * kk], a1 = sv[2 * kk + 1];
+              if constexpr (PART) {
+                a0 = ((mbits[ch] >> (2 * kk)) & 1u) ? -INFINITY : a0;
+                a1 = ((mbits[ch] >> (2 * kk + 1)) & 1u) ? -INFINITY : a1;
+              }
+              const uint64_t x2 = f2fma(f2pack(a0, a1), sl2x2, negm2);
+              float p0, p1;
+              if ((k & 7) >= 8 - FM_POLY_PAIRS) {
+                exp2_poly2(x2, p0, p1);
+              } else {
+                float x0, x1;
+                f2unpack(x2, x0, x1);
+                p0 = ex2(x0);
+                p1 = ex2(x1);
+              }
+              acc[k & 3] = f2add(acc[k & 3], f2pack(p0, p1));
+              pk[kk] = pack_bf16(p0, p1);
+            }
+            tmem_st16(tS + ch * 16, pk);
+          }
+        };
+        if (cls == 1)
+          pass2(std::true_type{});
+        else
+          pass2(std::false_type{});
+        {
+          const uint64_t a01 = f2add(acc[0], acc[1]), a23 = f2add(acc[2], acc[3]);
+          float u0, u1;
+          f2unpack(f2add(a01, a23), u0, u1);
+          l += u0 + u1;
         }
-        l += ls0 + ls1;
-#pragma unroll
-        for (int c = 0; c < 4; ++c) tmem_st16(tS + c * 16, pk + c * 16);
+        if (row_t == 0 && q == 0) FT(12, e);
         tmem_wait_st();
+        if (row_t == 0 && q == 0) FT(13, e);
         tc_fence_before();
         mbar_arrive(&sm.p_full[q]);
+        if (row_t == 0) FT(2 + q, e);
         ++cnt;
       }
       __syncwarp();
@@ -376,3 +451,9 @@ cudaError_t launch_fwd(const Dims& d, const CUtensorMap& tq, const CUtensorMap& 
 }
 
 }  // namespace fm
+
+#ifdef FM_TRACE
+extern "C" __attribute__((visibility("default"))) int flashmask_debug_trace_fwd(long long* host) {
+  return cudaMemcpyFromSymbol(host, fm::g_fm_trace_fwd, sizeof(long long) * 64 * 16) == cudaSuccess ? 0 : 1;
+}
+#endif

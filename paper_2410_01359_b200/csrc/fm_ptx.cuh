@@ -203,6 +203,57 @@ FM_DEV float ex2(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+FM_DEV float fmax3(float a, float b, float c) {
+  float d;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
+// Packed fp32x2 arithmetic (Blackwell FFMA2 / FADD2 / FMUL2): one instruction, two lanes.
+FM_DEV uint64_t f2pack(float lo, float hi) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+FM_DEV void f2unpack(uint64_t v, float& lo, float& hi) { asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v)); }
+FM_DEV uint64_t f2fma(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t r;
+  asm("fma.rn.ftz.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+FM_DEV uint64_t f2add(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("add.rn.ftz.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+FM_DEV uint64_t f2mul(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("mul.rn.ftz.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+// 2^x for a pair on the FMA/ALU pipes instead of the MUFU: x = n + f with n = rint(x) via the
+// 1.5*2^23 magic-number add, 2^f by a degree-3 minimax polynomial on [-1/2, 1/2]
+// (max rel. error 1.1e-4, below the bf16 rounding P is stored with), 2^n by adding n to the
+// exponent field.  x <= -127 (incl. -inf) returns exactly +0 (ex2.approx.ftz flushes below
+// -126; in between this returns a denormal, a difference far below the bf16 rounding of P).
+FM_DEV void exp2_poly2(uint64_t x2, float& r0, float& r1) {
+  float x0, x1;
+  f2unpack(x2, x0, x1);
+  // clamp: -inf (masked) and anything below -127 become -127, whose result below is exactly +0
+  x2 = f2pack(fmaxf(x0, -127.f), fmaxf(x1, -127.f));
+  const uint64_t t = f2add(x2, f2pack(12582912.f, 12582912.f));
+  const uint64_t n = f2add(t, f2pack(-12582912.f, -12582912.f));
+  const uint64_t f = f2fma(n, f2pack(-1.f, -1.f), x2);
+  uint64_t p = f2fma(f2pack(0.0546542853f, 0.0546542853f), f, f2pack(0.242217956f, 0.242217956f));
+  p = f2fma(p, f, f2pack(0.693356001f, 0.693356001f));
+  p = f2fma(p, f, f2pack(1.f, 1.f));
+  float t0, t1, p0, p1;
+  f2unpack(t, t0, t1);
+  f2unpack(p, p0, p1);
+  // 2^n * p: n sits in the low mantissa bits of t, so (bits(t) << 23) == n << 23 (mod 2^32).
+  // For x = -127: p = 1.0 = 0x3F800000 = 127 << 23, so the sum is exactly 0.
+  r0 = __int_as_float(__float_as_int(p0) + (__float_as_int(t0) << 23));
+  r1 = __int_as_float(__float_as_int(p1) + (__float_as_int(t1) << 23));
+}
 FM_DEV uint32_t pack_bf16(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&v);
