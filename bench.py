@@ -175,6 +175,16 @@ def effective_flops(call, fm):
     return fwd, 2.5 * fwd, rho
 
 
+def reduce_max_over_ranks(x: float, dist=None, device="cpu") -> float:
+    """Max of a per-rank scalar (timings are reported as the slowest rank).  NCCL on the GPU
+    path, gloo in the CPU tests; the only collective bench.py issues besides barriers."""
+    if dist is None or not dist.is_initialized():
+        return x
+    t = torch.tensor([x], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 class ClockSampler:
     FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
@@ -323,11 +333,7 @@ def main():
         torch.cuda.synchronize()
 
     def max_over_ranks(x):
-        if dist is None:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
+        return reduce_max_over_ranks(x, dist, dev)
 
     for _ in range(args.warmup):
         step()
