@@ -397,6 +397,10 @@ def main():
     value = world * (F_fwd + F_bwd) / (ms_step * 1e-3) / 1e12
     peaks, peak_src = load_peaks()
     peak_sust = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", f"traffic_{args.config}.json")
+    if os.path.exists(tpath):
+        traffic = json.load(open(tpath)).get("fm_bwd_kernel_bytes_per_launch")
     k_bwd_ms, k_bwd_n = ktimes["bwd"]
     k_fwd_ms, k_fwd_n = ktimes["fwd"]
     bwd_tf = F_bwd * args.steps / (k_bwd_ms * 1e-3) / 1e12 if k_bwd_ms > 0 else None
@@ -425,7 +429,8 @@ def main():
             "kernels_ms_per_step": {k: round(v[0] / args.steps, 4) for k, v in ktimes.items()},
             "roofline": {"kernel": "fm_bwd_kernel (K4)", "bound": "tensor",
                          "achieved": round(bwd_tf, 2) if bwd_tf else None, "peak": peak_sust, "unit": "TFLOP/s",
-                         "frac": round(bwd_tf / peak_sust, 4) if bwd_tf else None, "traffic": None,
+                         "frac": round(bwd_tf / peak_sust, 4) if bwd_tf else None, "traffic": traffic,
+                         "traffic_unit": "bytes per launch (dram read+write, ncu --set full)",
                          "algorithmic": "10*128^2*d FLOPs per non-SKIP 128x128 tile (SURVEY d.5)"},
             "e2e": e2e, "gpu_launches": launches, "clocks": clk, "cpu_baseline": cpu,
         }
