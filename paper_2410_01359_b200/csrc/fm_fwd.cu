@@ -1,15 +1,15 @@
 // fm_fwd.cu — K2: FlashMask forward (Alg. 1) for sm_100a.
 //
 // One CTA owns a pair of 128-row query tiles (Q0, Q1) of one (batch, head).  Warp roles:
-//   warps 0-3  softmax WG0  (thread = one row of Q0 = one TMEM lane)
-//   warps 4-7  softmax WG1  (rows of Q1)
-//   warp  8    TMA producer (lane 0): Q once, then K_j, V_j and the mask slice of tile j
-//   warp  9    TMEM allocator + tcgen05 MMA issuer (lane 0)
+//   warps 0-7   softmax of Q0: two warpgroups, each one half (64) of the key columns
+//   warps 8-15  softmax of Q1  (thread = one row = one TMEM lane)
+//   warp  16    TMA producer (lane 0): Q once, then K_j, V_j and the mask slice of tile j
+//   warp  17    TMEM allocator + tcgen05 MMA issuer (lane 0)
 // The visit list — the column tiles j that are not SKIP for Q0 or Q1 — is built from the
 // K1 class map before the roles split, so fully masked tiles issue no load and no MMA
 // (Alg. 1 lines 9-14).  S_q = Q_q K_j^T (tcgen05, fp32 in TMEM), softmax in
 // registers with the element-wise interval mask applied only on PARTIAL tiles (Alg. 1
-// lines 15-21), P_q written back to TMEM as bf16 (aliasing S_q) and
+// lines 15-21), P_q written back to TMEM as bf16 (aliasing consumed S_q columns) and
 // O_q += P_q V_j issued with P as the TMEM A operand.  The two query tiles ping-pong: while
 // one WG runs its softmax the tensor core computes the other tile's S / PV.
 // TMEM columns: S0 [0,128)  S1 [128,256)  O0 [256,256+D)  O1 [256+D, 256+2D).
@@ -40,7 +40,7 @@ namespace fm {
 
 namespace fwd {
 
-constexpr int NT = 320;
+constexpr int NT = 576;   // 16 softmax warps + TMA producer + MMA issuer
 constexpr int KST = 2, VST = 2, MST = 4;
 
 template <int D>
@@ -55,10 +55,14 @@ struct Smem {
   uint64_t k_full[KST], k_empty[KST], v_full[VST], v_empty[VST];
   uint64_t m_full[MST], m_empty[MST];
   uint64_t s_full[2], p_full[2], o_full[2];
+  float xmax[2][2][2][128];  // [tile][parity][column half][row]: row-max exchange between halves
+  float xsum[2][2][128];     // [tile][column half][row]: final row-sum exchange
   uint32_t tmem_base;
   int n_entries;
   int warp_cnt[NT / 32];
 };
+
+constexpr int PRODUCER_WARP = 16, MMA_WARP = 17;
 
 __device__ __forceinline__ int ent_cls(uint32_t ent, int q) { return (ent >> (24 + 2 * q)) & 3; }
 
@@ -83,19 +87,19 @@ __global__ void __launch_bounds__(fwd::NT, 1)
   const size_t bhm = static_cast<size_t>(b) * a.Hm + hm;
 
   // ---- setup: barriers (warp 8), TMEM (warp 9) ----
-  if (warp == 8 && lane == 0) {
+  if (warp == PRODUCER_WARP && lane == 0) {
     mbar_init(&sm.bar_q, 1);
     for (int s = 0; s < KST; ++s) { mbar_init(&sm.k_full[s], 1); mbar_init(&sm.k_empty[s], 1); }
     for (int s = 0; s < VST; ++s) { mbar_init(&sm.v_full[s], 1); mbar_init(&sm.v_empty[s], 1); }
-    for (int s = 0; s < MST; ++s) { mbar_init(&sm.m_full[s], 1); mbar_init(&sm.m_empty[s], 8); }
+    for (int s = 0; s < MST; ++s) { mbar_init(&sm.m_full[s], 1); mbar_init(&sm.m_empty[s], 16); }
     for (int q = 0; q < 2; ++q) {
       mbar_init(&sm.s_full[q], 1);
-      mbar_init(&sm.p_full[q], 128);
+      mbar_init(&sm.p_full[q], 256);
       mbar_init(&sm.o_full[q], 1);
     }
     fence_barrier_init();
   }
-  if (warp == 9) tmem_alloc<512>(&sm.tmem_base);
+  if (warp == MMA_WARP) tmem_alloc<512>(&sm.tmem_base);
 
   // ---- visit list: union of the non-SKIP column tiles of Q0 and Q1 (K1 class map) ----
   {
@@ -133,7 +137,7 @@ __global__ void __launch_bounds__(fwd::NT, 1)
   const int nE = sm.n_entries;
   const uint32_t tbase = sm.tmem_base;
 
-  if (warp == 8) {
+  if (warp == PRODUCER_WARP) {
     // ================================ TMA producer ================================
     if (lane == 0) {
       tma_prefetch_desc(&tmQ);
@@ -170,8 +174,11 @@ __global__ void __launch_bounds__(fwd::NT, 1)
         for (int c = 0; c < D / 64; ++c) tma_load_4d(sm.v[vs] + c * 16384, &tmV, &sm.v_full[vs], c * 64, h, j * 128, b);
       }
     }
-  } else if (warp == 9) {
+  } else if (warp == MMA_WARP) {
     // ================================ MMA issuer ================================
+    // One issuer for both tiles, in the order PV0(e-1), S0(e), PV1(e-1), S1(e): this keeps the
+    // two tiles' softmax phases staggered (ping-pong).  Two independent issuers were measured
+    // to fall into lock-step and lose ~30 %.
     if (lane == 0) {
       constexpr uint32_t ID_S = idesc_bf16(128, 128, 0, 0);  // S = Q K^T, both K-major
       constexpr uint32_t ID_PV = idesc_bf16(128, D, 0, 1);   // O += P V, V is MN-major
@@ -191,7 +198,8 @@ __global__ void __launch_bounds__(fwd::NT, 1)
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
           const uint64_t bd = sdesc_sw128(v_addr + kk * 2048, 16384, 1024);
-          mma_ts(tO[q], tS[q] + kk * 8, bd, ID_PV, (pv_cnt[q] > 0 || kk > 0) ? 1u : 0u);
+          // P of keys [0,64) sits in S columns [0,32), of keys [64,128) in S columns [64,96)
+          mma_ts(tO[q], tS[q] + kk * 8 + (kk >= 4 ? 32u : 0u), bd, ID_PV, (pv_cnt[q] > 0 || kk > 0) ? 1u : 0u);
         }
         pv_cnt[q]++;
         const uint32_t ent = sm.list[pe];
@@ -234,16 +242,24 @@ __global__ void __launch_bounds__(fwd::NT, 1)
     }
   } else {
     // ================================ softmax WGs ================================
-    const int q = warp >> 2;
+    // Four warpgroups: tile q = warp / 8, column half hh = (warp / 4) % 2.  The two halves of a
+    // tile share TMEM lanes (rows) and split the 128 key columns, exchanging row maxima (and at
+    // the end the row sums) through shared memory under a 256-thread named barrier.
+    const int q = warp >> 3;
+    const int hh = (warp >> 2) & 1;
     const int wl = warp & 3;
     const int row_t = wl * 32 + lane;
     const int row = (q == 0 ? i0 : i1) * 128 + row_t;
     const uint32_t lane_off = static_cast<uint32_t>(wl * 32) << 16;
     const uint32_t tS = tbase + lane_off + (q == 0 ? 0u : 128u);
+    const uint32_t tSh = tS + hh * 64;                      // this half's 64 S columns
+    const uint32_t tPh = tS + hh * 64;                      // its packed P (32 columns) — see MMA
     const uint32_t tO = tbase + lane_off + 256u + (q == 0 ? 0u : static_cast<uint32_t>(D));
+    const uint32_t tOh = tO + hh * (D / 2);                 // this half's O columns
     const float sl2 = a.scale_log2;
+    const uint32_t bar_id = 1 + q;
     float m_used = -INFINITY;  // running max of the scaled logits, log2 units (threshold-updated)
-    float l = 0.f;
+    float l = 0.f;             // this half's share of the row sum
     uint32_t cnt = 0;
     for (int e = 0; e < nE; ++e) {
       const uint32_t ent = sm.list[e];
@@ -253,26 +269,25 @@ __global__ void __launch_bounds__(fwd::NT, 1)
       if (cls != 0) {
         const int j = static_cast<int>(ent & 0xFFFFFFu);
         mbar_wait(&sm.s_full[q], cnt & 1);
-        if (row_t == 0) FT(0 + q, e);
+        if (row_t == 0 && hh == 0) FT(0 + q, e);
         tc_fence_after();
-        // Pass 1: row max over the 128 columns, 32 at a time from TMEM (S stays in TMEM and is
-        // re-read in pass 2, which keeps register pressure low).  On PARTIAL tiles the element
-        // mask (Alg. 1 lines 15-21) is evaluated here once and kept as 4 x 32 bits.
-        uint32_t mbits[4] = {0u, 0u, 0u, 0u};
+        // Pass 1: max over this half's 64 columns, 32 at a time (S stays in TMEM for pass 2).
+        // On PARTIAL tiles the element mask (Alg. 1 lines 15-21) is evaluated once, kept as bits.
+        uint32_t mbits[2] = {0u, 0u};
         float mx0 = -INFINITY, mx1 = -INFINITY, mx2 = -INFINITY, mx3 = -INFINITY;
-        uint32_t sr[2][32];
-        tmem_ld32(tS, sr[0]);
+        uint32_t sr[2][16];
+        tmem_ld16(tSh, sr[0]);
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
           tmem_wait_ld();
-          if (c + 1 < 4) tmem_ld32(tS + (c + 1) * 32, sr[(c + 1) & 1]);
+          if (c + 1 < 4) tmem_ld16(tSh + (c + 1) * 16, sr[(c + 1) & 1]);
           float* sv = reinterpret_cast<float*>(sr[c & 1]);
           if (cls == 1) {
-            const int4* mk = sm.mask[ms] + c * 32;
-            const int y0 = j * 128 + c * 32;
+            const int4* mk = sm.mask[ms] + hh * 64 + c * 16;
+            const int y0 = j * 128 + hh * 64 + c * 16;
             uint32_t bits = 0u;
 #pragma unroll
-            for (int t = 0; t < 32; ++t) {
+            for (int t = 0; t < 16; ++t) {
               const int4 mv = mk[t];
               bool msk = static_cast<unsigned>(row - mv.x) < static_cast<unsigned>(mv.y - mv.x);
               if constexpr (CAUSAL)
@@ -282,22 +297,25 @@ __global__ void __launch_bounds__(fwd::NT, 1)
               bits |= (msk ? 1u : 0u) << t;
               sv[t] = msk ? -INFINITY : sv[t];
             }
-            mbits[c] = bits;
+            mbits[c >> 1] |= bits << ((c & 1) * 16);
           }
 #pragma unroll
-          for (int t = 0; t < 32; t += 8) {
+          for (int t = 0; t < 16; t += 8) {
             mx0 = fmax3(mx0, sv[t], sv[t + 1]);
             mx1 = fmax3(mx1, sv[t + 2], sv[t + 3]);
             mx2 = fmax3(mx2, sv[t + 4], sv[t + 5]);
             mx3 = fmax3(mx3, sv[t + 6], sv[t + 7]);
           }
         }
-        if (row_t == 0 && q == 0) FT(9, e);
-        const float m_tile = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3)) * sl2;
-        if (row_t == 0 && q == 0) FT(10, e);
+        const float mh = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3));
+        if (row_t == 0 && q == 0 && hh == 0) FT(10, e);
+        sm.xmax[q][cnt & 1][hh][row_t] = mh;
+        named_bar_sync(bar_id, 256);
+        const float m_tile = fmaxf(mh, sm.xmax[q][cnt & 1][hh ^ 1][row_t]) * sl2;
+        if (row_t == 0 && q == 0 && hh == 0) FT(9, e);
         // Conditional rescale: the running max only moves when it grows by more than 2^8
-        // (exact: P is computed against the same m that scales l and O).  The decision is
-        // made per warp so the TMEM accesses stay warp-collective.
+        // (exact: P is computed against the same m that scales l and O).  Both halves see the
+        // same m_tile and take the same decision; the TMEM accesses stay warp-collective.
         const bool need = m_tile > m_used + 8.0f;
         float alpha = 1.0f;
         if (need) {
@@ -307,41 +325,38 @@ __global__ void __launch_bounds__(fwd::NT, 1)
         }
         if (__any_sync(0xffffffffu, need) && cnt > 0) {
 #pragma unroll 1
-          for (int c = 0; c < D / 32; ++c) {
+          for (int c = 0; c < D / 64; ++c) {
             uint32_t ov[32];
-            tmem_ld32(tO + c * 32, ov);
+            tmem_ld32(tOh + c * 32, ov);
             tmem_wait_ld();
 #pragma unroll
             for (int t = 0; t < 32; ++t) ov[t] = __float_as_uint(__uint_as_float(ov[t]) * alpha);
-            tmem_st32(tO + c * 32, ov);
+            tmem_st32(tOh + c * 32, ov);
           }
         }
-        if (row_t == 0 && q == 0) FT(11, e);
         const float m_use = (m_used == -INFINITY) ? 0.f : m_used;
-        // P = exp2(S*scale*log2e - m): packed FFMA2 for the argument; 5 of every 8 pairs on the
-        // MUFU (ex2.approx), 3 of 8 on the FMA pipe (exp2_poly2) so that neither unit alone
-        // bounds the tile; row sums with packed FADD2.
+        // Pass 2: P = exp2(S*scale*log2e - m) over this half's columns; packed FFMA2 for the
+        // argument, MUFU ex2 for most pairs and the FMA-pipe polynomial for FM_POLY_PAIRS of 8;
+        // row sums with packed FADD2; packed bf16 P written back over consumed S columns.
         const uint64_t sl2x2 = f2pack(sl2, sl2), negm2 = f2pack(-m_use, -m_use);
         uint64_t acc[4] = {0ull, 0ull, 0ull, 0ull};
-        // Pass 2: re-read S in 32-column chunks (prefetching the next), apply the kept mask bits,
-        // exponentiate and write the packed bf16 P of each chunk straight back to TMEM (it lands
-        // on S columns already consumed by this pass).
         auto pass2 = [&](auto partial_tag) {
           constexpr bool PART = decltype(partial_tag)::value;
-          tmem_ld32(tS, sr[0]);
+          tmem_ld16(tSh, sr[0]);
 #pragma unroll
           for (int ch = 0; ch < 4; ++ch) {
             tmem_wait_ld();
-            if (ch + 1 < 4) tmem_ld32(tS + (ch + 1) * 32, sr[(ch + 1) & 1]);
+            if (ch + 1 < 4) tmem_ld16(tSh + (ch + 1) * 16, sr[(ch + 1) & 1]);
             const float* sv = reinterpret_cast<const float*>(sr[ch & 1]);
-            uint32_t pk[16];
+            const uint32_t bits = PART ? (mbits[ch >> 1] >> ((ch & 1) * 16)) : 0u;
+            uint32_t pk[8];
 #pragma unroll
-            for (int kk = 0; kk < 16; ++kk) {
-              const int k = ch * 16 + kk;
+            for (int kk = 0; kk < 8; ++kk) {
+              const int k = ch * 8 + kk;
               float a0 = sv[2 * kk], a1 = sv[2 * kk + 1];
               if constexpr (PART) {
-                a0 = ((mbits[ch] >> (2 * kk)) & 1u) ? -INFINITY : a0;
-                a1 = ((mbits[ch] >> (2 * kk + 1)) & 1u) ? -INFINITY : a1;
+                a0 = ((bits >> (2 * kk)) & 1u) ? -INFINITY : a0;
+                a1 = ((bits >> (2 * kk + 1)) & 1u) ? -INFINITY : a1;
               }
               const uint64_t x2 = f2fma(f2pack(a0, a1), sl2x2, negm2);
               float p0, p1;
@@ -356,43 +371,47 @@ __global__ void __launch_bounds__(fwd::NT, 1)
               acc[k & 3] = f2add(acc[k & 3], f2pack(p0, p1));
               pk[kk] = pack_bf16(p0, p1);
             }
-            tmem_st16(tS + ch * 16, pk);
+            tmem_st8(tPh + ch * 8, pk);
           }
         };
+        if (row_t == 0 && q == 0 && hh == 0) FT(11, e);
         if (cls == 1)
           pass2(std::true_type{});
         else
           pass2(std::false_type{});
+        if (row_t == 0 && q == 0 && hh == 0) FT(12, e);
         {
           const uint64_t a01 = f2add(acc[0], acc[1]), a23 = f2add(acc[2], acc[3]);
           float u0, u1;
           f2unpack(f2add(a01, a23), u0, u1);
           l += u0 + u1;
         }
-        if (row_t == 0 && q == 0) FT(12, e);
         tmem_wait_st();
-        if (row_t == 0 && q == 0) FT(13, e);
+        if (row_t == 0 && q == 0 && hh == 0) FT(13, e);
         tc_fence_before();
         mbar_arrive(&sm.p_full[q]);
-        if (row_t == 0) FT(2 + q, e);
+        if (row_t == 0 && hh == 0) FT(2 + q, e);
         ++cnt;
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&sm.m_empty[ms]);
     }
     // ---- epilogue: O = O / l, L = m + ln(l) (Alg. 1 lines 27-28) ----
+    sm.xsum[q][hh][row_t] = l;
+    named_bar_sync(bar_id, 256);
+    l += sm.xsum[q][hh ^ 1][row_t];
     const bool live = (cnt > 0) && (l > 0.f);
     if (cnt > 0) {
       mbar_wait(&sm.o_full[q], 0);
       tc_fence_after();
     }
     const float inv = live ? 1.0f / l : 0.f;
-    const size_t orow = ((static_cast<size_t>(b) * a.N + row) * a.H + h) * D;
+    const size_t orow = ((static_cast<size_t>(b) * a.N + row) * a.H + h) * D + hh * (D / 2);
 #pragma unroll 1
-    for (int c = 0; c < D / 32; ++c) {
+    for (int c = 0; c < D / 64; ++c) {
       uint32_t ov[32];
       if (cnt > 0) {  // WG-uniform: the tcgen05.ld stays warp-collective
-        tmem_ld32(tO + c * 32, ov);
+        tmem_ld32(tOh + c * 32, ov);
         tmem_wait_ld();
       }
       float f[32];
@@ -412,14 +431,14 @@ __global__ void __launch_bounds__(fwd::NT, 1)
         }
       }
     }
-    if (row < a.N)
+    if (row < a.N && hh == 0)
       a.lse[(static_cast<size_t>(b) * a.H + h) * a.N + row] =
           live ? (m_used + __log2f(l)) * 0.6931471805599453f : -INFINITY;
   }
 
   tc_fence_before();
   __syncthreads();
-  if (warp == 9) {
+  if (warp == MMA_WARP) {
     tc_fence_after();
     tmem_dealloc<512>(tbase);
   }

@@ -1,0 +1,71 @@
+// Forward MMA mix (S: SS N=128 x8, PV: TS N=128 x8 with P from TMEM) with optional concurrent
+// TMEM load/store traffic from 16 warps, and optional concurrent bulk smem writes.
+#include <cstdio>
+#include <cuda_runtime.h>
+#include "../paper_2410_01359_b200/csrc/fm_ptx.cuh"
+using namespace fm;
+__global__ void __launch_bounds__(544, 1) k(long long* out, int iters, int tm_traffic) {
+  extern __shared__ uint8_t raw[];
+  uint8_t* sm = smem_align1024<uint8_t>(raw);
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tb_s;
+  __shared__ volatile int stop;
+  const int warp = threadIdx.x / 32;
+  for (int i = threadIdx.x; i < 98304 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(sm)[i] = 0;
+  if (threadIdx.x == 0) { mbar_init(&bar, 1); fence_barrier_init(); stop = 0; }
+  if (warp == 16) tmem_alloc<512>(&tb_s);
+  fence_proxy_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tb = tb_s;
+  if (warp == 16) {
+    if (threadIdx.x == 512) {
+      const uint32_t idS = idesc_bf16(128, 128, 0, 0), idPV = idesc_bf16(128, 128, 0, 1);
+      const uint32_t qa = smem_u32(sm), ka = qa + 32768, va = qa + 65536;
+      const long long t0 = clock64();
+      for (int it = 0; it < iters; ++it) {
+        const uint32_t sc = (it & 1) ? 128 : 0;
+        for (int kk = 0; kk < 8; ++kk) {
+          const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
+          mma_ss(tb + sc, sdesc_sw128(qa + off, 16, 1024), sdesc_sw128(ka + off, 16, 1024), idS, kk > 0);
+        }
+        for (int kk = 0; kk < 8; ++kk)
+          mma_ts(tb + 256 + ((it & 1) ? 128 : 0), tb + (sc ^ 128) + kk * 8, sdesc_sw128(va + kk * 2048, 16384, 1024), idPV, 1);
+      }
+      mma_commit(&bar);
+      mbar_wait(&bar, 0);
+      out[blockIdx.x] = clock64() - t0;
+      stop = 1;
+    }
+  } else if (tm_traffic) {
+    const uint32_t lo = static_cast<uint32_t>((warp & 3) * 32) << 16;
+    uint32_t r[16];
+    unsigned acc = 0;
+    while (!stop) {
+      for (int c = 0; c < 8; ++c) {
+        tmem_ld16(tb + lo + 128 * (warp >> 3) + c * 16, r);
+        tmem_wait_ld();
+        acc += r[3];
+        if (tm_traffic > 1) tmem_st16(tb + lo + 128 * (warp >> 3) + c * 16, r);
+      }
+    }
+    if (acc == 12345) out[2000] = acc;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 16) { tc_fence_after(); tmem_dealloc<512>(tb); }
+}
+int main() {
+  long long* d; cudaMalloc(&d, 2001 * 8);
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 98304 + 1024);
+  for (int m = 0; m < 3; ++m) {
+    const int iters = 1024;
+    k<<<148, 544, 98304 + 1024>>>(d, iters, m);
+    cudaError_t e = cudaDeviceSynchronize();
+    long long h[148]; cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
+    double avg = 0; for (int i = 0; i < 148; ++i) avg += h[i]; avg /= 148;
+    printf("fwd MMA mix (8 SS N128 + 8 TS N128), TMEM traffic=%d: %.0f clk per tile (ideal 1024) %s\n", m, avg / iters, cudaGetErrorString(e));
+  }
+  return 0;
+}

@@ -15,7 +15,7 @@ fm._lib.flashmask_debug_trace_fwd.argtypes = [ctypes.c_void_p]
 fm._lib.flashmask_debug_trace_fwd(buf)
 a = np.array(buf).reshape(64, 16)
 t0 = a[0, 8]
-names = ["sm0_sfull", "sm1_sfull", "sm0_pfull", "sm1_pfull", "mma_p0", "mma_p1", "mma_s0iss", "mma_s1iss", "mma_kfull", "s0_ld", "s0_max", "s0_resc", "s0_exp", "s0_st"]
+names = ["sm0_sfull", "sm1_sfull", "sm0_pfull", "sm1_pfull", "mma_p0", "mma_p1", "mma_s0iss", "mma_s1iss", "mma_kfull", "s0_bar", "s0_p1", "s0_p2beg", "s0_p2end", "s0_stw"]
 print("e  " + " ".join(f"{n[:8]:>8s}" for n in names))
 for e in range(40):
     print(f"{e:2d} " + " ".join(f"{a[e, s] - t0:8d}" for s in range(14)))
