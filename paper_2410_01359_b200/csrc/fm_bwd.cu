@@ -114,11 +114,11 @@ __device__ __forceinline__ void pds_chunk(const uint32_t* sr, const uint32_t* dr
       p[u] = ex2(fmaf(__uint_as_float(sr[c + u]), sl2, -l4[u]));
       if constexpr (PART) {
         const int r = r0 + c + u;
-        bool msk = static_cast<unsigned>(r - mv.x) < static_cast<unsigned>(mv.y - mv.x);
+        bool msk = static_cast<unsigned>(r - mv.x) < static_cast<unsigned>(mv.y);
         if constexpr (CAUSAL)
           msk |= r < key;
         else
-          msk |= static_cast<unsigned>(r - mv.z) < static_cast<unsigned>(mv.w - mv.z);
+          msk |= static_cast<unsigned>(r - mv.z) < static_cast<unsigned>(mv.w);
         p[u] = msk ? 0.f : p[u];
       }
       ds[u] = p[u] * (__uint_as_float(dr[c + u]) - d4[u]);
@@ -315,7 +315,7 @@ __global__ void __launch_bounds__(bwd::NT, 1)
     const int key_t = wl * 32 + lane;
     const int key = j * 128 + key_t;
     const uint32_t lane_off = static_cast<uint32_t>(wl * 32) << 16;
-    const int4 mv = a.vec4[(bhm * a.Tc) * 128 + key];  // this key's (LTS, LTE, UTS, UTE), normalised
+    const int4 mv = a.vec4[(bhm * a.Tc) * 128 + key];  // this key's (LTS, len, UTS, len), normalised
     const float sl2 = a.scale_log2;
     constexpr int CH = C::CH_PER_WG;
     if constexpr (C::KA_TMEM) {

@@ -272,8 +272,8 @@ __global__ void __launch_bounds__(fwd::NT, 1)
         if (row_t == 0 && hh == 0) FT(0 + q, e);
         tc_fence_after();
         // Pass 1: max over this half's 64 columns, 32 at a time (S stays in TMEM for pass 2).
-        // On PARTIAL tiles the element mask (Alg. 1 lines 15-21) is evaluated once, kept as bits.
-        uint32_t mbits[2] = {0u, 0u};
+        // On PARTIAL tiles the element mask (Alg. 1 lines 15-21) is applied here and the masked S
+        // written back to TMEM, so pass 2 is identical for PARTIAL and UNMASKED tiles.
         float mx0 = -INFINITY, mx1 = -INFINITY, mx2 = -INFINITY, mx3 = -INFINITY;
         uint32_t sr[2][16];
         tmem_ld16(tSh, sr[0]);
@@ -283,21 +283,21 @@ __global__ void __launch_bounds__(fwd::NT, 1)
           if (c + 1 < 4) tmem_ld16(tSh + (c + 1) * 16, sr[(c + 1) & 1]);
           float* sv = reinterpret_cast<float*>(sr[c & 1]);
           if (cls == 1) {
+            // element mask of Alg. 1 lines 15-21: row r is masked for key y iff
+            // (unsigned)(r - start_y) < len_y for either interval, or (causal) r < y
             const int4* mk = sm.mask[ms] + hh * 64 + c * 16;
-            const int y0 = j * 128 + hh * 64 + c * 16;
-            uint32_t bits = 0u;
+            const int rmy = row - (j * 128 + hh * 64 + c * 16);
 #pragma unroll
             for (int t = 0; t < 16; ++t) {
               const int4 mv = mk[t];
-              bool msk = static_cast<unsigned>(row - mv.x) < static_cast<unsigned>(mv.y - mv.x);
+              bool msk = static_cast<unsigned>(row - mv.x) < static_cast<unsigned>(mv.y);
               if constexpr (CAUSAL)
-                msk |= row < y0 + t;
+                msk |= rmy < t;
               else
-                msk |= static_cast<unsigned>(row - mv.z) < static_cast<unsigned>(mv.w - mv.z);
-              bits |= (msk ? 1u : 0u) << t;
+                msk |= static_cast<unsigned>(row - mv.z) < static_cast<unsigned>(mv.w);
               sv[t] = msk ? -INFINITY : sv[t];
             }
-            mbits[c >> 1] |= bits << ((c & 1) * 16);
+            tmem_st16(tSh + c * 16, sr[c & 1]);  // masked S back to TMEM: pass 2 needs no mask work
           }
 #pragma unroll
           for (int t = 0; t < 16; t += 8) {
@@ -307,6 +307,7 @@ __global__ void __launch_bounds__(fwd::NT, 1)
             mx3 = fmax3(mx3, sv[t + 6], sv[t + 7]);
           }
         }
+        if (cls == 1) tmem_wait_st();
         const float mh = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3));
         if (row_t == 0 && q == 0 && hh == 0) FT(10, e);
         sm.xmax[q][cnt & 1][hh][row_t] = mh;
@@ -340,45 +341,31 @@ __global__ void __launch_bounds__(fwd::NT, 1)
         // row sums with packed FADD2; packed bf16 P written back over consumed S columns.
         const uint64_t sl2x2 = f2pack(sl2, sl2), negm2 = f2pack(-m_use, -m_use);
         uint64_t acc[4] = {0ull, 0ull, 0ull, 0ull};
-        auto pass2 = [&](auto partial_tag) {
-          constexpr bool PART = decltype(partial_tag)::value;
-          tmem_ld16(tSh, sr[0]);
+        tmem_ld16(tSh, sr[0]);
 #pragma unroll
-          for (int ch = 0; ch < 4; ++ch) {
-            tmem_wait_ld();
-            if (ch + 1 < 4) tmem_ld16(tSh + (ch + 1) * 16, sr[(ch + 1) & 1]);
-            const float* sv = reinterpret_cast<const float*>(sr[ch & 1]);
-            const uint32_t bits = PART ? (mbits[ch >> 1] >> ((ch & 1) * 16)) : 0u;
-            uint32_t pk[8];
+        for (int ch = 0; ch < 4; ++ch) {
+          tmem_wait_ld();
+          if (ch + 1 < 4) tmem_ld16(tSh + (ch + 1) * 16, sr[(ch + 1) & 1]);
+          const float* sv = reinterpret_cast<const float*>(sr[ch & 1]);
+          uint32_t pk[8];
 #pragma unroll
-            for (int kk = 0; kk < 8; ++kk) {
-              const int k = ch * 8 + kk;
-              float a0 = sv[2 * kk], a1 = sv[2 * kk + 1];
-              if constexpr (PART) {
-                a0 = ((bits >> (2 * kk)) & 1u) ? -INFINITY : a0;
-                a1 = ((bits >> (2 * kk + 1)) & 1u) ? -INFINITY : a1;
-              }
-              const uint64_t x2 = f2fma(f2pack(a0, a1), sl2x2, negm2);
-              float p0, p1;
-              if ((k & 7) >= 8 - FM_POLY_PAIRS) {
-                exp2_poly2(x2, p0, p1);
-              } else {
-                float x0, x1;
-                f2unpack(x2, x0, x1);
-                p0 = ex2(x0);
-                p1 = ex2(x1);
-              }
-              acc[k & 3] = f2add(acc[k & 3], f2pack(p0, p1));
-              pk[kk] = pack_bf16(p0, p1);
+          for (int kk = 0; kk < 8; ++kk) {
+            const int k = ch * 8 + kk;
+            const uint64_t x2 = f2fma(f2pack(sv[2 * kk], sv[2 * kk + 1]), sl2x2, negm2);
+            float p0, p1;
+            if ((k & 7) >= 8 - FM_POLY_PAIRS) {
+              exp2_poly2(x2, p0, p1);
+            } else {
+              float x0, x1;
+              f2unpack(x2, x0, x1);
+              p0 = ex2(x0);
+              p1 = ex2(x1);
             }
-            tmem_st8(tPh + ch * 8, pk);
+            acc[k & 3] = f2add(acc[k & 3], f2pack(p0, p1));
+            pk[kk] = pack_bf16(p0, p1);
           }
-        };
-        if (row_t == 0 && q == 0 && hh == 0) FT(11, e);
-        if (cls == 1)
-          pass2(std::true_type{});
-        else
-          pass2(std::false_type{});
+          tmem_st8(tPh + ch * 8, pk);
+        }
         if (row_t == 0 && q == 0 && hh == 0) FT(12, e);
         {
           const uint64_t a01 = f2add(acc[0], acc[1]), a23 = f2add(acc[2], acc[3]);

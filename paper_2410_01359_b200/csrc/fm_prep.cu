@@ -11,8 +11,9 @@ namespace fm {
 // K1a: expand startend_row_indices with the C-table defaults (flashmask.h) and reduce the
 // per-column-tile min/max of LTS, LTE, UTS, UTE (Alg. 1 lines 3-4).  Optionally
 // also writes the per-column normalised interval vector used by the attention kernels:
-// (LTS, LTE, UTS, UTE) clamped to [0, N] with empty intervals as [0, 0); padded columns
-// y >= N get the lower interval [0, INT_MAX) so that they are masked for every row.
+// (LTS, LTE - LTS, UTS, UTE - UTS) after clamping to [0, N], empty intervals as (0, 0), so a
+// row r is masked iff (unsigned)(r - start) < length for either interval; padded columns
+// y >= N get the lower interval (0, INT_MAX) so that they are masked for every row.
 // Grid (Tc, B*Hm), 128 threads; one CTA reduces one column tile.
 // ---------------------------------------------------------------------------------------
 __device__ __forceinline__ void expand_col(const int32_t* s, int C, int causal, int N, int& lts, int& lte, int& uts,
@@ -58,7 +59,7 @@ __global__ void __launch_bounds__(128) k1_expand(const int32_t* __restrict__ sri
       int a = clampi(v[0], 0, N), b = clampi(v[1], 0, N), u = clampi(v[2], 0, N), w = clampi(v[3], 0, N);
       if (a >= b) a = b = 0;
       if (u >= w) u = w = 0;
-      nv = make_int4(a, b, u, w);
+      nv = make_int4(a, b - a, u, w - u);  // (start, length) per interval
     } else {
       nv = make_int4(0, INT_MAX, 0, 0);
     }
