@@ -297,3 +297,104 @@ def effective_flops(vec: Vectors, d: int, Br: int = 128, Bc: int = 128):
     area = (rows[:, None] * cols[None, :])[cm != SKIP].sum()
     fwd = 4.0 * d * area
     return fwd, 2.5 * fwd
+
+
+# ------------------------------------------------------------------ Q = 0 closed forms (any N)
+def visible_counts(vec: Vectors) -> np.ndarray:
+    """count_r = number of key columns row r may attend to, in O(N) without the dense mask:
+    N minus the columns masked by the lower interval, the upper interval, and (causal) the
+    r<y triangle, with inclusion-exclusion done per column on the row axis via difference
+    arrays.  Exact for any vectors (each column's masked row set is the union of at most
+    three row intervals: [LTS, LTE), [UTS, UTE), and [0, y) if causal)."""
+    N = vec.N
+    diff = np.zeros(N + 1, dtype=np.int64)
+    y = np.arange(N, dtype=np.int64)
+    # represent each column's masked rows as a union of disjoint intervals: sort & merge the
+    # (up to) three intervals per column, then add +1/-1 on the difference array.
+    ivs = [(np.clip(vec.lts, 0, N), np.clip(vec.lte, 0, N)), (np.clip(vec.uts, 0, N), np.clip(vec.ute, 0, N))]
+    if vec.causal:
+        ivs.append((np.zeros(N, dtype=np.int64), y))
+    starts = np.stack([a for a, _ in ivs], 1)
+    ends = np.stack([b for _, b in ivs], 1)
+    ends = np.where(ends > starts, ends, starts)          # empty intervals
+    order = np.argsort(starts, axis=1, kind="stable")
+    starts = np.take_along_axis(starts, order, 1)
+    ends = np.take_along_axis(ends, order, 1)
+    cur_s, cur_e = starts[:, 0].copy(), ends[:, 0].copy()
+    for k in range(1, starts.shape[1]):
+        s, e = starts[:, k], ends[:, k]
+        merge = s <= cur_e
+        # flush the current interval where the next one does not overlap
+        flush = ~merge
+        np.add.at(diff, cur_s[flush], 1)
+        np.add.at(diff, cur_e[flush], -1)
+        cur_e = np.where(merge, np.maximum(cur_e, e), e)
+        cur_s = np.where(merge, cur_s, s)
+    np.add.at(diff, cur_s, 1)
+    np.add.at(diff, cur_e, -1)
+    masked_cols = np.cumsum(diff)[:N]
+    return N - masked_cols
+
+
+def forward_q_zero(v, vec: Vectors):
+    """Q = 0: every visible logit is 0, so L_r = ln(count_r) and O_r = mean of the V rows that
+    row r sees (empty rows: O=0, L=-inf) — Eq. 2 with S = 0 on visible cells.  O(N·d): per
+    key column the visible rows are the complement of its masked union, accumulated on the
+    row axis with difference arrays.  Used only at sizes where the dense oracle is too slow;
+    pinned against ``forward`` (tests/test_oracle_attention.py)."""
+    v = np.asarray(v, dtype=np.float64)
+    N, d = v.shape
+    cnt = visible_counts(vec)
+    # sum_{y visible to r} V_y = sum over columns y of V_y * [r visible]; the visible rows of
+    # column y are the complement of its masked union inside [0, N): accumulate V_y on the
+    # row axis with difference arrays over the visible row intervals.
+    acc = np.zeros((N + 1, d))
+    ivs = [(np.clip(vec.lts, 0, N), np.clip(vec.lte, 0, N)), (np.clip(vec.uts, 0, N), np.clip(vec.ute, 0, N))]
+    y = np.arange(N, dtype=np.int64)
+    if vec.causal:
+        ivs.append((np.zeros(N, dtype=np.int64), y))
+    for col in range(N):
+        segs = sorted((int(a[col]), int(b[col])) for a, b in ivs if b[col] > a[col])
+        pos = 0
+        for s, e in segs:
+            if s > pos:
+                acc[pos] += v[col]
+                acc[s] -= v[col]
+            pos = max(pos, e)
+        if pos < N:
+            acc[pos] += v[col]
+            acc[N] -= v[col]
+    sums = np.cumsum(acc, axis=0)[:N]
+    live = cnt > 0
+    O = np.zeros((N, d))
+    O[live] = sums[live] / cnt[live, None]
+    L = np.full(N, -np.inf)
+    L[live] = np.log(cnt[live])
+    return O, L
+
+
+def dv_q_zero(do, vec: Vectors):
+    """Q = 0: P[r, y] = 1/count_r on visible cells, so dV_y = sum over rows r that see y of
+    dO_r / count_r (Alg. 2 line 22, with P written out).  Per column, the visible rows
+    are the complement of its masked union: prefix sums of w_r = dO_r / count_r."""
+    do = np.asarray(do, dtype=np.float64)
+    N, d = do.shape
+    cnt = visible_counts(vec)
+    w = np.where(cnt[:, None] > 0, do / np.maximum(cnt, 1)[:, None], 0.0)
+    pre = np.vstack([np.zeros((1, d)), np.cumsum(w, axis=0)])
+    ivs = [(np.clip(vec.lts, 0, N), np.clip(vec.lte, 0, N)), (np.clip(vec.uts, 0, N), np.clip(vec.ute, 0, N))]
+    y = np.arange(N, dtype=np.int64)
+    if vec.causal:
+        ivs.append((np.zeros(N, dtype=np.int64), y))
+    dv = np.zeros((N, d))
+    for col in range(N):
+        segs = sorted((int(a[col]), int(b[col])) for a, b in ivs if b[col] > a[col])
+        pos, tot = 0, np.zeros(d)
+        for s, e in segs:
+            if s > pos:
+                tot += pre[s] - pre[pos]
+            pos = max(pos, e)
+        if pos < N:
+            tot += pre[N] - pre[pos]
+        dv[col] = tot
+    return dv

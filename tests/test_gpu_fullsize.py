@@ -1,0 +1,127 @@
+"""GPU parity at BASELINE.json's full sizes, in the launch configuration bench.py times.
+
+The workloads are built by bench.build_workload (C2, C3, C4) with inputs from bench.make_inputs;
+the oracle checks what it can compute at that size:
+* C2 (N=8192, H=32): two whole heads per mask, every output (O, lse, dQ, dK, dV);
+* C3 (N=32768, B=4): 128 sampled rows of one head per batch entry (O, lse, dQ via
+  backward_rows), plus the Q=0 closed forms (O, lse, dV) for one batch entry, all heads;
+* C4 (N=131072, H=64): 64 sampled rows (O, lse, dQ) of one head per mask, and the Q=0 closed
+  forms for two heads.
+Bars as in test_gpu_parity (fp32 outputs); bf16 outputs (what bench.py times) are checked
+against the same oracle with the bf16 rounding of the output added to the tolerance (R27).
+"""
+import numpy as np
+import pytest
+import torch
+
+import bench
+from oracle import flashmask_oracle as fo
+
+from gpu_util import TOL_LSE, TOL_MAX, TOL_MEAN, assert_close, assert_lse
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def fm():
+    assert torch.cuda.is_available()
+    from paper_2410_01359_b200 import flashmask
+    return flashmask
+
+
+def _run(fm, c, x, out_dtype):
+    o, lse = fm.flashmask_fwd(x["q"], x["k"], x["v"], x["sri"], c["causal"], out_dtype=out_dtype)
+    dq, dk, dv = fm.flashmask_bwd(x["q"], x["k"], x["v"], o, x["do"], lse, x["sri"], c["causal"], out_dtype=out_dtype)
+    torch.cuda.synchronize()
+    return o, lse, dq, dk, dv
+
+
+def _head(x, name, b, h):
+    return x[name][b, :, h, :].float().cpu().double().numpy()
+
+
+def _check_bf16(name, got, ref):
+    got = np.asarray(got, dtype=np.float64)
+    err = np.abs(got - ref)
+    bound = TOL_MAX + np.abs(ref) * 2.0 ** -8
+    assert (err <= bound).all(), f"{name}: worst excess {float((err - bound).max()):.3e}"
+    assert err.mean() <= TOL_MEAN, f"{name}: mean {err.mean():.3e}"
+
+
+def test_c2_full_heads(fm):
+    calls, _, _ = bench.build_workload("C2", 0, 1, bench.rho_oracle)
+    dev = torch.device("cuda", 0)
+    for c in calls:
+        x = bench.make_inputs(c, dev)
+        r32 = _run(fm, c, x, torch.float32)
+        r16 = _run(fm, c, x, torch.bfloat16)
+        m = c["masks"][0]
+        vec = fo.expand(m.sri, m.causal, m.N)
+        for h in (0, 17):
+            q, k, v, do = (_head(x, n, 0, h) for n in ("q", "k", "v", "do"))
+            O, L = fo.forward(q, k, v, vec)
+            gq, gk, gv = fo.backward(q, k, v, do, vec)
+            for name, idx, ref in (("O", 0, O), ("dQ", 2, gq), ("dK", 3, gk), ("dV", 4, gv)):
+                assert_close(f"{m.family} {name}[h{h}]", r32[idx][0, :, h].cpu().numpy(), ref)
+                _check_bf16(f"{m.family} {name}[h{h}] bf16", r16[idx][0, :, h].float().cpu().numpy(), ref)
+            assert_lse(r32[1][0, h].cpu().numpy(), L)
+
+
+def test_c3_sampled_rows_and_q_zero(fm):
+    calls, _, _ = bench.build_workload("C3", 0, 1, bench.rho_oracle)
+    c = calls[0]
+    dev = torch.device("cuda", 0)
+    x = bench.make_inputs(c, dev)
+    o, lse, dq, dk, dv = _run(fm, c, x, torch.float32)
+    rng = np.random.default_rng(0)
+    N = c["N"]
+    for b, m in enumerate(c["masks"]):
+        vec = fo.expand(m.sri, m.causal, N)
+        rows = np.sort(rng.choice(N, 128, replace=False))
+        q, k, v, do = (_head(x, n, b, 3) for n in ("q", "k", "v", "do"))
+        O, L = fo.forward(q, k, v, vec, rows=rows)
+        gq, _, _ = fo.backward_rows(q, k, v, do, vec, rows)
+        assert_close(f"b{b} O rows", o[b, rows, 3].cpu().numpy(), O)
+        assert_lse(lse[b, 3, rows].cpu().numpy(), L)
+        assert_close(f"b{b} dQ rows", dq[b, rows, 3].cpu().numpy(), gq)
+    # Q = 0 closed forms on batch entry 3 (highest sparsity), all heads
+    xz = dict(x)
+    xz["q"] = torch.zeros_like(x["q"])
+    o, lse, dq, dk, dv = _run(fm, c, xz, torch.float32)
+    m = c["masks"][3]
+    vec = fo.expand(m.sri, m.causal, N)
+    for h in (0, 31):
+        O, L = fo.forward_q_zero(_head(x, "v", 3, h), vec)
+        assert_close(f"Q=0 O h{h}", o[3, :, h].cpu().numpy(), O)
+        assert_lse(lse[3, h].cpu().numpy(), L)
+        assert_close(f"Q=0 dV h{h}", dv[3, :, h].cpu().numpy(), fo.dv_q_zero(_head(x, "do", 3, h), vec))
+
+
+def test_c4_sampled_rows_and_q_zero(fm):
+    calls, _, _ = bench.build_workload("C4", 0, 1, bench.rho_oracle)
+    dev = torch.device("cuda", 0)
+    rng = np.random.default_rng(1)
+    for c in calls:
+        x = bench.make_inputs(c, dev)
+        o, lse, dq, dk, dv = _run(fm, c, x, torch.float32)
+        N = c["N"]
+        m = c["masks"][0]
+        vec = fo.expand(m.sri, m.causal, N)
+        rows = np.sort(rng.choice(N, 64, replace=False))
+        q, k, v, do = (_head(x, n, 0, 5) for n in ("q", "k", "v", "do"))
+        O, L = fo.forward(q, k, v, vec, rows=rows, row_block=16)
+        gq, _, _ = fo.backward_rows(q, k, v, do, vec, rows)
+        assert_close("C4 O rows", o[0, rows, 5].cpu().numpy(), O)
+        assert_lse(lse[0, 5, rows].cpu().numpy(), L)
+        assert_close("C4 dQ rows", dq[0, rows, 5].cpu().numpy(), gq)
+        del o, lse, dq, dk, dv
+        xz = dict(x)
+        xz["q"] = torch.zeros_like(x["q"])
+        o, lse, dq, dk, dv = _run(fm, c, xz, torch.float32)
+        for h in (0, 63):
+            O, L = fo.forward_q_zero(_head(x, "v", 0, h), vec)
+            assert_close(f"C4 Q=0 O h{h}", o[0, :, h].cpu().numpy(), O)
+            assert_lse(lse[0, h].cpu().numpy(), L)
+            assert_close(f"C4 Q=0 dV h{h}", dv[0, :, h].cpu().numpy(), fo.dv_q_zero(_head(x, "do", 0, h), vec))
+        del x, xz, o, lse, dq, dk, dv
+        torch.cuda.empty_cache()

@@ -220,3 +220,22 @@ def test_backward_rows_partition_sums_to_backward():
         acc_k += gk
         acc_v += gv
     assert np.abs(acc_k - dk).max() < 1e-12 and np.abs(acc_v - dv).max() < 1e-12
+
+
+@pytest.mark.parametrize("fam", wm.FAMILIES)
+def test_q_zero_linear_forms_match_dense(fam):
+    """The O(N) Q=0 forms used for full-size GPU checks equal the dense oracle."""
+    rng = np.random.default_rng(31)
+    m = wm.sample_family(fam, 150, rng, (2, 5))
+    vv = vec(m)
+    N, d = m.N, 5
+    q = np.zeros((N, d))
+    k, v_, do = rnd(rng, N, d), rnd(rng, N, d), rnd(rng, N, d)
+    assert np.array_equal(fo.visible_counts(vv), (~fo.to_dense(vv)).sum(axis=1))
+    O, L = fo.forward(q, k, v_, vv)
+    O2, L2 = fo.forward_q_zero(v_, vv)
+    assert np.abs(O - O2).max() < 1e-12 and np.array_equal(np.isneginf(L), np.isneginf(L2))
+    fin = np.isfinite(L)
+    assert np.abs(L[fin] - L2[fin]).max() < 1e-12
+    _, _, dv = fo.backward(q, k, v_, do, vv)
+    assert np.abs(dv - fo.dv_q_zero(do, vv)).max() < 1e-12
