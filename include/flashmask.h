@@ -23,8 +23,9 @@
  *    No C++ exception crosses the ABI.  There is no fallback path.
  *  - The library is stateless and re-entrant (a call_once device-attribute and
  *    driver-entry-point cache is its only global state).
- *  - q, k, v, o, dout, dq, dk, dv: [batch, seqlen, num_heads, head_dim] contiguous,
- *    16-byte aligned.  lse: [batch, num_heads, seqlen] fp32, natural log of the
+ *  - q, o, dout, dq: [batch, seqlen, num_heads, head_dim]; k, v, dk, dv: [batch, seqlen,
+ *    num_kv_heads, head_dim] (grouped-query attention: query head h reads key/value head
+ *    h / (num_heads / num_kv_heads)); all contiguous and 16-byte aligned.  lse: [batch, num_heads, seqlen] fp32, natural log of the
  *    scaled logits (Alg. 1 line 28); -inf for a row masked in every column
  *    (then its O row is 0 and it contributes nothing to the gradients; R7).
  *  - startend_row_indices: int32 [batch, mask_heads, seqlen, C], 16-byte aligned.
@@ -82,13 +83,14 @@ typedef struct {
   int64_t seqlen;      /* N >= 1 (queries = keys)                                  */
   int64_t num_heads;   /* H >= 1                                                    */
   int64_t head_dim;    /* d in {64, 128}                                            */
-  int64_t mask_heads;  /* 1 (one mask per batch entry, broadcast) or num_heads      */
+  int64_t mask_heads;  /* 1 (one mask per batch entry, broadcast) or num_kv_heads   */
   int64_t mask_cols;   /* C in {1, 2, 4}; must match `causal` per the table above   */
   int32_t causal;      /* 0 or 1                                                    */
   float   scale;       /* softmax scale; <= 0 means 1/sqrt(head_dim) (Eq. 1)        */
   int32_t in_dtype;    /* fm_dtype of q, k, v, dout: FM_BF16 only in this build    */
   int32_t out_dtype;   /* fm_dtype of o, dq, dk, dv: FM_BF16 or FM_FP32            */
   int32_t flags;       /* FM_FLAG_*                                                 */
+  int64_t num_kv_heads;/* key/value heads; 0 means num_heads; must divide num_heads   */
 } fm_params;
 
 enum { FM_PASS_FWD = 0, FM_PASS_BWD = 1 };

@@ -43,18 +43,18 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   return g_encode;
 }
 
-// [B, N, H, D] bf16 tensor viewed as the 4-D box grid (D, H, N, B); box = 64 x 1 x rows x 1,
-// 128-byte swizzle, out-of-bounds rows zero-filled.
-bool make_map(CUtensorMap* m, const void* ptr, const fm::Dims& d, int box_rows, std::string* err) {
+// [B, N, heads, D] bf16 tensor viewed as the 4-D box grid (D, heads, N, B); box = 64 x 1 x rows
+// x 1, 128-byte swizzle, out-of-bounds rows zero-filled.
+bool make_map(CUtensorMap* m, const void* ptr, const fm::Dims& d, int heads, int box_rows, std::string* err) {
   auto enc = get_encode();
   if (!enc) {
     *err = "cuTensorMapEncodeTiled unavailable";
     return false;
   }
-  cuuint64_t dims[4] = {static_cast<cuuint64_t>(d.D), static_cast<cuuint64_t>(d.H), static_cast<cuuint64_t>(d.N),
+  cuuint64_t dims[4] = {static_cast<cuuint64_t>(d.D), static_cast<cuuint64_t>(heads), static_cast<cuuint64_t>(d.N),
                         static_cast<cuuint64_t>(d.B)};
-  cuuint64_t strides[3] = {static_cast<cuuint64_t>(d.D) * 2, static_cast<cuuint64_t>(d.H) * d.D * 2,
-                           static_cast<cuuint64_t>(d.N) * d.H * d.D * 2};
+  cuuint64_t strides[3] = {static_cast<cuuint64_t>(d.D) * 2, static_cast<cuuint64_t>(heads) * d.D * 2,
+                           static_cast<cuuint64_t>(d.N) * heads * d.D * 2};
   cuuint32_t box[4] = {64, 1, static_cast<cuuint32_t>(box_rows), 1};
   cuuint32_t estr[4] = {1, 1, 1, 1};
   CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(ptr), dims, strides, box, estr,
@@ -73,8 +73,11 @@ fm_status check_params(const fm_params* p, fm::Dims* d, bool need_attention) {
     return fail(FM_ERR_INVALID_ARGUMENT, "batch, seqlen and num_heads must be >= 1");
   if (p->batch > 65535 || p->num_heads > 65535 || p->seqlen > (1LL << 30))
     return fail(FM_ERR_UNSUPPORTED, "batch/num_heads > 65535 or seqlen > 2^30");
-  if (p->mask_heads != 1 && p->mask_heads != p->num_heads)
-    return fail(FM_ERR_INVALID_ARGUMENT, "mask_heads must be 1 or num_heads");
+  const int64_t hkv = p->num_kv_heads > 0 ? p->num_kv_heads : p->num_heads;
+  if (p->num_kv_heads < 0 || p->num_heads % hkv != 0)
+    return fail(FM_ERR_INVALID_ARGUMENT, "num_kv_heads must divide num_heads");
+  if (p->mask_heads != 1 && p->mask_heads != hkv)
+    return fail(FM_ERR_INVALID_ARGUMENT, "mask_heads must be 1 or num_kv_heads");
   const int C = static_cast<int>(p->mask_cols);
   const bool ok_c = p->causal ? (C == 1 || C == 2) : (C == 2 || C == 4);
   if ((p->causal != 0 && p->causal != 1) || !ok_c)
@@ -90,6 +93,8 @@ fm_status check_params(const fm_params* p, fm::Dims* d, bool need_attention) {
   d->H = static_cast<int>(p->num_heads);
   d->D = static_cast<int>(p->head_dim);
   d->Hm = static_cast<int>(p->mask_heads);
+  d->Hkv = static_cast<int>(hkv);
+  d->G = d->H / d->Hkv;
   d->C = C;
   d->causal = p->causal;
   d->Tr = (d->N + fm::kTile - 1) / fm::kTile;
@@ -233,7 +238,8 @@ fm_status flashmask_fwd(const fm_params* p, const void* q, const void* k, const 
   carve(d, FM_PASS_FWD, workspace, &w);
   std::string err;
   CUtensorMap tq, tk, tv;
-  if (!make_map(&tq, q, d, 128, &err) || !make_map(&tk, k, d, 128, &err) || !make_map(&tv, v, d, 128, &err))
+  if (!make_map(&tq, q, d, d.H, 128, &err) || !make_map(&tk, k, d, d.Hkv, 128, &err) ||
+      !make_map(&tv, v, d, d.Hkv, 128, &err))
     return fail(FM_ERR_CUDA, err);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   cudaError_t e = timed(FM_KERNEL_EXPAND, st, [&] { return fm::launch_expand(sri, d, fm::kTile, w.ext8, w.vec4, st); });
@@ -241,7 +247,7 @@ fm_status flashmask_fwd(const fm_params* p, const void* q, const void* k, const 
   e = timed(FM_KERNEL_CLASSIFY, st, [&] { return fm::launch_classify(w.ext8, d, fm::kTile, fm::kTile, w.fmap, 0, 1, nullptr, st); });
   if (e != cudaSuccess) return cuda_fail(e, "classify");
   fm::FwdArgs a{};
-  a.B = d.B; a.N = d.N; a.H = d.H; a.Hm = d.Hm; a.Tr = d.Tr; a.Tc = d.Tc;
+  a.B = d.B; a.N = d.N; a.H = d.H; a.Hm = d.Hm; a.Tr = d.Tr; a.Tc = d.Tc; a.G = d.G;
   a.scale_log2 = d.scale * 1.4426950408889634f;
   a.fmap = w.fmap;
   a.vec4 = w.vec4;
@@ -271,8 +277,8 @@ fm_status flashmask_bwd(const fm_params* p, const void* q, const void* k, const 
   carve(d, FM_PASS_BWD, workspace, &w);
   std::string err;
   CUtensorMap tq, tk, tv, tdo;
-  if (!make_map(&tq, q, d, d.Brb, &err) || !make_map(&tk, k, d, 128, &err) || !make_map(&tv, v, d, 128, &err) ||
-      !make_map(&tdo, dout, d, d.Brb, &err))
+  if (!make_map(&tq, q, d, d.H, d.Brb, &err) || !make_map(&tk, k, d, d.Hkv, 128, &err) ||
+      !make_map(&tv, v, d, d.Hkv, 128, &err) || !make_map(&tdo, dout, d, d.H, d.Brb, &err))
     return fail(FM_ERR_CUDA, err);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   cudaError_t e = timed(FM_KERNEL_EXPAND, st, [&] { return fm::launch_expand(sri, d, fm::kTile, w.ext8, w.vec4, st); });
@@ -283,6 +289,7 @@ fm_status flashmask_bwd(const fm_params* p, const void* q, const void* k, const 
   if (e != cudaSuccess) return cuda_fail(e, "bwd preprocess");
   fm::BwdArgs a{};
   a.B = d.B; a.N = d.N; a.H = d.H; a.Hm = d.Hm; a.Tc = d.Tc; a.Trb = d.Trb; a.Npb = d.Npb;
+  a.Hkv = d.Hkv; a.G = d.G;
   a.scale_log2 = d.scale * 1.4426950408889634f;
   a.scale = d.scale;
   a.bmap = w.bmap;

@@ -146,10 +146,10 @@ __global__ void __launch_bounds__(bwd::NT, 1)
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int j = static_cast<int>(blockIdx.x);
-  const int h = blockIdx.y, b = blockIdx.z;
-  const int hm = (a.Hm == 1) ? 0 : h;
+  const int hk = blockIdx.y, b = blockIdx.z;  // key/value head; its G query heads are looped over
+  const int hm = (a.Hm == 1) ? 0 : hk;
   const size_t bhm = static_cast<size_t>(b) * a.Hm + hm;
-  const size_t bh = static_cast<size_t>(b) * a.H + h;
+  const int G = a.G;
 
   if (warp == 12 && lane == 0) {
     mbar_init(&sm.kv_full, 1);
@@ -199,7 +199,9 @@ __global__ void __launch_bounds__(bwd::NT, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const int nE = sm.n_entries;
+  // work items t = (query head of the group, visited row tile): t / nE1 selects the head
+  const int nE1 = sm.n_entries;
+  const int nE = nE1 * G;
   const uint32_t tbase = sm.tmem_base;
 
   if (warp == 12) {
@@ -212,18 +214,20 @@ __global__ void __launch_bounds__(bwd::NT, 1)
       mbar_expect_tx(&sm.kv_full, 2 * C::KV_TILE);
 #pragma unroll
       for (int c = 0; c < D / 64; ++c) {
-        tma_load_4d(sm.k + c * 16384, &tmK, &sm.kv_full, c * 64, h, j * 128, b);
-        tma_load_4d(sm.v + c * 16384, &tmV, &sm.kv_full, c * 64, h, j * 128, b);
+        tma_load_4d(sm.k + c * 16384, &tmK, &sm.kv_full, c * 64, hk, j * 128, b);
+        tma_load_4d(sm.v + c * 16384, &tmV, &sm.kv_full, c * 64, hk, j * 128, b);
       }
       for (int t = 0; t < nE; ++t) {
-        const int i = sm.list[t];
+        const int i = sm.list[t % nE1];
+        const int hq = hk * G + t / nE1;
+        const size_t bh = static_cast<size_t>(b) * a.H + hq;
         const int st = t % QST;
         mbar_wait(&sm.q_empty[st], ((t / QST) & 1) ^ 1);
         mbar_expect_tx(&sm.q_full[st], 2 * C::Q_TILE + 2 * BR * 4);
 #pragma unroll
         for (int c = 0; c < D / 64; ++c) {
-          tma_load_4d(sm.q[st] + c * (BR * 128), &tmQ, &sm.q_full[st], c * 64, h, i * BR, b);
-          tma_load_4d(sm.dO[st] + c * (BR * 128), &tmdO, &sm.q_full[st], c * 64, h, i * BR, b);
+          tma_load_4d(sm.q[st] + c * (BR * 128), &tmQ, &sm.q_full[st], c * 64, hq, i * BR, b);
+          tma_load_4d(sm.dO[st] + c * (BR * 128), &tmdO, &sm.q_full[st], c * 64, hq, i * BR, b);
         }
         bulk_g2s(sm.lvec[st], a.l2 + bh * a.Npb + static_cast<size_t>(i) * BR, BR * 4, &sm.q_full[st]);
         bulk_g2s(sm.dvec[st], a.dvec + bh * a.Npb + static_cast<size_t>(i) * BR, BR * 4, &sm.q_full[st]);
@@ -341,8 +345,9 @@ __global__ void __launch_bounds__(bwd::NT, 1)
       }
     }
     for (int t = 0; t < nE; ++t) {
-      const int i = sm.list[t];
-      const bool partial = (sm.part_bits[t >> 5] >> (t & 31)) & 1u;
+      const int t1 = t % nE1;
+      const int i = sm.list[t1];
+      const bool partial = (sm.part_bits[t1 >> 5] >> (t1 & 31)) & 1u;
       const int st = t % QST;
       mbar_wait(&sm.q_full[st], (t / QST) & 1);
       mbar_wait(&sm.s_full, t & 1);
@@ -417,7 +422,7 @@ __global__ void __launch_bounds__(bwd::NT, 1)
       mbar_wait(&sm.done, 0);
       tc_fence_after();
     }
-    const size_t orow = ((static_cast<size_t>(b) * a.N + key) * a.H + h) * D;
+    const size_t orow = ((static_cast<size_t>(b) * a.N + key) * a.Hkv + hk) * D;
     // WG0 writes dV, WG1 writes dK
     const uint32_t col = wg == 0 ? C::DV_COL : C::DK_COL;
     const float mul = wg == 0 ? 1.0f : a.scale;
@@ -452,7 +457,8 @@ __global__ void __launch_bounds__(bwd::NT, 1)
     const int t_id = wl * 32 + lane;  // TMEM lane: d index (d=128) or query (d=64)
     const uint32_t lane_off = static_cast<uint32_t>(wl * 32) << 16;
     for (int t = 0; t < nE; ++t) {
-      const int i = sm.list[t];
+      const int i = sm.list[t % nE1];
+      const size_t bh = static_cast<size_t>(b) * a.H + hk * G + t / nE1;
       mbar_wait(&sm.dq_full, t & 1);
       if (t_id == 0) FM_T(9, t);
       tc_fence_after();
@@ -494,7 +500,7 @@ static cudaError_t launch_bwd_t(const Dims& d, const CUtensorMap& tq, const CUte
   const size_t smem = sizeof(bwd::Smem<D>) + 1024;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (e != cudaSuccess) return e;
-  dim3 grid(d.Tc, d.H, d.B);
+  dim3 grid(d.Tc, d.Hkv, d.B);
   kern<<<grid, bwd::NT, smem, st>>>(tq, tk, tv, tdo, a);
   return cudaGetLastError();
 }

@@ -81,7 +81,8 @@ __global__ void __launch_bounds__(fwd::NT, 1)
   const int npairs = (a.Tr + 1) >> 1;
   const int pair = npairs - 1 - static_cast<int>(blockIdx.x);  // heaviest (last) row tiles first
   const int h = blockIdx.y, b = blockIdx.z;
-  const int hm = (a.Hm == 1) ? 0 : h;
+  const int hk = h / a.G;                      // key/value head of this query head (GQA)
+  const int hm = (a.Hm == 1) ? 0 : hk;
   const int i0 = 2 * pair, i1 = 2 * pair + 1;
   const bool has_q1 = i1 < a.Tr;
   const size_t bhm = static_cast<size_t>(b) * a.Hm + hm;
@@ -160,7 +161,7 @@ __global__ void __launch_bounds__(fwd::NT, 1)
         mbar_wait(&sm.k_empty[ks], ((e / KST) & 1) ^ 1);
         mbar_expect_tx(&sm.k_full[ks], TB);
 #pragma unroll
-        for (int c = 0; c < D / 64; ++c) tma_load_4d(sm.k[ks] + c * 16384, &tmK, &sm.k_full[ks], c * 64, h, j * 128, b);
+        for (int c = 0; c < D / 64; ++c) tma_load_4d(sm.k[ks] + c * 16384, &tmK, &sm.k_full[ks], c * 64, hk, j * 128, b);
         mbar_wait(&sm.m_empty[ms], ((e / MST) & 1) ^ 1);
         if (ent_cls(ent, 0) == 1 || ent_cls(ent, 1) == 1) {
           mbar_expect_tx(&sm.m_full[ms], 128 * 16);
@@ -171,7 +172,7 @@ __global__ void __launch_bounds__(fwd::NT, 1)
         mbar_wait(&sm.v_empty[vs], ((e / VST) & 1) ^ 1);
         mbar_expect_tx(&sm.v_full[vs], TB);
 #pragma unroll
-        for (int c = 0; c < D / 64; ++c) tma_load_4d(sm.v[vs] + c * 16384, &tmV, &sm.v_full[vs], c * 64, h, j * 128, b);
+        for (int c = 0; c < D / 64; ++c) tma_load_4d(sm.v[vs] + c * 16384, &tmV, &sm.v_full[vs], c * 64, hk, j * 128, b);
       }
     }
   } else if (warp == MMA_WARP) {

@@ -24,6 +24,7 @@ struct Workspace {
 
 struct Dims {
   int B, N, H, D, Hm, C, causal;
+  int Hkv, G;       // key/value heads, query heads per key/value head
   int Tr, Tc;       // 128-row / 128-column tile counts
   int Brb, Trb, Npb;  // backward row tile, its count, padded rows
   float scale;
@@ -32,7 +33,7 @@ struct Dims {
 };
 
 struct FwdArgs {
-  int B, N, H, Hm, Tr, Tc;
+  int B, N, H, Hm, Tr, Tc, G;
   float scale_log2;
   const uint8_t* fmap;
   const int4* vec4;
@@ -41,7 +42,7 @@ struct FwdArgs {
 };
 
 struct BwdArgs {
-  int B, N, H, Hm, Tc, Trb, Npb;
+  int B, N, H, Hm, Tc, Trb, Npb, Hkv, G;
   float scale_log2;
   float scale;
   const uint8_t* bmap;

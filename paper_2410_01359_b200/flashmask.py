@@ -30,7 +30,7 @@ class FmParams(ctypes.Structure):
     _fields_ = [("batch", ctypes.c_int64), ("seqlen", ctypes.c_int64), ("num_heads", ctypes.c_int64),
                 ("head_dim", ctypes.c_int64), ("mask_heads", ctypes.c_int64), ("mask_cols", ctypes.c_int64),
                 ("causal", ctypes.c_int32), ("scale", ctypes.c_float), ("in_dtype", ctypes.c_int32),
-                ("out_dtype", ctypes.c_int32), ("flags", ctypes.c_int32)]
+                ("out_dtype", ctypes.c_int32), ("flags", ctypes.c_int32), ("num_kv_heads", ctypes.c_int64)]
 
 
 class FlashMaskError(RuntimeError):
@@ -84,11 +84,12 @@ def _stream(stream):
 
 
 def make_params(B, N, H, d, sri: torch.Tensor, causal: bool, scale=None, out_dtype=torch.bfloat16,
-                flags: int = 0) -> FmParams:
+                flags: int = 0, num_kv_heads: int = 0) -> FmParams:
     assert sri.dim() == 4 and sri.shape[0] == B and sri.shape[2] == N, sri.shape
     return FmParams(batch=B, seqlen=N, num_heads=H, head_dim=d, mask_heads=sri.shape[1], mask_cols=sri.shape[3],
                     causal=int(bool(causal)), scale=float(scale) if scale else 0.0, in_dtype=FM_BF16,
-                    out_dtype=FM_FP32 if out_dtype == torch.float32 else FM_BF16, flags=int(flags))
+                    out_dtype=FM_FP32 if out_dtype == torch.float32 else FM_BF16, flags=int(flags),
+                    num_kv_heads=int(num_kv_heads))
 
 
 def flashmask_workspace_size(params: FmParams, pass_: int) -> int:
@@ -124,9 +125,10 @@ def _workspace(params, pass_, workspace, dev):
 
 def flashmask_fwd(q, k, v, sri, causal: bool, scale=None, out_dtype=torch.bfloat16, flags: int = 0,
                   out=None, lse=None, workspace=None, stream=None):
-    """o, lse = FlashMask forward.  q/k/v: bf16 cuda [B, N, H, d]; sri: int32 [B, Hm, N, C]."""
+    """o, lse = FlashMask forward.  q: bf16 cuda [B, N, H, d]; k/v: [B, N, Hkv, d] (Hkv divides H,
+    grouped-query attention); sri: int32 [B, Hm, N, C] with Hm in {1, Hkv}."""
     B, N, H, d = q.shape
-    p = make_params(B, N, H, d, sri, causal, scale, out_dtype, flags)
+    p = make_params(B, N, H, d, sri, causal, scale, out_dtype, flags, num_kv_heads=k.shape[2])
     o = out if out is not None else torch.empty(B, N, H, d, dtype=out_dtype, device=q.device)
     lse = lse if lse is not None else torch.empty(B, H, N, dtype=torch.float32, device=q.device)
     ws, need = _workspace(p, FM_PASS_FWD, workspace, q.device)
@@ -137,11 +139,13 @@ def flashmask_fwd(q, k, v, sri, causal: bool, scale=None, out_dtype=torch.bfloat
 
 def flashmask_bwd(q, k, v, o, do, lse, sri, causal: bool, scale=None, out_dtype=torch.bfloat16, flags: int = 0,
                   dq=None, dk=None, dv=None, workspace=None, stream=None):
-    """dq, dk, dv = FlashMask backward (o in out_dtype, lse from flashmask_fwd)."""
+    """dq, dk, dv = FlashMask backward (o in out_dtype, lse from flashmask_fwd); dk, dv have the
+    key/value head count of k, v."""
     B, N, H, d = q.shape
-    p = make_params(B, N, H, d, sri, causal, scale, out_dtype, flags)
-    mk = lambda t: t if t is not None else torch.empty(B, N, H, d, dtype=out_dtype, device=q.device)
-    dq, dk, dv = mk(dq), mk(dk), mk(dv)
+    Hkv = k.shape[2]
+    p = make_params(B, N, H, d, sri, causal, scale, out_dtype, flags, num_kv_heads=Hkv)
+    mk = lambda t, h: t if t is not None else torch.empty(B, N, h, d, dtype=out_dtype, device=q.device)
+    dq, dk, dv = mk(dq, H), mk(dk, Hkv), mk(dv, Hkv)
     ws, need = _workspace(p, FM_PASS_BWD, workspace, q.device)
     _check(_lib.flashmask_bwd(ctypes.byref(p), _ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(do), _ptr(lse), _ptr(sri),
                               _ptr(dq), _ptr(dk), _ptr(dv), _ptr(ws), ws.numel(), _stream(stream)), "flashmask_bwd")

@@ -52,7 +52,7 @@ def test_host_validation_without_gpu(lib_path):
     from paper_2410_01359_b200 import flashmask as fm
     lib = fm._lib
     p = fm.FmParams(batch=1, seqlen=128, num_heads=1, head_dim=96, mask_heads=1, mask_cols=1, causal=1, scale=0.0,
-                    in_dtype=0, out_dtype=0, flags=0)
+                    in_dtype=0, out_dtype=0, flags=0, num_kv_heads=0)
     st = lib.flashmask_fwd(ctypes.byref(p), None, None, None, None, None, None, None, 0, None)
     assert st == fm.FM_ERR_INVALID_ARGUMENT
     assert b"head_dim" in lib.flashmask_last_error()
@@ -75,7 +75,7 @@ def test_workspace_size_is_linear_in_n(lib_path):
     sizes = {}
     for N in (8192, 16384):
         p = fm.FmParams(batch=1, seqlen=N, num_heads=32, head_dim=128, mask_heads=1, mask_cols=1, causal=1,
-                        scale=0.0, in_dtype=0, out_dtype=0, flags=0)
+                        scale=0.0, in_dtype=0, out_dtype=0, flags=0, num_kv_heads=0)
         sizes[N] = (fm.flashmask_workspace_size(p, fm.FM_PASS_FWD), fm.flashmask_workspace_size(p, fm.FM_PASS_BWD))
     # forward: O(N) vectors + O(T^2) bytes of class map; backward dominated by the O(N H d) dQ accumulator
     assert sizes[8192][0] < 2 * 1024 * 1024

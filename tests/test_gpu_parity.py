@@ -183,3 +183,45 @@ def test_abi_errors(fmlib):
     with pytest.raises(fmlib.FlashMaskError) as e:
         fmlib.flashmask_fwd(q, q, q, sri4, True)   # causal with C=4 is not in the C-table
     assert e.value.status == fmlib.FM_ERR_INVALID_ARGUMENT
+
+
+# ------------------------------------------------------------------------- grouped-query attention
+GQA_CASES = [("causal_document", 700, 128, 4, 2), ("document", 513, 128, 4, 1), ("share_question", 640, 64, 6, 3),
+             ("global_sliding_window", 384, 64, 2, 1)]
+
+
+@pytest.mark.parametrize("fam,N,d,H,Hkv", GQA_CASES)
+def test_gqa_parity(fmlib, fam, N, d, H, Hkv):
+    """SURVEY §8(f) f2: query head h attends with key/value head h // (H/Hkv); dK/dV of a
+    key/value head are the sums over its query heads (accumulated atomic-free in one CTA)."""
+    from workloads import tensors as wt
+    rng = np.random.default_rng(N + H)
+    masks = [wm.sample_family(fam, N, rng, (2, 5))]
+    sri = torch.from_numpy(wm.stack(masks, 1))
+    q = wt.make_tensor("q", 1, N, H, d, base=9)
+    do = wt.make_tensor("do", 1, N, H, d, base=9)
+    k = wt.make_tensor("k", 1, N, Hkv, d, base=9)
+    v = wt.make_tensor("v", 1, N, Hkv, d, base=9)
+    causal = masks[0].causal
+    qc, kc, vc, doc, sc = q.cuda(), k.cuda(), v.cuda(), do.cuda(), sri.cuda()
+    o, lse = fmlib.flashmask_fwd(qc, kc, vc, sc, causal, out_dtype=torch.float32)
+    dq, dk, dv = fmlib.flashmask_bwd(qc, kc, vc, o, doc, lse, sc, causal, out_dtype=torch.float32)
+    torch.cuda.synchronize()
+    assert dk.shape == (1, N, Hkv, d) and dq.shape == (1, N, H, d)
+    vec = fo.expand(masks[0].sri, causal, N)
+    G = H // Hkv
+    f = lambda t, hh: t[0, :, hh, :].double().numpy()
+    gk_sum = [np.zeros((N, d)) for _ in range(Hkv)]
+    gv_sum = [np.zeros((N, d)) for _ in range(Hkv)]
+    for h in range(H):
+        hk = h // G
+        O, L = fo.forward(f(q, h), f(k, hk), f(v, hk), vec)
+        gq, gk, gv = fo.backward(f(q, h), f(k, hk), f(v, hk), f(do, h), vec)
+        gk_sum[hk] += gk
+        gv_sum[hk] += gv
+        assert_close(f"O[{h}]", o[0, :, h].cpu().numpy(), O)
+        assert_lse(lse[0, h].cpu().numpy(), L)
+        assert_close(f"dQ[{h}]", dq[0, :, h].cpu().numpy(), gq)
+    for hk in range(Hkv):
+        assert_close(f"dK[{hk}]", dk[0, :, hk].cpu().numpy(), gk_sum[hk], tol_max=2e-2 * G ** 0.5)
+        assert_close(f"dV[{hk}]", dv[0, :, hk].cpu().numpy(), gv_sum[hk], tol_max=2e-2 * G ** 0.5)
