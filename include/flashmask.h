@@ -75,7 +75,11 @@ typedef enum { FM_TILE_SKIP = 0, FM_TILE_PARTIAL = 1, FM_TILE_UNMASKED = 2 } fm_
 enum {
   /* Debug: visit SKIP tiles as PARTIAL (masked element-wise).  The outputs must be
    * bitwise identical to the default run — the exactness claim of §4.4. */
-  FM_FLAG_NO_SKIP = 1
+  FM_FLAG_NO_SKIP = 1,
+  /* flashmask_bwd: compute dQ row-parallel in a separate kernel that accumulates over the key
+   * tiles in ascending order on chip (no fp32 atomics), so dq is bitwise reproducible run to
+   * run ("deterministic control").  Costs two extra GEMMs per visited tile. */
+  FM_FLAG_DETERMINISTIC = 2
 };
 
 typedef struct {
@@ -141,7 +145,8 @@ enum {
   FM_KERNEL_BWD_PRE = 3,     /* K3   D = rowsum(dO o O), zero dQ accumulator (Alg. 2 l.3-4)  */
   FM_KERNEL_BWD = 4,         /* K4   backward main loop (Alg. 2)                             */
   FM_KERNEL_DQ_CONVERT = 5,  /* K5   dQ = scale * dQacc -> out dtype                         */
-  FM_NUM_KERNELS = 6
+  FM_KERNEL_DQ = 6,          /* K6   deterministic dQ (FM_FLAG_DETERMINISTIC)                */
+  FM_NUM_KERNELS = 7
 };
 
 /* Optional per-kernel timing for roofline reporting (off by default).  While enabled,

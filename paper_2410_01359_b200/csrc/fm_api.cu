@@ -101,7 +101,7 @@ fm_status check_params(const fm_params* p, fm::Dims* d, bool need_attention) {
   d->Tc = d->Tr;
   d->Brb = (d->D == 128) ? 64 : 128;
   d->Trb = (d->N + d->Brb - 1) / d->Brb;
-  d->Npb = d->Trb * d->Brb;
+  d->Npb = d->Tr * fm::kTile;  // covers both the 64/128-row backward tiles and K6's 128-row tiles
   d->scale = (p->scale > 0.f) ? p->scale : 1.0f / std::sqrt(static_cast<float>(p->head_dim > 0 ? p->head_dim : 1));
   d->out_f32 = p->out_dtype == FM_FP32;
   d->flags = p->flags;
@@ -127,6 +127,7 @@ size_t carve(const fm::Dims& d, int pass, void* base, fm::Workspace* w) {
   if (pass == FM_PASS_FWD) {
     w->fmap = take(bhm * d.Tr * d.Tc);
   } else {
+    w->fmap = take(bhm * d.Tr * d.Tc);  // used by the deterministic dQ kernel (K6)
     w->bmap = take(bhm * d.Tc * d.Trb);
     w->dvec = reinterpret_cast<float*>(take(bh * d.Npb * sizeof(float)));
     w->l2 = reinterpret_cast<float*>(take(bh * d.Npb * sizeof(float)));
@@ -299,10 +300,32 @@ fm_status flashmask_bwd(const fm_params* p, const void* q, const void* k, const 
   a.dqacc = w.dqacc;
   a.dk = dk;
   a.dv = dv;
+  const bool deterministic = (p->flags & FM_FLAG_DETERMINISTIC) != 0;
+  a.with_dq = deterministic ? 0 : 1;
   e = timed(FM_KERNEL_BWD, st, [&] { return fm::launch_bwd(d, tq, tk, tv, tdo, a, st); });
   if (e != cudaSuccess) return cuda_fail(e, "backward kernel");
-  e = timed(FM_KERNEL_DQ_CONVERT, st, [&] { return fm::launch_dq_convert(d, w.dqacc, dq, st); });
-  if (e != cudaSuccess) return cuda_fail(e, "dq convert");
+  if (!deterministic) {
+    e = timed(FM_KERNEL_DQ_CONVERT, st, [&] { return fm::launch_dq_convert(d, w.dqacc, dq, st); });
+    if (e != cudaSuccess) return cuda_fail(e, "dq convert");
+    return FM_OK;
+  }
+  // deterministic dQ: row-parallel recomputation (K6) over the forward class map
+  CUtensorMap tq128, tdo128;
+  if (!make_map(&tq128, q, d, d.H, 128, &err) || !make_map(&tdo128, dout, d, d.H, 128, &err))
+    return fail(FM_ERR_CUDA, err);
+  e = timed(FM_KERNEL_CLASSIFY, st, [&] { return fm::launch_classify(w.ext8, d, fm::kTile, fm::kTile, w.fmap, 0, 1, nullptr, st); });
+  if (e != cudaSuccess) return cuda_fail(e, "classify");
+  fm::DqArgs qa{};
+  qa.B = d.B; qa.N = d.N; qa.H = d.H; qa.Hm = d.Hm; qa.G = d.G; qa.Tr = d.Tr; qa.Tc = d.Tc; qa.Npb = d.Npb;
+  qa.scale_log2 = a.scale_log2;
+  qa.scale = d.scale;
+  qa.fmap = w.fmap;
+  qa.vec4 = w.vec4;
+  qa.dvec = w.dvec;
+  qa.l2 = w.l2;
+  qa.dq = dq;
+  e = timed(FM_KERNEL_DQ, st, [&] { return fm::launch_dq(d, tq128, tk, tv, tdo128, qa, st); });
+  if (e != cudaSuccess) return cuda_fail(e, "deterministic dq kernel");
   return FM_OK;
 }
 

@@ -294,6 +294,7 @@ __global__ void __launch_bounds__(bwd::NT, 1)
           // d=64: dQ(t) overwrites the P/dS columns — issued after dV/dK(t) by this thread (in
           // order), and the compute WGs stored P/dS(t) only after dQ(t-1) was read (dq_empty).
           // d=128: dQ^T has its own columns; wait until the dQ WG has read dQ^T(t-1).
+          if (!a.with_dq) continue;
           if constexpr (!C::DQ_ALIAS) mbar_wait(&sm.dq_empty, (t & 1) ^ 1);
           tc_fence_after();
           const uint32_t ds_addr = smem_u32(sm.ds[t & 1]);
@@ -384,10 +385,10 @@ __global__ void __launch_bounds__(bwd::NT, 1)
       if (tid == 0) FM_T(5, t);
       // dS^T row of this key into the SW128 MN-major smem operand of the dQ GEMM
       // (first: it only needs dQ(t-1) to have finished reading the buffer)
-      mbar_wait(&sm.ds_empty[t & 1], ((t >> 1) & 1) ^ 1);  // dQ(t-2) has read this buffer
+      if (a.with_dq) mbar_wait(&sm.ds_empty[t & 1], ((t >> 1) & 1) ^ 1);  // dQ(t-2) has read this buffer
       if (tid == 0) FM_T(7, t);
 #pragma unroll
-      for (int ch = 0; ch < CH; ++ch) {
+      for (int ch = 0; ch < (a.with_dq ? CH : 0); ++ch) {
         const int q0 = (wg * CH + ch) * 32;
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
@@ -399,7 +400,7 @@ __global__ void __launch_bounds__(bwd::NT, 1)
         }
       }
       // P / dS TMEM columns free: dV/dK(t-1) done (d=64: dQ(t-1), which reuses them, read out)
-      if constexpr (C::DQ_ALIAS)
+      if (C::DQ_ALIAS && a.with_dq)
         mbar_wait(&sm.dq_empty, (t & 1) ^ 1);
       else
         mbar_wait(&sm.pds_free, (t & 1) ^ 1);
@@ -456,7 +457,7 @@ __global__ void __launch_bounds__(bwd::NT, 1)
     const int wl = warp - 8;
     const int t_id = wl * 32 + lane;  // TMEM lane: d index (d=128) or query (d=64)
     const uint32_t lane_off = static_cast<uint32_t>(wl * 32) << 16;
-    for (int t = 0; t < nE; ++t) {
+    for (int t = 0; t < (a.with_dq ? nE : 0); ++t) {
       const int i = sm.list[t % nE1];
       const size_t bh = static_cast<size_t>(b) * a.H + hk * G + t / nE1;
       mbar_wait(&sm.dq_full, t & 1);

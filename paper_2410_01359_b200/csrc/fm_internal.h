@@ -26,7 +26,7 @@ struct Dims {
   int B, N, H, D, Hm, C, causal;
   int Hkv, G;       // key/value heads, query heads per key/value head
   int Tr, Tc;       // 128-row / 128-column tile counts
-  int Brb, Trb, Npb;  // backward row tile, its count, padded rows
+  int Brb, Trb, Npb;  // backward row tile, its count, padded rows (a multiple of 128)
   float scale;
   int out_f32;
   int flags;
@@ -52,6 +52,18 @@ struct BwdArgs {
   float* dqacc;
   void* dk;
   void* dv;
+  int with_dq;  // 0 under FM_FLAG_DETERMINISTIC: dQ comes from K6 instead
+};
+
+struct DqArgs {
+  int B, N, H, Hm, G, Tr, Tc, Npb;
+  float scale_log2;
+  float scale;
+  const uint8_t* fmap;
+  const int4* vec4;
+  const float* dvec;
+  const float* l2;
+  void* dq;
 };
 
 // launchers (return cudaError_t of the launch)
@@ -65,5 +77,7 @@ cudaError_t launch_bwd_pre(const Dims& d, const void* o, const void* dout, const
 cudaError_t launch_bwd(const Dims& d, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
                        const CUtensorMap& tdo, const BwdArgs& a, cudaStream_t st);
 cudaError_t launch_dq_convert(const Dims& d, const float* dqacc, void* dq, cudaStream_t st);
+cudaError_t launch_dq(const Dims& d, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
+                      const CUtensorMap& tdo, const DqArgs& a, cudaStream_t st);
 
 }  // namespace fm

@@ -19,11 +19,12 @@ FM_OK, FM_ERR_INVALID_ARGUMENT, FM_ERR_UNSUPPORTED, FM_ERR_WORKSPACE_TOO_SMALL, 
 FM_BF16, FM_FP32 = 0, 1
 FM_TILE_SKIP, FM_TILE_PARTIAL, FM_TILE_UNMASKED = 0, 1, 2
 FM_FLAG_NO_SKIP = 1
+FM_FLAG_DETERMINISTIC = 2
 FM_PASS_FWD, FM_PASS_BWD = 0, 1
 
 EXPORTED = ["flashmask_workspace_size", "flashmask_classify", "flashmask_fwd", "flashmask_bwd",
             "flashmask_status_string", "flashmask_last_error", "flashmask_timing_enable", "flashmask_timing_collect"]
-KERNEL_NAMES = ["expand", "classify", "fwd", "bwd_pre", "bwd", "dq_convert"]
+KERNEL_NAMES = ["expand", "classify", "fwd", "bwd_pre", "bwd", "dq_convert", "dq"]
 
 
 class FmParams(ctypes.Structure):

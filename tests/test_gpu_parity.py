@@ -225,3 +225,21 @@ def test_gqa_parity(fmlib, fam, N, d, H, Hkv):
     for hk in range(Hkv):
         assert_close(f"dK[{hk}]", dk[0, :, hk].cpu().numpy(), gk_sum[hk], tol_max=2e-2 * G ** 0.5)
         assert_close(f"dV[{hk}]", dv[0, :, hk].cpu().numpy(), gv_sum[hk], tol_max=2e-2 * G ** 0.5)
+
+
+# ------------------------------------------------------------------------- deterministic dQ
+@pytest.mark.parametrize("fam,N,d,B,H", [("causal_document", 1000, 128, 2, 2), ("document", 640, 64, 1, 2),
+                                         ("random_eviction", 513, 128, 1, 1), ("global_sliding_window", 384, 64, 1, 1),
+                                         ("causal", 129, 128, 1, 1), ("full", 1, 128, 1, 1)])
+def test_deterministic_dq(fmlib, fam, N, d, B, H):
+    """SURVEY f1 / P:300: FM_FLAG_DETERMINISTIC gives bitwise reproducible dQ (two runs equal),
+    within tolerance of the oracle; dK and dV are bitwise those of the default mode."""
+    masks, sri, t, r0 = _run(fmlib, fam, N, d, B, H, seed=7, flags=fmlib.FM_FLAG_DETERMINISTIC)
+    _, _, _, r1 = _run(fmlib, fam, N, d, B, H, seed=7, flags=fmlib.FM_FLAG_DETERMINISTIC)
+    _, _, _, rd = _run(fmlib, fam, N, d, B, H, seed=7)
+    assert torch.equal(r0[2], r1[2])
+    assert torch.equal(r0[3], rd[3]) and torch.equal(r0[4], rd[4])
+    for b in range(B):
+        for h in range(H):
+            _, _, (gq, _, _) = oracle_head(t, masks, sri.numpy(), b, h, 1, masks[0].causal)
+            assert_close(f"det dQ[{b},{h}]", r0[2][b, :, h].cpu().numpy(), gq)
