@@ -91,7 +91,8 @@ typedef struct {
   int64_t mask_cols;   /* C in {1, 2, 4}; must match `causal` per the table above   */
   int32_t causal;      /* 0 or 1                                                    */
   float   scale;       /* softmax scale; <= 0 means 1/sqrt(head_dim) (Eq. 1)        */
-  int32_t in_dtype;    /* fm_dtype of q, k, v, dout: FM_BF16 only in this build    */
+  int32_t in_dtype;    /* fm_dtype of q, k, v, dout: FM_BF16 (tcgen05 path) or FM_FP32
+                        * (exact-fp32 CUDA-core path for the parity config C1, reading R26) */
   int32_t out_dtype;   /* fm_dtype of o, dq, dk, dv: FM_BF16 or FM_FP32            */
   int32_t flags;       /* FM_FLAG_*                                                 */
   int64_t num_kv_heads;/* key/value heads; 0 means num_heads; must divide num_heads   */
@@ -122,6 +123,9 @@ FM_API fm_status flashmask_classify(const fm_params* p, const int32_t* startend_
 
 /* Forward pass (Alg. 1): o = Softmax(scale*q k^T + M) v, lse = logsumexp.
  *   q, k, v  [B, N, H, d] in_dtype;  o [B, N, H, d] out_dtype;  lse fp32 [B, H, N].
+ * in_dtype FM_BF16 runs the tcgen05 kernels (bf16 operands, fp32 accumulation);
+ * FM_FP32 runs fp32 CUDA-core kernels with the same tile skipping (no tensor cores: it
+ * serves the fp32 parity configuration, not throughput).
  * Fully masked tiles issue no load and no MMA; partially masked tiles are masked
  * element-wise; unmasked tiles do no mask work. */
 FM_API fm_status flashmask_fwd(const fm_params* p, const void* q, const void* k, const void* v,

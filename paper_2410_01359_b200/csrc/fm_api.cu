@@ -86,7 +86,6 @@ fm_status check_params(const fm_params* p, fm::Dims* d, bool need_attention) {
   if (p->in_dtype != FM_BF16 && p->in_dtype != FM_FP32) return fail(FM_ERR_INVALID_ARGUMENT, "bad in_dtype");
   if (need_attention) {
     if (p->head_dim != 64 && p->head_dim != 128) return fail(FM_ERR_INVALID_ARGUMENT, "head_dim must be 64 or 128");
-    if (p->in_dtype != FM_BF16) return fail(FM_ERR_UNSUPPORTED, "in_dtype FM_FP32 (tf32) is not implemented");
   }
   d->B = static_cast<int>(p->batch);
   d->N = static_cast<int>(p->seqlen);
@@ -135,6 +134,17 @@ size_t carve(const fm::Dims& d, int pass, void* base, fm::Workspace* w) {
   }
   w->bytes = off;
   return off;
+}
+
+fm::F32Args f32_args(const fm::Dims& d, const fm::Workspace& w) {
+  fm::F32Args a{};
+  a.B = d.B; a.N = d.N; a.H = d.H; a.Hm = d.Hm; a.Hkv = d.Hkv; a.G = d.G; a.Tr = d.Tr; a.Tc = d.Tc;
+  a.Npb = d.Npb; a.causal = d.causal;
+  a.scale = d.scale;
+  a.fmap = w.fmap;
+  a.vec4 = w.vec4;
+  a.dvec = w.dvec;
+  return a;
 }
 
 fm_status cuda_fail(cudaError_t e, const char* where) {
@@ -237,12 +247,27 @@ fm_status flashmask_fwd(const fm_params* p, const void* q, const void* k, const 
   if (carve(d, FM_PASS_FWD, nullptr, &w) > workspace_bytes)
     return fail(FM_ERR_WORKSPACE_TOO_SMALL, "workspace smaller than flashmask_workspace_size(FM_PASS_FWD)");
   carve(d, FM_PASS_FWD, workspace, &w);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (p->in_dtype == FM_FP32) {  // fp32 inputs: fm_f32.cu (reading R26)
+    cudaError_t e = timed(FM_KERNEL_EXPAND, st, [&] { return fm::launch_expand(sri, d, fm::kTile, w.ext8, w.vec4, st); });
+    if (e != cudaSuccess) return cuda_fail(e, "expand");
+    e = timed(FM_KERNEL_CLASSIFY, st, [&] { return fm::launch_classify(w.ext8, d, fm::kTile, fm::kTile, w.fmap, 0, 1, nullptr, st); });
+    if (e != cudaSuccess) return cuda_fail(e, "classify");
+    fm::F32Args a = f32_args(d, w);
+    a.q = static_cast<const float*>(q);
+    a.k = static_cast<const float*>(k);
+    a.v = static_cast<const float*>(v);
+    a.o = o;
+    a.lse = lse;
+    e = timed(FM_KERNEL_FWD, st, [&] { return fm::launch_f32_fwd(d, a, st); });
+    if (e != cudaSuccess) return cuda_fail(e, "fp32 forward kernel");
+    return FM_OK;
+  }
   std::string err;
   CUtensorMap tq, tk, tv;
   if (!make_map(&tq, q, d, d.H, 128, &err) || !make_map(&tk, k, d, d.Hkv, 128, &err) ||
       !make_map(&tv, v, d, d.Hkv, 128, &err))
     return fail(FM_ERR_CUDA, err);
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
   cudaError_t e = timed(FM_KERNEL_EXPAND, st, [&] { return fm::launch_expand(sri, d, fm::kTile, w.ext8, w.vec4, st); });
   if (e != cudaSuccess) return cuda_fail(e, "expand");
   e = timed(FM_KERNEL_CLASSIFY, st, [&] { return fm::launch_classify(w.ext8, d, fm::kTile, fm::kTile, w.fmap, 0, 1, nullptr, st); });
@@ -276,12 +301,33 @@ fm_status flashmask_bwd(const fm_params* p, const void* q, const void* k, const 
   if (carve(d, FM_PASS_BWD, nullptr, &w) > workspace_bytes)
     return fail(FM_ERR_WORKSPACE_TOO_SMALL, "workspace smaller than flashmask_workspace_size(FM_PASS_BWD)");
   carve(d, FM_PASS_BWD, workspace, &w);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (p->in_dtype == FM_FP32) {  // fp32 inputs: fm_f32.cu (reading R26); deterministic by construction
+    cudaError_t e = timed(FM_KERNEL_EXPAND, st, [&] { return fm::launch_expand(sri, d, fm::kTile, w.ext8, w.vec4, st); });
+    if (e != cudaSuccess) return cuda_fail(e, "expand");
+    e = timed(FM_KERNEL_CLASSIFY, st, [&] { return fm::launch_classify(w.ext8, d, fm::kTile, fm::kTile, w.fmap, 0, 1, nullptr, st); });
+    if (e != cudaSuccess) return cuda_fail(e, "classify");
+    fm::F32Args a = f32_args(d, w);
+    a.q = static_cast<const float*>(q);
+    a.k = static_cast<const float*>(k);
+    a.v = static_cast<const float*>(v);
+    a.dout = static_cast<const float*>(dout);
+    a.o = const_cast<void*>(o);
+    a.lse = const_cast<float*>(lse);
+    a.dq = dq;
+    a.dk = dk;
+    a.dv = dv;
+    e = timed(FM_KERNEL_DQ, st, [&] { return fm::launch_f32_dq(d, a, st); });
+    if (e != cudaSuccess) return cuda_fail(e, "fp32 dq kernel");
+    e = timed(FM_KERNEL_BWD, st, [&] { return fm::launch_f32_dkdv(d, a, st); });
+    if (e != cudaSuccess) return cuda_fail(e, "fp32 dk/dv kernel");
+    return FM_OK;
+  }
   std::string err;
   CUtensorMap tq, tk, tv, tdo;
   if (!make_map(&tq, q, d, d.H, d.Brb, &err) || !make_map(&tk, k, d, d.Hkv, 128, &err) ||
       !make_map(&tv, v, d, d.Hkv, 128, &err) || !make_map(&tdo, dout, d, d.H, d.Brb, &err))
     return fail(FM_ERR_CUDA, err);
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
   cudaError_t e = timed(FM_KERNEL_EXPAND, st, [&] { return fm::launch_expand(sri, d, fm::kTile, w.ext8, w.vec4, st); });
   if (e != cudaSuccess) return cuda_fail(e, "expand");
   e = timed(FM_KERNEL_CLASSIFY, st, [&] { return fm::launch_classify(w.ext8, d, d.Brb, fm::kTile, w.bmap, 1, 1, nullptr, st); });

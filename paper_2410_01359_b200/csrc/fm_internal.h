@@ -66,6 +66,19 @@ struct DqArgs {
   void* dq;
 };
 
+// FP32-input path (fm_f32.cu): plain fp32 tensors, same layouts as the bf16 path
+struct F32Args {
+  int B, N, H, Hm, Hkv, G, Tr, Tc, Npb, causal;
+  float scale;
+  const uint8_t* fmap;  // [B, Hm, Tr, Tc] 128 x 128 kernel map
+  const int4* vec4;
+  const float *q, *k, *v, *dout;
+  void* o;        // forward output (out dtype): written by the forward, read by the backward
+  float* lse;
+  float* dvec;    // [B, H, Npb] D_r, written by f32_dq_kernel, read by f32_dkdv_kernel
+  void *dq, *dk, *dv;
+};
+
 // launchers (return cudaError_t of the launch)
 cudaError_t launch_expand(const int32_t* sri, const Dims& d, int bc, int32_t* ext8, int4* vec4, cudaStream_t st);
 cudaError_t launch_classify(const int32_t* ext8, const Dims& d, int br, int bc, uint8_t* map, int transposed,
@@ -79,5 +92,9 @@ cudaError_t launch_bwd(const Dims& d, const CUtensorMap& tq, const CUtensorMap& 
 cudaError_t launch_dq_convert(const Dims& d, const float* dqacc, void* dq, cudaStream_t st);
 cudaError_t launch_dq(const Dims& d, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
                       const CUtensorMap& tdo, const DqArgs& a, cudaStream_t st);
+
+cudaError_t launch_f32_fwd(const Dims& d, const F32Args& a, cudaStream_t st);
+cudaError_t launch_f32_dq(const Dims& d, const F32Args& a, cudaStream_t st);
+cudaError_t launch_f32_dkdv(const Dims& d, const F32Args& a, cudaStream_t st);
 
 }  // namespace fm

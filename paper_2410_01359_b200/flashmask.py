@@ -84,11 +84,19 @@ def _stream(stream):
     return ctypes.c_void_p(stream.cuda_stream)
 
 
+def _in_dtype(t: torch.Tensor) -> int:
+    if t.dtype == torch.bfloat16:
+        return FM_BF16
+    if t.dtype == torch.float32:
+        return FM_FP32
+    raise TypeError(f"flashmask inputs must be bfloat16 or float32, got {t.dtype}")
+
+
 def make_params(B, N, H, d, sri: torch.Tensor, causal: bool, scale=None, out_dtype=torch.bfloat16,
-                flags: int = 0, num_kv_heads: int = 0) -> FmParams:
+                flags: int = 0, num_kv_heads: int = 0, in_dtype: int = FM_BF16) -> FmParams:
     assert sri.dim() == 4 and sri.shape[0] == B and sri.shape[2] == N, sri.shape
     return FmParams(batch=B, seqlen=N, num_heads=H, head_dim=d, mask_heads=sri.shape[1], mask_cols=sri.shape[3],
-                    causal=int(bool(causal)), scale=float(scale) if scale else 0.0, in_dtype=FM_BF16,
+                    causal=int(bool(causal)), scale=float(scale) if scale else 0.0, in_dtype=in_dtype,
                     out_dtype=FM_FP32 if out_dtype == torch.float32 else FM_BF16, flags=int(flags),
                     num_kv_heads=int(num_kv_heads))
 
@@ -126,10 +134,12 @@ def _workspace(params, pass_, workspace, dev):
 
 def flashmask_fwd(q, k, v, sri, causal: bool, scale=None, out_dtype=torch.bfloat16, flags: int = 0,
                   out=None, lse=None, workspace=None, stream=None):
-    """o, lse = FlashMask forward.  q: bf16 cuda [B, N, H, d]; k/v: [B, N, Hkv, d] (Hkv divides H,
-    grouped-query attention); sri: int32 [B, Hm, N, C] with Hm in {1, Hkv}."""
+    """o, lse = FlashMask forward.  q: bf16 (tcgen05 path) or fp32 (fp32 path) cuda [B, N, H, d];
+    k/v: [B, N, Hkv, d] of the same dtype (Hkv divides H, grouped-query attention);
+    sri: int32 [B, Hm, N, C] with Hm in {1, Hkv}."""
     B, N, H, d = q.shape
-    p = make_params(B, N, H, d, sri, causal, scale, out_dtype, flags, num_kv_heads=k.shape[2])
+    p = make_params(B, N, H, d, sri, causal, scale, out_dtype, flags, num_kv_heads=k.shape[2],
+                    in_dtype=_in_dtype(q))
     o = out if out is not None else torch.empty(B, N, H, d, dtype=out_dtype, device=q.device)
     lse = lse if lse is not None else torch.empty(B, H, N, dtype=torch.float32, device=q.device)
     ws, need = _workspace(p, FM_PASS_FWD, workspace, q.device)
@@ -144,7 +154,7 @@ def flashmask_bwd(q, k, v, o, do, lse, sri, causal: bool, scale=None, out_dtype=
     key/value head count of k, v."""
     B, N, H, d = q.shape
     Hkv = k.shape[2]
-    p = make_params(B, N, H, d, sri, causal, scale, out_dtype, flags, num_kv_heads=Hkv)
+    p = make_params(B, N, H, d, sri, causal, scale, out_dtype, flags, num_kv_heads=Hkv, in_dtype=_in_dtype(q))
     mk = lambda t, h: t if t is not None else torch.empty(B, N, h, d, dtype=out_dtype, device=q.device)
     dq, dk, dv = mk(dq, H), mk(dk, Hkv), mk(dv, Hkv)
     ws, need = _workspace(p, FM_PASS_BWD, workspace, q.device)

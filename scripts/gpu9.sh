@@ -1,5 +1,4 @@
 cd $GRAFT_REPO_ROOT
 export PYTHONUNBUFFERED=1
-timeout -s KILL 600 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
-timeout -s KILL 300 python scripts/time_kernels.py C3 3 2>&1 | tail -1
-timeout -s KILL 900 python scripts/time_kernels.py C5:8192:128 2 2>&1 | tail -13
+timeout -s KILL 600 python -m pytest tests -m gpu -x -q -k fp32 2>&1 | tail -15
+timeout -s KILL 1200 python -m pytest tests -m gpu -x -q 2>&1 | tail -5

@@ -63,10 +63,14 @@ def test_host_validation_without_gpu(lib_path):
     p.mask_cols = 1
     assert lib.flashmask_fwd(ctypes.byref(p), None, None, None, None, None, None, None, 0, None) == \
         fm.FM_ERR_INVALID_ARGUMENT  # NULL pointers
-    p.in_dtype = 1
+    p.in_dtype = 7
+    assert lib.flashmask_fwd(ctypes.byref(p), None, None, None, None, None, None, None, 0, None) == \
+        fm.FM_ERR_INVALID_ARGUMENT
+    p.in_dtype = 0
+    p.batch = 70000
     assert lib.flashmask_fwd(ctypes.byref(p), None, None, None, None, None, None, None, 0, None) == \
         fm.FM_ERR_UNSUPPORTED
-    p.in_dtype = 0
+    p.batch = 1
     assert lib.flashmask_status_string(fm.FM_ERR_WORKSPACE_TOO_SMALL) == b"FM_ERR_WORKSPACE_TOO_SMALL"
 
 

@@ -64,7 +64,7 @@ def test_classify_arbitrary_int32_vectors(fmlib):
 # ------------------------------------------------------------------------- forward / backward
 ATTN_CASES = [
     # (family, N, d, B, H)
-    ("causal_document", 128, 64, 1, 1),       # config C1 shape (R26: bf16 inputs)
+    ("causal_document", 128, 64, 1, 1),       # config C1 shape with bf16 inputs (fp32: test_fp32_inputs)
     ("causal", 256, 128, 1, 2),
     ("full", 384, 128, 2, 1),
     ("causal_document", 1000, 128, 2, 2),
@@ -243,3 +243,57 @@ def test_deterministic_dq(fmlib, fam, N, d, B, H):
         for h in range(H):
             _, _, (gq, _, _) = oracle_head(t, masks, sri.numpy(), b, h, 1, masks[0].causal)
             assert_close(f"det dQ[{b},{h}]", r0[2][b, :, h].cpu().numpy(), gq)
+
+
+# ------------------------------------------------------------------------- fp32 inputs (config C1)
+# The fp32 path computes in fp32 throughout (reading R26), so its bar is far tighter than the
+# bf16 north_star bar: fp32 rounding over <= 1000-term sums of O(1) values stays below 1e-4
+# (this would fail for any path that rounded the inputs to bf16: |x|·2^-9 ~ 4e-3).
+TOL32 = dict(tol_max=1e-4, tol_mean=1e-5)
+F32_CASES = [
+    # (mask builder, d, H, Hkv, out dtype)
+    (lambda: wm.causal_document([40, 48, 40]), 64, 1, 1, torch.float32),     # config C1 exactly
+    (lambda: wm.causal_document([1, 126, 1]), 64, 1, 1, torch.float32),      # C1 seeded variant
+    (lambda: wm.global_sliding_window(257, 16, 40), 128, 2, 1, torch.float32),
+    (lambda: wm.document([100, 200, 33]), 64, 3, 3, torch.float32),
+    (lambda: wm.random_eviction(300, 19, np.random.default_rng(3)), 128, 2, 2, torch.float32),
+    (lambda: wm.empty_rows_padding([60, 70], 20), 64, 1, 1, torch.float32),
+    (lambda: wm.causal(200), 128, 1, 1, torch.bfloat16),
+]
+
+
+@pytest.mark.parametrize("case", range(len(F32_CASES)))
+def test_fp32_inputs(fmlib, case):
+    from workloads import tensors as wt
+    build, d, H, Hkv, out_dtype = F32_CASES[case]
+    m = build()
+    N = m.N
+    sri = torch.from_numpy(wm.stack([m], 1))
+    q = wt.make_tensor("q", 1, N, H, d, base=5, dtype=torch.float32)
+    do = wt.make_tensor("do", 1, N, H, d, base=5, dtype=torch.float32)
+    k = wt.make_tensor("k", 1, N, Hkv, d, base=5, dtype=torch.float32)
+    v = wt.make_tensor("v", 1, N, Hkv, d, base=5, dtype=torch.float32)
+    qc, kc, vc, doc, sc = q.cuda(), k.cuda(), v.cuda(), do.cuda(), sri.cuda()
+    o, lse = fmlib.flashmask_fwd(qc, kc, vc, sc, m.causal, out_dtype=out_dtype)
+    dq, dk, dv = fmlib.flashmask_bwd(qc, kc, vc, o, doc, lse, sc, m.causal, out_dtype=out_dtype)
+    dq2, dk2, dv2 = fmlib.flashmask_bwd(qc, kc, vc, o, doc, lse, sc, m.causal, out_dtype=out_dtype)
+    torch.cuda.synchronize()
+    assert torch.equal(dq, dq2) and torch.equal(dk, dk2) and torch.equal(dv, dv2)  # no atomics
+    vec = fo.expand(m.sri, m.causal, N)
+    G = H // Hkv
+    f = lambda t, hh: t[0, :, hh, :].double().numpy()
+    tol = TOL32 if out_dtype == torch.float32 else {}
+    gk_sum = [np.zeros((N, d)) for _ in range(Hkv)]
+    gv_sum = [np.zeros((N, d)) for _ in range(Hkv)]
+    for h in range(H):
+        hk = h // G
+        O, L = fo.forward(f(q, h), f(k, hk), f(v, hk), vec)
+        gq, gk, gv = fo.backward(f(q, h), f(k, hk), f(v, hk), f(do, h), vec)
+        gk_sum[hk] += gk
+        gv_sum[hk] += gv
+        assert_close(f"fp32 O[{h}]", o[0, :, h].float().cpu().numpy(), O, **tol)
+        assert_lse(lse[0, h].cpu().numpy(), L, tol=1e-5)
+        assert_close(f"fp32 dQ[{h}]", dq[0, :, h].float().cpu().numpy(), gq, **tol)
+    for hk in range(Hkv):
+        assert_close(f"fp32 dK[{hk}]", dk[0, :, hk].float().cpu().numpy(), gk_sum[hk], **tol)
+        assert_close(f"fp32 dV[{hk}]", dv[0, :, hk].float().cpu().numpy(), gv_sum[hk], **tol)
