@@ -239,7 +239,7 @@ __global__ void __launch_bounds__(bwd::NT, 1)
     // dependency wait in a single issuer starves it.  Warp 13 issues S^T/dP^T(t) as soon as the
     // compute WGs have released tile t-1; warp 14 issues dV/dK/dQ(t) once P/dS(t) are ready.
     // Each warp commits only to barriers that track its own MMAs.
-    if (lane == 0 && nE > 0) {
+    if (nE > 0) {  // the whole warp runs converged; one elected lane issues (fm_ptx.cuh)
       constexpr uint32_t ID_S = idesc_bf16(128, BR, 0, 0);   // S^T, dP^T: A, B K-major
       constexpr uint32_t ID_G = idesc_bf16(128, D, 0, 1);    // dV, dK: A in TMEM, B MN-major
       constexpr uint32_t ID_Q = idesc_bf16(128, 64, 1, 1);   // dQ^T (d=128) / dQ (d=64), both MN-major
@@ -250,9 +250,9 @@ __global__ void __launch_bounds__(bwd::NT, 1)
         for (int t = 0; t < nE; ++t) {
           const int st = t % QST;
           if (t > 0) mbar_wait(&sm.sdp_free, (t - 1) & 1);  // compute WGs hold S^T/dP^T(t-1) in registers
-          FM_T(1, t);
+          if (lane == 0) FM_T(1, t);
           mbar_wait(&sm.q_full[st], (t / QST) & 1);
-          FM_T(14, t);
+          if (lane == 0) FM_T(14, t);
           tc_fence_after();
           const uint32_t q_addr = smem_u32(sm.q[st]), do_addr = smem_u32(sm.dO[st]);
 #pragma unroll
@@ -260,37 +260,37 @@ __global__ void __launch_bounds__(bwd::NT, 1)
             const uint32_t ao = (kk >> 2) * 16384 + (kk & 3) * 32;
             const uint32_t bo = (kk >> 2) * (BR * 128) + (kk & 3) * 32;
             if constexpr (C::KA_TMEM)
-              mma_ts(tbase + C::S_COL, tbase + C::KA_COL + kk * 8, sdesc_sw128(q_addr + bo, 16, 1024), ID_S,
+              mma_ts_w(tbase + C::S_COL, tbase + C::KA_COL + kk * 8, sdesc_sw128(q_addr + bo, 16, 1024), ID_S,
                      kk > 0 ? 1u : 0u);
             else
-              mma_ss(tbase + C::S_COL, sdesc_sw128(k_addr + ao, 16, 1024), sdesc_sw128(q_addr + bo, 16, 1024), ID_S,
+              mma_ss_w(tbase + C::S_COL, sdesc_sw128(k_addr + ao, 16, 1024), sdesc_sw128(q_addr + bo, 16, 1024), ID_S,
                      kk > 0 ? 1u : 0u);
-            mma_ss(tbase + C::DP_COL, sdesc_sw128(v_addr + ao, 16, 1024), sdesc_sw128(do_addr + bo, 16, 1024), ID_S,
+            mma_ss_w(tbase + C::DP_COL, sdesc_sw128(v_addr + ao, 16, 1024), sdesc_sw128(do_addr + bo, 16, 1024), ID_S,
                    kk > 0 ? 1u : 0u);
           }
-          mma_commit(&sm.s_full);
-          FM_T(11, t);
+          mma_commit_w(&sm.s_full);
+          if (lane == 0) FM_T(11, t);
         }
       } else {
         for (int t = 0; t < nE; ++t) {
           const int st = t % QST;
-          FM_T(0, t);
+          if (lane == 0) FM_T(0, t);
           mbar_wait(&sm.p_full, t & 1);
-          FM_T(2, t);
+          if (lane == 0) FM_T(2, t);
           tc_fence_after();
           const uint32_t q_addr = smem_u32(sm.q[st]), do_addr = smem_u32(sm.dO[st]);
 #pragma unroll
           for (int kk = 0; kk < BR / 16; ++kk) {
             const uint32_t acc = (t > 0 || kk > 0) ? 1u : 0u;
-            mma_ts(tbase + C::DV_COL, tbase + C::P_COL + kk * 8, sdesc_sw128(do_addr + kk * 2048, BR * 128, 1024),
+            mma_ts_w(tbase + C::DV_COL, tbase + C::P_COL + kk * 8, sdesc_sw128(do_addr + kk * 2048, BR * 128, 1024),
                    ID_G, acc);
-            mma_ts(tbase + C::DK_COL, tbase + C::DS_COL + kk * 8, sdesc_sw128(q_addr + kk * 2048, BR * 128, 1024),
+            mma_ts_w(tbase + C::DK_COL, tbase + C::DS_COL + kk * 8, sdesc_sw128(q_addr + kk * 2048, BR * 128, 1024),
                    ID_G, acc);
           }
           // S^T/dP^T(t) (warp 13) completed before the compute WGs produced P/dS(t)
-          mma_commit(&sm.q_empty[st]);
-          mma_commit(&sm.pds_free);
-          FM_T(12, t);
+          mma_commit_w(&sm.q_empty[st]);
+          mma_commit_w(&sm.pds_free);
+          if (lane == 0) FM_T(12, t);
           // d=64: dQ(t) overwrites the P/dS columns — issued after dV/dK(t) by this thread (in
           // order), and the compute WGs stored P/dS(t) only after dQ(t-1) was read (dq_empty).
           // d=128: dQ^T has its own columns; wait until the dQ WG has read dQ^T(t-1).
@@ -301,17 +301,17 @@ __global__ void __launch_bounds__(bwd::NT, 1)
 #pragma unroll
           for (int kk = 0; kk < 8; ++kk) {
             if constexpr (C::DQT)
-              mma_ss(tbase + C::DQ_COL, sdesc_sw128(k_addr + kk * 2048, 16384, 1024),
+              mma_ss_w(tbase + C::DQ_COL, sdesc_sw128(k_addr + kk * 2048, 16384, 1024),
                      sdesc_sw128(ds_addr + kk * 2048, 16384, 1024), ID_Q, kk > 0 ? 1u : 0u);
             else
-              mma_ss(tbase + C::DQ_COL, sdesc_sw128(ds_addr + kk * 2048, 16384, 1024),
+              mma_ss_w(tbase + C::DQ_COL, sdesc_sw128(ds_addr + kk * 2048, 16384, 1024),
                      sdesc_sw128(k_addr + kk * 2048, 16384, 1024), ID_Q, kk > 0 ? 1u : 0u);
           }
-          mma_commit(&sm.dq_full);
-          mma_commit(&sm.ds_empty[t & 1]);
-          FM_T(13, t);
+          mma_commit_w(&sm.dq_full);
+          mma_commit_w(&sm.ds_empty[t & 1]);
+          if (lane == 0) FM_T(13, t);
         }
-        mma_commit(&sm.done);  // all S^T/dP^T completed earlier (they precede every p_full)
+        mma_commit_w(&sm.done);  // all S^T/dP^T completed earlier (they precede every p_full)
       }
     }
   } else if (warp < 8) {

@@ -137,7 +137,7 @@ __global__ void __launch_bounds__(dqk::NT, 1)
     }
   } else if (warp == 9) {
     // ================================ MMA issuer ================================
-    if (lane == 0 && nE > 0) {
+    if (nE > 0) {  // converged warp, one elected lane issues
       constexpr uint32_t ID_S = idesc_bf16(128, 128, 0, 0);  // S, dP: A, B K-major
       constexpr uint32_t ID_Q = idesc_bf16(128, D, 0, 1);    // dQ: A = dS in TMEM, B = K MN-major
       const uint32_t q_addr = smem_u32(sm.q), do_addr = smem_u32(sm.dO);
@@ -151,22 +151,22 @@ __global__ void __launch_bounds__(dqk::NT, 1)
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
           const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
-          mma_ss(tbase + S_COL, sdesc_sw128(q_addr + off, 16, 1024), sdesc_sw128(k_addr + off, 16, 1024), ID_S,
+          mma_ss_w(tbase + S_COL, sdesc_sw128(q_addr + off, 16, 1024), sdesc_sw128(k_addr + off, 16, 1024), ID_S,
                  kk > 0 ? 1u : 0u);
-          mma_ss(tbase + DP_COL, sdesc_sw128(do_addr + off, 16, 1024), sdesc_sw128(v_addr + off, 16, 1024), ID_S,
+          mma_ss_w(tbase + DP_COL, sdesc_sw128(do_addr + off, 16, 1024), sdesc_sw128(v_addr + off, 16, 1024), ID_S,
                  kk > 0 ? 1u : 0u);
         }
-        mma_commit(&sm.s_full);
+        mma_commit_w(&sm.s_full);
         mbar_wait(&sm.ds_full, e & 1);
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk)
-          mma_ts(tbase + DQ_COL, tbase + DS_COL + kk * 8, sdesc_sw128(k_addr + kk * 2048, 16384, 1024), ID_Q,
+          mma_ts_w(tbase + DQ_COL, tbase + DS_COL + kk * 8, sdesc_sw128(k_addr + kk * 2048, 16384, 1024), ID_Q,
                  (e > 0 || kk > 0) ? 1u : 0u);
-        mma_commit(&sm.ds_free);
-        mma_commit(&sm.kv_empty[ks]);
+        mma_commit_w(&sm.ds_free);
+        mma_commit_w(&sm.kv_empty[ks]);
       }
-      mma_commit(&sm.done);
+      mma_commit_w(&sm.done);
     }
   } else {
     // ====================== compute WGs (thread = query row, WG = 64-key half) ======================

@@ -180,7 +180,7 @@ __global__ void __launch_bounds__(fwd::NT, 1)
     // One issuer for both tiles, in the order PV0(e-1), S0(e), PV1(e-1), S1(e): this keeps the
     // two tiles' softmax phases staggered (ping-pong).  Two independent issuers were measured
     // to fall into lock-step and lose ~30 %.
-    if (lane == 0) {
+    {  // the whole warp runs the issue loop converged; one elected lane issues
       constexpr uint32_t ID_S = idesc_bf16(128, 128, 0, 0);  // S = Q K^T, both K-major
       constexpr uint32_t ID_PV = idesc_bf16(128, D, 0, 1);   // O += P V, V is MN-major
       const uint32_t tS[2] = {tbase + 0, tbase + 128};
@@ -191,7 +191,7 @@ __global__ void __launch_bounds__(fwd::NT, 1)
       auto issue_pv = [&](int q) {
         const int pe = pend[q];
         mbar_wait(&sm.p_full[q], pv_cnt[q] & 1);
-        FT(4 + q, pe);
+        if (lane == 0) FT(4 + q, pe);
         const int vs = pe % VST;
         mbar_wait(&sm.v_full[vs], (pe / VST) & 1);
         tc_fence_after();
@@ -200,12 +200,12 @@ __global__ void __launch_bounds__(fwd::NT, 1)
         for (int kk = 0; kk < 8; ++kk) {
           const uint64_t bd = sdesc_sw128(v_addr + kk * 2048, 16384, 1024);
           // P of keys [0,64) sits in S columns [0,32), of keys [64,128) in S columns [64,96)
-          mma_ts(tO[q], tS[q] + kk * 8 + (kk >= 4 ? 32u : 0u), bd, ID_PV, (pv_cnt[q] > 0 || kk > 0) ? 1u : 0u);
+          mma_ts_w(tO[q], tS[q] + kk * 8 + (kk >= 4 ? 32u : 0u), bd, ID_PV, (pv_cnt[q] > 0 || kk > 0) ? 1u : 0u);
         }
         pv_cnt[q]++;
         const uint32_t ent = sm.list[pe];
         const int last = (ent_cls(ent, 1) != 0) ? 1 : 0;
-        if (q == last) mma_commit(&sm.v_empty[vs]);
+        if (q == last) mma_commit_w(&sm.v_empty[vs]);
         pend[q] = -1;
       };
       if (nE > 0) {
@@ -216,7 +216,7 @@ __global__ void __launch_bounds__(fwd::NT, 1)
         const uint32_t ent = sm.list[e];
         const int ks = e % KST;
         mbar_wait(&sm.k_full[ks], (e / KST) & 1);
-        FT(8, e);
+        if (lane == 0) FT(8, e);
         tc_fence_after();
         const uint32_t k_addr = smem_u32(sm.k[ks]);
 #pragma unroll
@@ -226,20 +226,20 @@ __global__ void __launch_bounds__(fwd::NT, 1)
 #pragma unroll
             for (int kk = 0; kk < D / 16; ++kk) {
               const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
-              mma_ss(tS[q], sdesc_sw128(q_addr[q] + off, 16, 1024), sdesc_sw128(k_addr + off, 16, 1024), ID_S,
+              mma_ss_w(tS[q], sdesc_sw128(q_addr[q] + off, 16, 1024), sdesc_sw128(k_addr + off, 16, 1024), ID_S,
                      kk > 0 ? 1u : 0u);
             }
-            mma_commit(&sm.s_full[q]);
-            FT(6 + q, e);
+            mma_commit_w(&sm.s_full[q]);
+            if (lane == 0) FT(6 + q, e);
             pend[q] = e;
           }
         }
-        mma_commit(&sm.k_empty[ks]);
+        mma_commit_w(&sm.k_empty[ks]);
       }
       for (int q = 0; q < 2; ++q)
         if (pend[q] >= 0) issue_pv(q);
-      mma_commit(&sm.o_full[0]);
-      mma_commit(&sm.o_full[1]);
+      mma_commit_w(&sm.o_full[0]);
+      mma_commit_w(&sm.o_full[1]);
     }
   } else {
     // ================================ softmax WGs ================================

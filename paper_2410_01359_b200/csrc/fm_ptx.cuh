@@ -141,6 +141,37 @@ FM_DEV void mma_commit(uint64_t* bar) {
                : "memory");
 }
 
+// Warp-converged issue: called by all 32 lanes of the issuing warp with warp-uniform operands;
+// elect.sync picks the one lane that issues.  Keeping the warp converged lets the compiler
+// keep descriptors in uniform registers and issue UTCHMMA back to back (no per-MMA
+// elect/waterfall loop as for a lane-0-only region), which matters because the issuer shares
+// its SM sub-partition with busy softmax warps.
+FM_DEV void mma_ss_w(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+FM_DEV void mma_ts_w(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+FM_DEV void mma_commit_w(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(smem_u32(bar))
+      : "memory");
+}
+
 // 32 lanes x 32 bit, 32 consecutive columns per thread (thread i <-> lane base+i).
 FM_DEV void tmem_ld32(uint32_t taddr, uint32_t* r) {
   asm volatile(

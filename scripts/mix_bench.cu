@@ -4,7 +4,7 @@
 #include <cuda_runtime.h>
 #include "../paper_2410_01359_b200/csrc/fm_ptx.cuh"
 using namespace fm;
-__global__ void __launch_bounds__(544, 1) k(long long* out, int iters, int tm_traffic) {
+__global__ void __launch_bounds__(544, 1) k(long long* out, int iters, int tm_traffic, int half) {
   extern __shared__ uint8_t raw[];
   uint8_t* sm = smem_align1024<uint8_t>(raw);
   __shared__ uint64_t bar;
@@ -24,6 +24,20 @@ __global__ void __launch_bounds__(544, 1) k(long long* out, int iters, int tm_tr
       const uint32_t idS = idesc_bf16(128, 128, 0, 0), idPV = idesc_bf16(128, 128, 0, 1);
       const uint32_t qa = smem_u32(sm), ka = qa + 32768, va = qa + 65536;
       const long long t0 = clock64();
+      if (half) {
+        // sub-step mix: S (SS M128 N64) x8 into a 64-column buffer, PV (TS N128, K=16) x4 from the other
+        const uint32_t idS64 = idesc_bf16(128, 64, 0, 0);
+        for (int it = 0; it < 2 * iters; ++it) {
+          const uint32_t sc = (it & 3) * 64;
+          for (int kk = 0; kk < 8; ++kk) {
+            const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
+            mma_ss(tb + sc, sdesc_sw128(qa + off, 16, 1024), sdesc_sw128(ka + (it & 1) * 8192 + off, 16, 1024), idS64, kk > 0);
+          }
+          for (int kk = 0; kk < 4; ++kk)
+            mma_ts(tb + 256 + ((it >> 1) & 1) * 128, tb + (sc ^ 64) + kk * 8,
+                   sdesc_sw128(va + (it & 1) * 8192 + kk * 2048, 16384, 1024), idPV, 1);
+        }
+      } else
       for (int it = 0; it < iters; ++it) {
         const uint32_t sc = (it & 1) ? 128 : 0;
         for (int kk = 0; kk < 8; ++kk) {
@@ -59,13 +73,16 @@ __global__ void __launch_bounds__(544, 1) k(long long* out, int iters, int tm_tr
 int main() {
   long long* d; cudaMalloc(&d, 2001 * 8);
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 98304 + 1024);
+  for (int hm = 0; hm < 2; ++hm)
   for (int m = 0; m < 3; ++m) {
     const int iters = 1024;
-    k<<<148, 544, 98304 + 1024>>>(d, iters, m);
+    k<<<148, 544, 98304 + 1024>>>(d, iters, m, hm);
     cudaError_t e = cudaDeviceSynchronize();
     long long h[148]; cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
     double avg = 0; for (int i = 0; i < 148; ++i) avg += h[i]; avg /= 148;
-    printf("fwd MMA mix (8 SS N128 + 8 TS N128), TMEM traffic=%d: %.0f clk per tile (ideal 1024) %s\n", m, avg / iters, cudaGetErrorString(e));
+    printf("fwd MMA mix (%s), TMEM traffic=%d: %.0f clk per 128x128 tile (ideal %d) %s\n",
+           hm ? "2 x (8 SS N64 + 4 TS N128)" : "8 SS N128 + 8 TS N128", m, avg / iters, hm ? 1280 : 1024,
+           cudaGetErrorString(e));
   }
   return 0;
 }

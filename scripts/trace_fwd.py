@@ -1,10 +1,12 @@
+"""Read the FM_TRACE clock64 trace of one forward CTA (build: scripts/build_variant.sh trace -DFM_TRACE)."""
 import ctypes, os, sys
 sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), ".."))
 os.environ["FLASHMASK_LIB"] = os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", "paper_2410_01359_b200", "libflashmask_trace.so")
-import numpy as np, torch
-import bench
-from paper_2410_01359_b200 import flashmask as fm
-calls, conf, _ = bench.build_workload("C3", 0, 1, bench.rho_gpu(fm))
+import numpy as np, torch  # noqa: E402
+import bench  # noqa: E402
+from paper_2410_01359_b200 import flashmask as fm  # noqa: E402
+cfg = sys.argv[1] if len(sys.argv) > 1 else "C3"
+calls, conf, _ = bench.build_workload(cfg, 0, 1, bench.rho_gpu(fm))
 c = calls[0]
 x = bench.make_inputs(c, torch.device("cuda", 0))
 for _ in range(2):
@@ -15,8 +17,9 @@ fm._lib.flashmask_debug_trace_fwd.argtypes = [ctypes.c_void_p]
 fm._lib.flashmask_debug_trace_fwd(buf)
 a = np.array(buf).reshape(64, 16)
 t0 = a[0, 8]
-names = ["sm0_sfull", "sm1_sfull", "sm0_pfull", "sm1_pfull", "mma_p0", "mma_p1", "mma_s0iss", "mma_s1iss", "mma_kfull", "s0_bar", "s0_p1", "s0_p2beg", "s0_p2end", "s0_stw"]
+names = ["s0full", "s1full", "p0full", "p1full", "mma_p0", "mma_p1", "mma_s0", "mma_s1", "mma_kf", "s0_xchg",
+         "s0_pass1", "-", "s0_pass2", "s0_stw"]
 print("e  " + " ".join(f"{n[:8]:>8s}" for n in names))
 for e in range(40):
-    print(f"{e:2d} " + " ".join(f"{a[e, s] - t0:8d}" for s in range(14)))
+    print(f"{e:2d} " + " ".join(f"{a[e, s] - t0:8d}" for s in range(len(names))))
 print("period", np.median(np.diff(a[5:40, 0])))
