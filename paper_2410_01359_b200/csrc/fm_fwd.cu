@@ -32,6 +32,13 @@ namespace fm { __device__ long long g_fm_trace_fwd[64 * 16]; }
   } while (0)
 #endif
 
+#ifndef FM_WAIT_P
+#define FM_WAIT_P mbar_wait  // MMA issuer waiting for P (mbar_wait_spin measured ~2% slower)
+#endif
+#ifndef FM_WAIT_S
+#define FM_WAIT_S mbar_wait  // softmax waiting for S
+#endif
+
 #ifndef FM_POLY_PAIRS
 #define FM_POLY_PAIRS 3  // of every 8 column pairs, how many use the FMA-pipe exp2 (rest: MUFU)
 #endif
@@ -162,6 +169,7 @@ __global__ void __launch_bounds__(fwd::NT, 1)
         mbar_expect_tx(&sm.k_full[ks], TB);
 #pragma unroll
         for (int c = 0; c < D / 64; ++c) tma_load_4d(sm.k[ks] + c * 16384, &tmK, &sm.k_full[ks], c * 64, hk, j * 128, b);
+        FT(11, e);
         mbar_wait(&sm.m_empty[ms], ((e / MST) & 1) ^ 1);
         if (ent_cls(ent, 0) == 1 || ent_cls(ent, 1) == 1) {
           mbar_expect_tx(&sm.m_full[ms], 128 * 16);
@@ -173,6 +181,7 @@ __global__ void __launch_bounds__(fwd::NT, 1)
         mbar_expect_tx(&sm.v_full[vs], TB);
 #pragma unroll
         for (int c = 0; c < D / 64; ++c) tma_load_4d(sm.v[vs] + c * 16384, &tmV, &sm.v_full[vs], c * 64, hk, j * 128, b);
+        FT(14, e);
       }
     }
   } else if (warp == MMA_WARP) {
@@ -190,10 +199,11 @@ __global__ void __launch_bounds__(fwd::NT, 1)
       uint32_t pv_cnt[2] = {0, 0};
       auto issue_pv = [&](int q) {
         const int pe = pend[q];
-        mbar_wait(&sm.p_full[q], pv_cnt[q] & 1);
+        FM_WAIT_P(&sm.p_full[q], pv_cnt[q] & 1);
         if (lane == 0) FT(4 + q, pe);
         const int vs = pe % VST;
         mbar_wait(&sm.v_full[vs], (pe / VST) & 1);
+        if (lane == 0 && q == 0) FT(15, pe);
         tc_fence_after();
         const uint32_t v_addr = smem_u32(sm.v[vs]);
 #pragma unroll
@@ -245,7 +255,7 @@ __global__ void __launch_bounds__(fwd::NT, 1)
     // ================================ softmax WGs ================================
     // Four warpgroups: tile q = warp / 8, column half hh = (warp / 4) % 2.  The two halves of a
     // tile share TMEM lanes (rows) and split the 128 key columns, exchanging row maxima (and at
-    // the end the row sums) through shared memory under a 256-thread named barrier.
+    // the end the row sums) through shared memory under a 64-thread named barrier per warp pair.
     const int q = warp >> 3;
     const int hh = (warp >> 2) & 1;
     const int wl = warp & 3;
@@ -258,7 +268,8 @@ __global__ void __launch_bounds__(fwd::NT, 1)
     const uint32_t tO = tbase + lane_off + 256u + (q == 0 ? 0u : static_cast<uint32_t>(D));
     const uint32_t tOh = tO + hh * (D / 2);                 // this half's O columns
     const float sl2 = a.scale_log2;
-    const uint32_t bar_id = 1 + q;
+    // the two warps holding the same 32 rows (column halves 0/1) exchange through a 64-thread barrier
+    const uint32_t bar_id = 1 + q * 4 + wl;
     float m_used = -INFINITY;  // running max of the scaled logits, log2 units (threshold-updated)
     float l = 0.f;             // this half's share of the row sum
     uint32_t cnt = 0;
@@ -269,7 +280,7 @@ __global__ void __launch_bounds__(fwd::NT, 1)
       mbar_wait(&sm.m_full[ms], (e / MST) & 1);
       if (cls != 0) {
         const int j = static_cast<int>(ent & 0xFFFFFFu);
-        mbar_wait(&sm.s_full[q], cnt & 1);
+        FM_WAIT_S(&sm.s_full[q], cnt & 1);
         if (row_t == 0 && hh == 0) FT(0 + q, e);
         tc_fence_after();
         // Pass 1: max over this half's 64 columns, 32 at a time (S stays in TMEM for pass 2).
@@ -312,7 +323,7 @@ __global__ void __launch_bounds__(fwd::NT, 1)
         const float mh = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3));
         if (row_t == 0 && q == 0 && hh == 0) FT(10, e);
         sm.xmax[q][cnt & 1][hh][row_t] = mh;
-        named_bar_sync(bar_id, 256);
+        named_bar_sync(bar_id, 64);
         const float m_tile = fmaxf(mh, sm.xmax[q][cnt & 1][hh ^ 1][row_t]) * sl2;
         if (row_t == 0 && q == 0 && hh == 0) FT(9, e);
         // Conditional rescale: the running max only moves when it grows by more than 2^8
@@ -386,7 +397,7 @@ __global__ void __launch_bounds__(fwd::NT, 1)
     }
     // ---- epilogue: O = O / l, L = m + ln(l) (Alg. 1 lines 27-28) ----
     sm.xsum[q][hh][row_t] = l;
-    named_bar_sync(bar_id, 256);
+    named_bar_sync(bar_id, 64);
     l += sm.xsum[q][hh ^ 1][row_t];
     const bool live = (cnt > 0) && (l > 0.f);
     if (cnt > 0) {

@@ -48,6 +48,23 @@ FM_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
   while (!mbar_try_wait(bar, parity)) {
   }
 }
+// Non-suspending poll (mbarrier.test_wait): for latency-critical waits where a suspended
+// try_wait was measured to wake up hundreds of cycles after the phase completed.
+FM_DEV bool mbar_test_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+FM_DEV void mbar_wait_spin(uint64_t* bar, uint32_t parity) {
+  while (!mbar_test_wait(bar, parity)) {
+  }
+}
 
 // ------------------------------------------------------------------ named barriers
 FM_DEV void named_bar_sync(uint32_t id, uint32_t nthreads) {

@@ -18,7 +18,7 @@ fm._lib.flashmask_debug_trace_fwd(buf)
 a = np.array(buf).reshape(64, 16)
 t0 = a[0, 8]
 names = ["s0full", "s1full", "p0full", "p1full", "mma_p0", "mma_p1", "mma_s0", "mma_s1", "mma_kf", "s0_xchg",
-         "s0_pass1", "-", "s0_pass2", "s0_stw"]
+         "s0_pass1", "prod_K", "s0_pass2", "s0_stw", "prod_V", "mma_vf"]
 print("e  " + " ".join(f"{n[:8]:>8s}" for n in names))
 for e in range(40):
     print(f"{e:2d} " + " ".join(f"{a[e, s] - t0:8d}" for s in range(len(names))))
