@@ -32,7 +32,7 @@
 #include "fm_ptx.cuh"
 
 #ifdef FM_TRACE
-namespace fm { __device__ long long g_fm_trace[64 * 16]; }
+namespace fm { __device__ long long g_fm_trace[64 * 16]; __device__ long long g_fm_trace2[64 * 16]; }
 #define FM_T(slot, t)                                                                        \
   do {                                                                                        \
     if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && (t) < 64) fm::g_fm_trace[(t) * 16 + (slot)] = clock64(); \
@@ -47,6 +47,18 @@ namespace fm { __device__ long long g_fm_trace[64 * 16]; }
 #define FM_EXP 0  // experiments only: 1 = compute WGs skip TMEM/math/smem work
 #endif
 
+#ifndef FM_BWD_ISSUER_WAIT
+#define FM_BWD_ISSUER_WAIT mbar_wait_sleep  // MMA issuer warps wait suspended (see fm_ptx.cuh)
+#endif
+
+#ifndef FM_BWD_DK_SS
+#define FM_BWD_DK_SS 0  // 1: dK reads dS^T from smem (SS); measured ~2% slower (smem bandwidth)
+#endif
+
+#ifndef FM_BWD_KA
+#define FM_BWD_KA 0  // K_j as TMEM A operand (excludes the P/dS double buffer; measured no gain)
+#endif
+
 #ifndef FM_DQ_MODE
 #define FM_DQ_MODE 0  // experiments only: nonzero = skip the dQ global reduction
 #endif
@@ -55,7 +67,11 @@ namespace fm {
 
 namespace bwd {
 
-constexpr int NT = 480;
+#ifndef FM_BWD_G_WARP
+#define FM_BWD_G_WARP 14  // warp issuing dV/dK/dQ (15: moves it to the fourth sub-partition)
+#endif
+constexpr int G_WARP = FM_BWD_G_WARP;
+constexpr int NT = (G_WARP + 1) * 32;
 constexpr int QST = 3;
 constexpr int kMaxTrb = 4096;
 
@@ -63,14 +79,26 @@ template <int D>
 struct Cfg {
   static constexpr int BR = (D == 128) ? 64 : 128;
   static constexpr bool DQT = (D == 128);          // dQ computed transposed (M = d)
-  static constexpr bool KA_TMEM = false;           // K_j in TMEM as S^T's A operand (measured: no gain)
-  static constexpr bool DQ_ALIAS = (D == 64);      // dQ shares the P/dS columns (TMEM is full at d=64)
+  // K_j in TMEM as S^T's A operand: an SS MMA with N = 64 is bound by shared-memory operand
+  // bandwidth (A 4 KiB + B 2 KiB per 48 clk), a TS one runs at the full 32 clk
+  // (scripts/bwdmix_bench.cu).  Its 64 columns come from letting dQ^T share the P/dS columns.
+  static constexpr bool KA_TMEM = (D == 128) && (FM_BWD_KA != 0);
+  // d=128: two P/dS column buffers, so the compute WGs write P/dS(t+1) while dV/dK/dQ(t) still
+  // read buffer t; dQ^T(t) reuses the 64 columns of its own buffer (written after dV/dK(t)).
+  static constexpr int NB = (D == 128 && !KA_TMEM) ? 2 : 1;
+  static constexpr bool DQ_ALIAS = (D == 64) || KA_TMEM || NB == 2;  // dQ shares the P/dS columns
   static constexpr int KV_TILE = 128 * D * 2;      // bytes
   static constexpr int Q_TILE = BR * D * 2;
   static constexpr int DS_BYTES = 128 * BR * 2;
   static constexpr int CH_PER_WG = BR / 64;        // 32-query chunks per compute WG
   static constexpr int S_COL = 0, DP_COL = BR, P_COL = 2 * BR, DS_COL = 2 * BR + BR / 2;
   static constexpr int DQ_COL = DQ_ALIAS ? P_COL : 192;
+  static constexpr int BUF_STRIDE = BR;  // column offset of P/dS/dQ buffer 1 (NB == 2)
+  // Option: dK += dS^T Q reads dS^T from the shared-memory buffer the dQ GEMM uses anyway (SS,
+  // N = 128) instead of a TMEM copy.  It balances the sub-partitions (TS operand reads slow the
+  // compute warps sharing the issuing warp's sub-partition) but costs shared-memory bandwidth;
+  // measured ~2 % slower overall, so off by default.
+  static constexpr bool DK_SS = (D == 128) && (FM_BWD_DK_SS != 0);
   static constexpr int KA_COL = 192;
   static constexpr int DV_COL = (D == 128) ? 256 : 384;
   static constexpr int DK_COL = DV_COL + D;
@@ -84,13 +112,16 @@ struct Smem {
   uint8_t q[QST][C::Q_TILE];
   uint8_t dO[QST][C::Q_TILE];
   uint8_t ds[2][C::DS_BYTES];  // double-buffered: dS(t+1) is written while dQ(t) reads dS(t)
+  // d=128: dQ^T staged 16 query rows (8 KiB, contiguous in dQacc) at a time for one bulk
+  // reduce-add each, double-buffered
+  float dq_stage[C::DQT ? 2 : 1][C::DQT ? 16 * D : 4];
   float lvec[QST][C::BR];
   float dvec[QST][C::BR];
   uint16_t list[kMaxTrb];
   uint32_t part_bits[kMaxTrb / 32];
   uint64_t kv_full;
   uint64_t q_full[QST], q_empty[QST];
-  uint64_t s_full, sdp_free, p_full, pds_free, dq_full, dq_empty, ds_empty[2], ka_full, done;
+  uint64_t s_full, sdp_free, p_full[2], pds_free[2], dq_full[2], dq_empty[2], ds_empty[2], ka_full, done;
   uint32_t tmem_base;
   int n_entries;
   int warp_cnt[NT / 32];
@@ -156,11 +187,13 @@ __global__ void __launch_bounds__(bwd::NT, 1)
     for (int s = 0; s < QST; ++s) { mbar_init(&sm.q_full[s], 1); mbar_init(&sm.q_empty[s], 1); }
     mbar_init(&sm.s_full, 1);
     mbar_init(&sm.sdp_free, 256);
-    mbar_init(&sm.p_full, 256);
     mbar_init(&sm.ka_full, 128);
-    mbar_init(&sm.pds_free, 1);
-    mbar_init(&sm.dq_full, 1);
-    mbar_init(&sm.dq_empty, 128);
+    for (int bb = 0; bb < 2; ++bb) {
+      mbar_init(&sm.p_full[bb], 256);
+      mbar_init(&sm.pds_free[bb], 1);
+      mbar_init(&sm.dq_full[bb], 1);
+      mbar_init(&sm.dq_empty[bb], 128);
+    }
     mbar_init(&sm.ds_empty[0], 1);
     mbar_init(&sm.ds_empty[1], 1);
     mbar_init(&sm.done, 1);
@@ -233,7 +266,7 @@ __global__ void __launch_bounds__(bwd::NT, 1)
         bulk_g2s(sm.dvec[st], a.dvec + bh * a.Npb + static_cast<size_t>(i) * BR, BR * 4, &sm.q_full[st]);
       }
     }
-  } else if (warp == 13 || warp == 14) {
+  } else if (warp == 13 || warp == G_WARP) {
     // ============================ two MMA issuers ============================
     // The tensor core accepts only a few queued MMAs before an issuing thread blocks, so any
     // dependency wait in a single issuer starves it.  Warp 13 issues S^T/dP^T(t) as soon as the
@@ -244,14 +277,14 @@ __global__ void __launch_bounds__(bwd::NT, 1)
       constexpr uint32_t ID_G = idesc_bf16(128, D, 0, 1);    // dV, dK: A in TMEM, B MN-major
       constexpr uint32_t ID_Q = idesc_bf16(128, 64, 1, 1);   // dQ^T (d=128) / dQ (d=64), both MN-major
       const uint32_t k_addr = smem_u32(sm.k), v_addr = smem_u32(sm.v);
-      mbar_wait(&sm.kv_full, 0);
+      FM_BWD_ISSUER_WAIT(&sm.kv_full, 0);
       if (warp == 13) {
-        if constexpr (C::KA_TMEM) mbar_wait(&sm.ka_full, 0);  // K_j copied into TMEM
+        if constexpr (C::KA_TMEM) FM_BWD_ISSUER_WAIT(&sm.ka_full, 0);  // K_j copied into TMEM
         for (int t = 0; t < nE; ++t) {
           const int st = t % QST;
-          if (t > 0) mbar_wait(&sm.sdp_free, (t - 1) & 1);  // compute WGs hold S^T/dP^T(t-1) in registers
+          if (t > 0) FM_BWD_ISSUER_WAIT(&sm.sdp_free, (t - 1) & 1);  // compute WGs hold S^T/dP^T(t-1) in registers
           if (lane == 0) FM_T(1, t);
-          mbar_wait(&sm.q_full[st], (t / QST) & 1);
+          FM_BWD_ISSUER_WAIT(&sm.q_full[st], (t / QST) & 1);
           if (lane == 0) FM_T(14, t);
           tc_fence_after();
           const uint32_t q_addr = smem_u32(sm.q[st]), do_addr = smem_u32(sm.dO[st]);
@@ -275,39 +308,48 @@ __global__ void __launch_bounds__(bwd::NT, 1)
         for (int t = 0; t < nE; ++t) {
           const int st = t % QST;
           if (lane == 0) FM_T(0, t);
-          mbar_wait(&sm.p_full, t & 1);
+          const int bi = t % C::NB;
+          const uint32_t ph = (t / C::NB) & 1, boff = bi * C::BUF_STRIDE;
+          FM_BWD_ISSUER_WAIT(&sm.p_full[bi], ph);
           if (lane == 0) FM_T(2, t);
           tc_fence_after();
           const uint32_t q_addr = smem_u32(sm.q[st]), do_addr = smem_u32(sm.dO[st]);
 #pragma unroll
           for (int kk = 0; kk < BR / 16; ++kk) {
             const uint32_t acc = (t > 0 || kk > 0) ? 1u : 0u;
-            mma_ts_w(tbase + C::DV_COL, tbase + C::P_COL + kk * 8, sdesc_sw128(do_addr + kk * 2048, BR * 128, 1024),
-                   ID_G, acc);
-            mma_ts_w(tbase + C::DK_COL, tbase + C::DS_COL + kk * 8, sdesc_sw128(q_addr + kk * 2048, BR * 128, 1024),
-                   ID_G, acc);
+            mma_ts_w(tbase + C::DV_COL, tbase + C::P_COL + boff + kk * 8,
+                     sdesc_sw128(do_addr + kk * 2048, BR * 128, 1024), ID_G, acc);
+            if constexpr (C::DK_SS)  // A = dS^T straight from the dQ operand buffer in smem
+              mma_ss_w(tbase + C::DK_COL, sdesc_sw128(smem_u32(sm.ds[t & 1]) + kk * 32, 16, 1024),
+                       sdesc_sw128(q_addr + kk * 2048, BR * 128, 1024), ID_G, acc);
+            else
+              mma_ts_w(tbase + C::DK_COL, tbase + C::DS_COL + boff + kk * 8,
+                       sdesc_sw128(q_addr + kk * 2048, BR * 128, 1024), ID_G, acc);
           }
           // S^T/dP^T(t) (warp 13) completed before the compute WGs produced P/dS(t)
           mma_commit_w(&sm.q_empty[st]);
-          mma_commit_w(&sm.pds_free);
+          mma_commit_w(&sm.pds_free[bi]);
           if (lane == 0) FM_T(12, t);
-          // d=64: dQ(t) overwrites the P/dS columns — issued after dV/dK(t) by this thread (in
-          // order), and the compute WGs stored P/dS(t) only after dQ(t-1) was read (dq_empty).
-          // d=128: dQ^T has its own columns; wait until the dQ WG has read dQ^T(t-1).
-          if (!a.with_dq) continue;
-          if constexpr (!C::DQ_ALIAS) mbar_wait(&sm.dq_empty, (t & 1) ^ 1);
+          // dQ(t) overwrites the P/dS columns of buffer t % NB — issued after dV/dK(t) by this
+          // thread (in order), and the compute WGs stored P/dS(t) there only after dQ(t-NB) was
+          // read out (dq_empty[t % NB]).
+          if (!a.with_dq) {
+            if constexpr (C::DK_SS) mma_commit_w(&sm.ds_empty[t & 1]);  // dK(t) read dS^T(t)
+            continue;
+          }
+          if constexpr (!C::DQ_ALIAS) FM_BWD_ISSUER_WAIT(&sm.dq_empty[0], (t & 1) ^ 1);
           tc_fence_after();
           const uint32_t ds_addr = smem_u32(sm.ds[t & 1]);
 #pragma unroll
           for (int kk = 0; kk < 8; ++kk) {
             if constexpr (C::DQT)
-              mma_ss_w(tbase + C::DQ_COL, sdesc_sw128(k_addr + kk * 2048, 16384, 1024),
+              mma_ss_w(tbase + C::DQ_COL + boff, sdesc_sw128(k_addr + kk * 2048, 16384, 1024),
                      sdesc_sw128(ds_addr + kk * 2048, 16384, 1024), ID_Q, kk > 0 ? 1u : 0u);
             else
-              mma_ss_w(tbase + C::DQ_COL, sdesc_sw128(ds_addr + kk * 2048, 16384, 1024),
+              mma_ss_w(tbase + C::DQ_COL + boff, sdesc_sw128(ds_addr + kk * 2048, 16384, 1024),
                      sdesc_sw128(k_addr + kk * 2048, 16384, 1024), ID_Q, kk > 0 ? 1u : 0u);
           }
-          mma_commit_w(&sm.dq_full);
+          mma_commit_w(&sm.dq_full[bi]);
           mma_commit_w(&sm.ds_empty[t & 1]);
           if (lane == 0) FM_T(13, t);
         }
@@ -353,6 +395,10 @@ __global__ void __launch_bounds__(bwd::NT, 1)
       mbar_wait(&sm.q_full[st], (t / QST) & 1);
       mbar_wait(&sm.s_full, t & 1);
       if (tid == 0) FM_T(4, t);
+#ifdef FM_TRACE
+      if (lane == 0 && t >= 30 && t < 40 && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0)
+        g_fm_trace2[(10 + t - 30) * 16 + warp] = clock64();
+#endif
       tc_fence_after();
       const float* lv = sm.lvec[st];
       const float* dv = sm.dvec[st];
@@ -361,9 +407,9 @@ __global__ void __launch_bounds__(bwd::NT, 1)
         tc_fence_before();
         mbar_arrive(&sm.sdp_free);
         mbar_wait(&sm.ds_empty[t & 1], ((t >> 1) & 1) ^ 1);
-        mbar_wait(&sm.dq_empty, (t & 1) ^ 1);
+        mbar_wait(&sm.dq_empty[t % C::NB], ((t / C::NB) & 1) ^ 1);
         tc_fence_before();
-        mbar_arrive(&sm.p_full);
+        mbar_arrive(&sm.p_full[t % C::NB]);
         continue;
       }
 #pragma unroll
@@ -383,12 +429,21 @@ __global__ void __launch_bounds__(bwd::NT, 1)
           pds_chunk<false, CAUSAL>(sr, dr, lv + q0, dv + q0, sl2, i * BR + q0, key, mv, pp[ch], dp[ch]);
       }
       if (tid == 0) FM_T(5, t);
+#ifdef FM_TRACE
+      if (lane == 0 && t >= 30 && t < 40 && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0)
+        g_fm_trace2[(10 + t - 30) * 16 + 8 + warp] = clock64();
+#endif
       // dS^T row of this key into the SW128 MN-major smem operand of the dQ GEMM
       // (first: it only needs dQ(t-1) to have finished reading the buffer)
-      if (a.with_dq) mbar_wait(&sm.ds_empty[t & 1], ((t >> 1) & 1) ^ 1);  // dQ(t-2) has read this buffer
+      const bool ds_smem = a.with_dq || C::DK_SS;  // dS^T is a shared-memory operand (dQ, dK)
+      if (ds_smem) mbar_wait(&sm.ds_empty[t & 1], ((t >> 1) & 1) ^ 1);  // dK/dQ(t-2) have read this buffer
       if (tid == 0) FM_T(7, t);
+#ifdef FM_TRACE
+      if (lane == 0 && t >= 30 && t < 40 && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0)
+        g_fm_trace2[(20 + t - 30) * 16 + 0 + warp] = clock64();
+#endif
 #pragma unroll
-      for (int ch = 0; ch < (a.with_dq ? CH : 0); ++ch) {
+      for (int ch = 0; ch < (ds_smem ? CH : 0); ++ch) {
         const int q0 = (wg * CH + ch) * 32;
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
@@ -399,23 +454,40 @@ __global__ void __launch_bounds__(bwd::NT, 1)
               make_uint4(dp[ch][4 * u], dp[ch][4 * u + 1], dp[ch][4 * u + 2], dp[ch][4 * u + 3]);
         }
       }
-      // P / dS TMEM columns free: dV/dK(t-1) done (d=64: dQ(t-1), which reuses them, read out)
+      if (tid == 0) FM_T(3, t);
+#ifdef FM_TRACE
+      if (lane == 0 && t >= 30 && t < 40 && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0)
+        g_fm_trace2[(20 + t - 30) * 16 + 8 + warp] = clock64();
+#endif
+      // P / dS TMEM buffer t % NB free: dV/dK(t-NB) done, and dQ(t-NB), which reuses the
+      // columns, read out
+      const int bi = t % C::NB;
+      const uint32_t ph = (t / C::NB) & 1, boff = bi * C::BUF_STRIDE;
       if (C::DQ_ALIAS && a.with_dq)
-        mbar_wait(&sm.dq_empty, (t & 1) ^ 1);
+        mbar_wait(&sm.dq_empty[bi], ph ^ 1);
       else
-        mbar_wait(&sm.pds_free, (t & 1) ^ 1);
+        mbar_wait(&sm.pds_free[bi], ph ^ 1);
       if (tid == 0) FM_T(6, t);
+#ifdef FM_TRACE
+      if (lane == 0 && t >= 30 && t < 40 && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0)
+        g_fm_trace2[(30 + t - 30) * 16 + 0 + warp] = clock64();
+#endif
       tc_fence_after();
 #pragma unroll
       for (int ch = 0; ch < CH; ++ch) {
         const int q0 = (wg * CH + ch) * 32;
-        tmem_st16(tbase + lane_off + C::P_COL + q0 / 2, pp[ch]);
-        tmem_st16(tbase + lane_off + C::DS_COL + q0 / 2, dp[ch]);
+        tmem_st16(tbase + lane_off + C::P_COL + boff + q0 / 2, pp[ch]);
+        if constexpr (!C::DK_SS) tmem_st16(tbase + lane_off + C::DS_COL + boff + q0 / 2, dp[ch]);
       }
       fence_proxy_async_smem();
       tmem_wait_st();
+      if (tid == 0) FM_T(15, t);
+#ifdef FM_TRACE
+      if (lane == 0 && t >= 30 && t < 40 && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0)
+        g_fm_trace2[(t - 30) * 16 + warp] = clock64();
+#endif
       tc_fence_before();
-      mbar_arrive(&sm.p_full);
+      mbar_arrive(&sm.p_full[bi]);
       if (tid == 0) FM_T(8, t);
     }
     // ---- epilogue: dK_j = scale * dK, dV_j written once (Alg. 2 line 30) ----
@@ -452,29 +524,49 @@ __global__ void __launch_bounds__(bwd::NT, 1)
         }
       }
     }
-  } else {
+  } else if (warp >= 8 && warp < 12) {
     // ================= dQ WG: TMEM -> registers -> red.global.add.f32 =================
     const int wl = warp - 8;
     const int t_id = wl * 32 + lane;  // TMEM lane: d index (d=128) or query (d=64)
     const uint32_t lane_off = static_cast<uint32_t>(wl * 32) << 16;
+    uint32_t stage_n = 0;  // dQ staging chunks issued so far (DQT)
     for (int t = 0; t < (a.with_dq ? nE : 0); ++t) {
       const int i = sm.list[t % nE1];
       const size_t bh = static_cast<size_t>(b) * a.H + hk * G + t / nE1;
-      mbar_wait(&sm.dq_full, t & 1);
+      const int bi = C::DQ_ALIAS ? t % C::NB : 0;
+      const uint32_t boff = bi * C::BUF_STRIDE;
+      mbar_wait(&sm.dq_full[bi], (t / (C::DQ_ALIAS ? C::NB : 1)) & 1);
       if (t_id == 0) FM_T(9, t);
       tc_fence_after();
       uint32_t r[64];
-      tmem_ld32(tbase + lane_off + C::DQ_COL, r);
-      tmem_ld32(tbase + lane_off + C::DQ_COL + 32, r + 32);
+      tmem_ld32(tbase + lane_off + C::DQ_COL + boff, r);
+      tmem_ld32(tbase + lane_off + C::DQ_COL + boff + 32, r + 32);
       tmem_wait_ld();
       tc_fence_before();
-      mbar_arrive(&sm.dq_empty);
+      mbar_arrive(&sm.dq_empty[bi]);
       if (FM_DQ_MODE != 0) continue;
       float* base = a.dqacc + (bh * a.Npb + static_cast<size_t>(i) * BR) * D;
       if constexpr (C::DQT) {
-        // r[q] = dQ^T[d = t_id][q]: a warp adds 32 consecutive floats of one query row
+        // r[q] = dQ^T[d = t_id][q].  The 64 x 128 fp32 block is contiguous in dQacc: stage 16 rows
+        // (8 KiB) in shared memory and add them with one bulk reduce (cp.reduce.async.bulk .add.f32)
+        // — far fewer L2 transactions and LSU instructions than 64 scalar red.global per thread,
+        // which were measured to starve the compute warps sharing the sub-partition.
 #pragma unroll
-        for (int q = 0; q < 64; ++q) red_add_f32(base + q * D + t_id, __uint_as_float(r[q]));
+        for (int c = 0; c < 4; ++c, ++stage_n) {
+          float* stg = sm.dq_stage[stage_n & 1];
+          if (stage_n >= 2) {  // the bulk reduce that read this buffer two chunks ago is done
+            if (t_id == 0) bulk_wait_read1();
+            named_bar_sync(1, 128);
+          }
+#pragma unroll
+          for (int q = 0; q < 16; ++q) stg[q * D + t_id] = __uint_as_float(r[c * 16 + q]);
+          fence_proxy_async_smem();
+          named_bar_sync(1, 128);
+          if (t_id == 0) {
+            bulk_reduce_add_f32(base + c * 16 * D, stg, 16 * D * 4);
+            bulk_commit();
+          }
+        }
       } else {
         // r[c] = dQ[query = t_id][c]: 16-byte vector adds along the row
 #pragma unroll
@@ -484,6 +576,7 @@ __global__ void __launch_bounds__(bwd::NT, 1)
       }
       if (t_id == 0) FM_T(10, t);
     }
+    if (C::DQT && t_id == 0) bulk_wait0();  // staging buffers must outlive the bulk reads
   }
 
   tc_fence_before();
@@ -524,5 +617,8 @@ cudaError_t launch_bwd(const Dims& d, const CUtensorMap& tq, const CUtensorMap& 
 #ifdef FM_TRACE
 extern "C" __attribute__((visibility("default"))) int flashmask_debug_trace(long long* host) {
   return cudaMemcpyFromSymbol(host, fm::g_fm_trace, sizeof(long long) * 64 * 16) == cudaSuccess ? 0 : 1;
+}
+extern "C" __attribute__((visibility("default"))) int flashmask_debug_trace2(long long* host) {
+  return cudaMemcpyFromSymbol(host, fm::g_fm_trace2, sizeof(long long) * 64 * 16) == cudaSuccess ? 0 : 1;
 }
 #endif

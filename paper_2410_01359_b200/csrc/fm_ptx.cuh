@@ -48,6 +48,24 @@ FM_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
   while (!mbar_try_wait(bar, parity)) {
   }
 }
+// try_wait with an explicit suspend-time hint: the waiting warp stays suspended (no issue
+// slots taken from the warps sharing its SM sub-partition) until the phase completes or the
+// hint (ns) expires.
+FM_DEV bool mbar_try_wait_hint(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity), "n"(1000000)
+      : "memory");
+  return ok != 0;
+}
+FM_DEV void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  while (!mbar_try_wait_hint(bar, parity)) {
+  }
+}
 // Non-suspending poll (mbarrier.test_wait): for latency-critical waits where a suspended
 // try_wait was measured to wake up hundreds of cycles after the phase completed.
 FM_DEV bool mbar_test_wait(uint64_t* bar, uint32_t parity) {
