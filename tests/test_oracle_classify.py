@@ -207,3 +207,23 @@ def test_ragged_tiles():
                     assert blk.all()
                 if cm[i, j] == fo.UNMASKED:
                     assert not blk.any()
+
+
+@pytest.mark.parametrize("fam", wm.FAMILIES)
+def test_rule_r_matches_exact_skip_on_families(fam):
+    """SURVEY §8(f) f3 evaluation: an exact (union-coverage) classification cannot skip more
+    tiles than rule R on the benchmark mask families — every fully masked 128×128 tile
+    (brute force on the dense mask) is already SKIP under Eq. 4 + causal — and it
+    would turn only a few per cent of all tiles from PARTIAL into UNMASKED (which saves mask
+    ALU work, not MMAs)."""
+    N, T = 4096, 32
+    rng = np.random.default_rng(11)
+    for _ in range(2):
+        m = wm.sample_family(fam, N, rng, (3, 7))
+        vec = fo.expand(m.sri, m.causal, N)
+        _, cnt, _ = fo.classify(vec, 128, 128)
+        dense = fo.to_dense(vec).reshape(T, 128, T, 128).transpose(0, 2, 1, 3).reshape(T, T, -1)
+        all_masked = int(dense.all(-1).sum())
+        none_masked = int((~dense.any(-1)).sum())
+        assert cnt[0] == all_masked, (fam, cnt, all_masked)
+        assert none_masked - cnt[2] <= 0.03 * T * T, (fam, cnt, none_masked)
