@@ -67,6 +67,27 @@ bool make_map(CUtensorMap* m, const void* ptr, const fm::Dims& d, int heads, int
   return true;
 }
 
+// fp32 dQ accumulator [B*H*Npb, D] viewed 2-D for TMA tensor reduce-adds: box = 16 rows x 32
+// columns (128 B), 128-byte swizzle (d=64 backward, fm_bwd.cu).
+bool make_dq_map(CUtensorMap* m, float* dqacc, const fm::Dims& d, std::string* err) {
+  auto enc = get_encode();
+  if (!enc) {
+    *err = "cuTensorMapEncodeTiled unavailable";
+    return false;
+  }
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(d.D), static_cast<cuuint64_t>(d.B) * d.H * d.Npb};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(d.D) * 4};
+  cuuint32_t box[2] = {32, 16};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, dqacc, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    *err = "cuTensorMapEncodeTiled (dQ accumulator) failed with CUresult " + std::to_string(static_cast<int>(r));
+    return false;
+  }
+  return true;
+}
+
 fm_status check_params(const fm_params* p, fm::Dims* d, bool need_attention) {
   if (!p) return fail(FM_ERR_INVALID_ARGUMENT, "params is NULL");
   if (p->batch < 1 || p->seqlen < 1 || p->num_heads < 1)
@@ -348,7 +369,9 @@ fm_status flashmask_bwd(const fm_params* p, const void* q, const void* k, const 
   a.dv = dv;
   const bool deterministic = (p->flags & FM_FLAG_DETERMINISTIC) != 0;
   a.with_dq = deterministic ? 0 : 1;
-  e = timed(FM_KERNEL_BWD, st, [&] { return fm::launch_bwd(d, tq, tk, tv, tdo, a, st); });
+  CUtensorMap tdq;
+  if (!make_dq_map(&tdq, w.dqacc, d, &err)) return fail(FM_ERR_CUDA, err);
+  e = timed(FM_KERNEL_BWD, st, [&] { return fm::launch_bwd(d, tq, tk, tv, tdo, tdq, a, st); });
   if (e != cudaSuccess) return cuda_fail(e, "backward kernel");
   if (!deterministic) {
     e = timed(FM_KERNEL_DQ_CONVERT, st, [&] { return fm::launch_dq_convert(d, w.dqacc, dq, st); });

@@ -63,6 +63,12 @@ namespace fm { __device__ long long g_fm_trace[64 * 16]; __device__ long long g_
 #define FM_DQ_MODE 0  // experiments only: nonzero = skip the dQ global reduction
 #endif
 
+#ifndef FM_DQ_RED
+// d=128 dQ^T reduction path: 0 = stage through shared memory + bulk reduce-add,
+// 1 = scalar red.global from registers, 2 = lane-quad transposes + red.global.v4
+#define FM_DQ_RED 0
+#endif
+
 namespace fm {
 
 namespace bwd {
@@ -72,8 +78,28 @@ namespace bwd {
 #endif
 constexpr int G_WARP = FM_BWD_G_WARP;
 constexpr int NT = (G_WARP + 1) * 32;
-constexpr int QST = 3;
-constexpr int kMaxTrb = 4096;
+#ifndef FM_QST
+#define FM_QST 3
+#endif
+constexpr int QST = FM_QST;
+#ifndef FM_DQ_NSTAGE
+#define FM_DQ_NSTAGE 2
+#endif
+constexpr int DQ_NSTAGE = FM_DQ_NSTAGE;  // 8 KiB dQ^T staging buffers (d=128)
+#ifndef FM_MAXTRB
+#define FM_MAXTRB 4096
+#endif
+constexpr int kMaxTrb = FM_MAXTRB;  // d=128 (Br=64); d=64 (Br=128) uses half: the same max N
+// d=64 dQ reduction: each dQ warp stages its 32 query rows as 16-row x 32-column fp32 boxes
+// (2 KiB, 128-byte swizzle) for TMA tensor reduce-adds, DQ64_NBUF boxes in flight per warp
+constexpr int DQ64_NBUF = 3;
+#ifndef FM_DQ_CROWS
+#define FM_DQ_CROWS 16
+#endif
+constexpr int DQ_CROWS = FM_DQ_CROWS;  // query rows per dQ^T staging chunk (d=128)
+#ifndef FM_BWD_ROT
+#define FM_BWD_ROT 0  // experiment: start each key tile's row loop at its diagonal (wrap around)
+#endif
 
 template <int D>
 struct Cfg {
@@ -102,6 +128,7 @@ struct Cfg {
   static constexpr int KA_COL = 192;
   static constexpr int DV_COL = (D == 128) ? 256 : 384;
   static constexpr int DK_COL = DV_COL + D;
+  static constexpr int MAXTRB = (D == 128) ? kMaxTrb : kMaxTrb / 2;
 };
 
 template <int D>
@@ -114,16 +141,17 @@ struct Smem {
   uint8_t ds[2][C::DS_BYTES];  // double-buffered: dS(t+1) is written while dQ(t) reads dS(t)
   // d=128: dQ^T staged 16 query rows (8 KiB, contiguous in dQacc) at a time for one bulk
   // reduce-add each, double-buffered
-  float dq_stage[C::DQT ? 2 : 1][C::DQT ? 16 * D : 4];
+  float dq_stage[C::DQT ? DQ_NSTAGE : 4 * DQ64_NBUF][C::DQT ? DQ_CROWS * D : 16 * 32];
   float lvec[QST][C::BR];
   float dvec[QST][C::BR];
-  uint16_t list[kMaxTrb];
-  uint32_t part_bits[kMaxTrb / 32];
+  uint16_t list[C::MAXTRB];
+  uint32_t part_bits[C::MAXTRB / 32];
   uint64_t kv_full;
   uint64_t q_full[QST], q_empty[QST];
   uint64_t s_full, sdp_free, p_full[2], pds_free[2], dq_full[2], dq_empty[2], ds_empty[2], ka_full, done;
   uint32_t tmem_base;
   int n_entries;
+  int rot;
   int warp_cnt[NT / 32];
 };
 
@@ -167,7 +195,7 @@ template <int D, bool CAUSAL, bool OUT_F32>
 __global__ void __launch_bounds__(bwd::NT, 1)
     fm_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                   const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO,
-                  const BwdArgs a) {
+                  const __grid_constant__ CUtensorMap tmDQ, const BwdArgs a) {
   using namespace bwd;
   using C = Cfg<D>;
   using S = Smem<D>;
@@ -228,12 +256,24 @@ __global__ void __launch_bounds__(bwd::NT, 1)
       __syncthreads();
     }
     if (tid == 0) sm.n_entries = base;
+    if (FM_BWD_ROT) {
+      if (tid == 0) sm.rot = 0;
+      __syncthreads();
+      // first list entry at or below the diagonal of this key tile
+      for (int t = tid; t < base; t += NT)
+        if (sm.list[t] * BR >= j * 128 && (t == 0 || sm.list[t - 1] * BR < j * 128)) sm.rot = t;
+    }
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   // work items t = (query head of the group, visited row tile): t / nE1 selects the head
   const int nE1 = sm.n_entries;
+  const int rot = FM_BWD_ROT ? sm.rot : 0;
+  auto lidx = [&](int t) {
+    int x = t % nE1 + rot;
+    return x >= nE1 ? x - nE1 : x;
+  };
   const int nE = nE1 * G;
   const uint32_t tbase = sm.tmem_base;
 
@@ -251,7 +291,7 @@ __global__ void __launch_bounds__(bwd::NT, 1)
         tma_load_4d(sm.v + c * 16384, &tmV, &sm.kv_full, c * 64, hk, j * 128, b);
       }
       for (int t = 0; t < nE; ++t) {
-        const int i = sm.list[t % nE1];
+        const int i = sm.list[lidx(t)];
         const int hq = hk * G + t / nE1;
         const size_t bh = static_cast<size_t>(b) * a.H + hq;
         const int st = t % QST;
@@ -388,7 +428,7 @@ __global__ void __launch_bounds__(bwd::NT, 1)
       }
     }
     for (int t = 0; t < nE; ++t) {
-      const int t1 = t % nE1;
+      const int t1 = lidx(t);
       const int i = sm.list[t1];
       const bool partial = (sm.part_bits[t1 >> 5] >> (t1 & 31)) & 1u;
       const int st = t % QST;
@@ -531,7 +571,7 @@ __global__ void __launch_bounds__(bwd::NT, 1)
     const uint32_t lane_off = static_cast<uint32_t>(wl * 32) << 16;
     uint32_t stage_n = 0;  // dQ staging chunks issued so far (DQT)
     for (int t = 0; t < (a.with_dq ? nE : 0); ++t) {
-      const int i = sm.list[t % nE1];
+      const int i = sm.list[lidx(t)];
       const size_t bh = static_cast<size_t>(b) * a.H + hk * G + t / nE1;
       const int bi = C::DQ_ALIAS ? t % C::NB : 0;
       const uint32_t boff = bi * C::BUF_STRIDE;
@@ -544,39 +584,88 @@ __global__ void __launch_bounds__(bwd::NT, 1)
       tmem_wait_ld();
       tc_fence_before();
       mbar_arrive(&sm.dq_empty[bi]);
-      if (FM_DQ_MODE != 0) continue;
+      if (FM_DQ_MODE == 1) continue;
       float* base = a.dqacc + (bh * a.Npb + static_cast<size_t>(i) * BR) * D;
-      if constexpr (C::DQT) {
+      if constexpr (C::DQT && FM_DQ_RED == 1) {
+        // r[q] = dQ^T[d = t_id][q]: one coalesced 128-B scalar reduction per warp and query
+#pragma unroll
+        for (int q = 0; q < 64; ++q) red_add_f32(base + q * D + t_id, __uint_as_float(r[q]));
+      } else if constexpr (C::DQT && FM_DQ_RED == 2) {
+        // 4 x 4 transposes inside each lane quad (two xor butterflies), then 16-B vector
+        // reductions: lane 4g+c ends with dQ[q = 4m+c][d = wl*32 + 4g .. +3] in x[0..3].
+        const bool b1 = (lane & 2) != 0, b0 = (lane & 1) != 0;
+        float* rowp = base + (lane & 3) * D + wl * 32 + (lane & ~3);
+#pragma unroll
+        for (int m = 0; m < 16; ++m) {
+          float x0 = __uint_as_float(r[4 * m]), x1 = __uint_as_float(r[4 * m + 1]);
+          float x2 = __uint_as_float(r[4 * m + 2]), x3 = __uint_as_float(r[4 * m + 3]);
+          {
+            const float s0 = b1 ? x0 : x2, s1 = b1 ? x1 : x3;
+            const float g0 = __shfl_xor_sync(0xffffffffu, s0, 2), g1 = __shfl_xor_sync(0xffffffffu, s1, 2);
+            if (b1) { x0 = g0; x1 = g1; } else { x2 = g0; x3 = g1; }
+          }
+          {
+            const float s0 = b0 ? x0 : x1, s1 = b0 ? x2 : x3;
+            const float g0 = __shfl_xor_sync(0xffffffffu, s0, 1), g1 = __shfl_xor_sync(0xffffffffu, s1, 1);
+            if (b0) { x0 = g0; x2 = g1; } else { x1 = g0; x3 = g1; }
+          }
+          red_add_v4_f32(rowp + 4 * m * D, x0, x1, x2, x3);
+        }
+      } else if constexpr (C::DQT) {
         // r[q] = dQ^T[d = t_id][q].  The 64 x 128 fp32 block is contiguous in dQacc: stage 16 rows
         // (8 KiB) in shared memory and add them with one bulk reduce (cp.reduce.async.bulk .add.f32)
         // — far fewer L2 transactions and LSU instructions than 64 scalar red.global per thread,
         // which were measured to starve the compute warps sharing the sub-partition.
 #pragma unroll
-        for (int c = 0; c < 4; ++c, ++stage_n) {
-          float* stg = sm.dq_stage[stage_n & 1];
-          if (stage_n >= 2) {  // the bulk reduce that read this buffer two chunks ago is done
-            if (t_id == 0) bulk_wait_read1();
+        for (int c = 0; c < 64 / DQ_CROWS; ++c, ++stage_n) {
+          float* stg = sm.dq_stage[stage_n % DQ_NSTAGE];
+          if (stage_n >= DQ_NSTAGE) {  // the bulk reduce that read this buffer DQ_NSTAGE chunks ago is done
+            if (t_id == 0) bulk_wait_read<DQ_NSTAGE - 1>();
             named_bar_sync(1, 128);
           }
+          if (FM_DQ_MODE != 3) {
 #pragma unroll
-          for (int q = 0; q < 16; ++q) stg[q * D + t_id] = __uint_as_float(r[c * 16 + q]);
+            for (int q = 0; q < DQ_CROWS; ++q) stg[q * D + t_id] = __uint_as_float(r[c * DQ_CROWS + q]);
+          }
           fence_proxy_async_smem();
           named_bar_sync(1, 128);
-          if (t_id == 0) {
-            bulk_reduce_add_f32(base + c * 16 * D, stg, 16 * D * 4);
+          if (t_id == 0 && FM_DQ_MODE != 2) {
+            bulk_reduce_add_f32(base + c * DQ_CROWS * D, stg, DQ_CROWS * D * 4);
             bulk_commit();
           }
         }
       } else {
-        // r[c] = dQ[query = t_id][c]: 16-byte vector adds along the row
+        // d=64: r[c] = dQ[query = t_id][c].  The warp's 32 rows go out as four 16-row x 32-column
+        // boxes, each written into a 128-byte-swizzled stage (16-B chunk c of row l at c ^ (l & 7):
+        // conflict-free, no lane-dependent register index) and added by one TMA tensor reduce.
+        const int row0 = static_cast<int>(bh * a.Npb) + i * BR + wl * 32;
 #pragma unroll
-        for (int c4 = 0; c4 < 16; ++c4)
-          red_add_v4_f32(base + t_id * D + c4 * 4, __uint_as_float(r[4 * c4]), __uint_as_float(r[4 * c4 + 1]),
-                         __uint_as_float(r[4 * c4 + 2]), __uint_as_float(r[4 * c4 + 3]));
+        for (int bx = 0; bx < 4; ++bx, ++stage_n) {
+          const int rh = bx >> 1, ch = bx & 1;  // 16-row half, 32-column half
+          float* stg = sm.dq_stage[wl * DQ64_NBUF + stage_n % DQ64_NBUF];
+          if (stage_n >= DQ64_NBUF) {
+            if (lane == 0) bulk_wait_read<DQ64_NBUF - 1>();
+            __syncwarp();
+          }
+          if ((lane >> 4) == rh) {
+            const int rl = lane & 15;
+#pragma unroll
+            for (int c = 0; c < 8; ++c)
+              *reinterpret_cast<float4*>(reinterpret_cast<uint8_t*>(stg) + rl * 128 + ((c ^ (rl & 7)) << 4)) =
+                  make_float4(__uint_as_float(r[ch * 32 + 4 * c]), __uint_as_float(r[ch * 32 + 4 * c + 1]),
+                              __uint_as_float(r[ch * 32 + 4 * c + 2]), __uint_as_float(r[ch * 32 + 4 * c + 3]));
+          }
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            tma_reduce_add_2d(&tmDQ, stg, ch * 32, row0 + rh * 16);
+            bulk_commit();
+          }
+        }
       }
       if (t_id == 0) FM_T(10, t);
     }
-    if (C::DQT && t_id == 0) bulk_wait0();  // staging buffers must outlive the bulk reads
+    if (C::DQT ? t_id == 0 : lane == 0) bulk_wait0();  // staging buffers must outlive the bulk reads
   }
 
   tc_fence_before();
@@ -589,19 +678,20 @@ __global__ void __launch_bounds__(bwd::NT, 1)
 
 template <int D, bool CAUSAL, bool OUT_F32>
 static cudaError_t launch_bwd_t(const Dims& d, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
-                                const CUtensorMap& tdo, const BwdArgs& a, cudaStream_t st) {
+                                const CUtensorMap& tdo, const CUtensorMap& tdq, const BwdArgs& a, cudaStream_t st) {
   auto kern = fm_bwd_kernel<D, CAUSAL, OUT_F32>;
   const size_t smem = sizeof(bwd::Smem<D>) + 1024;
+  static_assert(sizeof(bwd::Smem<D>) + 1024 <= 232448, "shared memory budget");
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (e != cudaSuccess) return e;
   dim3 grid(d.Tc, d.Hkv, d.B);
-  kern<<<grid, bwd::NT, smem, st>>>(tq, tk, tv, tdo, a);
+  kern<<<grid, bwd::NT, smem, st>>>(tq, tk, tv, tdo, tdq, a);
   return cudaGetLastError();
 }
 
 cudaError_t launch_bwd(const Dims& d, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
-                       const CUtensorMap& tdo, const BwdArgs& a, cudaStream_t st) {
-#define FM_B(DD, CC, FF) return launch_bwd_t<DD, CC, FF>(d, tq, tk, tv, tdo, a, st)
+                       const CUtensorMap& tdo, const CUtensorMap& tdq, const BwdArgs& a, cudaStream_t st) {
+#define FM_B(DD, CC, FF) return launch_bwd_t<DD, CC, FF>(d, tq, tk, tv, tdo, tdq, a, st)
   if (d.D == 128) {
     if (d.causal) { if (d.out_f32) FM_B(128, true, true); else FM_B(128, true, false); }
     else { if (d.out_f32) FM_B(128, false, true); else FM_B(128, false, false); }

@@ -88,7 +88,7 @@ cudaError_t launch_fwd(const Dims& d, const CUtensorMap& tq, const CUtensorMap& 
 cudaError_t launch_bwd_pre(const Dims& d, const void* o, const void* dout, const float* lse, float* dvec, float* l2,
                            float* dqacc, cudaStream_t st);
 cudaError_t launch_bwd(const Dims& d, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
-                       const CUtensorMap& tdo, const BwdArgs& a, cudaStream_t st);
+                       const CUtensorMap& tdo, const CUtensorMap& tdq, const BwdArgs& a, cudaStream_t st);
 cudaError_t launch_dq_convert(const Dims& d, const float* dqacc, void* dq, cudaStream_t st);
 cudaError_t launch_dq(const Dims& d, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
                       const CUtensorMap& tdo, const DqArgs& a, cudaStream_t st);

@@ -118,6 +118,13 @@ FM_DEV void bulk_reduce_add_f32(float* gdst, const void* smem_src, uint32_t byte
                "r"(smem_u32(smem_src)), "r"(bytes)
                : "memory");
 }
+// TMA tensor add-reduction shared -> global, 2-D tile (coordinates innermost first).
+FM_DEV void tma_reduce_add_2d(const CUtensorMap* m, const void* smem_src, int c0, int c1) {
+  asm volatile("cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.tile.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(m)),
+               "r"(smem_u32(smem_src)), "r"(c0), "r"(c1)
+               : "memory");
+}
 // TMA tensor add-reduction shared -> global, 3-D tile (coordinates innermost first).
 FM_DEV void tma_reduce_add_3d(const CUtensorMap* m, const void* smem_src, int c0, int c1, int c2) {
   asm volatile(
@@ -127,6 +134,8 @@ FM_DEV void tma_reduce_add_3d(const CUtensorMap* m, const void* smem_src, int c0
       : "memory");
 }
 FM_DEV void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
+template <int N>
+FM_DEV void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory"); }
 // fp32 reductions into global memory (no return value)
 FM_DEV void red_add_f32(float* p, float v) { asm volatile("red.global.add.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory"); }
 FM_DEV void red_add_v4_f32(float* p, float a, float b, float c, float d) {
