@@ -171,54 +171,74 @@ cudaError_t launch_classify(const int32_t* ext8, const Dims& d, int br, int bc, 
   return cudaGetLastError();
 }
 
+__device__ __forceinline__ uint32_t pack_bf16_rn(float a, float b) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+
 // ---------------------------------------------------------------------------------------
-// K3: backward preprocess (Alg. 2 line 4, D per row — DESIGN.md R5).  One warp per
-// (b, h, r), r < Npb: D = sum_c dO[r,c] * O[r,c]; l2 = lse * log2(e), or +inf when the row
-// is empty (lse = -inf) or padded (r >= N) so that exp2(S - l2) = 0 exactly; zero dQacc.
+// K3: backward preprocess (Alg. 2 line 4, D per row — DESIGN.md R5).  A group of D/8
+// threads per (b, h, r), r < Npb, each owning 8 consecutive columns (16-byte loads):
+// D = sum_c dO[r,c] * O[r,c]; l2 = lse * log2(e), or +inf when the row is empty (lse = -inf)
+// or padded (r >= N) so that exp2(S - l2) = 0 exactly; zero the row of dQacc.
 // ---------------------------------------------------------------------------------------
+__device__ __forceinline__ void bf16x8_to_f32(const uint4& u, float* f) {
+  const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    f[2 * k] = __uint_as_float(w[k] << 16);
+    f[2 * k + 1] = __uint_as_float(w[k] & 0xFFFF0000u);
+  }
+}
+
 template <int D, bool OUT_F32>
 __global__ void __launch_bounds__(256) k3_bwd_pre(const void* __restrict__ o, const __nv_bfloat16* __restrict__ dout,
                                                   const float* __restrict__ lse, int B, int N, int H, int Npb,
                                                   float* __restrict__ dvec, float* __restrict__ l2,
                                                   float* __restrict__ dqacc) {
-  const long gw = (static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
+  constexpr int G = D / 8;  // threads per row
+  const long gt = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const long row = gt / G;
+  const int part = static_cast<int>(gt % G);
   const long total = static_cast<long>(B) * H * Npb;
-  if (gw >= total) return;
-  const int r = static_cast<int>(gw % Npb);
-  const long bh = gw / Npb;
+  const bool active = row < total;
+  const long rr = active ? row : 0;
+  const int r = static_cast<int>(rr % Npb);
+  const long bh = rr / Npb;
   const int h = static_cast<int>(bh % H), b = static_cast<int>(bh / H);
-  constexpr int PER = D / 32;
   float acc = 0.f;
-  if (r < N) {
-    const size_t off = ((static_cast<size_t>(b) * N + r) * H + h) * D + lane * PER;
-#pragma unroll
-    for (int t = 0; t < PER; ++t) {
-      float ov;
-      if constexpr (OUT_F32)
-        ov = static_cast<const float*>(o)[off + t];
-      else
-        ov = __bfloat162float(static_cast<const __nv_bfloat16*>(o)[off + t]);
-      acc += ov * __bfloat162float(dout[off + t]);
+  if (active && r < N) {
+    const size_t off = ((static_cast<size_t>(b) * N + r) * H + h) * D + part * 8;
+    float ov[8], dv[8];
+    bf16x8_to_f32(*reinterpret_cast<const uint4*>(dout + off), dv);
+    if constexpr (OUT_F32) {
+      const float4 a = *reinterpret_cast<const float4*>(static_cast<const float*>(o) + off);
+      const float4 c = *reinterpret_cast<const float4*>(static_cast<const float*>(o) + off + 4);
+      ov[0] = a.x; ov[1] = a.y; ov[2] = a.z; ov[3] = a.w; ov[4] = c.x; ov[5] = c.y; ov[6] = c.z; ov[7] = c.w;
+    } else {
+      bf16x8_to_f32(*reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(o) + off), ov);
     }
 #pragma unroll
-    for (int s = 16; s > 0; s >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, s);
+    for (int t = 0; t < 8; ++t) acc = fmaf(ov[t], dv[t], acc);
   }
-  if (lane == 0) {
+#pragma unroll
+  for (int s = G / 2; s > 0; s >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, s);
+  if (!active) return;
+  if (part == 0) {
     const size_t ri = static_cast<size_t>(bh) * Npb + r;
     dvec[ri] = (r < N) ? acc : 0.f;
-    float lv = (r < N) ? lse[static_cast<size_t>(bh) * N + r] : -INFINITY;
+    const float lv = (r < N) ? lse[static_cast<size_t>(bh) * N + r] : -INFINITY;
     l2[ri] = (lv == -INFINITY) ? INFINITY : lv * 1.4426950408889634f;
   }
-  float* dq = dqacc + (static_cast<size_t>(bh) * Npb + r) * D + lane * PER;
-#pragma unroll
-  for (int t = 0; t < PER; ++t) dq[t] = 0.f;
+  float4* dq = reinterpret_cast<float4*>(dqacc + (static_cast<size_t>(bh) * Npb + r) * D + part * 8);
+  dq[0] = make_float4(0.f, 0.f, 0.f, 0.f);
+  dq[1] = make_float4(0.f, 0.f, 0.f, 0.f);
 }
 
 cudaError_t launch_bwd_pre(const Dims& d, const void* o, const void* dout, const float* lse, float* dvec, float* l2,
                            float* dqacc, cudaStream_t st) {
-  const long warps = static_cast<long>(d.B) * d.H * d.Npb;
-  const long blocks = (warps * 32 + 255) / 256;
+  const long threads = static_cast<long>(d.B) * d.H * d.Npb * (d.D / 8);
+  const long blocks = (threads + 255) / 256;
   const __nv_bfloat16* dob = static_cast<const __nv_bfloat16*>(dout);
 #define FM_PRE(DD, F32) \
   k3_bwd_pre<DD, F32><<<blocks, 256, 0, st>>>(o, dob, lse, d.B, d.N, d.H, d.Npb, dvec, l2, dqacc)
@@ -233,36 +253,36 @@ cudaError_t launch_bwd_pre(const Dims& d, const void* o, const void* dout, const
 
 // ---------------------------------------------------------------------------------------
 // K5: dQ = scale * dQacc (the scale of Eq. 1 carried into dQ, R4) -> out dtype,
-// [B,H,Npb,D] -> [B,N,H,D].  One thread per 4 elements.
+// [B,H,Npb,D] -> [B,N,H,D].  One thread per 8 elements (two 16-byte loads).
 // ---------------------------------------------------------------------------------------
 template <int D, bool OUT_F32>
 __global__ void __launch_bounds__(256) k5_dq_convert(const float* __restrict__ dqacc, int B, int N, int H, int Npb,
                                                      float scale, void* __restrict__ dq) {
-  const long idx4 = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const long total4 = static_cast<long>(B) * N * H * D / 4;
-  if (idx4 >= total4) return;
-  const long e = idx4 * 4;
+  const long idx8 = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const long total8 = static_cast<long>(B) * N * H * D / 8;
+  if (idx8 >= total8) return;
+  const long e = idx8 * 8;
   const int c = static_cast<int>(e % D);
   const long row = e / D;  // (b, r, h)
   const int h = static_cast<int>(row % H);
   const long br = row / H;
   const int r = static_cast<int>(br % N), b = static_cast<int>(br / N);
-  const float4 v = *reinterpret_cast<const float4*>(dqacc + ((static_cast<size_t>(b) * H + h) * Npb + r) * D + c);
+  const float4* src = reinterpret_cast<const float4*>(dqacc + ((static_cast<size_t>(b) * H + h) * Npb + r) * D + c);
+  const float4 v0 = src[0], v1 = src[1];
   if constexpr (OUT_F32) {
-    reinterpret_cast<float4*>(dq)[idx4] = make_float4(v.x * scale, v.y * scale, v.z * scale, v.w * scale);
+    float4* dst = reinterpret_cast<float4*>(dq) + idx8 * 2;
+    dst[0] = make_float4(v0.x * scale, v0.y * scale, v0.z * scale, v0.w * scale);
+    dst[1] = make_float4(v1.x * scale, v1.y * scale, v1.z * scale, v1.w * scale);
   } else {
-    __nv_bfloat162 lo = __floats2bfloat162_rn(v.x * scale, v.y * scale);
-    __nv_bfloat162 hi = __floats2bfloat162_rn(v.z * scale, v.w * scale);
-    uint2 pk;
-    pk.x = *reinterpret_cast<uint32_t*>(&lo);
-    pk.y = *reinterpret_cast<uint32_t*>(&hi);
-    reinterpret_cast<uint2*>(dq)[idx4] = pk;
+    reinterpret_cast<uint4*>(dq)[idx8] =
+        make_uint4(pack_bf16_rn(v0.x * scale, v0.y * scale), pack_bf16_rn(v0.z * scale, v0.w * scale),
+                   pack_bf16_rn(v1.x * scale, v1.y * scale), pack_bf16_rn(v1.z * scale, v1.w * scale));
   }
 }
 
 cudaError_t launch_dq_convert(const Dims& d, const float* dqacc, void* dq, cudaStream_t st) {
-  const long total4 = static_cast<long>(d.B) * d.N * d.H * d.D / 4;
-  const long blocks = (total4 + 255) / 256;
+  const long total8 = static_cast<long>(d.B) * d.N * d.H * d.D / 8;
+  const long blocks = (total8 + 255) / 256;
 #define FM_CV(DD, F32) k5_dq_convert<DD, F32><<<blocks, 256, 0, st>>>(dqacc, d.B, d.N, d.H, d.Npb, d.scale, dq)
   if (d.D == 128) {
     if (d.out_f32) FM_CV(128, true); else FM_CV(128, false);
