@@ -130,11 +130,15 @@ fm_status check_params(const fm_params* p, fm::Dims* d, bool need_attention) {
 }
 
 // Carve the workspace.  Returns the total size; pointers valid only when base != nullptr.
+// Every buffer starts on a 4 KiB boundary of the device address space (the caller's base is
+// first rounded up to 64 KiB; the size bound includes that slack): the backward's 8 KiB bulk
+// reduce-adds into dqacc measured ~10 % slower when the accumulator was only 256-B aligned.
 size_t carve(const fm::Dims& d, int pass, void* base, fm::Workspace* w) {
-  size_t off = 0;
+  constexpr size_t kBaseAlign = 65536, kBufAlign = 4096;
+  size_t off = base ? (kBaseAlign - reinterpret_cast<uintptr_t>(base) % kBaseAlign) % kBaseAlign : kBaseAlign;
   auto take = [&](size_t bytes) {
     const size_t o = off;
-    off = align_up(off + bytes, 256);
+    off = align_up(off + bytes, kBufAlign);
     return base ? static_cast<uint8_t*>(base) + o : nullptr;
   };
   const size_t bhm = static_cast<size_t>(d.B) * d.Hm;

@@ -10,7 +10,7 @@ namespace fm {
 constexpr int kTile = 128;      // column (key) tile Bc, forward row (query) tile Br
 constexpr int kMaxTc = 2048;    // forward visit-list capacity -> N <= 262144
 
-// Workspace layout (all offsets 256-byte aligned), produced by flashmask_fwd/bwd.
+// Workspace layout (buffers 4 KiB-aligned in the device address space), produced by flashmask_fwd/bwd.
 struct Workspace {
   int32_t* ext8;    // [B, Hm, Tc, 8] raw extrema (Alg. 1 line 4)
   int4* vec4;       // [B, Hm, Tc*128] normalised (LTS, LTE, UTS, UTE) per column, padded columns masked

@@ -1,0 +1,549 @@
+// fm_fwd.cu — K2: FlashMask forward (Alg. 1) for sm_100a.
+//
+// One CTA owns a pair of 128-row query tiles (Q0, Q1) of one (batch, head).  Warp roles:
+//   warps 0-7   softmax of Q0: two warpgroups, each one half (64) of the key columns
+//   warps 8-15  softmax of Q1  (thread = one row = one TMEM lane)
+//   warp  16    TMA producer (lane 0): Q once, then K_j, V_j and the mask slice of tile j
+//   warp  17    TMEM allocator + tcgen05 MMA issuer (lane 0)
+// The visit list — the column tiles j that are not SKIP for Q0 or Q1 — is built from the
+// K1 class map before the roles split, so fully masked tiles issue no load and no MMA
+// (Alg. 1 lines 9-14).  S_q = Q_q K_j^T (tcgen05, fp32 in TMEM), softmax in
+// registers with the element-wise interval mask applied only on PARTIAL tiles (Alg. 1
+// lines 15-21), P_q written back to TMEM as bf16 (aliasing consumed S_q columns) and
+// O_q += P_q V_j issued with P as the TMEM A operand.  The two query tiles ping-pong: while
+// one WG runs its softmax the tensor core computes the other tile's S / PV.
+// TMEM columns: S0 [0,128)  S1 [128,256)  O0 [256,256+D)  O1 [256+D, 256+2D).
+#include <cuda_bf16.h>
+#include <cmath>
+#include <type_traits>
+
+#include "fm_internal.h"
+#include "fm_ptx.cuh"
+
+#ifdef FM_TRACE
+namespace fm { __device__ long long g_fm_trace_fwd[64 * 16]; }
+#define FT(slot, e)                                                                                   \
+  do {                                                                                                 \
+    if (blockIdx.x == 64 && blockIdx.y == 0 && blockIdx.z == 0 && (e) < 64) fm::g_fm_trace_fwd[(e) * 16 + (slot)] = clock64(); \
+  } while (0)
+#else
+#define FT(slot, e) \
+  do {              \
+  } while (0)
+#endif
+
+#ifndef FM_WAIT_P
+#define FM_WAIT_P mbar_wait  // MMA issuer waiting for P (mbar_wait_spin measured ~2% slower)
+#endif
+#ifndef FM_WAIT_S
+#define FM_WAIT_S mbar_wait  // softmax waiting for S
+#endif
+
+#ifndef FM_POLY_PAIRS
+#define FM_POLY_PAIRS 3  // of every 8 column pairs, how many use the FMA-pipe exp2 (rest: MUFU)
+#endif
+
+namespace fm {
+
+namespace fwd {
+
+constexpr int NT = 576;   // 16 softmax warps + TMA producer + MMA issuer
+constexpr int KST = 2, VST = 2, MST = 4;
+
+template <int D>
+struct Smem {
+  static constexpr int TILE = 128 * D * 2;
+  uint8_t q[2][TILE];
+  uint8_t k[KST][TILE];
+  uint8_t v[VST][TILE];
+  int4 mask[MST][128];
+  uint32_t list[2][kMaxTc];   // visit lists of two consecutive work units (double-buffered)
+  int info[2][4];             // per list slot: b, h, pair, number of entries (-1: no more units)
+  uint64_t bar_q, q_empty;
+  uint64_t k_full[KST], k_empty[KST], v_full[VST], v_empty[VST];
+  uint64_t m_full[MST], m_empty[MST];
+  uint64_t s_full[2], p_full[2], o_full[2], o_empty[2];
+  uint64_t u_full[2], u_empty[2];
+  float xmax[2][2][2][128];  // [tile][parity][column half][row]: row-max exchange between halves
+  float xsum[2][2][128];     // [tile][column half][row]: final row-sum exchange
+  uint32_t tmem_base;
+};
+
+constexpr int PRODUCER_WARP = 16, MMA_WARP = 17;
+constexpr int U_EMPTY_ARRIVALS = 17;  // 16 softmax warps + the MMA warp
+
+__device__ __forceinline__ int ent_cls(uint32_t ent, int q) { return (ent >> (24 + 2 * q)) & 3; }
+
+// Work unit u (0 .. npairs*H*B-1) -> (b, h, pair): (batch, head)-major so that the ~148 units in
+// flight share K/V tiles in L2 (head-minor order streamed every head's K/V from HBM: -20 %),
+// heaviest (last) row-tile pairs of each head first.
+__device__ __forceinline__ void decode_unit(int u, int npairs, int H, int B, int& b, int& h, int& pair) {
+  const int bh = u / npairs;
+  pair = npairs - 1 - (u - bh * npairs);
+  h = bh % H;
+  b = bh / H;
+}
+
+}  // namespace fwd
+
+// Persistent CTAs (one per SM) pull work units — a pair of 128-row query tiles (Q0, Q1) of one
+// (batch, head) — from a global counter.  The producer builds unit n+1's visit list and loads
+// its Q while the softmax warps finish unit n, and the MMA warp issues unit n+1's first S tiles
+// while the softmax warps run unit n's epilogue, so per-unit setup and epilogue overlap the
+// tensor core instead of idling it (visits per unit are few at high block sparsity).
+template <int D, bool CAUSAL, bool OUT_F32>
+__global__ void __launch_bounds__(fwd::NT, 1)
+    fm_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                  const __grid_constant__ CUtensorMap tmV, const FwdArgs a) {
+  using namespace fwd;
+  using S = Smem<D>;
+  extern __shared__ uint8_t smem_raw[];
+  S& sm = *smem_align1024<S>(smem_raw);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int npairs = (a.Tr + 1) >> 1;
+  const int n_units = npairs * a.H * a.B;
+
+  if (warp == PRODUCER_WARP && lane == 0) {
+    mbar_init(&sm.bar_q, 1);
+    mbar_init(&sm.q_empty, 1);
+    for (int s = 0; s < KST; ++s) { mbar_init(&sm.k_full[s], 1); mbar_init(&sm.k_empty[s], 1); }
+    for (int s = 0; s < VST; ++s) { mbar_init(&sm.v_full[s], 1); mbar_init(&sm.v_empty[s], 1); }
+    for (int s = 0; s < MST; ++s) { mbar_init(&sm.m_full[s], 1); mbar_init(&sm.m_empty[s], 16); }
+    for (int q = 0; q < 2; ++q) {
+      mbar_init(&sm.s_full[q], 1);
+      mbar_init(&sm.p_full[q], 256);
+      mbar_init(&sm.o_full[q], 1);
+      mbar_init(&sm.o_empty[q], 8);
+      mbar_init(&sm.u_full[q], 32);
+      mbar_init(&sm.u_empty[q], U_EMPTY_ARRIVALS);
+    }
+    fence_barrier_init();
+  }
+  if (warp == MMA_WARP) tmem_alloc<512>(&sm.tmem_base);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = sm.tmem_base;
+
+  if (warp == PRODUCER_WARP) {
+    // ================================ scheduler + TMA producer ================================
+    if (lane == 0) {
+      tma_prefetch_desc(&tmQ);
+      tma_prefetch_desc(&tmK);
+      tma_prefetch_desc(&tmV);
+    }
+    constexpr uint32_t TB = S::TILE;
+    uint32_t nq = 0;  // Q tile loads so far
+    int g = 0;        // global visit index (K/V/mask ring position)
+    for (int nu = 0;; ++nu) {
+      const int slot = nu & 1;
+      mbar_wait(&sm.u_empty[slot], ((nu >> 1) & 1) ^ 1);  // consumers done with unit nu-2
+      int u = 0;
+      if (lane == 0) u = atomicAdd(a.sched, 1);
+      u = __shfl_sync(0xffffffffu, u, 0);
+      if (u >= n_units) {
+        if (lane == 0) sm.info[slot][3] = -1;
+        __syncwarp();
+        mbar_arrive(&sm.u_full[slot]);
+        break;
+      }
+      int b, h, pair;
+      decode_unit(u, npairs, a.H, a.B, b, h, pair);
+      const int hk = h / a.G;
+      const int hm = (a.Hm == 1) ? 0 : hk;
+      const int i0 = 2 * pair, i1 = 2 * pair + 1;
+      const bool has_q1 = i1 < a.Tr;
+      const size_t bhm = static_cast<size_t>(b) * a.Hm + hm;
+      // visit list: union of the non-SKIP column tiles of Q0 and Q1 (K1 class map), ascending j
+      const uint8_t* row0 = a.fmap + (bhm * a.Tr + i0) * a.Tc;
+      const uint8_t* row1 = row0 + a.Tc;
+      uint32_t* list = sm.list[slot];
+      int nE = 0;
+      for (int j0 = 0; j0 < a.Tc; j0 += 32 * 8) {
+        uint32_t c0[8], c1[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const int j = j0 + 32 * k + lane;
+          c0[k] = (j < a.Tc) ? row0[j] : 0u;
+          c1[k] = (j < a.Tc && has_q1) ? row1[j] : 0u;
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const bool vis = (c0[k] | c1[k]) != 0u;
+          const unsigned bal = __ballot_sync(0xffffffffu, vis);
+          if (vis)
+            list[nE + __popc(bal & ((1u << lane) - 1u))] =
+                static_cast<uint32_t>(j0 + 32 * k + lane) | (c0[k] << 24) | (c1[k] << 26);
+          nE += __popc(bal);
+        }
+      }
+      if (lane == 0) {
+        sm.info[slot][0] = b;
+        sm.info[slot][1] = h;
+        sm.info[slot][2] = pair;
+        sm.info[slot][3] = nE;
+      }
+      __syncwarp();
+      mbar_arrive(&sm.u_full[slot]);  // 32 arrivals: every lane's list writes are released
+      if (lane == 0) {
+        if (nE > 0) {
+          if (nq > 0) mbar_wait(&sm.q_empty, (nq - 1) & 1);  // all S MMAs of the previous unit done
+          mbar_expect_tx(&sm.bar_q, has_q1 ? 2 * TB : TB);
+#pragma unroll
+          for (int c = 0; c < D / 64; ++c) {
+            tma_load_4d(sm.q[0] + c * 16384, &tmQ, &sm.bar_q, c * 64, h, i0 * 128, b);
+            if (has_q1) tma_load_4d(sm.q[1] + c * 16384, &tmQ, &sm.bar_q, c * 64, h, i1 * 128, b);
+          }
+          ++nq;
+        }
+        const int4* vec_bh = a.vec4 + bhm * static_cast<size_t>(a.Tc) * 128;
+        for (int e = 0; e < nE; ++e) {
+          const uint32_t ent = list[e];
+          const int j = static_cast<int>(ent & 0xFFFFFFu);
+          const int ge = g + e;
+          const int ks = ge % KST, vs = ge % VST, ms = ge % MST;
+          mbar_wait(&sm.k_empty[ks], ((ge / KST) & 1) ^ 1);
+          mbar_expect_tx(&sm.k_full[ks], TB);
+#pragma unroll
+          for (int c = 0; c < D / 64; ++c) tma_load_4d(sm.k[ks] + c * 16384, &tmK, &sm.k_full[ks], c * 64, hk, j * 128, b);
+          mbar_wait(&sm.m_empty[ms], ((ge / MST) & 1) ^ 1);
+          if (ent_cls(ent, 0) == 1 || ent_cls(ent, 1) == 1) {
+            mbar_expect_tx(&sm.m_full[ms], 128 * 16);
+            bulk_g2s(sm.mask[ms], vec_bh + static_cast<size_t>(j) * 128, 128 * 16, &sm.m_full[ms]);
+          } else {
+            mbar_arrive(&sm.m_full[ms]);
+          }
+          mbar_wait(&sm.v_empty[vs], ((ge / VST) & 1) ^ 1);
+          mbar_expect_tx(&sm.v_full[vs], TB);
+#pragma unroll
+          for (int c = 0; c < D / 64; ++c) tma_load_4d(sm.v[vs] + c * 16384, &tmV, &sm.v_full[vs], c * 64, hk, j * 128, b);
+        }
+      }
+      __syncwarp();
+      g += nE;
+    }
+  } else if (warp == MMA_WARP) {
+    // ================================ MMA issuer ================================
+    // One issuer for both tiles, in the order PV0(e-1), S0(e), PV1(e-1), S1(e): this keeps the
+    // two tiles' softmax phases staggered (ping-pong).  Two independent issuers were measured
+    // to fall into lock-step and lose ~30 %.  The whole warp runs converged; one elected lane
+    // issues (fm_ptx.cuh).
+    constexpr uint32_t ID_S = idesc_bf16(128, 128, 0, 0);  // S = Q K^T, both K-major
+    constexpr uint32_t ID_PV = idesc_bf16(128, D, 0, 1);   // O += P V, V is MN-major
+    const uint32_t tS[2] = {tbase + 0, tbase + 128};
+    const uint32_t tO[2] = {tbase + 256, tbase + 256 + D};
+    const uint32_t q_addr[2] = {smem_u32(sm.q[0]), smem_u32(sm.q[1])};
+    uint32_t nq = 0;
+    uint32_t pv_glob[2] = {0, 0};  // PV batches issued per tile (p_full phase)
+    int g = 0;
+    for (int nu = 0;; ++nu) {
+      const int slot = nu & 1;
+      mbar_wait(&sm.u_full[slot], (nu >> 1) & 1);
+      const int nE = sm.info[slot][3];
+      if (nE < 0) break;
+      const uint32_t* list = sm.list[slot];
+      int pend[2] = {-1, -1};
+      uint32_t pv_unit[2] = {0, 0};
+      bool need_oe[2] = {nu > 0, nu > 0};  // O of the previous unit still being read out
+      auto issue_pv = [&](int q) {
+        const int pe = pend[q];
+        FM_WAIT_P(&sm.p_full[q], pv_glob[q] & 1);
+        if (need_oe[q]) {
+          mbar_wait(&sm.o_empty[q], (nu - 1) & 1);
+          need_oe[q] = false;
+        }
+        const int vs = (g + pe) % VST;
+        mbar_wait(&sm.v_full[vs], ((g + pe) / VST) & 1);
+        tc_fence_after();
+        const uint32_t v_addr = smem_u32(sm.v[vs]);
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          const uint64_t bd = sdesc_sw128(v_addr + kk * 2048, 16384, 1024);
+          // P of keys [0,64) sits in S columns [0,32), of keys [64,128) in S columns [64,96)
+          mma_ts_w(tO[q], tS[q] + kk * 8 + (kk >= 4 ? 32u : 0u), bd, ID_PV, (pv_unit[q] > 0 || kk > 0) ? 1u : 0u);
+        }
+        pv_unit[q]++;
+        pv_glob[q]++;
+        const uint32_t ent = list[pe];
+        const int last = (ent_cls(ent, 1) != 0) ? 1 : 0;
+        if (q == last) mma_commit_w(&sm.v_empty[vs]);
+        pend[q] = -1;
+      };
+      if (nE > 0) {
+        mbar_wait(&sm.bar_q, nq & 1);
+        tc_fence_after();
+      }
+      for (int e = 0; e < nE; ++e) {
+        const uint32_t ent = list[e];
+        const int ks = (g + e) % KST;
+        mbar_wait(&sm.k_full[ks], ((g + e) / KST) & 1);
+        tc_fence_after();
+        const uint32_t k_addr = smem_u32(sm.k[ks]);
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          if (pend[q] >= 0) issue_pv(q);
+          if (ent_cls(ent, q) != 0) {
+#pragma unroll
+            for (int kk = 0; kk < D / 16; ++kk) {
+              const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
+              mma_ss_w(tS[q], sdesc_sw128(q_addr[q] + off, 16, 1024), sdesc_sw128(k_addr + off, 16, 1024), ID_S,
+                       kk > 0 ? 1u : 0u);
+            }
+            mma_commit_w(&sm.s_full[q]);
+            pend[q] = e;
+          }
+        }
+        mma_commit_w(&sm.k_empty[ks]);
+        if (e == nE - 1) mma_commit_w(&sm.q_empty);  // Q0/Q1 free once these S MMAs complete
+      }
+#pragma unroll
+      for (int q = 0; q < 2; ++q)
+        if (pend[q] >= 0) issue_pv(q);
+      mma_commit_w(&sm.o_full[0]);
+      mma_commit_w(&sm.o_full[1]);
+      if (nE > 0) ++nq;
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sm.u_empty[slot]);
+      g += nE;
+    }
+  } else {
+    // ================================ softmax WGs ================================
+    // Four warpgroups: tile q = warp / 8, column half hh = (warp / 4) % 2.  The two halves of a
+    // tile share TMEM lanes (rows) and split the 128 key columns, exchanging row maxima (and at
+    // the end the row sums) through shared memory under a 64-thread named barrier per warp pair.
+    const int q = warp >> 3;
+    const int hh = (warp >> 2) & 1;
+    const int wl = warp & 3;
+    const int row_t = wl * 32 + lane;
+    const uint32_t lane_off = static_cast<uint32_t>(wl * 32) << 16;
+    const uint32_t tS = tbase + lane_off + (q == 0 ? 0u : 128u);
+    const uint32_t tSh = tS + hh * 64;                      // this half's 64 S columns
+    const uint32_t tPh = tS + hh * 64;                      // its packed P (32 columns) — see MMA
+    const uint32_t tO = tbase + lane_off + 256u + (q == 0 ? 0u : static_cast<uint32_t>(D));
+    const uint32_t tOh = tO + hh * (D / 2);                 // this half's O columns
+    const float sl2 = a.scale_log2;
+    // the two warps holding the same 32 rows (column halves 0/1) exchange through a 64-thread barrier
+    const uint32_t bar_id = 1 + q * 4 + wl;
+    uint32_t cnt = 0;  // tiles processed by this tile slot over all units (s_full / p_full phase)
+    int g = 0;
+    for (int nu = 0;; ++nu) {
+      const int slot = nu & 1;
+      mbar_wait(&sm.u_full[slot], (nu >> 1) & 1);
+      const int nE = sm.info[slot][3];
+      if (nE < 0) break;
+      const int b = sm.info[slot][0], h = sm.info[slot][1], pair = sm.info[slot][2];
+      const uint32_t* list = sm.list[slot];
+      const int row = (2 * pair + q) * 128 + row_t;
+      float m_used = -INFINITY;  // running max of the scaled logits, log2 units (threshold-updated)
+      float l = 0.f;             // this half's share of the row sum
+      uint32_t ucnt = 0;         // tiles of this unit processed
+      for (int e = 0; e < nE; ++e) {
+        const uint32_t ent = list[e];
+        const int cls = ent_cls(ent, q);
+        const int ms = (g + e) % MST;
+        mbar_wait(&sm.m_full[ms], ((g + e) / MST) & 1);
+        if (cls != 0) {
+          const int j = static_cast<int>(ent & 0xFFFFFFu);
+          FM_WAIT_S(&sm.s_full[q], cnt & 1);
+          tc_fence_after();
+          // Pass 1: max over this half's 64 columns, 16 at a time (S stays in TMEM for pass 2).
+          // On PARTIAL tiles the element mask (Alg. 1 lines 15-21) is applied here and the masked
+          // S written back to TMEM, so pass 2 is identical for PARTIAL and UNMASKED tiles.
+          float mx0 = -INFINITY, mx1 = -INFINITY, mx2 = -INFINITY, mx3 = -INFINITY;
+          uint32_t sr[2][16];
+          tmem_ld16(tSh, sr[0]);
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            tmem_wait_ld();
+            if (c + 1 < 4) tmem_ld16(tSh + (c + 1) * 16, sr[(c + 1) & 1]);
+            float* sv = reinterpret_cast<float*>(sr[c & 1]);
+            if (cls == 1) {
+              // element mask of Alg. 1 lines 15-21: row r is masked for key y iff
+              // (unsigned)(r - start_y) < len_y for either interval, or (causal) r < y
+              const int4* mk = sm.mask[ms] + hh * 64 + c * 16;
+              const int rmy = row - (j * 128 + hh * 64 + c * 16);
+#pragma unroll
+              for (int t = 0; t < 16; ++t) {
+                const int4 mv = mk[t];
+                bool msk = static_cast<unsigned>(row - mv.x) < static_cast<unsigned>(mv.y);
+                if constexpr (CAUSAL)
+                  msk |= rmy < t;
+                else
+                  msk |= static_cast<unsigned>(row - mv.z) < static_cast<unsigned>(mv.w);
+                sv[t] = msk ? -INFINITY : sv[t];
+              }
+              tmem_st16(tSh + c * 16, sr[c & 1]);  // masked S back to TMEM: pass 2 needs no mask work
+            }
+#pragma unroll
+            for (int t = 0; t < 16; t += 8) {
+              mx0 = fmax3(mx0, sv[t], sv[t + 1]);
+              mx1 = fmax3(mx1, sv[t + 2], sv[t + 3]);
+              mx2 = fmax3(mx2, sv[t + 4], sv[t + 5]);
+              mx3 = fmax3(mx3, sv[t + 6], sv[t + 7]);
+            }
+          }
+          if (cls == 1) tmem_wait_st();
+          const float mh = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3));
+          sm.xmax[q][cnt & 1][hh][row_t] = mh;
+          named_bar_sync(bar_id, 64);
+          const float m_tile = fmaxf(mh, sm.xmax[q][cnt & 1][hh ^ 1][row_t]) * sl2;
+          // Conditional rescale: the running max only moves when it grows by more than 2^8
+          // (exact: P is computed against the same m that scales l and O).  Both halves see the
+          // same m_tile and take the same decision; the TMEM accesses stay warp-collective.
+          const bool need = m_tile > m_used + 8.0f;
+          float alpha = 1.0f;
+          if (need) {
+            alpha = ex2(m_used - m_tile);  // Alg. 1 line 25 factor e^{m_old - m_new}
+            l *= alpha;
+            m_used = m_tile;
+          }
+          if (__any_sync(0xffffffffu, need) && ucnt > 0) {
+#pragma unroll 1
+            for (int c = 0; c < D / 64; ++c) {
+              uint32_t ov[32];
+              tmem_ld32(tOh + c * 32, ov);
+              tmem_wait_ld();
+#pragma unroll
+              for (int t = 0; t < 32; ++t) ov[t] = __float_as_uint(__uint_as_float(ov[t]) * alpha);
+              tmem_st32(tOh + c * 32, ov);
+            }
+          }
+          const float m_use = (m_used == -INFINITY) ? 0.f : m_used;
+          // Pass 2: P = exp2(S*scale*log2e - m) over this half's columns; packed FFMA2 for the
+          // argument, MUFU ex2 for most pairs and the FMA-pipe polynomial for FM_POLY_PAIRS of 8;
+          // row sums with packed FADD2; packed bf16 P written back over consumed S columns.
+          const uint64_t sl2x2 = f2pack(sl2, sl2), negm2 = f2pack(-m_use, -m_use);
+          uint64_t acc[4] = {0ull, 0ull, 0ull, 0ull};
+          tmem_ld16(tSh, sr[0]);
+#pragma unroll
+          for (int ch = 0; ch < 4; ++ch) {
+            tmem_wait_ld();
+            if (ch + 1 < 4) tmem_ld16(tSh + (ch + 1) * 16, sr[(ch + 1) & 1]);
+            const float* sv = reinterpret_cast<const float*>(sr[ch & 1]);
+            uint32_t pk[8];
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk) {
+              const int k = ch * 8 + kk;
+              const uint64_t x2 = f2fma(f2pack(sv[2 * kk], sv[2 * kk + 1]), sl2x2, negm2);
+              float p0, p1;
+              if ((k & 7) >= 8 - FM_POLY_PAIRS) {
+                exp2_poly2(x2, p0, p1);
+              } else {
+                float x0, x1;
+                f2unpack(x2, x0, x1);
+                p0 = ex2(x0);
+                p1 = ex2(x1);
+              }
+              acc[k & 3] = f2add(acc[k & 3], f2pack(p0, p1));
+              pk[kk] = pack_bf16(p0, p1);
+            }
+            tmem_st8(tPh + ch * 8, pk);
+          }
+          {
+            const uint64_t a01 = f2add(acc[0], acc[1]), a23 = f2add(acc[2], acc[3]);
+            float u0, u1;
+            f2unpack(f2add(a01, a23), u0, u1);
+            l += u0 + u1;
+          }
+          tmem_wait_st();
+          tc_fence_before();
+          mbar_arrive(&sm.p_full[q]);
+          ++cnt;
+          ++ucnt;
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sm.m_empty[ms]);
+      }
+      // ---- epilogue: O = O / l, L = m + ln(l) (Alg. 1 lines 27-28) ----
+      sm.xsum[q][hh][row_t] = l;
+      named_bar_sync(bar_id, 64);
+      l += sm.xsum[q][hh ^ 1][row_t];
+      named_bar_sync(bar_id, 64);  // xsum is rewritten by the next unit's epilogue
+      const bool live = (ucnt > 0) && (l > 0.f);
+      mbar_wait(&sm.o_full[q], nu & 1);
+      tc_fence_after();
+      const float inv = live ? 1.0f / l : 0.f;
+      const size_t orow = ((static_cast<size_t>(b) * a.N + row) * a.H + h) * D + hh * (D / 2);
+#pragma unroll
+      for (int c = 0; c < D / 64; ++c) {
+        uint32_t ov[32];
+        if (ucnt > 0) {  // warp-uniform: the tcgen05.ld stays warp-collective
+          tmem_ld32(tOh + c * 32, ov);
+          tmem_wait_ld();
+        }
+        if (c == D / 64 - 1) {  // O read out: the next unit's first PV may overwrite it
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&sm.o_empty[q]);
+        }
+        if (row < a.N) {
+          float f[32];
+#pragma unroll
+          for (int t = 0; t < 32; ++t) f[t] = live ? __uint_as_float(ov[t]) * inv : 0.f;
+          if constexpr (OUT_F32) {
+            float4* dst = reinterpret_cast<float4*>(static_cast<float*>(a.o) + orow + c * 32);
+#pragma unroll
+            for (int t = 0; t < 8; ++t) dst[t] = make_float4(f[4 * t], f[4 * t + 1], f[4 * t + 2], f[4 * t + 3]);
+          } else {
+            uint4* dst = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(a.o) + orow + c * 32);
+#pragma unroll
+            for (int t = 0; t < 4; ++t)
+              dst[t] = make_uint4(pack_bf16(f[8 * t], f[8 * t + 1]), pack_bf16(f[8 * t + 2], f[8 * t + 3]),
+                                  pack_bf16(f[8 * t + 4], f[8 * t + 5]), pack_bf16(f[8 * t + 6], f[8 * t + 7]));
+          }
+        }
+      }
+      if (row < a.N && hh == 0)
+        a.lse[(static_cast<size_t>(b) * a.H + h) * a.N + row] =
+            live ? (m_used + __log2f(l)) * 0.6931471805599453f : -INFINITY;
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sm.u_empty[slot]);
+      g += nE;
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == MMA_WARP) {
+    tc_fence_after();
+    tmem_dealloc<512>(tbase);
+  }
+}
+
+template <int D, bool CAUSAL, bool OUT_F32>
+static cudaError_t launch_fwd_t(const Dims& d, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
+                                const FwdArgs& a, cudaStream_t st) {
+  auto kern = fm_fwd_kernel<D, CAUSAL, OUT_F32>;
+  const size_t smem = sizeof(fwd::Smem<D>) + 1024;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  static_assert(sizeof(fwd::Smem<D>) + 1024 <= 232448, "shared memory budget");
+  int dev = 0, nsm = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  const long units = static_cast<long>((d.Tr + 1) / 2) * d.H * d.B;
+  dim3 grid(static_cast<unsigned>(units < nsm ? units : nsm));
+  kern<<<grid, fwd::NT, smem, st>>>(tq, tk, tv, a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fwd(const Dims& d, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
+                       const FwdArgs& a, cudaStream_t st) {
+#define FM_F(DD, CC, FF) return launch_fwd_t<DD, CC, FF>(d, tq, tk, tv, a, st)
+  if (d.D == 128) {
+    if (d.causal) { if (d.out_f32) FM_F(128, true, true); else FM_F(128, true, false); }
+    else { if (d.out_f32) FM_F(128, false, true); else FM_F(128, false, false); }
+  } else {
+    if (d.causal) { if (d.out_f32) FM_F(64, true, true); else FM_F(64, true, false); }
+    else { if (d.out_f32) FM_F(64, false, true); else FM_F(64, false, false); }
+  }
+#undef FM_F
+}
+
+}  // namespace fm
+
+#ifdef FM_TRACE
+extern "C" __attribute__((visibility("default"))) int flashmask_debug_trace_fwd(long long* host) {
+  return cudaMemcpyFromSymbol(host, fm::g_fm_trace_fwd, sizeof(long long) * 64 * 16) == cudaSuccess ? 0 : 1;
+}
+#endif
