@@ -289,9 +289,13 @@ fm_status flashmask_fwd(const fm_params* p, const void* q, const void* k, const 
     return FM_OK;
   }
   std::string err;
-  CUtensorMap tq, tk, tv;
+  CUtensorMap tq, tk, tv, to;
   if (!make_map(&tq, q, d, d.H, 128, &err) || !make_map(&tk, k, d, d.Hkv, 128, &err) ||
       !make_map(&tv, v, d, d.Hkv, 128, &err))
+    return fail(FM_ERR_CUDA, err);
+  if (d.out_f32)
+    to = tq;  // fp32 O is stored directly by the kernel (the map is not used)
+  else if (!make_map(&to, o, d, d.H, 128, &err))
     return fail(FM_ERR_CUDA, err);
   cudaError_t e = timed(FM_KERNEL_EXPAND, st, [&] { return fm::launch_expand(sri, d, fm::kTile, w.ext8, w.vec4, st); });
   if (e != cudaSuccess) return cuda_fail(e, "expand");
@@ -304,7 +308,7 @@ fm_status flashmask_fwd(const fm_params* p, const void* q, const void* k, const 
   a.vec4 = w.vec4;
   a.o = o;
   a.lse = lse;
-  e = timed(FM_KERNEL_FWD, st, [&] { return fm::launch_fwd(d, tq, tk, tv, a, st); });
+  e = timed(FM_KERNEL_FWD, st, [&] { return fm::launch_fwd(d, tq, tk, tv, to, a, st); });
   if (e != cudaSuccess) return cuda_fail(e, "forward kernel");
   return FM_OK;
 }
@@ -373,9 +377,15 @@ fm_status flashmask_bwd(const fm_params* p, const void* q, const void* k, const 
   a.dv = dv;
   const bool deterministic = (p->flags & FM_FLAG_DETERMINISTIC) != 0;
   a.with_dq = deterministic ? 0 : 1;
-  CUtensorMap tdq;
+  CUtensorMap tdq, tdk, tdv;
   if (!make_dq_map(&tdq, w.dqacc, d, &err)) return fail(FM_ERR_CUDA, err);
-  e = timed(FM_KERNEL_BWD, st, [&] { return fm::launch_bwd(d, tq, tk, tv, tdo, tdq, a, st); });
+  if (d.out_f32) {  // fp32 dK / dV are stored directly by the kernel (the maps are not used)
+    tdk = tk;
+    tdv = tv;
+  } else if (!make_map(&tdk, dk, d, d.Hkv, 128, &err) || !make_map(&tdv, dv, d, d.Hkv, 128, &err)) {
+    return fail(FM_ERR_CUDA, err);
+  }
+  e = timed(FM_KERNEL_BWD, st, [&] { return fm::launch_bwd(d, tq, tk, tv, tdo, tdq, tdk, tdv, a, st); });
   if (e != cudaSuccess) return cuda_fail(e, "backward kernel");
   if (!deterministic) {
     e = timed(FM_KERNEL_DQ_CONVERT, st, [&] { return fm::launch_dq_convert(d, w.dqacc, dq, st); });

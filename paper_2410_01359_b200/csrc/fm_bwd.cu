@@ -195,7 +195,8 @@ template <int D, bool CAUSAL, bool OUT_F32>
 __global__ void __launch_bounds__(bwd::NT, 1)
     fm_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                   const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO,
-                  const __grid_constant__ CUtensorMap tmDQ, const BwdArgs a) {
+                  const __grid_constant__ CUtensorMap tmDQ, const __grid_constant__ CUtensorMap tmDK,
+                  const __grid_constant__ CUtensorMap tmDV, const BwdArgs a) {
   using namespace bwd;
   using C = Cfg<D>;
   using S = Smem<D>;
@@ -540,8 +541,41 @@ __global__ void __launch_bounds__(bwd::NT, 1)
     const uint32_t col = wg == 0 ? C::DV_COL : C::DK_COL;
     const float mul = wg == 0 ? 1.0f : a.scale;
     void* outp = wg == 0 ? a.dv : a.dk;
+    if constexpr (!OUT_F32) {
+      // bf16 dV / dK go out through shared memory (the V / K tile buffers: every MMA that read
+      // them completed before `done`) and TMA stores — a thread holds one key row, so direct
+      // 16-byte stores would scatter each warp instruction over 32 rows.  Keys >= N are clipped.
+      uint8_t* stg = wg == 0 ? sm.v : sm.k;
 #pragma unroll 1
-    for (int c = 0; c < D / 32; ++c) {
+      for (int c = 0; c < D / 32; ++c) {
+        uint32_t r[32];
+        if (nE > 0) {
+          tmem_ld32(tbase + lane_off + col + c * 32, r);
+          tmem_wait_ld();
+        }
+        uint8_t* blk = stg + (c / 2) * (128 * 128) + key_t * 128;
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          float f[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) f[u] = nE > 0 ? __uint_as_float(r[8 * t + u]) * mul : 0.f;
+          const int chunk = (c % 2) * 4 + t;
+          *reinterpret_cast<uint4*>(blk + ((chunk ^ (key_t & 7)) << 4)) =
+              make_uint4(pack_bf16(f[0], f[1]), pack_bf16(f[2], f[3]), pack_bf16(f[4], f[5]), pack_bf16(f[6], f[7]));
+        }
+      }
+      fence_proxy_async_smem();
+      named_bar_sync(2 + wg, 128);
+      if (wl == 0 && lane == 0) {
+#pragma unroll
+        for (int c = 0; c < D / 64; ++c)
+          tma_store_4d(wg == 0 ? &tmDV : &tmDK, stg + c * (128 * 128), c * 64, hk, j * 128, b);
+        bulk_commit();
+        bulk_wait_read0();  // the staging buffer must outlive the TMA reads
+      }
+    }
+#pragma unroll 1
+    for (int c = 0; c < (OUT_F32 ? D / 32 : 0); ++c) {
       uint32_t r[32];
       if (nE > 0) {
         tmem_ld32(tbase + lane_off + col + c * 32, r);
@@ -678,20 +712,22 @@ __global__ void __launch_bounds__(bwd::NT, 1)
 
 template <int D, bool CAUSAL, bool OUT_F32>
 static cudaError_t launch_bwd_t(const Dims& d, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
-                                const CUtensorMap& tdo, const CUtensorMap& tdq, const BwdArgs& a, cudaStream_t st) {
+                                const CUtensorMap& tdo, const CUtensorMap& tdq, const CUtensorMap& tdk,
+                                const CUtensorMap& tdv, const BwdArgs& a, cudaStream_t st) {
   auto kern = fm_bwd_kernel<D, CAUSAL, OUT_F32>;
   const size_t smem = sizeof(bwd::Smem<D>) + 1024;
   static_assert(sizeof(bwd::Smem<D>) + 1024 <= 232448, "shared memory budget");
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (e != cudaSuccess) return e;
   dim3 grid(d.Tc, d.Hkv, d.B);
-  kern<<<grid, bwd::NT, smem, st>>>(tq, tk, tv, tdo, tdq, a);
+  kern<<<grid, bwd::NT, smem, st>>>(tq, tk, tv, tdo, tdq, tdk, tdv, a);
   return cudaGetLastError();
 }
 
 cudaError_t launch_bwd(const Dims& d, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
-                       const CUtensorMap& tdo, const CUtensorMap& tdq, const BwdArgs& a, cudaStream_t st) {
-#define FM_B(DD, CC, FF) return launch_bwd_t<DD, CC, FF>(d, tq, tk, tv, tdo, tdq, a, st)
+                       const CUtensorMap& tdo, const CUtensorMap& tdq, const CUtensorMap& tdk, const CUtensorMap& tdv,
+                       const BwdArgs& a, cudaStream_t st) {
+#define FM_B(DD, CC, FF) return launch_bwd_t<DD, CC, FF>(d, tq, tk, tv, tdo, tdq, tdk, tdv, a, st)
   if (d.D == 128) {
     if (d.causal) { if (d.out_f32) FM_B(128, true, true); else FM_B(128, true, false); }
     else { if (d.out_f32) FM_B(128, false, true); else FM_B(128, false, false); }

@@ -21,15 +21,27 @@
 #include "fm_ptx.cuh"
 
 #ifdef FM_TRACE
-namespace fm { __device__ long long g_fm_trace_fwd[64 * 16]; }
+#ifndef FM_TRACE_BX
+#define FM_TRACE_BX 64
+#endif
+namespace fm { __device__ long long g_fm_trace_fwd[64 * 16]; __device__ long long g_fm_trace_fwd_ev[16]; }
 #define FT(slot, e)                                                                                   \
   do {                                                                                                 \
-    if (blockIdx.x == 64 && blockIdx.y == 0 && blockIdx.z == 0 && (e) < 64) fm::g_fm_trace_fwd[(e) * 16 + (slot)] = clock64(); \
+    if (blockIdx.x == FM_TRACE_BX && blockIdx.y == 0 && blockIdx.z == 0 && (e) < 64) fm::g_fm_trace_fwd[(e) * 16 + (slot)] = clock64(); \
   } while (0)
+#define FTE(k)                                                                                          \
+  do {                                                                                                 \
+    if (blockIdx.x == FM_TRACE_BX && blockIdx.y == 0 && blockIdx.z == 0) fm::g_fm_trace_fwd_ev[k] = clock64(); \
+  } while (0)
+#define FM_TRACE_NE(n) (fm::g_fm_trace_fwd_ev[9] = (n))
 #else
 #define FT(slot, e) \
   do {              \
   } while (0)
+#define FTE(k) \
+  do {         \
+  } while (0)
+#define FM_TRACE_NE(n) ((void)0)
 #endif
 
 #ifndef FM_WAIT_P
@@ -78,7 +90,7 @@ __device__ __forceinline__ int ent_cls(uint32_t ent, int q) { return (ent >> (24
 template <int D, bool CAUSAL, bool OUT_F32>
 __global__ void __launch_bounds__(fwd::NT, 1)
     fm_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
-                  const __grid_constant__ CUtensorMap tmV, const FwdArgs a) {
+                  const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmO, const FwdArgs a) {
   using namespace fwd;
   using S = Smem<D>;
   extern __shared__ uint8_t smem_raw[];
@@ -94,6 +106,7 @@ __global__ void __launch_bounds__(fwd::NT, 1)
   const bool has_q1 = i1 < a.Tr;
   const size_t bhm = static_cast<size_t>(b) * a.Hm + hm;
 
+  if (tid == 0) FTE(0);
   // ---- setup: barriers (warp 8), TMEM (warp 9) ----
   if (warp == PRODUCER_WARP && lane == 0) {
     mbar_init(&sm.bar_q, 1);
@@ -144,6 +157,7 @@ __global__ void __launch_bounds__(fwd::NT, 1)
   tc_fence_after();
   const int nE = sm.n_entries;
   const uint32_t tbase = sm.tmem_base;
+  if (tid == 0) FTE(1);
 
   if (warp == PRODUCER_WARP) {
     // ================================ TMA producer ================================
@@ -222,6 +236,7 @@ __global__ void __launch_bounds__(fwd::NT, 1)
         mbar_wait(&sm.bar_q, 0);
         tc_fence_after();
       }
+      if (lane == 0) FTE(2);
       for (int e = 0; e < nE; ++e) {
         const uint32_t ent = sm.list[e];
         const int ks = e % KST;
@@ -246,10 +261,11 @@ __global__ void __launch_bounds__(fwd::NT, 1)
         }
         mma_commit_w(&sm.k_empty[ks]);
       }
-      for (int q = 0; q < 2; ++q)
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {  // O_q complete: its epilogue need not wait for the other tile
         if (pend[q] >= 0) issue_pv(q);
-      mma_commit_w(&sm.o_full[0]);
-      mma_commit_w(&sm.o_full[1]);
+        mma_commit_w(&sm.o_full[q]);
+      }
     }
   } else {
     // ================================ softmax WGs ================================
@@ -396,6 +412,7 @@ __global__ void __launch_bounds__(fwd::NT, 1)
       if (lane == 0) mbar_arrive(&sm.m_empty[ms]);
     }
     // ---- epilogue: O = O / l, L = m + ln(l) (Alg. 1 lines 27-28) ----
+    if (row_t == 0 && hh == 0) FTE(3 + q);
     sm.xsum[q][hh][row_t] = l;
     named_bar_sync(bar_id, 64);
     l += sm.xsum[q][hh ^ 1][row_t];
@@ -406,8 +423,43 @@ __global__ void __launch_bounds__(fwd::NT, 1)
     }
     const float inv = live ? 1.0f / l : 0.f;
     const size_t orow = ((static_cast<size_t>(b) * a.N + row) * a.H + h) * D + hh * (D / 2);
+    if constexpr (!OUT_F32) {
+      // bf16 O goes out through shared memory and one TMA store per 64-column block: a thread
+      // holds one row, so direct 16-byte stores would scatter every warp instruction over 32 rows
+      // (measured ~6K clk of LSU time per CTA).  The Q tile buffer of this tile is free: all its
+      // S MMAs completed before o_full.  Rows >= N are clipped by the TMA unit.
+      uint8_t* stg = sm.q[q];
+#pragma unroll
+      for (int c = 0; c < D / 64; ++c) {
+        uint32_t ov[32];
+        if (cnt > 0) {
+          tmem_ld32(tOh + c * 32, ov);
+          tmem_wait_ld();
+        }
+        const int col = hh * (D / 2) + c * 32;  // first of these 32 columns
+        uint8_t* blk = stg + (col / 64) * 16384 + row_t * 128;
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          float f[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) f[u] = live ? __uint_as_float(ov[8 * t + u]) * inv : 0.f;
+          const int chunk = (col % 64) / 8 + t;
+          *reinterpret_cast<uint4*>(blk + ((chunk ^ (row_t & 7)) << 4)) =
+              make_uint4(pack_bf16(f[0], f[1]), pack_bf16(f[2], f[3]), pack_bf16(f[4], f[5]), pack_bf16(f[6], f[7]));
+        }
+      }
+      fence_proxy_async_smem();
+      named_bar_sync(9 + q, 256);
+      const int row0 = (q == 0 ? i0 : i1) * 128;
+      if (warp == q * 8 && lane == 0 && row0 < a.N) {
+#pragma unroll
+        for (int c = 0; c < D / 64; ++c) tma_store_4d(&tmO, stg + c * 16384, c * 64, h, row0, b);
+        bulk_commit();
+        bulk_wait_read0();  // the staging buffer must outlive the TMA reads
+      }
+    }
 #pragma unroll 1
-    for (int c = 0; c < D / 64; ++c) {
+    for (int c = 0; c < (OUT_F32 ? D / 64 : 0); ++c) {
       uint32_t ov[32];
       if (cnt > 0) {  // WG-uniform: the tcgen05.ld stays warp-collective
         tmem_ld32(tOh + c * 32, ov);
@@ -433,6 +485,7 @@ __global__ void __launch_bounds__(fwd::NT, 1)
     if (row < a.N && hh == 0)
       a.lse[(static_cast<size_t>(b) * a.H + h) * a.N + row] =
           live ? (m_used + __log2f(l)) * 0.6931471805599453f : -INFINITY;
+    if (row_t == 0 && hh == 0) FTE(5 + q);
   }
 
   tc_fence_before();
@@ -441,23 +494,29 @@ __global__ void __launch_bounds__(fwd::NT, 1)
     tc_fence_after();
     tmem_dealloc<512>(tbase);
   }
+#ifdef FM_TRACE
+  if (tid == 0) {
+    FTE(7);
+    if (blockIdx.x == FM_TRACE_BX && blockIdx.y == 0 && blockIdx.z == 0) FM_TRACE_NE(nE);
+  }
+#endif
 }
 
 template <int D, bool CAUSAL, bool OUT_F32>
 static cudaError_t launch_fwd_t(const Dims& d, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
-                                const FwdArgs& a, cudaStream_t st) {
+                                const CUtensorMap& to, const FwdArgs& a, cudaStream_t st) {
   auto kern = fm_fwd_kernel<D, CAUSAL, OUT_F32>;
   const size_t smem = sizeof(fwd::Smem<D>) + 1024;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (e != cudaSuccess) return e;
   dim3 grid((d.Tr + 1) / 2, d.H, d.B);
-  kern<<<grid, fwd::NT, smem, st>>>(tq, tk, tv, a);
+  kern<<<grid, fwd::NT, smem, st>>>(tq, tk, tv, to, a);
   return cudaGetLastError();
 }
 
 cudaError_t launch_fwd(const Dims& d, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
-                       const FwdArgs& a, cudaStream_t st) {
-#define FM_F(DD, CC, FF) return launch_fwd_t<DD, CC, FF>(d, tq, tk, tv, a, st)
+                       const CUtensorMap& to, const FwdArgs& a, cudaStream_t st) {
+#define FM_F(DD, CC, FF) return launch_fwd_t<DD, CC, FF>(d, tq, tk, tv, to, a, st)
   if (d.D == 128) {
     if (d.causal) { if (d.out_f32) FM_F(128, true, true); else FM_F(128, true, false); }
     else { if (d.out_f32) FM_F(128, false, true); else FM_F(128, false, false); }
@@ -473,5 +532,8 @@ cudaError_t launch_fwd(const Dims& d, const CUtensorMap& tq, const CUtensorMap& 
 #ifdef FM_TRACE
 extern "C" __attribute__((visibility("default"))) int flashmask_debug_trace_fwd(long long* host) {
   return cudaMemcpyFromSymbol(host, fm::g_fm_trace_fwd, sizeof(long long) * 64 * 16) == cudaSuccess ? 0 : 1;
+}
+extern "C" __attribute__((visibility("default"))) int flashmask_debug_trace_fwd_ev(long long* host) {
+  return cudaMemcpyFromSymbol(host, fm::g_fm_trace_fwd_ev, sizeof(long long) * 16) == cudaSuccess ? 0 : 1;
 }
 #endif

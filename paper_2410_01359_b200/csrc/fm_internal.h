@@ -84,11 +84,12 @@ cudaError_t launch_expand(const int32_t* sri, const Dims& d, int bc, int32_t* ex
 cudaError_t launch_classify(const int32_t* ext8, const Dims& d, int br, int bc, uint8_t* map, int transposed,
                             int kernel_map, int64_t* counts, cudaStream_t st);
 cudaError_t launch_fwd(const Dims& d, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
-                       const FwdArgs& a, cudaStream_t st);
+                       const CUtensorMap& to, const FwdArgs& a, cudaStream_t st);
 cudaError_t launch_bwd_pre(const Dims& d, const void* o, const void* dout, const float* lse, float* dvec, float* l2,
                            float* dqacc, cudaStream_t st);
 cudaError_t launch_bwd(const Dims& d, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
-                       const CUtensorMap& tdo, const CUtensorMap& tdq, const BwdArgs& a, cudaStream_t st);
+                       const CUtensorMap& tdo, const CUtensorMap& tdq, const CUtensorMap& tdk, const CUtensorMap& tdv,
+                       const BwdArgs& a, cudaStream_t st);
 cudaError_t launch_dq_convert(const Dims& d, const float* dqacc, void* dq, cudaStream_t st);
 cudaError_t launch_dq(const Dims& d, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
                       const CUtensorMap& tdo, const DqArgs& a, cudaStream_t st);
