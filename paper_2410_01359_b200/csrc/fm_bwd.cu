@@ -227,6 +227,15 @@ __global__ void __launch_bounds__(bwd::NT, 1)
     mbar_init(&sm.ds_empty[1], 1);
     mbar_init(&sm.done, 1);
     fence_barrier_init();
+    // K_j, V_j do not depend on the visit list: start their loads before it is built
+    tma_prefetch_desc(&tmK);
+    tma_prefetch_desc(&tmV);
+    mbar_expect_tx(&sm.kv_full, 2 * C::KV_TILE);
+#pragma unroll
+    for (int c = 0; c < D / 64; ++c) {
+      tma_load_4d(sm.k + c * 16384, &tmK, &sm.kv_full, c * 64, hk, j * 128, b);
+      tma_load_4d(sm.v + c * 16384, &tmV, &sm.kv_full, c * 64, hk, j * 128, b);
+    }
   }
   if (warp == 13) tmem_alloc<512>(&sm.tmem_base);
 
@@ -280,17 +289,10 @@ __global__ void __launch_bounds__(bwd::NT, 1)
 
   if (warp == 12) {
     // ================================ TMA producer ================================
+    if (lane == 0 && nE == 0) mbar_wait(&sm.kv_full, 0);  // K/V must land before the CTA exits
     if (lane == 0 && nE > 0) {
       tma_prefetch_desc(&tmQ);
-      tma_prefetch_desc(&tmK);
-      tma_prefetch_desc(&tmV);
       tma_prefetch_desc(&tmdO);
-      mbar_expect_tx(&sm.kv_full, 2 * C::KV_TILE);
-#pragma unroll
-      for (int c = 0; c < D / 64; ++c) {
-        tma_load_4d(sm.k + c * 16384, &tmK, &sm.kv_full, c * 64, hk, j * 128, b);
-        tma_load_4d(sm.v + c * 16384, &tmV, &sm.kv_full, c * 64, hk, j * 128, b);
-      }
       for (int t = 0; t < nE; ++t) {
         const int i = sm.list[lidx(t)];
         const int hq = hk * G + t / nE1;
@@ -546,6 +548,7 @@ __global__ void __launch_bounds__(bwd::NT, 1)
       // them completed before `done`) and TMA stores — a thread holds one key row, so direct
       // 16-byte stores would scatter each warp instruction over 32 rows.  Keys >= N are clipped.
       uint8_t* stg = wg == 0 ? sm.v : sm.k;
+      mbar_wait(&sm.kv_full, 0);  // the K/V loads into these buffers have landed (even when nE == 0)
 #pragma unroll 1
       for (int c = 0; c < D / 32; ++c) {
         uint32_t r[32];

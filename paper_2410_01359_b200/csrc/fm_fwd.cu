@@ -119,6 +119,14 @@ __global__ void __launch_bounds__(fwd::NT, 1)
       mbar_init(&sm.o_full[q], 1);
     }
     fence_barrier_init();
+    // Q does not depend on the visit list: start its load before the list is built
+    tma_prefetch_desc(&tmQ);
+    mbar_expect_tx(&sm.bar_q, has_q1 ? 2 * S::TILE : S::TILE);
+#pragma unroll
+    for (int c = 0; c < D / 64; ++c) {
+      tma_load_4d(sm.q[0] + c * 16384, &tmQ, &sm.bar_q, c * 64, h, i0 * 128, b);
+      if (has_q1) tma_load_4d(sm.q[1] + c * 16384, &tmQ, &sm.bar_q, c * 64, h, i1 * 128, b);
+    }
   }
   if (warp == MMA_WARP) tmem_alloc<512>(&sm.tmem_base);
 
@@ -162,18 +170,10 @@ __global__ void __launch_bounds__(fwd::NT, 1)
   if (warp == PRODUCER_WARP) {
     // ================================ TMA producer ================================
     if (lane == 0) {
-      tma_prefetch_desc(&tmQ);
       tma_prefetch_desc(&tmK);
       tma_prefetch_desc(&tmV);
       constexpr uint32_t TB = S::TILE;
-      if (nE > 0) {
-        mbar_expect_tx(&sm.bar_q, has_q1 ? 2 * TB : TB);
-#pragma unroll
-        for (int c = 0; c < D / 64; ++c) {
-          tma_load_4d(sm.q[0] + c * 16384, &tmQ, &sm.bar_q, c * 64, h, i0 * 128, b);
-          if (has_q1) tma_load_4d(sm.q[1] + c * 16384, &tmQ, &sm.bar_q, c * 64, h, i1 * 128, b);
-        }
-      }
+      if (nE == 0) mbar_wait(&sm.bar_q, 0);  // no MMA will wait for Q: it must land before exit
       const int4* vec_bh = a.vec4 + bhm * static_cast<size_t>(a.Tc) * 128;
       for (int e = 0; e < nE; ++e) {
         const uint32_t ent = sm.list[e];
@@ -429,6 +429,7 @@ __global__ void __launch_bounds__(fwd::NT, 1)
       // (measured ~6K clk of LSU time per CTA).  The Q tile buffer of this tile is free: all its
       // S MMAs completed before o_full.  Rows >= N are clipped by the TMA unit.
       uint8_t* stg = sm.q[q];
+      mbar_wait(&sm.bar_q, 0);  // the Q load into this buffer has landed (even if no tile used it)
 #pragma unroll
       for (int c = 0; c < D / 64; ++c) {
         uint32_t ov[32];
