@@ -158,9 +158,27 @@ struct Smem {
 // P^T / dS^T for one 32-query chunk of one key (Alg. 2 lines 20-25):
 //   p = exp2(S*scale*log2e - L2_r) (masked to 0 on PARTIAL tiles), ds = p * (dP - D_r)
 // Branch-free per template so the compiler can overlap the shared loads, FMAs and MUFU ops.
+// Rows [r0, r0 + 32) masked for this thread's key, as a bit set (bit u = row r0 + u): the
+// interval test of Alg. 2 lines 20-23 evaluated once per 32 rows instead of per element.
+__device__ __forceinline__ uint32_t range_bits(int lo, int len) {
+  const int a = min(max(lo, 0), 32);
+  const int b = static_cast<int>(min(max(static_cast<long long>(lo) + len, 0ll), 32ll));
+  return b > a ? static_cast<uint32_t>(((1ull << b) - 1ull) & ~((1ull << a) - 1ull)) : 0u;
+}
+template <bool CAUSAL>
+__device__ __forceinline__ uint32_t row_mask_bits(int r0, int key, int4 mv) {
+  uint32_t m = range_bits(mv.x - r0, mv.y);
+  if constexpr (CAUSAL)
+    m |= range_bits(0, key - r0);  // rows r < key
+  else
+    m |= range_bits(mv.z - r0, mv.w);
+  return m;
+}
+
 template <bool PART, bool CAUSAL>
 __device__ __forceinline__ void pds_chunk(const uint32_t* sr, const uint32_t* dr, const float* lq, const float* dq,
                                           float sl2, int r0, int key, int4 mv, uint32_t* pp, uint32_t* dp) {
+  const uint32_t mb = PART ? row_mask_bits<CAUSAL>(r0, key, mv) : 0u;
 #pragma unroll
   for (int c = 0; c < 32; c += 4) {
     const float4 L4 = *reinterpret_cast<const float4*>(lq + c);
@@ -171,15 +189,7 @@ __device__ __forceinline__ void pds_chunk(const uint32_t* sr, const uint32_t* dr
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       p[u] = ex2(fmaf(__uint_as_float(sr[c + u]), sl2, -l4[u]));
-      if constexpr (PART) {
-        const int r = r0 + c + u;
-        bool msk = static_cast<unsigned>(r - mv.x) < static_cast<unsigned>(mv.y);
-        if constexpr (CAUSAL)
-          msk |= r < key;
-        else
-          msk |= static_cast<unsigned>(r - mv.z) < static_cast<unsigned>(mv.w);
-        p[u] = msk ? 0.f : p[u];
-      }
+      if constexpr (PART) p[u] = ((mb >> (c + u)) & 1u) ? 0.f : p[u];
       ds[u] = p[u] * (__uint_as_float(dr[c + u]) - d4[u]);
     }
     pp[c / 2] = pack_bf16(p[0], p[1]);

@@ -136,6 +136,67 @@ def test_bf16_outputs_close(fmlib):
     assert torch.equal(r32[1], r16[1])
 
 
+BF16_CASES = [("causal_document", 1000, 128, 2, 2), ("document", 257, 64, 1, 2), ("random_eviction", 129, 128, 1, 1),
+              ("full", 127, 64, 1, 1), ("global_sliding_window", 700, 128, 1, 1), ("sliding_window", 384, 64, 1, 2)]
+
+
+def _check_bf16_vs_fp32(r32, r16):
+    o32, lse32 = r32[0], r32[1]
+    # forward: the bf16 epilogue (shared-memory stage + TMA store) equals RNE(bf16) of the fp32
+    # epilogue's values bit for bit — any swizzle / row / clipping error shows up here
+    assert torch.equal(r16[0], o32.to(torch.bfloat16))
+    assert torch.equal(r16[1], lse32)
+    # backward: the only difference is D = rowsum(dO o O) seeing bf16 O (and the output rounding)
+    for name, a32, a16 in zip(("dQ", "dK", "dV"), r32[2:], r16[2:]):
+        bad = (a16.float() - a32).abs() > 2.0 ** -8 * a32.abs() + 2e-3
+        assert not bad.any(), (name, torch.nonzero(bad)[:5].tolist())
+
+
+@pytest.mark.parametrize("fam,N,d,B,H", BF16_CASES)
+def test_bf16_outputs(fmlib, fam, N, d, B, H):
+    """bf16 outputs (the timing configuration): ragged N, odd row-tile counts, d = 64 / 128."""
+    _, _, _, r32 = _run(fmlib, fam, N, d, B, H, seed=7)
+    masks, sri, t, r16 = _run(fmlib, fam, N, d, B, H, seed=7, out_dtype=torch.bfloat16)
+    _check_bf16_vs_fp32(r32, r16)
+    O, L, (gq, gk, gv) = oracle_head(t, masks, sri.numpy(), 0, 0, 1, masks[0].causal)
+    ulp = lambda ref: 2.0 ** -8 * np.abs(ref)   # bf16 output rounding on top of the north_star bar
+    for name, got, ref in (("O", r16[0], O), ("dK", r16[3], gk), ("dV", r16[4], gv)):
+        g = got[0, :, 0].float().cpu().numpy()
+        assert (np.abs(g - ref) <= 2e-2 + ulp(ref)).all(), name
+
+
+@pytest.mark.parametrize("d", [64, 128])
+def test_empty_tiles_bf16(fmlib, d):
+    """CTAs with nothing to compute still write their (zero) outputs through the TMA-store
+    epilogue: query rows [128, 256) masked for every key (an empty second query tile next to a
+    busy first one), keys [256, 384) masked for every row (a key tile with no visited row tile)."""
+    N = 640
+    sri = np.zeros((N, 4), np.int32)
+    sri[:, 0], sri[:, 1] = 128, 256          # lower interval [128, 256): rows 128..255 empty
+    sri[:, 2], sri[:, 3] = 0, 0              # no upper interval
+    sri[256:384, 0], sri[256:384, 1] = 0, N  # keys 256..383 masked for every row
+    m = wm.MaskInput(N, False, 4, sri, "empty_tiles")
+    sri_t, t = build_case([m], 2, d, base=11)
+    sri_c, tc = to_cuda(sri_t, t)
+    res = {}
+    for dt in (torch.float32, torch.bfloat16):
+        o, lse = fmlib.flashmask_fwd(tc["q"], tc["k"], tc["v"], sri_c, False, out_dtype=dt)
+        res[dt] = (o, lse, *fmlib.flashmask_bwd(tc["q"], tc["k"], tc["v"], o, tc["do"], lse, sri_c, False,
+                                                out_dtype=dt))
+    torch.cuda.synchronize()
+    r32, r16 = res[torch.float32], res[torch.bfloat16]
+    assert (r16[0][:, 128:256] == 0).all() and torch.isneginf(r16[1][:, :, 128:256]).all()
+    assert (r16[3][:, 256:384] == 0).all() and (r16[4][:, 256:384] == 0).all()
+    _check_bf16_vs_fp32(r32, r16)
+    for h in range(2):
+        O, L, (gq, gk, gv) = oracle_head(t, [m], sri_t.numpy(), 0, h, 1, False)
+        assert_close("O", r32[0][0, :, h].cpu().numpy(), O)
+        assert_lse(r32[1][0, h].cpu().numpy(), L)
+        assert_close("dQ", r32[2][0, :, h].cpu().numpy(), gq)
+        assert_close("dK", r32[3][0, :, h].cpu().numpy(), gk)
+        assert_close("dV", r32[4][0, :, h].cpu().numpy(), gv)
+
+
 def test_empty_rows(fmlib):
     """Rows masked in every column: O = 0, lse = -inf, zero dQ; padding keys get zero dK/dV."""
     m = wm.empty_rows_padding([100, 150], 50)
