@@ -85,25 +85,6 @@ constexpr int PRODUCER_WARP = 16, MMA_WARP = 17;
 
 __device__ __forceinline__ int ent_cls(uint32_t ent, int q) { return (ent >> (24 + 2 * q)) & 3; }
 
-// Bits [lo, lo + len) ∩ [0, 32) of a 32-bit word (lo may be negative or >= 32; len >= 0).
-__device__ __forceinline__ uint32_t range_bits(int lo, int len) {
-  const int a = min(max(lo, 0), 32);
-  const int b = static_cast<int>(min(max(static_cast<long long>(lo) + len, 0ll), 32ll));
-  return b > a ? static_cast<uint32_t>(((1ull << b) - 1ull) & ~((1ull << a) - 1ull)) : 0u;
-}
-
-// 32 x 32 bit-matrix transpose across the warp: lane c holds bit u = A[c][u]; returns, in lane u,
-// the word whose bit c is A[c][u] (five xor-butterfly stages).
-__device__ __forceinline__ uint32_t transpose32(uint32_t x, int lane) {
-#pragma unroll
-  for (int s = 16; s > 0; s >>= 1) {
-    const uint32_t m = s == 16 ? 0x0000FFFFu : s == 8 ? 0x00FF00FFu : s == 4 ? 0x0F0F0F0Fu : s == 2 ? 0x33333333u : 0x55555555u;
-    const uint32_t y = __shfl_xor_sync(0xffffffffu, x, s);
-    x = (lane & s) ? ((x & ~m) | ((y & ~m) >> s)) : ((x & m) | ((y & m) << s));
-  }
-  return x;
-}
-
 }  // namespace fwd
 
 template <int D, bool CAUSAL, bool OUT_F32>
@@ -318,27 +299,9 @@ __global__ void __launch_bounds__(fwd::NT, 1)
         FM_WAIT_S(&sm.s_full[q], cnt & 1);
         if (row_t == 0 && hh == 0) FT(0 + q, e);
         tc_fence_after();
-        // Element mask of Alg. 1 lines 15-21 on PARTIAL tiles: row r is masked for key y iff
-        // (unsigned)(r - start_y) < len_y for either interval, or (causal) r < y.  Built
-        // bit-parallel: lane c evaluates column c against this warp's 32 rows (a 32-bit row set
-        // per interval), a warp bit-transpose turns that into each row's 32-column mask word.
-        uint32_t mbits[2] = {0u, 0u};
-        if (cls == 1) {
-          const int rw0 = row - lane;  // first row of this warp
-#pragma unroll
-          for (int k = 0; k < 2; ++k) {
-            const int col = hh * 64 + 32 * k + lane;
-            const int4 mv = sm.mask[ms][col];
-            uint32_t cb = range_bits(mv.x - rw0, mv.y);
-            if constexpr (CAUSAL)
-              cb |= range_bits(0, j * 128 + col - rw0);  // rows r < y
-            else
-              cb |= range_bits(mv.z - rw0, mv.w);
-            mbits[k] = transpose32(cb, lane);
-          }
-        }
-        // Pass 1: max over this half's 64 columns, 16 at a time (S stays in TMEM for pass 2);
-        // masked elements excluded (the mask is re-applied in pass 2, no TMEM write-back).
+        // Pass 1: max over this half's 64 columns, 32 at a time (S stays in TMEM for pass 2).
+        // On PARTIAL tiles the element mask (Alg. 1 lines 15-21) is applied here and the masked S
+        // written back to TMEM, so pass 2 is identical for PARTIAL and UNMASKED tiles.
         float mx0 = -INFINITY, mx1 = -INFINITY, mx2 = -INFINITY, mx3 = -INFINITY;
         uint32_t sr[2][16];
         tmem_ld16(tSh, sr[0]);
@@ -348,9 +311,21 @@ __global__ void __launch_bounds__(fwd::NT, 1)
           if (c + 1 < 4) tmem_ld16(tSh + (c + 1) * 16, sr[(c + 1) & 1]);
           float* sv = reinterpret_cast<float*>(sr[c & 1]);
           if (cls == 1) {
-            const uint32_t w = mbits[c >> 1] >> ((c & 1) * 16);
+            // element mask of Alg. 1 lines 15-21: row r is masked for key y iff
+            // (unsigned)(r - start_y) < len_y for either interval, or (causal) r < y
+            const int4* mk = sm.mask[ms] + hh * 64 + c * 16;
+            const int rmy = row - (j * 128 + hh * 64 + c * 16);
 #pragma unroll
-            for (int t = 0; t < 16; ++t) sv[t] = ((w >> t) & 1u) ? -INFINITY : sv[t];
+            for (int t = 0; t < 16; ++t) {
+              const int4 mv = mk[t];
+              bool msk = static_cast<unsigned>(row - mv.x) < static_cast<unsigned>(mv.y);
+              if constexpr (CAUSAL)
+                msk |= rmy < t;
+              else
+                msk |= static_cast<unsigned>(row - mv.z) < static_cast<unsigned>(mv.w);
+              sv[t] = msk ? -INFINITY : sv[t];
+            }
+            tmem_st16(tSh + c * 16, sr[c & 1]);  // masked S back to TMEM: pass 2 needs no mask work
           }
 #pragma unroll
           for (int t = 0; t < 16; t += 8) {
@@ -360,6 +335,7 @@ __global__ void __launch_bounds__(fwd::NT, 1)
             mx3 = fmax3(mx3, sv[t + 6], sv[t + 7]);
           }
         }
+        if (cls == 1) tmem_wait_st();
         const float mh = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3));
         if (row_t == 0 && q == 0 && hh == 0) FT(10, e);
         sm.xmax[q][cnt & 1][hh][row_t] = mh;
@@ -398,12 +374,7 @@ __global__ void __launch_bounds__(fwd::NT, 1)
         for (int ch = 0; ch < 4; ++ch) {
           tmem_wait_ld();
           if (ch + 1 < 4) tmem_ld16(tSh + (ch + 1) * 16, sr[(ch + 1) & 1]);
-          float* sv = reinterpret_cast<float*>(sr[ch & 1]);
-          if (cls == 1) {  // exp2(-inf) = 0 on both exp paths
-            const uint32_t w = mbits[ch >> 1] >> ((ch & 1) * 16);
-#pragma unroll
-            for (int t = 0; t < 16; ++t) sv[t] = ((w >> t) & 1u) ? -INFINITY : sv[t];
-          }
+          const float* sv = reinterpret_cast<const float*>(sr[ch & 1]);
           uint32_t pk[8];
 #pragma unroll
           for (int kk = 0; kk < 8; ++kk) {
