@@ -94,9 +94,13 @@ constexpr int kMaxTrb = FM_MAXTRB;  // d=128 (Br=64); d=64 (Br=128) uses half: t
 // (2 KiB, 128-byte swizzle) for TMA tensor reduce-adds, DQ64_NBUF boxes in flight per warp
 constexpr int DQ64_NBUF = 3;
 #ifndef FM_DQ_CROWS
-#define FM_DQ_CROWS 16
+#define FM_DQ_CROWS 32
 #endif
 constexpr int DQ_CROWS = FM_DQ_CROWS;  // query rows per dQ^T staging chunk (d=128)
+#ifndef FM_BWD_NDS
+#define FM_BWD_NDS 1
+#endif
+constexpr int NDS = FM_BWD_NDS;  // dS shared-memory buffers
 #ifndef FM_BWD_ROT
 #define FM_BWD_ROT 0  // experiment: start each key tile's row loop at its diagonal (wrap around)
 #endif
@@ -138,7 +142,7 @@ struct Smem {
   uint8_t v[C::KV_TILE];
   uint8_t q[QST][C::Q_TILE];
   uint8_t dO[QST][C::Q_TILE];
-  uint8_t ds[2][C::DS_BYTES];  // double-buffered: dS(t+1) is written while dQ(t) reads dS(t)
+  uint8_t ds[NDS][C::DS_BYTES];  // NDS = 1: dS(t+1) waits for dQ(t) to finish reading (frees 16 KiB for dQ stages)
   // d=128: dQ^T staged 16 query rows (8 KiB, contiguous in dQacc) at a time for one bulk
   // reduce-add each, double-buffered
   float dq_stage[C::DQT ? DQ_NSTAGE : 4 * DQ64_NBUF][C::DQT ? DQ_CROWS * D : 16 * 32];
@@ -373,7 +377,7 @@ __global__ void __launch_bounds__(bwd::NT, 1)
             mma_ts_w(tbase + C::DV_COL, tbase + C::P_COL + boff + kk * 8,
                      sdesc_sw128(do_addr + kk * 2048, BR * 128, 1024), ID_G, acc);
             if constexpr (C::DK_SS)  // A = dS^T straight from the dQ operand buffer in smem
-              mma_ss_w(tbase + C::DK_COL, sdesc_sw128(smem_u32(sm.ds[t & 1]) + kk * 32, 16, 1024),
+              mma_ss_w(tbase + C::DK_COL, sdesc_sw128(smem_u32(sm.ds[t % NDS]) + kk * 32, 16, 1024),
                        sdesc_sw128(q_addr + kk * 2048, BR * 128, 1024), ID_G, acc);
             else
               mma_ts_w(tbase + C::DK_COL, tbase + C::DS_COL + boff + kk * 8,
@@ -387,12 +391,12 @@ __global__ void __launch_bounds__(bwd::NT, 1)
           // thread (in order), and the compute WGs stored P/dS(t) there only after dQ(t-NB) was
           // read out (dq_empty[t % NB]).
           if (!a.with_dq) {
-            if constexpr (C::DK_SS) mma_commit_w(&sm.ds_empty[t & 1]);  // dK(t) read dS^T(t)
+            if constexpr (C::DK_SS) mma_commit_w(&sm.ds_empty[t % NDS]);  // dK(t) read dS^T(t)
             continue;
           }
           if constexpr (!C::DQ_ALIAS) FM_BWD_ISSUER_WAIT(&sm.dq_empty[0], (t & 1) ^ 1);
           tc_fence_after();
-          const uint32_t ds_addr = smem_u32(sm.ds[t & 1]);
+          const uint32_t ds_addr = smem_u32(sm.ds[t % NDS]);
 #pragma unroll
           for (int kk = 0; kk < 8; ++kk) {
             if constexpr (C::DQT)
@@ -403,7 +407,7 @@ __global__ void __launch_bounds__(bwd::NT, 1)
                      sdesc_sw128(k_addr + kk * 2048, 16384, 1024), ID_Q, kk > 0 ? 1u : 0u);
           }
           mma_commit_w(&sm.dq_full[bi]);
-          mma_commit_w(&sm.ds_empty[t & 1]);
+          mma_commit_w(&sm.ds_empty[t % NDS]);
           if (lane == 0) FM_T(13, t);
         }
         mma_commit_w(&sm.done);  // all S^T/dP^T completed earlier (they precede every p_full)
@@ -459,7 +463,7 @@ __global__ void __launch_bounds__(bwd::NT, 1)
       if (FM_EXP == 1) {
         tc_fence_before();
         mbar_arrive(&sm.sdp_free);
-        mbar_wait(&sm.ds_empty[t & 1], ((t >> 1) & 1) ^ 1);
+        mbar_wait(&sm.ds_empty[t % NDS], ((t / NDS) & 1) ^ 1);
         mbar_wait(&sm.dq_empty[t % C::NB], ((t / C::NB) & 1) ^ 1);
         tc_fence_before();
         mbar_arrive(&sm.p_full[t % C::NB]);
@@ -489,7 +493,7 @@ __global__ void __launch_bounds__(bwd::NT, 1)
       // dS^T row of this key into the SW128 MN-major smem operand of the dQ GEMM
       // (first: it only needs dQ(t-1) to have finished reading the buffer)
       const bool ds_smem = a.with_dq || C::DK_SS;  // dS^T is a shared-memory operand (dQ, dK)
-      if (ds_smem) mbar_wait(&sm.ds_empty[t & 1], ((t >> 1) & 1) ^ 1);  // dK/dQ(t-2) have read this buffer
+      if (ds_smem) mbar_wait(&sm.ds_empty[t % NDS], ((t / NDS) & 1) ^ 1);  // dK/dQ(t-2) have read this buffer
       if (tid == 0) FM_T(7, t);
 #ifdef FM_TRACE
       if (lane == 0 && t >= 30 && t < 40 && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0)
@@ -502,7 +506,7 @@ __global__ void __launch_bounds__(bwd::NT, 1)
         for (int u = 0; u < 4; ++u) {
           const int g = (q0 >> 3) + u;  // 8-query group
           const int sub = g >> 3, gg = g & 7;
-          uint8_t* dst = sm.ds[t & 1] + sub * 16384 + key_t * 128 + ((gg ^ (key_t & 7)) << 4);
+          uint8_t* dst = sm.ds[t % NDS] + sub * 16384 + key_t * 128 + ((gg ^ (key_t & 7)) << 4);
           *reinterpret_cast<uint4*>(dst) =
               make_uint4(dp[ch][4 * u], dp[ch][4 * u + 1], dp[ch][4 * u + 2], dp[ch][4 * u + 3]);
         }
