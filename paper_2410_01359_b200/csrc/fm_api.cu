@@ -67,7 +67,7 @@ bool make_map(CUtensorMap* m, const void* ptr, const fm::Dims& d, int heads, int
   return true;
 }
 
-// fp32 dQ accumulator [B*H*Npb, D] viewed 2-D for TMA tensor reduce-adds: box = 16 rows x 32
+// fp32 dQ accumulator [B*H*Npb, D] viewed 2-D for TMA tensor reduce-adds: box = kDq64BoxRows x 32
 // columns (128 B), 128-byte swizzle (d=64 backward, fm_bwd.cu).
 bool make_dq_map(CUtensorMap* m, float* dqacc, const fm::Dims& d, std::string* err) {
   auto enc = get_encode();
@@ -77,7 +77,7 @@ bool make_dq_map(CUtensorMap* m, float* dqacc, const fm::Dims& d, std::string* e
   }
   cuuint64_t dims[2] = {static_cast<cuuint64_t>(d.D), static_cast<cuuint64_t>(d.B) * d.H * d.Npb};
   cuuint64_t strides[1] = {static_cast<cuuint64_t>(d.D) * 4};
-  cuuint32_t box[2] = {32, 16};
+  cuuint32_t box[2] = {32, static_cast<cuuint32_t>(fm::kDq64BoxRows)};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, dqacc, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                    CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);

@@ -90,9 +90,13 @@ constexpr int DQ_NSTAGE = FM_DQ_NSTAGE;  // 8 KiB dQ^T staging buffers (d=128)
 #define FM_MAXTRB 4096
 #endif
 constexpr int kMaxTrb = FM_MAXTRB;  // d=128 (Br=64); d=64 (Br=128) uses half: the same max N
-// d=64 dQ reduction: each dQ warp stages its 32 query rows as 16-row x 32-column fp32 boxes
-// (2 KiB, 128-byte swizzle) for TMA tensor reduce-adds, DQ64_NBUF boxes in flight per warp
+// d=64 dQ reduction (FM_DQ64_WG = 1): the dQ warpgroup stages the 128-row x 32-column fp32 half
+// tiles (16 KiB, 128-byte swizzle) for one TMA tensor reduce-add each, DQ64_NBUF in flight — two
+// operations per row tile (the cost of the reduction follows the number of operations, §6b).
+// FM_DQ64_WG = 0: each dQ warp stages 16-row x 32-column boxes (2 KiB), DQ64_NBUF per warp.
 constexpr int DQ64_NBUF = 3;
+constexpr int DQ64_STAGES = FM_DQ64_WG ? DQ64_NBUF : 4 * DQ64_NBUF;
+constexpr int DQ64_STAGE_FLOATS = kDq64BoxRows * 32;
 #ifndef FM_DQ_CROWS
 #define FM_DQ_CROWS 32
 #endif
@@ -145,7 +149,7 @@ struct Smem {
   uint8_t ds[NDS][C::DS_BYTES];  // NDS = 1: dS(t+1) waits for dQ(t) to finish reading (frees 16 KiB for dQ stages)
   // d=128: dQ^T staged 16 query rows (8 KiB, contiguous in dQacc) at a time for one bulk
   // reduce-add each, double-buffered
-  float dq_stage[C::DQT ? DQ_NSTAGE : 4 * DQ64_NBUF][C::DQT ? DQ_CROWS * D : 16 * 32];
+  float dq_stage[C::DQT ? DQ_NSTAGE : DQ64_STAGES][C::DQT ? DQ_CROWS * D : DQ64_STAGE_FLOATS];
   float lvec[QST][C::BR];
   float dvec[QST][C::BR];
   uint16_t list[C::MAXTRB];
@@ -685,6 +689,30 @@ __global__ void __launch_bounds__(bwd::NT, 1)
             bulk_commit();
           }
         }
+      } else if constexpr (FM_DQ64_WG != 0) {
+        // d=64: r[c] = dQ[query = t_id][c], t_id = 0..127 = the tile's rows.  Each 32-column half
+        // of the 128 x 64 tile is written into a 128-byte-swizzled stage (16-B chunk c of row q at
+        // c ^ (q & 7): conflict-free) and added by one TMA tensor reduce.
+        const int row0 = static_cast<int>(bh * a.Npb) + i * BR;
+#pragma unroll
+        for (int ch = 0; ch < 2; ++ch, ++stage_n) {
+          float* stg = sm.dq_stage[stage_n % DQ64_NBUF];
+          if (stage_n >= DQ64_NBUF) {  // the reduce that read this stage DQ64_NBUF operations ago is done
+            if (t_id == 0) bulk_wait_read<DQ64_NBUF - 1>();
+            named_bar_sync(1, 128);
+          }
+#pragma unroll
+          for (int c = 0; c < 8; ++c)
+            *reinterpret_cast<float4*>(reinterpret_cast<uint8_t*>(stg) + t_id * 128 + ((c ^ (t_id & 7)) << 4)) =
+                make_float4(__uint_as_float(r[ch * 32 + 4 * c]), __uint_as_float(r[ch * 32 + 4 * c + 1]),
+                            __uint_as_float(r[ch * 32 + 4 * c + 2]), __uint_as_float(r[ch * 32 + 4 * c + 3]));
+          fence_proxy_async_smem();
+          named_bar_sync(1, 128);
+          if (t_id == 0) {
+            tma_reduce_add_2d(&tmDQ, stg, ch * 32, row0);
+            bulk_commit();
+          }
+        }
       } else {
         // d=64: r[c] = dQ[query = t_id][c].  The warp's 32 rows go out as four 16-row x 32-column
         // boxes, each written into a 128-byte-swizzled stage (16-B chunk c of row l at c ^ (l & 7):
@@ -716,7 +744,7 @@ __global__ void __launch_bounds__(bwd::NT, 1)
       }
       if (t_id == 0) FM_T(10, t);
     }
-    if (C::DQT ? t_id == 0 : lane == 0) bulk_wait0();  // staging buffers must outlive the bulk reads
+    if ((C::DQT || FM_DQ64_WG) ? t_id == 0 : lane == 0) bulk_wait0();  // stages must outlive the bulk reads
   }
 
   tc_fence_before();
