@@ -284,6 +284,9 @@ def main():
     ap.add_argument("--impl", default="flashmask", choices=["flashmask", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=12.0)
+    ap.add_argument("--time-kernels", default="main", choices=["main", "all"],
+                    help="kernels bracketed by CUDA events inside the timed region: main = K2 and K4 only "
+                         "(events between kernels remove programmatic-dependent-launch overlap), all = every kernel")
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", "0"))
@@ -344,7 +347,8 @@ def main():
     clocks.start()
     stream = torch.cuda.current_stream()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    fm.flashmask_timing_enable(True)
+    main_kernels = [fm.FM_KERNEL_FWD, fm.FM_KERNEL_BWD]
+    fm.flashmask_timing_enable(True, kernels=None if args.time_kernels == "all" else main_kernels)
     barrier()
     ev0.record(stream)
     for _ in range(args.steps):
@@ -357,6 +361,14 @@ def main():
     clk = clocks.stop()
     ms_total = ev0.elapsed_time(ev1)
     ms_step = max_over_ranks(ms_total / args.steps)
+    # kernel split of the small kernels (K1, K3, K5) and the launch count: one extra untimed-for-
+    # value step with every kernel bracketed
+    fm.flashmask_timing_enable(True)
+    step()
+    torch.cuda.synchronize()
+    fm.flashmask_timing_enable(False)
+    ksplit = fm.flashmask_timing_collect()
+    launches_per_step = int(sum(n for _, n in ksplit.values()))
 
     # ---------------- end-to-end through host buffers ----------------
     e2e = None
@@ -432,7 +444,7 @@ def main():
     k_fwd_ms, k_fwd_n = ktimes["fwd"]
     bwd_tf = F_bwd * args.steps / (k_bwd_ms * 1e-3) / 1e12 if k_bwd_ms > 0 else None
     fwd_tf = F_fwd * args.steps / (k_fwd_ms * 1e-3) / 1e12 if k_fwd_ms > 0 else None
-    launches = int(sum(n for _, n in ktimes.values()))
+    launches = launches_per_step * args.steps
 
     cpu = None
     if rank == 0 and world == 1:
@@ -453,7 +465,11 @@ def main():
             "fwd_tflops_kernel": round(fwd_tf, 2) if fwd_tf else None,
             "bwd_tflops_kernel": round(bwd_tf, 2) if bwd_tf else None,
             "block_sparsity_128": [round(r, 4) for r in rhos],
-            "kernels_ms_per_step": {k: round(v[0] / args.steps, 4) for k, v in ktimes.items()},
+            "kernels_ms_per_step": {k: round((ktimes[k][0] / args.steps) if ktimes[k][1] else v[0], 4)
+                                    for k, v in ksplit.items()},
+            "kernel_timing": "fwd/bwd: CUDA events on the launch stream inside the timed region; others: one "
+                             "extra step with every kernel bracketed" if args.time_kernels == "main" else
+                             "every kernel bracketed inside the timed region",
             "roofline": {"kernel": "fm_bwd_kernel (K4)", "bound": "tensor",
                          "achieved": round(bwd_tf, 2) if bwd_tf else None, "peak": peak_sust, "unit": "TFLOP/s",
                          "frac": round(bwd_tf / peak_sust, 4) if bwd_tf else None, "traffic": traffic,

@@ -153,12 +153,17 @@ enum {
   FM_NUM_KERNELS = 7
 };
 
-/* Optional per-kernel timing for roofline reporting (off by default).  While enabled,
- * every kernel this thread launches through the calls above is bracketed by two CUDA
- * events recorded on the caller's stream (no extra synchronisation, same stream order).
+/* Optional per-kernel timing for roofline reporting (off by default).  enable = 0: off;
+ * 1: every kernel this thread launches through the calls above is bracketed by two CUDA
+ * events recorded on the caller's stream (no extra synchronisation, same stream order);
+ * FM_TIMING_SELECT | mask: only kernels whose id bit (1 << FM_KERNEL_*) is in mask.
+ * All kernels are launched with programmatic dependent launch (each may start while its
+ * stream predecessor drains); an event between two kernels removes that overlap, so time
+ * only the kernels you need when the step time matters.
  * flashmask_timing_collect() waits for the recorded events, ADDS the elapsed
  * milliseconds and the launch counts per kernel id into ms[FM_NUM_KERNELS] and
  * launches[FM_NUM_KERNELS] (caller-owned host arrays), and clears the record. */
+#define FM_TIMING_SELECT 0x10000
 FM_API fm_status flashmask_timing_enable(int enable);
 FM_API fm_status flashmask_timing_collect(double* ms, int64_t* launches);
 

@@ -183,6 +183,7 @@ struct TimingRec {
 };
 struct Timing {
   bool on = false;
+  uint32_t mask = 0xFFFFFFFFu;  // kernel ids to bracket
   std::vector<TimingRec> recs;
   std::vector<cudaEvent_t> pool;
   cudaEvent_t get() {
@@ -201,7 +202,7 @@ thread_local Timing g_timing;
 // Launch `fn` (returns cudaError_t) bracketed by events when timing is on.
 template <class F>
 cudaError_t timed(int kid, cudaStream_t st, F&& fn) {
-  if (!g_timing.on) return fn();
+  if (!g_timing.on || !((g_timing.mask >> kid) & 1u)) return fn();
   TimingRec r{kid, g_timing.get(), g_timing.get()};
   cudaEventRecord(r.a, st);
   cudaError_t e = fn();
@@ -414,6 +415,7 @@ fm_status flashmask_bwd(const fm_params* p, const void* q, const void* k, const 
 
 fm_status flashmask_timing_enable(int enable) {
   g_timing.on = enable != 0;
+  g_timing.mask = (enable & FM_TIMING_SELECT) ? static_cast<uint32_t>(enable & 0xFFFF) : 0xFFFFFFFFu;
   return FM_OK;
 }
 

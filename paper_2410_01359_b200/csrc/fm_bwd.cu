@@ -292,6 +292,10 @@ __global__ void __launch_bounds__(bwd::NT, 1)
         if (sm.list[t] * BR >= j * 128 && (t == 0 || sm.list[t - 1] * BR < j * 128)) sm.rot = t;
     }
   }
+  // The class map came from K1b, two launches back (complete, see pdl_wait in fm_ptx.cuh);
+  // D, L2 and the zeroed dQ accumulator come from K3, the stream predecessor.
+  pdl_wait();
+  pdl_launch();
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -765,8 +769,7 @@ static cudaError_t launch_bwd_t(const Dims& d, const CUtensorMap& tq, const CUte
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (e != cudaSuccess) return e;
   dim3 grid(d.Tc, d.Hkv, d.B);
-  kern<<<grid, bwd::NT, smem, st>>>(tq, tk, tv, tdo, tdq, tdk, tdv, a);
-  return cudaGetLastError();
+  return launch_pdl(kern, grid, dim3(bwd::NT), smem, st, tq, tk, tv, tdo, tdq, tdk, tdv, a);
 }
 
 cudaError_t launch_bwd(const Dims& d, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,

@@ -129,6 +129,8 @@ __global__ void __launch_bounds__(fwd::NT, 1)
     }
   }
   if (warp == MMA_WARP) tmem_alloc<512>(&sm.tmem_base);
+  pdl_wait();  // the class map (K1b, the stream predecessor) is complete from here on
+  pdl_launch();
 
   // ---- visit list: union of the non-SKIP column tiles of Q0 and Q1 (K1 class map) ----
   {
@@ -511,8 +513,7 @@ static cudaError_t launch_fwd_t(const Dims& d, const CUtensorMap& tq, const CUte
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (e != cudaSuccess) return e;
   dim3 grid((d.Tr + 1) / 2, d.H, d.B);
-  kern<<<grid, fwd::NT, smem, st>>>(tq, tk, tv, to, a);
-  return cudaGetLastError();
+  return launch_pdl(kern, grid, dim3(fwd::NT), smem, st, tq, tk, tv, to, a);
 }
 
 cudaError_t launch_fwd(const Dims& d, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,

@@ -4,6 +4,7 @@
 #include <climits>
 
 #include "fm_internal.h"
+#include "fm_ptx.cuh"
 
 namespace fm {
 
@@ -40,6 +41,8 @@ __device__ __forceinline__ int clampi(int x, int lo, int hi) { return x < lo ? l
 
 __global__ void __launch_bounds__(128) k1_expand(const int32_t* __restrict__ sri, int N, int C, int causal, int bc,
                                                  int Tc, int32_t* __restrict__ ext8, int4* __restrict__ vec4) {
+  pdl_wait();
+  pdl_launch();
   const int j = blockIdx.x;
   const int bh = blockIdx.y;
   const int32_t* base = sri + static_cast<size_t>(bh) * N * C;
@@ -107,6 +110,8 @@ __global__ void __launch_bounds__(128) k1_classify(const int32_t* __restrict__ e
                                                    int Tr, int Tc, uint8_t* __restrict__ map, int transposed,
                                                    int kernel_map, int no_skip,
                                                    unsigned long long* __restrict__ counts) {
+  pdl_wait();
+  pdl_launch();
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   const int i = blockIdx.y;
   const int bh = blockIdx.z;
@@ -154,8 +159,7 @@ __global__ void __launch_bounds__(128) k1_classify(const int32_t* __restrict__ e
 cudaError_t launch_expand(const int32_t* sri, const Dims& d, int bc, int32_t* ext8, int4* vec4, cudaStream_t st) {
   const int Tc = (d.N + bc - 1) / bc;
   dim3 grid(Tc, d.B * d.Hm);
-  k1_expand<<<grid, 128, 0, st>>>(sri, d.N, d.C, d.causal, bc, Tc, ext8, vec4);
-  return cudaGetLastError();
+  return launch_pdl(k1_expand, grid, dim3(128), 0, st, sri, d.N, d.C, d.causal, bc, Tc, ext8, vec4);
 }
 
 cudaError_t launch_classify(const int32_t* ext8, const Dims& d, int br, int bc, uint8_t* map, int transposed,
@@ -166,9 +170,8 @@ cudaError_t launch_classify(const int32_t* ext8, const Dims& d, int br, int bc, 
     if (e != cudaSuccess) return e;
   }
   dim3 grid((Tc + 127) / 128, Tr, d.B * d.Hm);
-  k1_classify<<<grid, 128, 0, st>>>(ext8, d.N, d.causal, br, bc, Tr, Tc, map, transposed, kernel_map,
-                                    (d.flags & 1) ? 1 : 0, reinterpret_cast<unsigned long long*>(counts));
-  return cudaGetLastError();
+  return launch_pdl(k1_classify, grid, dim3(128), 0, st, ext8, d.N, d.causal, br, bc, Tr, Tc, map, transposed,
+                    kernel_map, (d.flags & 1) ? 1 : 0, reinterpret_cast<unsigned long long*>(counts));
 }
 
 __device__ __forceinline__ uint32_t pack_bf16_rn(float a, float b) {
@@ -196,6 +199,8 @@ __global__ void __launch_bounds__(256) k3_bwd_pre(const void* __restrict__ o, co
                                                   const float* __restrict__ lse, int B, int N, int H, int Npb,
                                                   float* __restrict__ dvec, float* __restrict__ l2,
                                                   float* __restrict__ dqacc) {
+  pdl_wait();
+  pdl_launch();
   constexpr int G = D / 8;  // threads per row
   const long gt = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
   const long row = gt / G;
@@ -240,15 +245,16 @@ cudaError_t launch_bwd_pre(const Dims& d, const void* o, const void* dout, const
   const long threads = static_cast<long>(d.B) * d.H * d.Npb * (d.D / 8);
   const long blocks = (threads + 255) / 256;
   const __nv_bfloat16* dob = static_cast<const __nv_bfloat16*>(dout);
+  cudaError_t e;
 #define FM_PRE(DD, F32) \
-  k3_bwd_pre<DD, F32><<<blocks, 256, 0, st>>>(o, dob, lse, d.B, d.N, d.H, d.Npb, dvec, l2, dqacc)
+  e = launch_pdl(k3_bwd_pre<DD, F32>, dim3(blocks), dim3(256), 0, st, o, dob, lse, d.B, d.N, d.H, d.Npb, dvec, l2, dqacc)
   if (d.D == 128) {
     if (d.out_f32) FM_PRE(128, true); else FM_PRE(128, false);
   } else {
     if (d.out_f32) FM_PRE(64, true); else FM_PRE(64, false);
   }
 #undef FM_PRE
-  return cudaGetLastError();
+  return e;
 }
 
 // ---------------------------------------------------------------------------------------
@@ -258,6 +264,8 @@ cudaError_t launch_bwd_pre(const Dims& d, const void* o, const void* dout, const
 template <int D, bool OUT_F32>
 __global__ void __launch_bounds__(256) k5_dq_convert(const float* __restrict__ dqacc, int B, int N, int H, int Npb,
                                                      float scale, void* __restrict__ dq) {
+  pdl_wait();
+  pdl_launch();
   const long idx8 = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
   const long total8 = static_cast<long>(B) * N * H * D / 8;
   if (idx8 >= total8) return;
@@ -283,14 +291,15 @@ __global__ void __launch_bounds__(256) k5_dq_convert(const float* __restrict__ d
 cudaError_t launch_dq_convert(const Dims& d, const float* dqacc, void* dq, cudaStream_t st) {
   const long total8 = static_cast<long>(d.B) * d.N * d.H * d.D / 8;
   const long blocks = (total8 + 255) / 256;
-#define FM_CV(DD, F32) k5_dq_convert<DD, F32><<<blocks, 256, 0, st>>>(dqacc, d.B, d.N, d.H, d.Npb, d.scale, dq)
+  cudaError_t e;
+#define FM_CV(DD, F32) e = launch_pdl(k5_dq_convert<DD, F32>, dim3(blocks), dim3(256), 0, st, dqacc, d.B, d.N, d.H, d.Npb, d.scale, dq)
   if (d.D == 128) {
     if (d.out_f32) FM_CV(128, true); else FM_CV(128, false);
   } else {
     if (d.out_f32) FM_CV(64, true); else FM_CV(64, false);
   }
 #undef FM_CV
-  return cudaGetLastError();
+  return e;
 }
 
 }  // namespace fm

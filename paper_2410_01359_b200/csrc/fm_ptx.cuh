@@ -21,6 +21,15 @@ FM_DEV T* smem_align1024(uint8_t* raw) {
 
 FM_DEV uint32_t lane_id() { uint32_t r; asm volatile("mov.u32 %0, %%laneid;" : "=r"(r)); return r; }
 
+// ------------------------------------------------------------------ programmatic dependent launch
+// Every kernel of the library is launched with programmatic stream serialization.  Rule: a
+// kernel touches memory written or read by earlier kernels only after pdl_wait(), and it lets
+// its dependent launch (pdl_launch) only after its own pdl_wait() — so when a kernel starts, all
+// grids two or more launches back have completed, which makes reading the caller's inputs
+// (q, k, v, dO, mask) in a pre-wait prologue safe.
+FM_DEV void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+FM_DEV void pdl_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // ------------------------------------------------------------------ mbarrier
 FM_DEV void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");

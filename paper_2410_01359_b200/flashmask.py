@@ -25,6 +25,8 @@ FM_PASS_FWD, FM_PASS_BWD = 0, 1
 EXPORTED = ["flashmask_workspace_size", "flashmask_classify", "flashmask_fwd", "flashmask_bwd",
             "flashmask_status_string", "flashmask_last_error", "flashmask_timing_enable", "flashmask_timing_collect"]
 KERNEL_NAMES = ["expand", "classify", "fwd", "bwd_pre", "bwd", "dq_convert", "dq"]
+(FM_KERNEL_EXPAND, FM_KERNEL_CLASSIFY, FM_KERNEL_FWD, FM_KERNEL_BWD_PRE, FM_KERNEL_BWD, FM_KERNEL_DQ_CONVERT,
+ FM_KERNEL_DQ) = range(7)
 
 
 class FmParams(ctypes.Structure):
@@ -163,8 +165,16 @@ def flashmask_bwd(q, k, v, o, do, lse, sri, causal: bool, scale=None, out_dtype=
     return dq, dk, dv
 
 
-def flashmask_timing_enable(enable: bool = True):
-    _check(_lib.flashmask_timing_enable(int(bool(enable))), "flashmask_timing_enable")
+FM_TIMING_SELECT = 0x10000
+
+
+def flashmask_timing_enable(enable: bool = True, kernels=None):
+    """Per-kernel CUDA-event timing; `kernels` = iterable of FM_KERNEL_* ids (default: all)."""
+    if enable and kernels is not None:
+        code = FM_TIMING_SELECT | sum(1 << k for k in set(kernels))
+    else:
+        code = int(bool(enable))
+    _check(_lib.flashmask_timing_enable(code), "flashmask_timing_enable")
 
 
 def flashmask_timing_collect():
