@@ -56,7 +56,7 @@ namespace fm { __device__ long long g_fm_trace[64 * 16]; __device__ long long g_
 #endif
 
 #ifndef FM_BWD_KA
-#define FM_BWD_KA 0  // K_j as TMEM A operand (excludes the P/dS double buffer; measured no gain)
+#define FM_BWD_KA 1  // K_j as TMEM A operand of S^T (single P/dS TMEM buffer): +2-3 % since the dQ stages moved
 #endif
 
 #ifndef FM_DQ_MODE
