@@ -13,18 +13,19 @@
 //   dS^T = P^T o (dP^T - D_i)
 //   dV  += P^T dO_i,  dK += dS^T Q_i         (A operands bf16 from TMEM)
 //   d=128: dQ_i^T = K_j^T dS^T (M = d);  d=64: dQ_i = dS K_j (M = queries)
-// dQ tiles are added into the fp32 workspace with red.global.add straight from registers
-// (no read-modify-write, no shared-memory staging).
+// dQ tiles are added into the fp32 workspace by bulk / TMA reduce-adds from shared-memory stages
+// (no read-modify-write).
 //
 // Pipelining: the compute WGs copy S^T/dP^T of row tile t into registers and release them at
 // once, so the MMA warp issues S^T/dP^T of tile t+1 while P/dS of tile t are being computed;
-// P and dS live in their own TMEM columns (at d=64 the dQ GEMM of the same tile reuses them).
+// P and dS live in their own TMEM columns, which the dQ GEMM of the same tile then reuses.
 // TMEM columns:
-//   d=128: S [0,64) dP [64,128) P [128,160) dS [160,192) dQ^T [192,256) dV [256,384) dK [384,512)
+//   d=128: S [0,64) dP [64,128) P [128,160) dS [160,192) (dQ^T aliases [128,192)) K_j [192,256)
+//          dV [256,384) dK [384,512)
 //   d=64 : S [0,128) dP [128,256) P [256,320) dS [320,384) (dQ aliases [256,320))
 //          dV [384,448) dK [448,512)
-// Warp roles: 0-7 two compute WGs (query halves), 8-11 dQ WG (TMEM -> red.global.add),
-// 12 TMA producer, 13 TMEM allocator + S/dP MMA issuer, 14 dV/dK/dQ MMA issuer.
+// Warp roles: 0-7 two compute WGs (query halves), 8-11 dQ WG (TMEM -> shared-memory stage ->
+// bulk reduce-add), 12 TMA producer, 13 TMEM allocator + S/dP MMA issuer, 14 dV/dK/dQ issuer.
 #include <cuda_bf16.h>
 #include <cmath>
 
@@ -43,10 +44,6 @@ namespace fm { __device__ long long g_fm_trace[64 * 16]; __device__ long long g_
   } while (0)
 #endif
 
-#ifndef FM_EXP
-#define FM_EXP 0  // experiments only: 1 = compute WGs skip TMEM/math/smem work
-#endif
-
 #ifndef FM_BWD_ISSUER_WAIT
 #define FM_BWD_ISSUER_WAIT mbar_wait_sleep  // MMA issuer warps wait suspended (see fm_ptx.cuh)
 #endif
@@ -57,16 +54,6 @@ namespace fm { __device__ long long g_fm_trace[64 * 16]; __device__ long long g_
 
 #ifndef FM_BWD_KA
 #define FM_BWD_KA 1  // K_j as TMEM A operand of S^T (single P/dS TMEM buffer): +2-3 % since the dQ stages moved
-#endif
-
-#ifndef FM_DQ_MODE
-#define FM_DQ_MODE 0  // experiments only: nonzero = skip the dQ global reduction
-#endif
-
-#ifndef FM_DQ_RED
-// d=128 dQ^T reduction path: 0 = stage through shared memory + bulk reduce-add,
-// 1 = scalar red.global from registers, 2 = lane-quad transposes + red.global.v4
-#define FM_DQ_RED 0
 #endif
 
 namespace fm {
@@ -90,12 +77,11 @@ constexpr int DQ_NSTAGE = FM_DQ_NSTAGE;  // 8 KiB dQ^T staging buffers (d=128)
 #define FM_MAXTRB 4096
 #endif
 constexpr int kMaxTrb = FM_MAXTRB;  // d=128 (Br=64); d=64 (Br=128) uses half: the same max N
-// d=64 dQ reduction (FM_DQ64_WG = 1): the dQ warpgroup stages the 128-row x 32-column fp32 half
-// tiles (16 KiB, 128-byte swizzle) for one TMA tensor reduce-add each, DQ64_NBUF in flight — two
-// operations per row tile (the cost of the reduction follows the number of operations, §6b).
-// FM_DQ64_WG = 0: each dQ warp stages 16-row x 32-column boxes (2 KiB), DQ64_NBUF per warp.
+// d=64 dQ reduction: the dQ warpgroup stages the 128-row x 32-column fp32 half tiles (16 KiB,
+// 128-byte swizzle) for one TMA tensor reduce-add each, DQ64_NBUF in flight — two operations per
+// row tile (the cost of the reduction follows the number of operations).
 constexpr int DQ64_NBUF = 3;
-constexpr int DQ64_STAGES = FM_DQ64_WG ? DQ64_NBUF : 4 * DQ64_NBUF;
+constexpr int DQ64_STAGES = DQ64_NBUF;
 constexpr int DQ64_STAGE_FLOATS = kDq64BoxRows * 32;
 #ifndef FM_DQ_CROWS
 #define FM_DQ_CROWS 32
@@ -105,9 +91,6 @@ constexpr int DQ_CROWS = FM_DQ_CROWS;  // query rows per dQ^T staging chunk (d=1
 #define FM_BWD_NDS 1
 #endif
 constexpr int NDS = FM_BWD_NDS;  // dS shared-memory buffers
-#ifndef FM_BWD_ROT
-#define FM_BWD_ROT 0  // experiment: start each key tile's row loop at its diagonal (wrap around)
-#endif
 
 template <int D>
 struct Cfg {
@@ -159,7 +142,6 @@ struct Smem {
   uint64_t s_full, sdp_free, p_full[2], pds_free[2], dq_full[2], dq_empty[2], ds_empty[2], ka_full, done;
   uint32_t tmem_base;
   int n_entries;
-  int rot;
   int warp_cnt[NT / 32];
 };
 
@@ -284,13 +266,6 @@ __global__ void __launch_bounds__(bwd::NT, 1)
       __syncthreads();
     }
     if (tid == 0) sm.n_entries = base;
-    if (FM_BWD_ROT) {
-      if (tid == 0) sm.rot = 0;
-      __syncthreads();
-      // first list entry at or below the diagonal of this key tile
-      for (int t = tid; t < base; t += NT)
-        if (sm.list[t] * BR >= j * 128 && (t == 0 || sm.list[t - 1] * BR < j * 128)) sm.rot = t;
-    }
   }
   // The class map came from K1b, two launches back (complete, see pdl_wait in fm_ptx.cuh);
   // D, L2 and the zeroed dQ accumulator come from K3, the stream predecessor.
@@ -301,11 +276,7 @@ __global__ void __launch_bounds__(bwd::NT, 1)
   tc_fence_after();
   // work items t = (query head of the group, visited row tile): t / nE1 selects the head
   const int nE1 = sm.n_entries;
-  const int rot = FM_BWD_ROT ? sm.rot : 0;
-  auto lidx = [&](int t) {
-    int x = t % nE1 + rot;
-    return x >= nE1 ? x - nE1 : x;
-  };
+  auto lidx = [&](int t) { return t % nE1; };
   const int nE = nE1 * G;
   const uint32_t tbase = sm.tmem_base;
 
@@ -468,15 +439,6 @@ __global__ void __launch_bounds__(bwd::NT, 1)
       const float* lv = sm.lvec[st];
       const float* dv = sm.dvec[st];
       uint32_t pp[CH][16], dp[CH][16];
-      if (FM_EXP == 1) {
-        tc_fence_before();
-        mbar_arrive(&sm.sdp_free);
-        mbar_wait(&sm.ds_empty[t % NDS], ((t / NDS) & 1) ^ 1);
-        mbar_wait(&sm.dq_empty[t % C::NB], ((t / C::NB) & 1) ^ 1);
-        tc_fence_before();
-        mbar_arrive(&sm.p_full[t % C::NB]);
-        continue;
-      }
 #pragma unroll
       for (int ch = 0; ch < CH; ++ch) {
         const int q0 = (wg * CH + ch) * 32;  // first query of this chunk within the row tile
@@ -643,34 +605,8 @@ __global__ void __launch_bounds__(bwd::NT, 1)
       tmem_wait_ld();
       tc_fence_before();
       mbar_arrive(&sm.dq_empty[bi]);
-      if (FM_DQ_MODE == 1) continue;
       float* base = a.dqacc + (bh * a.Npb + static_cast<size_t>(i) * BR) * D;
-      if constexpr (C::DQT && FM_DQ_RED == 1) {
-        // r[q] = dQ^T[d = t_id][q]: one coalesced 128-B scalar reduction per warp and query
-#pragma unroll
-        for (int q = 0; q < 64; ++q) red_add_f32(base + q * D + t_id, __uint_as_float(r[q]));
-      } else if constexpr (C::DQT && FM_DQ_RED == 2) {
-        // 4 x 4 transposes inside each lane quad (two xor butterflies), then 16-B vector
-        // reductions: lane 4g+c ends with dQ[q = 4m+c][d = wl*32 + 4g .. +3] in x[0..3].
-        const bool b1 = (lane & 2) != 0, b0 = (lane & 1) != 0;
-        float* rowp = base + (lane & 3) * D + wl * 32 + (lane & ~3);
-#pragma unroll
-        for (int m = 0; m < 16; ++m) {
-          float x0 = __uint_as_float(r[4 * m]), x1 = __uint_as_float(r[4 * m + 1]);
-          float x2 = __uint_as_float(r[4 * m + 2]), x3 = __uint_as_float(r[4 * m + 3]);
-          {
-            const float s0 = b1 ? x0 : x2, s1 = b1 ? x1 : x3;
-            const float g0 = __shfl_xor_sync(0xffffffffu, s0, 2), g1 = __shfl_xor_sync(0xffffffffu, s1, 2);
-            if (b1) { x0 = g0; x1 = g1; } else { x2 = g0; x3 = g1; }
-          }
-          {
-            const float s0 = b0 ? x0 : x1, s1 = b0 ? x2 : x3;
-            const float g0 = __shfl_xor_sync(0xffffffffu, s0, 1), g1 = __shfl_xor_sync(0xffffffffu, s1, 1);
-            if (b0) { x0 = g0; x2 = g1; } else { x1 = g0; x3 = g1; }
-          }
-          red_add_v4_f32(rowp + 4 * m * D, x0, x1, x2, x3);
-        }
-      } else if constexpr (C::DQT) {
+      if constexpr (C::DQT) {
         // r[q] = dQ^T[d = t_id][q].  The 64 x 128 fp32 block is contiguous in dQacc: stage 16 rows
         // (8 KiB) in shared memory and add them with one bulk reduce (cp.reduce.async.bulk .add.f32)
         // — far fewer L2 transactions and LSU instructions than 64 scalar red.global per thread,
@@ -682,18 +618,16 @@ __global__ void __launch_bounds__(bwd::NT, 1)
             if (t_id == 0) bulk_wait_read<DQ_NSTAGE - 1>();
             named_bar_sync(1, 128);
           }
-          if (FM_DQ_MODE != 3) {
 #pragma unroll
-            for (int q = 0; q < DQ_CROWS; ++q) stg[q * D + t_id] = __uint_as_float(r[c * DQ_CROWS + q]);
-          }
+          for (int q = 0; q < DQ_CROWS; ++q) stg[q * D + t_id] = __uint_as_float(r[c * DQ_CROWS + q]);
           fence_proxy_async_smem();
           named_bar_sync(1, 128);
-          if (t_id == 0 && FM_DQ_MODE != 2) {
+          if (t_id == 0) {
             bulk_reduce_add_f32(base + c * DQ_CROWS * D, stg, DQ_CROWS * D * 4);
             bulk_commit();
           }
         }
-      } else if constexpr (FM_DQ64_WG != 0) {
+      } else {
         // d=64: r[c] = dQ[query = t_id][c], t_id = 0..127 = the tile's rows.  Each 32-column half
         // of the 128 x 64 tile is written into a 128-byte-swizzled stage (16-B chunk c of row q at
         // c ^ (q & 7): conflict-free) and added by one TMA tensor reduce.
@@ -717,38 +651,10 @@ __global__ void __launch_bounds__(bwd::NT, 1)
             bulk_commit();
           }
         }
-      } else {
-        // d=64: r[c] = dQ[query = t_id][c].  The warp's 32 rows go out as four 16-row x 32-column
-        // boxes, each written into a 128-byte-swizzled stage (16-B chunk c of row l at c ^ (l & 7):
-        // conflict-free, no lane-dependent register index) and added by one TMA tensor reduce.
-        const int row0 = static_cast<int>(bh * a.Npb) + i * BR + wl * 32;
-#pragma unroll
-        for (int bx = 0; bx < 4; ++bx, ++stage_n) {
-          const int rh = bx >> 1, ch = bx & 1;  // 16-row half, 32-column half
-          float* stg = sm.dq_stage[wl * DQ64_NBUF + stage_n % DQ64_NBUF];
-          if (stage_n >= DQ64_NBUF) {
-            if (lane == 0) bulk_wait_read<DQ64_NBUF - 1>();
-            __syncwarp();
-          }
-          if ((lane >> 4) == rh) {
-            const int rl = lane & 15;
-#pragma unroll
-            for (int c = 0; c < 8; ++c)
-              *reinterpret_cast<float4*>(reinterpret_cast<uint8_t*>(stg) + rl * 128 + ((c ^ (rl & 7)) << 4)) =
-                  make_float4(__uint_as_float(r[ch * 32 + 4 * c]), __uint_as_float(r[ch * 32 + 4 * c + 1]),
-                              __uint_as_float(r[ch * 32 + 4 * c + 2]), __uint_as_float(r[ch * 32 + 4 * c + 3]));
-          }
-          fence_proxy_async_smem();
-          __syncwarp();
-          if (lane == 0) {
-            tma_reduce_add_2d(&tmDQ, stg, ch * 32, row0 + rh * 16);
-            bulk_commit();
-          }
-        }
       }
       if (t_id == 0) FM_T(10, t);
     }
-    if ((C::DQT || FM_DQ64_WG) ? t_id == 0 : lane == 0) bulk_wait0();  // stages must outlive the bulk reads
+    if (t_id == 0) bulk_wait0();  // the staging buffers must outlive the bulk reads
   }
 
   tc_fence_before();

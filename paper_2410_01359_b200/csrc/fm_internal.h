@@ -29,11 +29,8 @@ inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, siz
 
 constexpr int kTile = 128;      // column (key) tile Bc, forward row (query) tile Br
 constexpr int kMaxTc = 2048;    // forward visit-list capacity -> N <= 262144
-#ifndef FM_DQ64_WG
-#define FM_DQ64_WG 1  // d=64 backward: dQ staged per dQ warpgroup (1) or per warp (0)
-#endif
-// rows of one d=64 dQ TMA reduce box (x 32 fp32 columns, 128-B swizzle)
-constexpr int kDq64BoxRows = FM_DQ64_WG ? 128 : 16;
+// rows of one d=64 dQ TMA reduce box (x 32 fp32 columns, 128-B swizzle; fm_bwd.cu)
+constexpr int kDq64BoxRows = 128;
 
 // Workspace layout (buffers 4 KiB-aligned in the device address space), produced by flashmask_fwd/bwd.
 struct Workspace {
