@@ -73,7 +73,7 @@ struct Smem {
   uint64_t bar_q;
   uint64_t k_full[KST], k_empty[KST], v_full[VST], v_empty[VST];
   uint64_t m_full[MST], m_empty[MST];
-  uint64_t s_full[2], p_full[2], o_full[2];
+  uint64_t s_full[2], p_full[2], o_full[2], s_read[2], pv_done[2];
   float xmax[2][2][2][128];  // [tile][parity][column half][row]: row-max exchange between halves
   float xsum[2][2][128];     // [tile][column half][row]: final row-sum exchange
   uint32_t tmem_base;
@@ -82,6 +82,14 @@ struct Smem {
 };
 
 constexpr int PRODUCER_WARP = 16, MMA_WARP = 17;
+// d=64 leaves 128 TMEM columns free (S0, S1 128 each, O0, O1 64 each): P gets its own buffers
+// [384, 448) / [448, 512), so S_q(e+1) is issued as soon as the softmax has read S_q(e) — the S
+// MMA then runs under the tail of the softmax instead of after it (d=128: P aliases S).
+template <int D>
+struct Layout {
+  static constexpr bool SEP_P = (D == 64);
+  static constexpr uint32_t P_COL = 384;
+};
 
 __device__ __forceinline__ int ent_cls(uint32_t ent, int q) { return (ent >> (24 + 2 * q)) & 3; }
 
@@ -117,6 +125,8 @@ __global__ void __launch_bounds__(fwd::NT, 1)
       mbar_init(&sm.s_full[q], 1);
       mbar_init(&sm.p_full[q], 256);
       mbar_init(&sm.o_full[q], 1);
+      mbar_init(&sm.s_read[q], 256);
+      mbar_init(&sm.pv_done[q], 1);
     }
     fence_barrier_init();
     // Q does not depend on the visit list: start its load before the list is built
@@ -225,9 +235,13 @@ __global__ void __launch_bounds__(fwd::NT, 1)
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
           const uint64_t bd = sdesc_sw128(v_addr + kk * 2048, 16384, 1024);
-          // P of keys [0,64) sits in S columns [0,32), of keys [64,128) in S columns [64,96)
-          mma_ts_w(tO[q], tS[q] + kk * 8 + (kk >= 4 ? 32u : 0u), bd, ID_PV, (pv_cnt[q] > 0 || kk > 0) ? 1u : 0u);
+          // P of keys [0,64) sits in S columns [0,32), of keys [64,128) in S columns [64,96);
+          // SEP_P: P of keys [16kk, 16kk+16) in columns P_COL + 64q + 8kk
+          const uint32_t a_tm = Layout<D>::SEP_P ? tbase + Layout<D>::P_COL + q * 64 + kk * 8
+                                                 : tS[q] + kk * 8 + (kk >= 4 ? 32u : 0u);
+          mma_ts_w(tO[q], a_tm, bd, ID_PV, (pv_cnt[q] > 0 || kk > 0) ? 1u : 0u);
         }
+        if constexpr (Layout<D>::SEP_P) mma_commit_w(&sm.pv_done[q]);
         pv_cnt[q]++;
         const uint32_t ent = sm.list[pe];
         const int last = (ent_cls(ent, 1) != 0) ? 1 : 0;
@@ -248,8 +262,11 @@ __global__ void __launch_bounds__(fwd::NT, 1)
         const uint32_t k_addr = smem_u32(sm.k[ks]);
 #pragma unroll
         for (int q = 0; q < 2; ++q) {
-          if (pend[q] >= 0) issue_pv(q);
+          if (!Layout<D>::SEP_P && pend[q] >= 0) issue_pv(q);
           if (ent_cls(ent, q) != 0) {
+            // SEP_P: S_q(e) overwrites S_q(pend) once the softmax has read it (s_read)
+            if (Layout<D>::SEP_P && pend[q] >= 0) mbar_wait(&sm.s_read[q], pv_cnt[q] & 1);
+            tc_fence_after();
 #pragma unroll
             for (int kk = 0; kk < D / 16; ++kk) {
               const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
@@ -258,8 +275,9 @@ __global__ void __launch_bounds__(fwd::NT, 1)
             }
             mma_commit_w(&sm.s_full[q]);
             if (lane == 0) FT(6 + q, e);
-            pend[q] = e;
           }
+          if (Layout<D>::SEP_P && pend[q] >= 0) issue_pv(q);
+          if (ent_cls(ent, q) != 0) pend[q] = e;
         }
         mma_commit_w(&sm.k_empty[ks]);
       }
@@ -282,7 +300,8 @@ __global__ void __launch_bounds__(fwd::NT, 1)
     const uint32_t lane_off = static_cast<uint32_t>(wl * 32) << 16;
     const uint32_t tS = tbase + lane_off + (q == 0 ? 0u : 128u);
     const uint32_t tSh = tS + hh * 64;                      // this half's 64 S columns
-    const uint32_t tPh = tS + hh * 64;                      // its packed P (32 columns) — see MMA
+    const uint32_t tPh = Layout<D>::SEP_P ? tbase + lane_off + Layout<D>::P_COL + q * 64 + hh * 32
+                                          : tS + hh * 64;   // its packed P (32 columns) — see MMA
     const uint32_t tO = tbase + lane_off + 256u + (q == 0 ? 0u : static_cast<uint32_t>(D));
     const uint32_t tOh = tO + hh * (D / 2);                 // this half's O columns
     const float sl2 = a.scale_log2;
@@ -354,6 +373,10 @@ __global__ void __launch_bounds__(fwd::NT, 1)
           l *= alpha;
           m_used = m_tile;
         }
+        if (Layout<D>::SEP_P && cnt > 0) {  // PV_q(e-1) (issued after S_q(e)) done with O and P
+          mbar_wait(&sm.pv_done[q], (cnt - 1) & 1);
+          tc_fence_after();
+        }
         if (__any_sync(0xffffffffu, need) && cnt > 0) {
 #pragma unroll 1
           for (int c = 0; c < D / 64; ++c) {
@@ -376,6 +399,10 @@ __global__ void __launch_bounds__(fwd::NT, 1)
         for (int ch = 0; ch < 4; ++ch) {
           tmem_wait_ld();
           if (ch + 1 < 4) tmem_ld16(tSh + (ch + 1) * 16, sr[(ch + 1) & 1]);
+          if (Layout<D>::SEP_P && ch == 3) {  // all of S_q(e) is in registers
+            tc_fence_before();
+            mbar_arrive(&sm.s_read[q]);
+          }
           const float* sv = reinterpret_cast<const float*>(sr[ch & 1]);
           uint32_t pk[8];
 #pragma unroll
