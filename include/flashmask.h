@@ -66,7 +66,7 @@ typedef enum {
   FM_ERR_CUDA = 4                /* a CUDA runtime/driver call or launch failed          */
 } fm_status;
 
-typedef enum { FM_BF16 = 0, FM_FP32 = 1 } fm_dtype;
+typedef enum { FM_BF16 = 0, FM_FP32 = 1, FM_FP16 = 2 } fm_dtype;
 
 /* Tile classes of Eq. 4, as written to class maps. */
 typedef enum { FM_TILE_SKIP = 0, FM_TILE_PARTIAL = 1, FM_TILE_UNMASKED = 2 } fm_tile_class;
@@ -91,9 +91,10 @@ typedef struct {
   int64_t mask_cols;   /* C in {1, 2, 4}; must match `causal` per the table above   */
   int32_t causal;      /* 0 or 1                                                    */
   float   scale;       /* softmax scale; <= 0 means 1/sqrt(head_dim) (Eq. 1)        */
-  int32_t in_dtype;    /* fm_dtype of q, k, v, dout: FM_BF16 (tcgen05 path) or FM_FP32
-                        * (exact-fp32 CUDA-core path for the parity config C1, reading R26) */
-  int32_t out_dtype;   /* fm_dtype of o, dq, dk, dv: FM_BF16 or FM_FP32            */
+  int32_t in_dtype;    /* fm_dtype of q, k, v, dout: FM_BF16 or FM_FP16 (tcgen05 path) or
+                        * FM_FP32 (exact-fp32 CUDA-core path for the parity config C1, reading R26) */
+  int32_t out_dtype;   /* fm_dtype of o, dq, dk, dv: FM_FP32 or the 16-bit type of in_dtype
+                        * (FM_BF16 for FM_BF16 / FM_FP32 inputs, FM_FP16 for FM_FP16 inputs) */
   int32_t flags;       /* FM_FLAG_*                                                 */
   int64_t num_kv_heads;/* key/value heads; 0 means num_heads; must divide num_heads   */
 } fm_params;
@@ -123,7 +124,7 @@ FM_API fm_status flashmask_classify(const fm_params* p, const int32_t* startend_
 
 /* Forward pass (Alg. 1): o = Softmax(scale*q k^T + M) v, lse = logsumexp.
  *   q, k, v  [B, N, H, d] in_dtype;  o [B, N, H, d] out_dtype;  lse fp32 [B, H, N].
- * in_dtype FM_BF16 runs the tcgen05 kernels (bf16 operands, fp32 accumulation);
+ * in_dtype FM_BF16 / FM_FP16 runs the tcgen05 kernels (16-bit operands, fp32 accumulation);
  * FM_FP32 runs fp32 CUDA-core kernels with the same tile skipping (no tensor cores: it
  * serves the fp32 parity configuration, not throughput).
  * Fully masked tiles issue no load and no MMA; partially masked tiles are masked

@@ -57,7 +57,8 @@ bool make_map(CUtensorMap* m, const void* ptr, const fm::Dims& d, int heads, int
                            static_cast<cuuint64_t>(d.N) * heads * d.D * 2};
   cuuint32_t box[4] = {64, 1, static_cast<cuuint32_t>(box_rows), 1};
   cuuint32_t estr[4] = {1, 1, 1, 1};
-  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(ptr), dims, strides, box, estr,
+  CUresult r = enc(m, d.in_f16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4,
+                   const_cast<void*>(ptr), dims, strides, box, estr,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
@@ -103,8 +104,12 @@ fm_status check_params(const fm_params* p, fm::Dims* d, bool need_attention) {
   const bool ok_c = p->causal ? (C == 1 || C == 2) : (C == 2 || C == 4);
   if ((p->causal != 0 && p->causal != 1) || !ok_c)
     return fail(FM_ERR_INVALID_ARGUMENT, "invalid (causal, mask_cols) combination; see the C-table in flashmask.h");
-  if (p->out_dtype != FM_BF16 && p->out_dtype != FM_FP32) return fail(FM_ERR_INVALID_ARGUMENT, "bad out_dtype");
-  if (p->in_dtype != FM_BF16 && p->in_dtype != FM_FP32) return fail(FM_ERR_INVALID_ARGUMENT, "bad in_dtype");
+  if (p->in_dtype != FM_BF16 && p->in_dtype != FM_FP32 && p->in_dtype != FM_FP16)
+    return fail(FM_ERR_INVALID_ARGUMENT, "bad in_dtype");
+  // 16-bit outputs have the 16-bit type of the inputs (fp32 inputs: bf16 outputs)
+  const int out16 = p->in_dtype == FM_FP16 ? FM_FP16 : FM_BF16;
+  if (p->out_dtype != out16 && p->out_dtype != FM_FP32)
+    return fail(FM_ERR_INVALID_ARGUMENT, "out_dtype must be FM_FP32 or the 16-bit type of in_dtype");
   if (need_attention) {
     if (p->head_dim != 64 && p->head_dim != 128) return fail(FM_ERR_INVALID_ARGUMENT, "head_dim must be 64 or 128");
   }
@@ -124,6 +129,7 @@ fm_status check_params(const fm_params* p, fm::Dims* d, bool need_attention) {
   d->Npb = d->Tr * fm::kTile;  // covers both the 64/128-row backward tiles and K6's 128-row tiles
   d->scale = (p->scale > 0.f) ? p->scale : 1.0f / std::sqrt(static_cast<float>(p->head_dim > 0 ? p->head_dim : 1));
   d->out_f32 = p->out_dtype == FM_FP32;
+  d->in_f16 = p->in_dtype == FM_FP16;
   d->flags = p->flags;
   if (need_attention && d->Tc > fm::kMaxTc) return fail(FM_ERR_UNSUPPORTED, "seqlen > 262144");
   return FM_OK;

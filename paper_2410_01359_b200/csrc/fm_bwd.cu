@@ -165,7 +165,7 @@ __device__ __forceinline__ uint32_t row_mask_bits(int r0, int key, int4 mv) {
   return m;
 }
 
-template <bool PART, bool CAUSAL>
+template <bool PART, bool CAUSAL, bool F16>
 __device__ __forceinline__ void pds_chunk(const uint32_t* sr, const uint32_t* dr, const float* lq, const float* dq,
                                           float sl2, int r0, int key, int4 mv, uint32_t* pp, uint32_t* dp) {
   const uint32_t mb = PART ? row_mask_bits<CAUSAL>(r0, key, mv) : 0u;
@@ -182,16 +182,16 @@ __device__ __forceinline__ void pds_chunk(const uint32_t* sr, const uint32_t* dr
       if constexpr (PART) p[u] = ((mb >> (c + u)) & 1u) ? 0.f : p[u];
       ds[u] = p[u] * (__uint_as_float(dr[c + u]) - d4[u]);
     }
-    pp[c / 2] = pack_bf16(p[0], p[1]);
-    pp[c / 2 + 1] = pack_bf16(p[2], p[3]);
-    dp[c / 2] = pack_bf16(ds[0], ds[1]);
-    dp[c / 2 + 1] = pack_bf16(ds[2], ds[3]);
+    pp[c / 2] = pack16<F16>(p[0], p[1]);
+    pp[c / 2 + 1] = pack16<F16>(p[2], p[3]);
+    dp[c / 2] = pack16<F16>(ds[0], ds[1]);
+    dp[c / 2 + 1] = pack16<F16>(ds[2], ds[3]);
   }
 }
 
 }  // namespace bwd
 
-template <int D, bool CAUSAL, bool OUT_F32>
+template <int D, bool CAUSAL, bool OUT_F32, bool F16>
 __global__ void __launch_bounds__(bwd::NT, 1)
     fm_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                   const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO,
@@ -309,9 +309,9 @@ __global__ void __launch_bounds__(bwd::NT, 1)
     // compute WGs have released tile t-1; warp 14 issues dV/dK/dQ(t) once P/dS(t) are ready.
     // Each warp commits only to barriers that track its own MMAs.
     if (nE > 0) {  // the whole warp runs converged; one elected lane issues (fm_ptx.cuh)
-      constexpr uint32_t ID_S = idesc_bf16(128, BR, 0, 0);   // S^T, dP^T: A, B K-major
-      constexpr uint32_t ID_G = idesc_bf16(128, D, 0, 1);    // dV, dK: A in TMEM, B MN-major
-      constexpr uint32_t ID_Q = idesc_bf16(128, 64, 1, 1);   // dQ^T (d=128) / dQ (d=64), both MN-major
+      constexpr uint32_t ID_S = idesc16<F16>(128, BR, 0, 0);   // S^T, dP^T: A, B K-major
+      constexpr uint32_t ID_G = idesc16<F16>(128, D, 0, 1);    // dV, dK: A in TMEM, B MN-major
+      constexpr uint32_t ID_Q = idesc16<F16>(128, 64, 1, 1);   // dQ^T (d=128) / dQ (d=64), both MN-major
       const uint32_t k_addr = smem_u32(sm.k), v_addr = smem_u32(sm.v);
       FM_BWD_ISSUER_WAIT(&sm.kv_full, 0);
       if (warp == 13) {
@@ -451,9 +451,9 @@ __global__ void __launch_bounds__(bwd::NT, 1)
           mbar_arrive(&sm.sdp_free);
         }
         if (partial)
-          pds_chunk<true, CAUSAL>(sr, dr, lv + q0, dv + q0, sl2, i * BR + q0, key, mv, pp[ch], dp[ch]);
+          pds_chunk<true, CAUSAL, F16>(sr, dr, lv + q0, dv + q0, sl2, i * BR + q0, key, mv, pp[ch], dp[ch]);
         else
-          pds_chunk<false, CAUSAL>(sr, dr, lv + q0, dv + q0, sl2, i * BR + q0, key, mv, pp[ch], dp[ch]);
+          pds_chunk<false, CAUSAL, F16>(sr, dr, lv + q0, dv + q0, sl2, i * BR + q0, key, mv, pp[ch], dp[ch]);
       }
       if (tid == 0) FM_T(5, t);
 #ifdef FM_TRACE
@@ -548,7 +548,7 @@ __global__ void __launch_bounds__(bwd::NT, 1)
           for (int u = 0; u < 8; ++u) f[u] = nE > 0 ? __uint_as_float(r[8 * t + u]) * mul : 0.f;
           const int chunk = (c % 2) * 4 + t;
           *reinterpret_cast<uint4*>(blk + ((chunk ^ (key_t & 7)) << 4)) =
-              make_uint4(pack_bf16(f[0], f[1]), pack_bf16(f[2], f[3]), pack_bf16(f[4], f[5]), pack_bf16(f[6], f[7]));
+              make_uint4(pack16<F16>(f[0], f[1]), pack16<F16>(f[2], f[3]), pack16<F16>(f[4], f[5]), pack16<F16>(f[6], f[7]));
         }
       }
       fence_proxy_async_smem();
@@ -577,11 +577,11 @@ __global__ void __launch_bounds__(bwd::NT, 1)
 #pragma unroll
           for (int t = 0; t < 8; ++t) dst[t] = make_float4(f[4 * t], f[4 * t + 1], f[4 * t + 2], f[4 * t + 3]);
         } else {
-          uint4* dst = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(outp) + orow + c * 32);
+          uint4* dst = reinterpret_cast<uint4*>(static_cast<uint16_t*>(outp) + orow + c * 32);
 #pragma unroll
           for (int t = 0; t < 4; ++t)
-            dst[t] = make_uint4(pack_bf16(f[8 * t], f[8 * t + 1]), pack_bf16(f[8 * t + 2], f[8 * t + 3]),
-                                pack_bf16(f[8 * t + 4], f[8 * t + 5]), pack_bf16(f[8 * t + 6], f[8 * t + 7]));
+            dst[t] = make_uint4(pack16<F16>(f[8 * t], f[8 * t + 1]), pack16<F16>(f[8 * t + 2], f[8 * t + 3]),
+                                pack16<F16>(f[8 * t + 4], f[8 * t + 5]), pack16<F16>(f[8 * t + 6], f[8 * t + 7]));
         }
       }
     }
@@ -665,11 +665,11 @@ __global__ void __launch_bounds__(bwd::NT, 1)
   }
 }
 
-template <int D, bool CAUSAL, bool OUT_F32>
+template <int D, bool CAUSAL, bool OUT_F32, bool F16>
 static cudaError_t launch_bwd_t(const Dims& d, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
                                 const CUtensorMap& tdo, const CUtensorMap& tdq, const CUtensorMap& tdk,
                                 const CUtensorMap& tdv, const BwdArgs& a, cudaStream_t st) {
-  auto kern = fm_bwd_kernel<D, CAUSAL, OUT_F32>;
+  auto kern = fm_bwd_kernel<D, CAUSAL, OUT_F32, F16>;
   const size_t smem = sizeof(bwd::Smem<D>) + 1024;
   static_assert(sizeof(bwd::Smem<D>) + 1024 <= 232448, "shared memory budget");
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
@@ -681,7 +681,9 @@ static cudaError_t launch_bwd_t(const Dims& d, const CUtensorMap& tq, const CUte
 cudaError_t launch_bwd(const Dims& d, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
                        const CUtensorMap& tdo, const CUtensorMap& tdq, const CUtensorMap& tdk, const CUtensorMap& tdv,
                        const BwdArgs& a, cudaStream_t st) {
-#define FM_B(DD, CC, FF) return launch_bwd_t<DD, CC, FF>(d, tq, tk, tv, tdo, tdq, tdk, tdv, a, st)
+#define FM_B(DD, CC, FF) \
+  return d.in_f16 ? launch_bwd_t<DD, CC, FF, true>(d, tq, tk, tv, tdo, tdq, tdk, tdv, a, st) \
+                  : launch_bwd_t<DD, CC, FF, false>(d, tq, tk, tv, tdo, tdq, tdk, tdv, a, st)
   if (d.D == 128) {
     if (d.causal) { if (d.out_f32) FM_B(128, true, true); else FM_B(128, true, false); }
     else { if (d.out_f32) FM_B(128, false, true); else FM_B(128, false, false); }

@@ -43,7 +43,7 @@ struct Smem {
 
 }  // namespace dqk
 
-template <int D, bool CAUSAL, bool OUT_F32>
+template <int D, bool CAUSAL, bool OUT_F32, bool F16>
 __global__ void __launch_bounds__(dqk::NT, 1)
     fm_dq_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                  const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO, const DqArgs a) {
@@ -138,8 +138,8 @@ __global__ void __launch_bounds__(dqk::NT, 1)
   } else if (warp == 9) {
     // ================================ MMA issuer ================================
     if (nE > 0) {  // converged warp, one elected lane issues
-      constexpr uint32_t ID_S = idesc_bf16(128, 128, 0, 0);  // S, dP: A, B K-major
-      constexpr uint32_t ID_Q = idesc_bf16(128, D, 0, 1);    // dQ: A = dS in TMEM, B = K MN-major
+      constexpr uint32_t ID_S = idesc16<F16>(128, 128, 0, 0);  // S, dP: A, B K-major
+      constexpr uint32_t ID_Q = idesc16<F16>(128, D, 0, 1);    // dQ: A = dS in TMEM, B = K MN-major
       const uint32_t q_addr = smem_u32(sm.q), do_addr = smem_u32(sm.dO);
       mbar_wait(&sm.bar_q, 0);
       for (int e = 0; e < nE; ++e) {
@@ -214,7 +214,7 @@ __global__ void __launch_bounds__(dqk::NT, 1)
             }
             ds2[u] = p * (__uint_as_float(dr[c][t + u]) - dval);
           }
-          pk[c * 16 + t / 2] = pack_bf16(ds2[0], ds2[1]);
+          pk[c * 16 + t / 2] = pack16<F16>(ds2[0], ds2[1]);
         }
       }
       mbar_wait(&sm.ds_free, (e & 1) ^ 1);  // dQ(e-1) has read the dS columns
@@ -246,11 +246,11 @@ __global__ void __launch_bounds__(dqk::NT, 1)
 #pragma unroll
           for (int t = 0; t < 8; ++t) dst[t] = make_float4(f[4 * t], f[4 * t + 1], f[4 * t + 2], f[4 * t + 3]);
         } else {
-          uint4* dst = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(a.dq) + orow + c * 32);
+          uint4* dst = reinterpret_cast<uint4*>(static_cast<uint16_t*>(a.dq) + orow + c * 32);
 #pragma unroll
           for (int t = 0; t < 4; ++t)
-            dst[t] = make_uint4(pack_bf16(f[8 * t], f[8 * t + 1]), pack_bf16(f[8 * t + 2], f[8 * t + 3]),
-                                pack_bf16(f[8 * t + 4], f[8 * t + 5]), pack_bf16(f[8 * t + 6], f[8 * t + 7]));
+            dst[t] = make_uint4(pack16<F16>(f[8 * t], f[8 * t + 1]), pack16<F16>(f[8 * t + 2], f[8 * t + 3]),
+                                pack16<F16>(f[8 * t + 4], f[8 * t + 5]), pack16<F16>(f[8 * t + 6], f[8 * t + 7]));
         }
       }
     }
@@ -264,10 +264,10 @@ __global__ void __launch_bounds__(dqk::NT, 1)
   }
 }
 
-template <int D, bool CAUSAL, bool OUT_F32>
+template <int D, bool CAUSAL, bool OUT_F32, bool F16>
 static cudaError_t launch_dq_t(const Dims& d, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
                                const CUtensorMap& tdo, const DqArgs& a, cudaStream_t st) {
-  auto kern = fm_dq_kernel<D, CAUSAL, OUT_F32>;
+  auto kern = fm_dq_kernel<D, CAUSAL, OUT_F32, F16>;
   const size_t smem = sizeof(dqk::Smem<D>) + 1024;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (e != cudaSuccess) return e;
@@ -278,7 +278,9 @@ static cudaError_t launch_dq_t(const Dims& d, const CUtensorMap& tq, const CUten
 
 cudaError_t launch_dq(const Dims& d, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
                       const CUtensorMap& tdo, const DqArgs& a, cudaStream_t st) {
-#define FM_Q(DD, CC, FF) return launch_dq_t<DD, CC, FF>(d, tq, tk, tv, tdo, a, st)
+#define FM_Q(DD, CC, FF) \
+  return d.in_f16 ? launch_dq_t<DD, CC, FF, true>(d, tq, tk, tv, tdo, a, st) \
+                  : launch_dq_t<DD, CC, FF, false>(d, tq, tk, tv, tdo, a, st)
   if (d.D == 128) {
     if (d.causal) { if (d.out_f32) FM_Q(128, true, true); else FM_Q(128, true, false); }
     else { if (d.out_f32) FM_Q(128, false, true); else FM_Q(128, false, false); }

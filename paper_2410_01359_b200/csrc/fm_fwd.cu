@@ -95,7 +95,7 @@ __device__ __forceinline__ int ent_cls(uint32_t ent, int q) { return (ent >> (24
 
 }  // namespace fwd
 
-template <int D, bool CAUSAL, bool OUT_F32>
+template <int D, bool CAUSAL, bool OUT_F32, bool F16>
 __global__ void __launch_bounds__(fwd::NT, 1)
     fm_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                   const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmO, const FwdArgs a) {
@@ -216,8 +216,8 @@ __global__ void __launch_bounds__(fwd::NT, 1)
     // two tiles' softmax phases staggered (ping-pong).  Two independent issuers were measured
     // to fall into lock-step and lose ~30 %.
     {  // the whole warp runs the issue loop converged; one elected lane issues
-      constexpr uint32_t ID_S = idesc_bf16(128, 128, 0, 0);  // S = Q K^T, both K-major
-      constexpr uint32_t ID_PV = idesc_bf16(128, D, 0, 1);   // O += P V, V is MN-major
+      constexpr uint32_t ID_S = idesc16<F16>(128, 128, 0, 0);  // S = Q K^T, both K-major
+      constexpr uint32_t ID_PV = idesc16<F16>(128, D, 0, 1);   // O += P V, V is MN-major
       const uint32_t tS[2] = {tbase + 0, tbase + 128};
       const uint32_t tO[2] = {tbase + 256, tbase + 256 + D};
       const uint32_t q_addr[2] = {smem_u32(sm.q[0]), smem_u32(sm.q[1])};
@@ -419,7 +419,7 @@ __global__ void __launch_bounds__(fwd::NT, 1)
               p1 = ex2(x1);
             }
             acc[k & 3] = f2add(acc[k & 3], f2pack(p0, p1));
-            pk[kk] = pack_bf16(p0, p1);
+            pk[kk] = pack16<F16>(p0, p1);
           }
           tmem_st8(tPh + ch * 8, pk);
         }
@@ -475,7 +475,7 @@ __global__ void __launch_bounds__(fwd::NT, 1)
           for (int u = 0; u < 8; ++u) f[u] = live ? __uint_as_float(ov[8 * t + u]) * inv : 0.f;
           const int chunk = (col % 64) / 8 + t;
           *reinterpret_cast<uint4*>(blk + ((chunk ^ (row_t & 7)) << 4)) =
-              make_uint4(pack_bf16(f[0], f[1]), pack_bf16(f[2], f[3]), pack_bf16(f[4], f[5]), pack_bf16(f[6], f[7]));
+              make_uint4(pack16<F16>(f[0], f[1]), pack16<F16>(f[2], f[3]), pack16<F16>(f[4], f[5]), pack16<F16>(f[6], f[7]));
         }
       }
       fence_proxy_async_smem();
@@ -504,11 +504,11 @@ __global__ void __launch_bounds__(fwd::NT, 1)
 #pragma unroll
           for (int t = 0; t < 8; ++t) dst[t] = make_float4(f[4 * t], f[4 * t + 1], f[4 * t + 2], f[4 * t + 3]);
         } else {
-          uint4* dst = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(a.o) + orow + c * 32);
+          uint4* dst = reinterpret_cast<uint4*>(static_cast<uint16_t*>(a.o) + orow + c * 32);
 #pragma unroll
           for (int t = 0; t < 4; ++t)
-            dst[t] = make_uint4(pack_bf16(f[8 * t], f[8 * t + 1]), pack_bf16(f[8 * t + 2], f[8 * t + 3]),
-                                pack_bf16(f[8 * t + 4], f[8 * t + 5]), pack_bf16(f[8 * t + 6], f[8 * t + 7]));
+            dst[t] = make_uint4(pack16<F16>(f[8 * t], f[8 * t + 1]), pack16<F16>(f[8 * t + 2], f[8 * t + 3]),
+                                pack16<F16>(f[8 * t + 4], f[8 * t + 5]), pack16<F16>(f[8 * t + 6], f[8 * t + 7]));
         }
       }
     }
@@ -532,10 +532,10 @@ __global__ void __launch_bounds__(fwd::NT, 1)
 #endif
 }
 
-template <int D, bool CAUSAL, bool OUT_F32>
+template <int D, bool CAUSAL, bool OUT_F32, bool F16>
 static cudaError_t launch_fwd_t(const Dims& d, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
                                 const CUtensorMap& to, const FwdArgs& a, cudaStream_t st) {
-  auto kern = fm_fwd_kernel<D, CAUSAL, OUT_F32>;
+  auto kern = fm_fwd_kernel<D, CAUSAL, OUT_F32, F16>;
   const size_t smem = sizeof(fwd::Smem<D>) + 1024;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (e != cudaSuccess) return e;
@@ -545,7 +545,9 @@ static cudaError_t launch_fwd_t(const Dims& d, const CUtensorMap& tq, const CUte
 
 cudaError_t launch_fwd(const Dims& d, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
                        const CUtensorMap& to, const FwdArgs& a, cudaStream_t st) {
-#define FM_F(DD, CC, FF) return launch_fwd_t<DD, CC, FF>(d, tq, tk, tv, to, a, st)
+#define FM_F(DD, CC, FF) \
+  return d.in_f16 ? launch_fwd_t<DD, CC, FF, true>(d, tq, tk, tv, to, a, st) \
+                  : launch_fwd_t<DD, CC, FF, false>(d, tq, tk, tv, to, a, st)
   if (d.D == 128) {
     if (d.causal) { if (d.out_f32) FM_F(128, true, true); else FM_F(128, true, false); }
     else { if (d.out_f32) FM_F(128, false, true); else FM_F(128, false, false); }

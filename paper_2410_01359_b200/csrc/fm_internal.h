@@ -51,6 +51,7 @@ struct Dims {
   int Brb, Trb, Npb;  // backward row tile, its count, padded rows (a multiple of 128)
   float scale;
   int out_f32;
+  int in_f16;       // 16-bit operands (and 16-bit outputs) are fp16 instead of bf16
   int flags;
 };
 

@@ -174,28 +174,14 @@ cudaError_t launch_classify(const int32_t* ext8, const Dims& d, int br, int bc, 
                     kernel_map, (d.flags & 1) ? 1 : 0, reinterpret_cast<unsigned long long*>(counts));
 }
 
-__device__ __forceinline__ uint32_t pack_bf16_rn(float a, float b) {
-  __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
-  return *reinterpret_cast<uint32_t*>(&v);
-}
-
 // ---------------------------------------------------------------------------------------
 // K3: backward preprocess (Alg. 2 line 4, D per row — DESIGN.md R5).  A group of D/8
 // threads per (b, h, r), r < Npb, each owning 8 consecutive columns (16-byte loads):
 // D = sum_c dO[r,c] * O[r,c]; l2 = lse * log2(e), or +inf when the row is empty (lse = -inf)
 // or padded (r >= N) so that exp2(S - l2) = 0 exactly; zero the row of dQacc.
 // ---------------------------------------------------------------------------------------
-__device__ __forceinline__ void bf16x8_to_f32(const uint4& u, float* f) {
-  const uint32_t w[4] = {u.x, u.y, u.z, u.w};
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    f[2 * k] = __uint_as_float(w[k] << 16);
-    f[2 * k + 1] = __uint_as_float(w[k] & 0xFFFF0000u);
-  }
-}
-
-template <int D, bool OUT_F32>
-__global__ void __launch_bounds__(256) k3_bwd_pre(const void* __restrict__ o, const __nv_bfloat16* __restrict__ dout,
+template <int D, bool OUT_F32, bool F16>
+__global__ void __launch_bounds__(256) k3_bwd_pre(const void* __restrict__ o, const uint16_t* __restrict__ dout,
                                                   const float* __restrict__ lse, int B, int N, int H, int Npb,
                                                   float* __restrict__ dvec, float* __restrict__ l2,
                                                   float* __restrict__ dqacc) {
@@ -215,13 +201,13 @@ __global__ void __launch_bounds__(256) k3_bwd_pre(const void* __restrict__ o, co
   if (active && r < N) {
     const size_t off = ((static_cast<size_t>(b) * N + r) * H + h) * D + part * 8;
     float ov[8], dv[8];
-    bf16x8_to_f32(*reinterpret_cast<const uint4*>(dout + off), dv);
+    unpack16x8<F16>(*reinterpret_cast<const uint4*>(dout + off), dv);
     if constexpr (OUT_F32) {
       const float4 a = *reinterpret_cast<const float4*>(static_cast<const float*>(o) + off);
       const float4 c = *reinterpret_cast<const float4*>(static_cast<const float*>(o) + off + 4);
       ov[0] = a.x; ov[1] = a.y; ov[2] = a.z; ov[3] = a.w; ov[4] = c.x; ov[5] = c.y; ov[6] = c.z; ov[7] = c.w;
     } else {
-      bf16x8_to_f32(*reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(o) + off), ov);
+      unpack16x8<F16>(*reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(o) + off), ov);
     }
 #pragma unroll
     for (int t = 0; t < 8; ++t) acc = fmaf(ov[t], dv[t], acc);
@@ -244,10 +230,13 @@ cudaError_t launch_bwd_pre(const Dims& d, const void* o, const void* dout, const
                            float* dqacc, cudaStream_t st) {
   const long threads = static_cast<long>(d.B) * d.H * d.Npb * (d.D / 8);
   const long blocks = (threads + 255) / 256;
-  const __nv_bfloat16* dob = static_cast<const __nv_bfloat16*>(dout);
+  const uint16_t* dob = static_cast<const uint16_t*>(dout);
   cudaError_t e;
-#define FM_PRE(DD, F32) \
-  e = launch_pdl(k3_bwd_pre<DD, F32>, dim3(blocks), dim3(256), 0, st, o, dob, lse, d.B, d.N, d.H, d.Npb, dvec, l2, dqacc)
+#define FM_PRE(DD, F32)                                                                                        \
+  e = d.in_f16 ? launch_pdl(k3_bwd_pre<DD, F32, true>, dim3(blocks), dim3(256), 0, st, o, dob, lse, d.B, d.N, d.H, \
+                            d.Npb, dvec, l2, dqacc)                                                              \
+               : launch_pdl(k3_bwd_pre<DD, F32, false>, dim3(blocks), dim3(256), 0, st, o, dob, lse, d.B, d.N,   \
+                            d.H, d.Npb, dvec, l2, dqacc)
   if (d.D == 128) {
     if (d.out_f32) FM_PRE(128, true); else FM_PRE(128, false);
   } else {
@@ -261,7 +250,7 @@ cudaError_t launch_bwd_pre(const Dims& d, const void* o, const void* dout, const
 // K5: dQ = scale * dQacc (the scale of Eq. 1 carried into dQ, R4) -> out dtype,
 // [B,H,Npb,D] -> [B,N,H,D].  One thread per 8 elements (two 16-byte loads).
 // ---------------------------------------------------------------------------------------
-template <int D, bool OUT_F32>
+template <int D, bool OUT_F32, bool F16>
 __global__ void __launch_bounds__(256) k5_dq_convert(const float* __restrict__ dqacc, int B, int N, int H, int Npb,
                                                      float scale, void* __restrict__ dq) {
   pdl_wait();
@@ -283,8 +272,8 @@ __global__ void __launch_bounds__(256) k5_dq_convert(const float* __restrict__ d
     dst[1] = make_float4(v1.x * scale, v1.y * scale, v1.z * scale, v1.w * scale);
   } else {
     reinterpret_cast<uint4*>(dq)[idx8] =
-        make_uint4(pack_bf16_rn(v0.x * scale, v0.y * scale), pack_bf16_rn(v0.z * scale, v0.w * scale),
-                   pack_bf16_rn(v1.x * scale, v1.y * scale), pack_bf16_rn(v1.z * scale, v1.w * scale));
+        make_uint4(pack16<F16>(v0.x * scale, v0.y * scale), pack16<F16>(v0.z * scale, v0.w * scale),
+                   pack16<F16>(v1.x * scale, v1.y * scale), pack16<F16>(v1.z * scale, v1.w * scale));
   }
 }
 
@@ -292,7 +281,11 @@ cudaError_t launch_dq_convert(const Dims& d, const float* dqacc, void* dq, cudaS
   const long total8 = static_cast<long>(d.B) * d.N * d.H * d.D / 8;
   const long blocks = (total8 + 255) / 256;
   cudaError_t e;
-#define FM_CV(DD, F32) e = launch_pdl(k5_dq_convert<DD, F32>, dim3(blocks), dim3(256), 0, st, dqacc, d.B, d.N, d.H, d.Npb, d.scale, dq)
+#define FM_CV(DD, F32)                                                                                      \
+  e = d.in_f16 ? launch_pdl(k5_dq_convert<DD, F32, true>, dim3(blocks), dim3(256), 0, st, dqacc, d.B, d.N, d.H, \
+                            d.Npb, d.scale, dq)                                                               \
+               : launch_pdl(k5_dq_convert<DD, F32, false>, dim3(blocks), dim3(256), 0, st, dqacc, d.B, d.N,   \
+                            d.H, d.Npb, d.scale, dq)
   if (d.D == 128) {
     if (d.out_f32) FM_CV(128, true); else FM_CV(128, false);
   } else {

@@ -5,6 +5,7 @@
 #include <cstdint>
 #include <cuda.h>
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 
 #define FM_DEV __device__ __forceinline__
 
@@ -278,6 +279,11 @@ __host__ __device__ constexpr uint32_t idesc_bf16(int M, int N, int a_mn, int b_
          (static_cast<uint32_t>(b_mn) << 16) | (static_cast<uint32_t>(N >> 3) << 17) |
          (static_cast<uint32_t>(M >> 4) << 24);
 }
+// Same for fp16 operands (A/B format code 0) when F16.
+template <bool F16>
+__host__ __device__ constexpr uint32_t idesc16(int M, int N, int a_mn, int b_mn) {
+  return F16 ? (idesc_bf16(M, N, a_mn, b_mn) & ~((7u << 7) | (7u << 10))) : idesc_bf16(M, N, a_mn, b_mn);
+}
 
 // ------------------------------------------------------------------ math
 FM_DEV float ex2(float x) {
@@ -339,6 +345,33 @@ FM_DEV void exp2_poly2(uint64_t x2, float& r0, float& r1) {
 FM_DEV uint32_t pack_bf16(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&v);
+}
+// Two floats -> packed 16-bit pair of the kernel's operand type (F16: fp16, else bf16), RNE.
+template <bool F16>
+FM_DEV uint32_t pack16(float lo, float hi) {
+  if constexpr (F16) {
+    __half2 v = __floats2half2_rn(lo, hi);
+    return *reinterpret_cast<uint32_t*>(&v);
+  } else {
+    return pack_bf16(lo, hi);
+  }
+}
+// Eight packed 16-bit values (one uint4) -> floats.
+template <bool F16>
+FM_DEV void unpack16x8(const uint4& u, float* f) {
+  const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    if constexpr (F16) {
+      const __half2 h = *reinterpret_cast<const __half2*>(&w[k]);
+      const float2 g = __half22float2(h);
+      f[2 * k] = g.x;
+      f[2 * k + 1] = g.y;
+    } else {
+      f[2 * k] = __uint_as_float(w[k] << 16);
+      f[2 * k + 1] = __uint_as_float(w[k] & 0xFFFF0000u);
+    }
+  }
 }
 
 }  // namespace fm

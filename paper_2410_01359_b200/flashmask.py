@@ -16,7 +16,7 @@ _PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("FLASHMASK_LIB", os.path.join(_PKG, "libflashmask.so"))
 
 FM_OK, FM_ERR_INVALID_ARGUMENT, FM_ERR_UNSUPPORTED, FM_ERR_WORKSPACE_TOO_SMALL, FM_ERR_CUDA = range(5)
-FM_BF16, FM_FP32 = 0, 1
+FM_BF16, FM_FP32, FM_FP16 = 0, 1, 2
 FM_TILE_SKIP, FM_TILE_PARTIAL, FM_TILE_UNMASKED = 0, 1, 2
 FM_FLAG_NO_SKIP = 1
 FM_FLAG_DETERMINISTIC = 2
@@ -86,12 +86,17 @@ def _stream(stream):
     return ctypes.c_void_p(stream.cuda_stream)
 
 
+_DTYPES = {torch.bfloat16: FM_BF16, torch.float32: FM_FP32, torch.float16: FM_FP16}
+
+
 def _in_dtype(t: torch.Tensor) -> int:
     if t.dtype == torch.bfloat16:
         return FM_BF16
+    if t.dtype == torch.float16:
+        return FM_FP16
     if t.dtype == torch.float32:
         return FM_FP32
-    raise TypeError(f"flashmask inputs must be bfloat16 or float32, got {t.dtype}")
+    raise TypeError(f"flashmask inputs must be bfloat16, float16 or float32, got {t.dtype}")
 
 
 def make_params(B, N, H, d, sri: torch.Tensor, causal: bool, scale=None, out_dtype=torch.bfloat16,
@@ -99,7 +104,7 @@ def make_params(B, N, H, d, sri: torch.Tensor, causal: bool, scale=None, out_dty
     assert sri.dim() == 4 and sri.shape[0] == B and sri.shape[2] == N, sri.shape
     return FmParams(batch=B, seqlen=N, num_heads=H, head_dim=d, mask_heads=sri.shape[1], mask_cols=sri.shape[3],
                     causal=int(bool(causal)), scale=float(scale) if scale else 0.0, in_dtype=in_dtype,
-                    out_dtype=FM_FP32 if out_dtype == torch.float32 else FM_BF16, flags=int(flags),
+                    out_dtype=_DTYPES[out_dtype], flags=int(flags),
                     num_kv_heads=int(num_kv_heads))
 
 
@@ -134,12 +139,20 @@ def _workspace(params, pass_, workspace, dev):
     return workspace, need
 
 
-def flashmask_fwd(q, k, v, sri, causal: bool, scale=None, out_dtype=torch.bfloat16, flags: int = 0,
+def _out_dtype(q, out_dtype):
+    """Default output type: the 16-bit type of the inputs (bf16 for fp32 inputs)."""
+    if out_dtype is not None:
+        return out_dtype
+    return torch.float16 if q.dtype == torch.float16 else torch.bfloat16
+
+
+def flashmask_fwd(q, k, v, sri, causal: bool, scale=None, out_dtype=None, flags: int = 0,
                   out=None, lse=None, workspace=None, stream=None):
     """o, lse = FlashMask forward.  q: bf16 (tcgen05 path) or fp32 (fp32 path) cuda [B, N, H, d];
     k/v: [B, N, Hkv, d] of the same dtype (Hkv divides H, grouped-query attention);
     sri: int32 [B, Hm, N, C] with Hm in {1, Hkv}."""
     B, N, H, d = q.shape
+    out_dtype = _out_dtype(q, out_dtype)
     p = make_params(B, N, H, d, sri, causal, scale, out_dtype, flags, num_kv_heads=k.shape[2],
                     in_dtype=_in_dtype(q))
     o = out if out is not None else torch.empty(B, N, H, d, dtype=out_dtype, device=q.device)
@@ -150,12 +163,13 @@ def flashmask_fwd(q, k, v, sri, causal: bool, scale=None, out_dtype=torch.bfloat
     return o, lse
 
 
-def flashmask_bwd(q, k, v, o, do, lse, sri, causal: bool, scale=None, out_dtype=torch.bfloat16, flags: int = 0,
+def flashmask_bwd(q, k, v, o, do, lse, sri, causal: bool, scale=None, out_dtype=None, flags: int = 0,
                   dq=None, dk=None, dv=None, workspace=None, stream=None):
     """dq, dk, dv = FlashMask backward (o in out_dtype, lse from flashmask_fwd); dk, dv have the
     key/value head count of k, v."""
     B, N, H, d = q.shape
     Hkv = k.shape[2]
+    out_dtype = _out_dtype(q, out_dtype)
     p = make_params(B, N, H, d, sri, causal, scale, out_dtype, flags, num_kv_heads=Hkv, in_dtype=_in_dtype(q))
     mk = lambda t, h: t if t is not None else torch.empty(B, N, h, d, dtype=out_dtype, device=q.device)
     dq, dk, dv = mk(dq, H), mk(dk, Hkv), mk(dv, Hkv)

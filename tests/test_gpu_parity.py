@@ -395,3 +395,51 @@ def test_back_to_back_shared_workspace(fmlib):
                 assert ((a.float() - b.float()).abs() <= 2.0 ** -7 * a.float().abs() + 1e-3).all(), name
             else:
                 assert torch.equal(a, b), name
+
+
+# ------------------------------------------------------------------------- fp16 inputs
+FP16_CASES = [("causal_document", 1000, 128, 1, 2), ("document", 257, 64, 1, 2), ("random_eviction", 384, 128, 1, 1),
+              ("global_sliding_window", 700, 64, 1, 1)]
+
+
+@pytest.mark.parametrize("fam,N,d,B,H", FP16_CASES)
+def test_fp16_inputs(fmlib, fam, N, d, B, H):
+    """fp16 q/k/v/dO run the same tcgen05 kernels with fp16 operands (P, dS packed as fp16):
+    fp32 outputs within the north_star bars of the fp64 oracle on the same fp16 values; fp16
+    outputs bit-equal to RNE(fp16) of the fp32 outputs (forward) / of the fp32-output backward
+    on the same fp16 O (dK, dV), dQ within fp16 rounding."""
+    from workloads import tensors as wt
+    rng = np.random.default_rng(N + d)
+    masks = [wm.sample_family(fam, N, rng, (2, 5)) for _ in range(B)]
+    sri = torch.from_numpy(wm.stack(masks, 1))
+    t = {n: wt.make_tensor(n, B, N, H, d, base=13, dtype=torch.float16) for n in ("q", "k", "v", "do")}
+    sri_c, tc = to_cuda(sri, t)
+    causal = masks[0].causal
+    o32, lse = fmlib.flashmask_fwd(tc["q"], tc["k"], tc["v"], sri_c, causal, out_dtype=torch.float32)
+    g32 = fmlib.flashmask_bwd(tc["q"], tc["k"], tc["v"], o32, tc["do"], lse, sri_c, causal, out_dtype=torch.float32)
+    o16, lse16 = fmlib.flashmask_fwd(tc["q"], tc["k"], tc["v"], sri_c, causal)
+    g16 = fmlib.flashmask_bwd(tc["q"], tc["k"], tc["v"], o16, tc["do"], lse16, sri_c, causal)
+    h32 = fmlib.flashmask_bwd(tc["q"], tc["k"], tc["v"], o16.float(), tc["do"], lse16, sri_c, causal,
+                              out_dtype=torch.float32)
+    torch.cuda.synchronize()
+    assert o16.dtype == torch.float16 and g16[0].dtype == torch.float16
+    assert torch.equal(o16, o32.to(torch.float16)) and torch.equal(lse16, lse)
+    assert torch.equal(g16[1], h32[1].to(torch.float16)) and torch.equal(g16[2], h32[2].to(torch.float16))
+    assert ((g16[0].float() - h32[0]).abs() <= 2.0 ** -10 * h32[0].abs() + 1e-4).all()
+    sri_np = sri.numpy()
+    for b in range(B):
+        for h in range(H):
+            O, L, (gq, gk, gv) = oracle_head(t, masks, sri_np, b, h, 1, causal)
+            assert_close(f"O[{b},{h}]", o32[b, :, h].cpu().numpy(), O)
+            assert_lse(lse[b, h].cpu().numpy(), L)
+            assert_close(f"dQ[{b},{h}]", g32[0][b, :, h].cpu().numpy(), gq)
+            assert_close(f"dK[{b},{h}]", g32[1][b, :, h].cpu().numpy(), gk)
+            assert_close(f"dV[{b},{h}]", g32[2][b, :, h].cpu().numpy(), gv)
+
+
+def test_fp16_dtype_errors(fmlib):
+    q = torch.zeros(1, 128, 1, 128, dtype=torch.float16, device="cuda")
+    sri = torch.full((1, 1, 128, 1), 128, dtype=torch.int32, device="cuda")
+    with pytest.raises(fmlib.FlashMaskError) as e:
+        fmlib.flashmask_fwd(q, q, q, sri, True, out_dtype=torch.bfloat16)   # fp16 in, bf16 out
+    assert e.value.status == fmlib.FM_ERR_INVALID_ARGUMENT
