@@ -139,7 +139,7 @@ struct Smem {
   uint32_t part_bits[C::MAXTRB / 32];
   uint64_t kv_full;
   uint64_t q_full[QST], q_empty[QST];
-  uint64_t s_full, sdp_free, p_full[2], pds_free[2], dq_full[2], dq_empty[2], ds_empty[2], ka_full, done;
+  uint64_t s_full, sdp_free, p_full[2], pds_free[2], dq_full[2], dq_empty[2], ds_empty[2], done;
   uint32_t tmem_base;
   int n_entries;
   int warp_cnt[NT / 32];
@@ -216,7 +216,6 @@ __global__ void __launch_bounds__(bwd::NT, 1)
     for (int s = 0; s < QST; ++s) { mbar_init(&sm.q_full[s], 1); mbar_init(&sm.q_empty[s], 1); }
     mbar_init(&sm.s_full, 1);
     mbar_init(&sm.sdp_free, 256);
-    mbar_init(&sm.ka_full, 128);
     for (int bb = 0; bb < 2; ++bb) {
       mbar_init(&sm.p_full[bb], 256);
       mbar_init(&sm.pds_free[bb], 1);
@@ -315,7 +314,16 @@ __global__ void __launch_bounds__(bwd::NT, 1)
       const uint32_t k_addr = smem_u32(sm.k), v_addr = smem_u32(sm.v);
       FM_BWD_ISSUER_WAIT(&sm.kv_full, 0);
       if (warp == 13) {
-        if constexpr (C::KA_TMEM) FM_BWD_ISSUER_WAIT(&sm.ka_full, 0);  // K_j copied into TMEM
+        if constexpr (C::KA_TMEM) {
+          // K_j (SW128 K-major smem tile) -> TMEM columns [KA_COL, KA_COL + 64) by the tensor core:
+          // k-step kk (16 d-values) of every key row lands in 8 columns, the A-operand layout of
+          // the TS MMA below; ordered before it (same issuing thread).
+          tc_fence_after();
+#pragma unroll
+          for (int kk = 0; kk < D / 16; ++kk)
+            tmem_cp_128x256b_w(tbase + C::KA_COL + kk * 8,
+                               sdesc_sw128(k_addr + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024));
+        }
         for (int t = 0; t < nE; ++t) {
           const int st = t % QST;
           if (t > 0) FM_BWD_ISSUER_WAIT(&sm.sdp_free, (t - 1) & 1);  // compute WGs hold S^T/dP^T(t-1) in registers
@@ -401,28 +409,6 @@ __global__ void __launch_bounds__(bwd::NT, 1)
     const int4 mv = a.vec4[(bhm * a.Tc) * 128 + key];  // this key's (LTS, len, UTS, len), normalised
     const float sl2 = a.scale_log2;
     constexpr int CH = C::CH_PER_WG;
-    if constexpr (C::KA_TMEM) {
-      // copy row key_t of K_j (SW128 smem, two 64-column boxes) into TMEM as the A operand of S^T
-      if (wg == 0 && nE > 0) {
-        mbar_wait(&sm.kv_full, 0);
-#pragma unroll
-        for (int bx = 0; bx < 2; ++bx) {
-          uint32_t kr[32];
-#pragma unroll
-          for (int c = 0; c < 8; ++c) {
-            const uint4 v4 = *reinterpret_cast<const uint4*>(sm.k + bx * 16384 + key_t * 128 + ((c ^ (key_t & 7)) << 4));
-            kr[4 * c] = v4.x;
-            kr[4 * c + 1] = v4.y;
-            kr[4 * c + 2] = v4.z;
-            kr[4 * c + 3] = v4.w;
-          }
-          tmem_st32(tbase + lane_off + C::KA_COL + bx * 32, kr);
-        }
-        tmem_wait_st();
-        tc_fence_before();
-        mbar_arrive(&sm.ka_full);
-      }
-    }
     for (int t = 0; t < nE; ++t) {
       const int t1 = lidx(t);
       const int i = sm.list[t1];

@@ -211,6 +211,17 @@ FM_DEV void mma_ts_w(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc, uint32_t 
       "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+// Shared memory -> TMEM copy by the tensor core (128 lanes x 256 bits = 8 columns), issued by a
+// converged warp like the MMAs; executes in issue order with the thread's tcgen05.mma, so a TS
+// MMA issued after it reads the copied operand.
+FM_DEV void tmem_cp_128x256b_w(uint32_t taddr, uint64_t sdesc) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.cp.cta_group::1.128x256b [%0], %1;\n\t}" ::"r"(taddr),
+      "l"(sdesc)
+      : "memory");
+}
 FM_DEV void mma_commit_w(uint64_t* bar) {
   asm volatile(
       "{\n\t.reg .pred e;\n\t"
