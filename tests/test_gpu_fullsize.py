@@ -125,3 +125,40 @@ def test_c4_sampled_rows_and_q_zero(fm):
             assert_close(f"C4 Q=0 dV h{h}", dv[0, :, h].cpu().numpy(), fo.dv_q_zero(_head(x, "do", 0, h), vec))
         del x, xz, o, lse, dq, dk, dv
         torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("cfg,fams", [("C5:131072:64", ("causal_document", "share_question")),
+                                      ("C5:32768:128", ("random_eviction", "qk_sparse"))])
+def test_c5_sampled_rows_and_q_zero(fm, cfg, fams):
+    """C5 kernel-sweep shapes the bench does not default to: d=64 at N=128K and the PARTIAL-heavy
+    families at N=32K — sampled rows (O, lse, dQ) of one head and the Q=0 closed forms (O, lse,
+    dV) of two heads, batch entry 0."""
+    calls, _, _ = bench.build_workload(cfg, 0, 1, bench.rho_oracle)
+    dev = torch.device("cuda", 0)
+    rng = np.random.default_rng(2)
+    for c in calls:
+        if c["family"] not in fams:
+            continue
+        c = dict(c, B=1, masks=c["masks"][:1], batch_ids=c["batch_ids"][:1], heads=range(4))
+        x = bench.make_inputs(c, dev)
+        o, lse, dq, dk, dv = _run(fm, c, x, torch.float32)
+        N = c["N"]
+        m = c["masks"][0]
+        vec = fo.expand(m.sri, m.causal, N)
+        rows = np.sort(rng.choice(N, 48, replace=False))
+        q, k, v, do = (_head(x, n, 0, 1) for n in ("q", "k", "v", "do"))
+        O, L = fo.forward(q, k, v, vec, rows=rows, row_block=16)
+        gq, _, _ = fo.backward_rows(q, k, v, do, vec, rows)
+        assert_close(f"{cfg} {m.family} O rows", o[0, rows, 1].cpu().numpy(), O)
+        assert_lse(lse[0, 1, rows].cpu().numpy(), L)
+        assert_close(f"{cfg} {m.family} dQ rows", dq[0, rows, 1].cpu().numpy(), gq)
+        xz = dict(x)
+        xz["q"] = torch.zeros_like(x["q"])
+        o, lse, dq, dk, dv = _run(fm, c, xz, torch.float32)
+        for h in (0, 3):
+            O, L = fo.forward_q_zero(_head(x, "v", 0, h), vec)
+            assert_close(f"{cfg} Q=0 O h{h}", o[0, :, h].cpu().numpy(), O)
+            assert_lse(lse[0, h].cpu().numpy(), L)
+            assert_close(f"{cfg} Q=0 dV h{h}", dv[0, :, h].cpu().numpy(), fo.dv_q_zero(_head(x, "do", 0, h), vec))
+        del x, xz, o, lse, dq, dk, dv
+        torch.cuda.empty_cache()
