@@ -4,7 +4,7 @@ os.environ["FLASHMASK_LIB"] = os.path.join(os.path.dirname(os.path.abspath(__fil
 import numpy as np, torch
 import bench
 from paper_2410_01359_b200 import flashmask as fm
-calls, conf, _ = bench.build_workload("C3", 0, 1, bench.rho_gpu(fm))
+calls, conf, _ = bench.build_workload(sys.argv[1] if len(sys.argv) > 1 else "C3", 0, 1, bench.rho_gpu(fm))
 c = calls[0]
 x = bench.make_inputs(c, torch.device("cuda", 0))
 o, lse = fm.flashmask_fwd(x["q"], x["k"], x["v"], x["sri"], c["causal"])
