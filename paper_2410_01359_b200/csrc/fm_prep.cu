@@ -43,12 +43,16 @@ __global__ void __launch_bounds__(128) k1_expand(const int32_t* __restrict__ sri
                                                  int Tc, int32_t* __restrict__ ext8, int4* __restrict__ vec4) {
   pdl_wait();
   pdl_launch();
-  const int j = blockIdx.x;
+  // one warp per column tile (4 per CTA): lanes stride over the tile's columns, the extrema
+  // are reduced with warp shuffles only
+  const int lane = threadIdx.x & 31;
+  const int j = blockIdx.x * 4 + (threadIdx.x >> 5);
   const int bh = blockIdx.y;
+  if (j >= Tc) return;
   const int32_t* base = sri + static_cast<size_t>(bh) * N * C;
   int mn[4] = {INT_MAX, INT_MAX, INT_MAX, INT_MAX};
   int mx[4] = {INT_MIN, INT_MIN, INT_MIN, INT_MIN};
-  for (int c = threadIdx.x; c < bc; c += blockDim.x) {
+  for (int c = lane; c < bc; c += 32) {
     const long y = static_cast<long>(j) * bc + c;
     int4 nv;
     if (y < N) {
@@ -68,8 +72,6 @@ __global__ void __launch_bounds__(128) k1_expand(const int32_t* __restrict__ sri
     }
     if (vec4) vec4[static_cast<size_t>(bh) * Tc * bc + y] = nv;
   }
-  // block reduce (128 threads = 4 warps)
-  __shared__ int red[4][8];
 #pragma unroll
   for (int t = 0; t < 4; ++t) {
 #pragma unroll
@@ -78,21 +80,13 @@ __global__ void __launch_bounds__(128) k1_expand(const int32_t* __restrict__ sri
       mx[t] = max(mx[t], __shfl_xor_sync(0xffffffffu, mx[t], o));
     }
   }
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (lane == 0) {
+  if (lane < 8) {
+    const int t = lane >> 1;
+    int r = (lane & 1) ? mx[0] : mn[0];
 #pragma unroll
-    for (int t = 0; t < 4; ++t) {
-      red[w][2 * t] = mn[t];
-      red[w][2 * t + 1] = mx[t];
-    }
-  }
-  __syncthreads();
-  if (threadIdx.x < 8) {
-    const int t = threadIdx.x;
-    int r = red[0][t];
-    const int nw = blockDim.x >> 5;
-    for (int k = 1; k < nw; ++k) r = (t & 1) ? max(r, red[k][t]) : min(r, red[k][t]);
-    ext8[(static_cast<size_t>(bh) * Tc + j) * 8 + t] = r;
+    for (int k = 1; k < 4; ++k)
+      if (t == k) r = (lane & 1) ? mx[k] : mn[k];
+    ext8[(static_cast<size_t>(bh) * Tc + j) * 8 + lane] = r;
   }
 }
 
@@ -187,7 +181,7 @@ __global__ void __launch_bounds__(128) k1_classify(const int32_t* __restrict__ e
 
 cudaError_t launch_expand(const int32_t* sri, const Dims& d, int bc, int32_t* ext8, int4* vec4, cudaStream_t st) {
   const int Tc = (d.N + bc - 1) / bc;
-  dim3 grid(Tc, d.B * d.Hm);
+  dim3 grid((Tc + 3) / 4, d.B * d.Hm);
   return launch_pdl(k1_expand, grid, dim3(128), 0, st, sri, d.N, d.C, d.causal, bc, Tc, ext8, vec4);
 }
 
