@@ -23,10 +23,14 @@
  *    No C++ exception crosses the ABI.  There is no fallback path.
  *  - The library is stateless and re-entrant (a call_once device-attribute and
  *    driver-entry-point cache is its only global state).
+ *  - Kernels are launched with programmatic dependent launch: each may begin while
+ *    its stream predecessor drains, but touches no memory an earlier kernel on the
+ *    stream writes or reads before that kernel has completed (griddepcontrol.wait),
+ *    so stream order semantics are unchanged for the caller.
  *  - q, o, dout, dq: [batch, seqlen, num_heads, head_dim]; k, v, dk, dv: [batch, seqlen,
  *    num_kv_heads, head_dim] (grouped-query attention: query head h reads key/value head
- *    h / (num_heads / num_kv_heads)); all contiguous and 16-byte aligned.  lse: [batch, num_heads, seqlen] fp32, natural log of the
- *    scaled logits (Alg. 1 line 28); -inf for a row masked in every column
+ *    h / (num_heads / num_kv_heads)); all contiguous and 16-byte aligned.
+ *    lse: [batch, num_heads, seqlen] fp32, natural log of the scaled logits (Alg. 1 line 28); -inf for a row masked in every column
  *    (then its O row is 0 and it contributes nothing to the gradients; R7).
  *  - startend_row_indices: int32 [batch, mask_heads, seqlen, C], 16-byte aligned.
  *    Column y = key token y.  Columns by (causal, C), missing vectors defaulted:
