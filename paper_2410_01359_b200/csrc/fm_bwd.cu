@@ -90,6 +90,12 @@ constexpr int DQ_CROWS = FM_DQ_CROWS;  // query rows per dQ^T staging chunk (d=1
 #ifndef FM_BWD_NDS
 #define FM_BWD_NDS 1
 #endif
+#ifndef FM_BWD_NDS64
+#define FM_BWD_NDS64 1
+#endif
+#ifndef FM_QST64
+#define FM_QST64 3
+#endif
 constexpr int NDS = FM_BWD_NDS;  // dS shared-memory buffers
 
 template <int D>
@@ -120,6 +126,9 @@ struct Cfg {
   static constexpr int DV_COL = (D == 128) ? 256 : 384;
   static constexpr int DK_COL = DV_COL + D;
   static constexpr int MAXTRB = (D == 128) ? kMaxTrb : kMaxTrb / 2;
+  // per-head-dim ring depths: Q/dO stages and dS shared-memory buffers
+  static constexpr int QST = (D == 64) ? FM_QST64 : FM_QST;
+  static constexpr int NDS = (D == 64) ? FM_BWD_NDS64 : FM_BWD_NDS;
 };
 
 template <int D>
@@ -127,18 +136,18 @@ struct Smem {
   using C = Cfg<D>;
   uint8_t k[C::KV_TILE];
   uint8_t v[C::KV_TILE];
-  uint8_t q[QST][C::Q_TILE];
-  uint8_t dO[QST][C::Q_TILE];
-  uint8_t ds[NDS][C::DS_BYTES];  // NDS = 1: dS(t+1) waits for dQ(t) to finish reading (frees 16 KiB for dQ stages)
+  uint8_t q[C::QST][C::Q_TILE];
+  uint8_t dO[C::QST][C::Q_TILE];
+  uint8_t ds[C::NDS][C::DS_BYTES];  // NDS = 1: dS(t+1) waits for dQ(t) to finish reading (frees room for dQ stages)
   // d=128: dQ^T staged 16 query rows (8 KiB, contiguous in dQacc) at a time for one bulk
   // reduce-add each, double-buffered
   float dq_stage[C::DQT ? DQ_NSTAGE : DQ64_STAGES][C::DQT ? DQ_CROWS * D : DQ64_STAGE_FLOATS];
-  float lvec[QST][C::BR];
-  float dvec[QST][C::BR];
+  float lvec[C::QST][C::BR];
+  float dvec[C::QST][C::BR];
   uint16_t list[C::MAXTRB];
   uint32_t part_bits[C::MAXTRB / 32];
   uint64_t kv_full;
-  uint64_t q_full[QST], q_empty[QST];
+  uint64_t q_full[C::QST], q_empty[C::QST];
   uint64_t s_full, sdp_free, p_full[2], pds_free[2], dq_full[2], dq_empty[2], ds_empty[2], done;
   uint32_t tmem_base;
   int n_entries;
@@ -213,7 +222,7 @@ __global__ void __launch_bounds__(bwd::NT, 1)
 
   if (warp == 12 && lane == 0) {
     mbar_init(&sm.kv_full, 1);
-    for (int s = 0; s < QST; ++s) { mbar_init(&sm.q_full[s], 1); mbar_init(&sm.q_empty[s], 1); }
+    for (int s = 0; s < C::QST; ++s) { mbar_init(&sm.q_full[s], 1); mbar_init(&sm.q_empty[s], 1); }
     mbar_init(&sm.s_full, 1);
     mbar_init(&sm.sdp_free, 256);
     for (int bb = 0; bb < 2; ++bb) {
@@ -289,8 +298,8 @@ __global__ void __launch_bounds__(bwd::NT, 1)
         const int i = sm.list[lidx(t)];
         const int hq = hk * G + t / nE1;
         const size_t bh = static_cast<size_t>(b) * a.H + hq;
-        const int st = t % QST;
-        mbar_wait(&sm.q_empty[st], ((t / QST) & 1) ^ 1);
+        const int st = t % C::QST;
+        mbar_wait(&sm.q_empty[st], ((t / C::QST) & 1) ^ 1);
         mbar_expect_tx(&sm.q_full[st], 2 * C::Q_TILE + 2 * BR * 4);
 #pragma unroll
         for (int c = 0; c < D / 64; ++c) {
@@ -325,10 +334,10 @@ __global__ void __launch_bounds__(bwd::NT, 1)
                                sdesc_sw128(k_addr + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024));
         }
         for (int t = 0; t < nE; ++t) {
-          const int st = t % QST;
+          const int st = t % C::QST;
           if (t > 0) FM_BWD_ISSUER_WAIT(&sm.sdp_free, (t - 1) & 1);  // compute WGs hold S^T/dP^T(t-1) in registers
           if (lane == 0) FM_T(1, t);
-          FM_BWD_ISSUER_WAIT(&sm.q_full[st], (t / QST) & 1);
+          FM_BWD_ISSUER_WAIT(&sm.q_full[st], (t / C::QST) & 1);
           if (lane == 0) FM_T(14, t);
           tc_fence_after();
           const uint32_t q_addr = smem_u32(sm.q[st]), do_addr = smem_u32(sm.dO[st]);
@@ -350,7 +359,7 @@ __global__ void __launch_bounds__(bwd::NT, 1)
         }
       } else {
         for (int t = 0; t < nE; ++t) {
-          const int st = t % QST;
+          const int st = t % C::QST;
           if (lane == 0) FM_T(0, t);
           const int bi = t % C::NB;
           const uint32_t ph = (t / C::NB) & 1, boff = bi * C::BUF_STRIDE;
@@ -364,7 +373,7 @@ __global__ void __launch_bounds__(bwd::NT, 1)
             mma_ts_w(tbase + C::DV_COL, tbase + C::P_COL + boff + kk * 8,
                      sdesc_sw128(do_addr + kk * 2048, BR * 128, 1024), ID_G, acc);
             if constexpr (C::DK_SS)  // A = dS^T straight from the dQ operand buffer in smem
-              mma_ss_w(tbase + C::DK_COL, sdesc_sw128(smem_u32(sm.ds[t % NDS]) + kk * 32, 16, 1024),
+              mma_ss_w(tbase + C::DK_COL, sdesc_sw128(smem_u32(sm.ds[t % C::NDS]) + kk * 32, 16, 1024),
                        sdesc_sw128(q_addr + kk * 2048, BR * 128, 1024), ID_G, acc);
             else
               mma_ts_w(tbase + C::DK_COL, tbase + C::DS_COL + boff + kk * 8,
@@ -378,12 +387,12 @@ __global__ void __launch_bounds__(bwd::NT, 1)
           // thread (in order), and the compute WGs stored P/dS(t) there only after dQ(t-NB) was
           // read out (dq_empty[t % NB]).
           if (!a.with_dq) {
-            if constexpr (C::DK_SS) mma_commit_w(&sm.ds_empty[t % NDS]);  // dK(t) read dS^T(t)
+            if constexpr (C::DK_SS) mma_commit_w(&sm.ds_empty[t % C::NDS]);  // dK(t) read dS^T(t)
             continue;
           }
           if constexpr (!C::DQ_ALIAS) FM_BWD_ISSUER_WAIT(&sm.dq_empty[0], (t & 1) ^ 1);
           tc_fence_after();
-          const uint32_t ds_addr = smem_u32(sm.ds[t % NDS]);
+          const uint32_t ds_addr = smem_u32(sm.ds[t % C::NDS]);
 #pragma unroll
           for (int kk = 0; kk < 8; ++kk) {
             if constexpr (C::DQT)
@@ -394,7 +403,7 @@ __global__ void __launch_bounds__(bwd::NT, 1)
                      sdesc_sw128(k_addr + kk * 2048, 16384, 1024), ID_Q, kk > 0 ? 1u : 0u);
           }
           mma_commit_w(&sm.dq_full[bi]);
-          mma_commit_w(&sm.ds_empty[t % NDS]);
+          mma_commit_w(&sm.ds_empty[t % C::NDS]);
           if (lane == 0) FM_T(13, t);
         }
         mma_commit_w(&sm.done);  // all S^T/dP^T completed earlier (they precede every p_full)
@@ -413,8 +422,8 @@ __global__ void __launch_bounds__(bwd::NT, 1)
       const int t1 = lidx(t);
       const int i = sm.list[t1];
       const bool partial = (sm.part_bits[t1 >> 5] >> (t1 & 31)) & 1u;
-      const int st = t % QST;
-      mbar_wait(&sm.q_full[st], (t / QST) & 1);
+      const int st = t % C::QST;
+      mbar_wait(&sm.q_full[st], (t / C::QST) & 1);
       mbar_wait(&sm.s_full, t & 1);
       if (tid == 0) FM_T(4, t);
 #ifdef FM_TRACE
@@ -449,7 +458,7 @@ __global__ void __launch_bounds__(bwd::NT, 1)
       // dS^T row of this key into the SW128 MN-major smem operand of the dQ GEMM
       // (first: it only needs dQ(t-1) to have finished reading the buffer)
       const bool ds_smem = a.with_dq || C::DK_SS;  // dS^T is a shared-memory operand (dQ, dK)
-      if (ds_smem) mbar_wait(&sm.ds_empty[t % NDS], ((t / NDS) & 1) ^ 1);  // dK/dQ(t-2) have read this buffer
+      if (ds_smem) mbar_wait(&sm.ds_empty[t % C::NDS], ((t / C::NDS) & 1) ^ 1);  // dK/dQ(t-2) have read this buffer
       if (tid == 0) FM_T(7, t);
 #ifdef FM_TRACE
       if (lane == 0 && t >= 30 && t < 40 && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0)
@@ -462,7 +471,7 @@ __global__ void __launch_bounds__(bwd::NT, 1)
         for (int u = 0; u < 4; ++u) {
           const int g = (q0 >> 3) + u;  // 8-query group
           const int sub = g >> 3, gg = g & 7;
-          uint8_t* dst = sm.ds[t % NDS] + sub * 16384 + key_t * 128 + ((gg ^ (key_t & 7)) << 4);
+          uint8_t* dst = sm.ds[t % C::NDS] + sub * 16384 + key_t * 128 + ((gg ^ (key_t & 7)) << 4);
           *reinterpret_cast<uint4*>(dst) =
               make_uint4(dp[ch][4 * u], dp[ch][4 * u + 1], dp[ch][4 * u + 2], dp[ch][4 * u + 3]);
         }
