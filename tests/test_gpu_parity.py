@@ -443,3 +443,26 @@ def test_fp16_dtype_errors(fmlib):
     with pytest.raises(fmlib.FlashMaskError) as e:
         fmlib.flashmask_fwd(q, q, q, sri, True, out_dtype=torch.bfloat16)   # fp16 in, bf16 out
     assert e.value.status == fmlib.FM_ERR_INVALID_ARGUMENT
+
+
+@pytest.mark.parametrize("d", [64, 128])
+def test_fp16_deterministic_dq(fmlib, d):
+    """fp16 inputs with FM_FLAG_DETERMINISTIC (row-parallel dQ kernel K6 with fp16 operands):
+    bitwise reproducible dQ, dK/dV bitwise those of the default fp16 run, dQ vs the oracle."""
+    from workloads import tensors as wt
+    N, H = 700, 2
+    masks = [wm.sample_family("causal_document", N, np.random.default_rng(d), (2, 5))]
+    sri = torch.from_numpy(wm.stack(masks, 1))
+    t = {n: wt.make_tensor(n, 1, N, H, d, base=17, dtype=torch.float16) for n in ("q", "k", "v", "do")}
+    sri_c, tc = to_cuda(sri, t)
+    outs = []
+    for flags in (fmlib.FM_FLAG_DETERMINISTIC, fmlib.FM_FLAG_DETERMINISTIC, 0):
+        o, lse = fmlib.flashmask_fwd(tc["q"], tc["k"], tc["v"], sri_c, True, out_dtype=torch.float32, flags=flags)
+        outs.append(fmlib.flashmask_bwd(tc["q"], tc["k"], tc["v"], o, tc["do"], lse, sri_c, True,
+                                        out_dtype=torch.float32, flags=flags))
+    torch.cuda.synchronize()
+    assert torch.equal(outs[0][0], outs[1][0])
+    assert torch.equal(outs[0][1], outs[2][1]) and torch.equal(outs[0][2], outs[2][2])
+    for h in range(H):
+        _, _, (gq, _, _) = oracle_head(t, masks, sri.numpy(), 0, h, 1, True)
+        assert_close(f"fp16 det dQ[{h}]", outs[0][0][0, :, h].cpu().numpy(), gq)
