@@ -381,7 +381,8 @@ def main():
         chunks = []
         for ci, (c, x) in enumerate(zip(calls, inputs)):
             H = len(c["heads"])
-            HG = 8 if H % 8 == 0 else H
+            HG = int(os.environ.get("FM_E2E_HEADS", "8"))
+            HG = HG if H % HG == 0 else H
             for bi in range(c["B"]):
                 for h0 in range(0, H, HG):
                     hx = {k: (v[bi:bi + 1, :, h0:h0 + HG] if k != "sri" else v[bi:bi + 1]).contiguous().cpu()
@@ -436,8 +437,8 @@ def main():
         e2e_ms = max_over_ranks(e0.elapsed_time(e1) / n_e2e)
         e2e = {"value": round(world * (F_fwd + F_bwd) / (e2e_ms * 1e-3) / 1e12, 2), "unit": "TFLOP/s",
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": round(e2e_ms, 3),
-               "pipeline": "one call per (batch entry, 8-head group), H2D / kernels / D2H on 3 streams; host "
-                           "buffers chunk-contiguous"}
+               "pipeline": f"one call per (batch entry, {HG}-head group), H2D / kernels / D2H on 3 streams; "
+                           "host buffers chunk-contiguous"}
 
     # ---------------- report ----------------
     value = world * (F_fwd + F_bwd) / (ms_step * 1e-3) / 1e12
