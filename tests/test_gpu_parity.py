@@ -466,3 +466,40 @@ def test_fp16_deterministic_dq(fmlib, d):
     for h in range(H):
         _, _, (gq, _, _) = oracle_head(t, masks, sri.numpy(), 0, h, 1, True)
         assert_close(f"fp16 det dQ[{h}]", outs[0][0][0, :, h].cpu().numpy(), gq)
+
+
+@pytest.mark.parametrize("d", [64, 128])
+def test_gqa_per_kv_head_masks(fmlib, d):
+    """one mask per key/value head (mask_heads = num_kv_heads): query head h uses the
+    mask of its key/value head h // G; different families per kv head."""
+    from workloads import tensors as wt
+    N, H, Hkv = 520, 4, 2
+    rng = np.random.default_rng(d)
+    masks = [wm.sample_family("causal_document", N, rng, (2, 5)), wm.sample_family("sliding_window", N, rng, (2, 5))]
+    assert masks[0].causal == masks[1].causal and masks[0].C == masks[1].C
+    sri = torch.from_numpy(np.stack([m.sri for m in masks])[None].copy())  # [1, Hkv, N, C]
+    q = wt.make_tensor("q", 1, N, H, d, base=23)
+    do = wt.make_tensor("do", 1, N, H, d, base=23)
+    k = wt.make_tensor("k", 1, N, Hkv, d, base=23)
+    v = wt.make_tensor("v", 1, N, Hkv, d, base=23)
+    qc, kc, vc, doc, sc = q.cuda(), k.cuda(), v.cuda(), do.cuda(), sri.cuda()
+    o, lse = fmlib.flashmask_fwd(qc, kc, vc, sc, True, out_dtype=torch.float32)
+    dq, dk, dv = fmlib.flashmask_bwd(qc, kc, vc, o, doc, lse, sc, True, out_dtype=torch.float32)
+    torch.cuda.synchronize()
+    G = H // Hkv
+    f = lambda t, hh: t[0, :, hh, :].double().numpy()
+    gk_sum = [np.zeros((N, d)) for _ in range(Hkv)]
+    gv_sum = [np.zeros((N, d)) for _ in range(Hkv)]
+    for h in range(H):
+        hk = h // G
+        vec = fo.expand(masks[hk].sri, True, N)
+        O, L = fo.forward(f(q, h), f(k, hk), f(v, hk), vec)
+        gq, gk, gv = fo.backward(f(q, h), f(k, hk), f(v, hk), f(do, h), vec)
+        gk_sum[hk] += gk
+        gv_sum[hk] += gv
+        assert_close(f"O[{h}]", o[0, :, h].cpu().numpy(), O)
+        assert_lse(lse[0, h].cpu().numpy(), L)
+        assert_close(f"dQ[{h}]", dq[0, :, h].cpu().numpy(), gq)
+    for hk in range(Hkv):
+        assert_close(f"dK[{hk}]", dk[0, :, hk].cpu().numpy(), gk_sum[hk], tol_max=2e-2 * G ** 0.5)
+        assert_close(f"dV[{hk}]", dv[0, :, hk].cpu().numpy(), gv_sum[hk], tol_max=2e-2 * G ** 0.5)
