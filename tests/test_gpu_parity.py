@@ -503,3 +503,52 @@ def test_gqa_per_kv_head_masks(fmlib, d):
     for hk in range(Hkv):
         assert_close(f"dK[{hk}]", dk[0, :, hk].cpu().numpy(), gk_sum[hk], tol_max=2e-2 * G ** 0.5)
         assert_close(f"dV[{hk}]", dv[0, :, hk].cpu().numpy(), gv_sum[hk], tol_max=2e-2 * G ** 0.5)
+
+
+RANDOM_CASES = list(range(48))
+
+
+@pytest.mark.parametrize("seed", RANDOM_CASES)
+def test_random_configurations(fmlib, seed):
+    """Seeded random configurations (family, ragged N, d, B, H / Hkv, input and output dtype,
+    deterministic flag) against the oracle — catches combinations the fixed cases miss."""
+    from workloads import tensors as wt
+    rng = np.random.default_rng(1000 + seed)
+    fam = wm.FAMILIES[int(rng.integers(len(wm.FAMILIES)))]
+    N = int(rng.integers(1, 600))
+    d = int(rng.choice([64, 128]))
+    Hkv = int(rng.integers(1, 3))
+    G = int(rng.integers(1, 3))
+    H = Hkv * G
+    B = int(rng.integers(1, 3))
+    in_dt = [torch.bfloat16, torch.float16][int(rng.integers(2))]
+    flags = fmlib.FM_FLAG_DETERMINISTIC if rng.random() < 0.3 else 0
+    masks = [wm.sample_family(fam, N, rng, (1, 4)) for _ in range(B)]
+    sri = torch.from_numpy(wm.stack(masks, 1))
+    t = {}
+    for n, heads in (("q", H), ("do", H), ("k", Hkv), ("v", Hkv)):
+        t[n] = wt.make_tensor(n, B, N, heads, d, base=seed, dtype=in_dt)
+    sri_c, tc = to_cuda(sri, t)
+    causal = masks[0].causal
+    o, lse = fmlib.flashmask_fwd(tc["q"], tc["k"], tc["v"], sri_c, causal, out_dtype=torch.float32, flags=flags)
+    dq, dk, dv = fmlib.flashmask_bwd(tc["q"], tc["k"], tc["v"], o, tc["do"], lse, sri_c, causal,
+                                     out_dtype=torch.float32, flags=flags)
+    torch.cuda.synchronize()
+    f = lambda x, b, hh: x[b, :, hh, :].double().numpy()
+    for b in range(B):
+        vec = fo.expand(masks[b].sri, causal, N)
+        gk_sum = [np.zeros((N, d)) for _ in range(Hkv)]
+        gv_sum = [np.zeros((N, d)) for _ in range(Hkv)]
+        for h in range(H):
+            hk = h // G
+            O, L = fo.forward(f(t["q"], b, h), f(t["k"], b, hk), f(t["v"], b, hk), vec)
+            gq, gk, gv = fo.backward(f(t["q"], b, h), f(t["k"], b, hk), f(t["v"], b, hk), f(t["do"], b, h), vec)
+            gk_sum[hk] += gk
+            gv_sum[hk] += gv
+            tag = f"{fam} N={N} d={d} B={B} H={H}/{Hkv} {in_dt} flags={flags} [{b},{h}]"
+            assert_close(f"O {tag}", o[b, :, h].cpu().numpy(), O)
+            assert_lse(lse[b, h].cpu().numpy(), L)
+            assert_close(f"dQ {tag}", dq[b, :, h].cpu().numpy(), gq)
+        for hk in range(Hkv):
+            assert_close(f"dK {fam} [{b},{hk}]", dk[b, :, hk].cpu().numpy(), gk_sum[hk], tol_max=2e-2 * G ** 0.5)
+            assert_close(f"dV {fam} [{b},{hk}]", dv[b, :, hk].cpu().numpy(), gv_sum[hk], tol_max=2e-2 * G ** 0.5)
