@@ -172,6 +172,16 @@ enum {
 FM_API fm_status flashmask_timing_enable(int enable);
 FM_API fm_status flashmask_timing_collect(double* ms, int64_t* launches);
 
+/* Sliding-window shortcut (the sliding-window family of Fig. 1 / §2.1):
+ * writes startend_row_indices for a window of `window` keys without the caller building
+ * the vectors.  causal = 1: int32 [batch, 1, seqlen, 1], LTS_y = min(y + window, seqlen)
+ * (row r sees keys r-window+1 .. r); causal = 0: int32 [batch, 1, seqlen, 2],
+ * (LTS_y, UTE_y) = (min(y + window, seqlen), max(y - window + 1, 0)) (row r sees keys with
+ * |r - y| < window).  window >= 1, seqlen >= 1; out is a 16-byte-aligned device buffer
+ * owned by the caller.  Asynchronous on `stream`; FM_ERR_INVALID_ARGUMENT otherwise. */
+FM_API fm_status flashmask_sliding_window_indices(int64_t batch, int64_t seqlen, int64_t window, int32_t causal,
+                                                  int32_t* startend_row_indices, void* stream);
+
 /* Static description of a status code. */
 FM_API const char* flashmask_status_string(fm_status s);
 

@@ -419,6 +419,20 @@ fm_status flashmask_bwd(const fm_params* p, const void* q, const void* k, const 
   return FM_OK;
 }
 
+fm_status flashmask_sliding_window_indices(int64_t batch, int64_t seqlen, int64_t window, int32_t causal,
+                                          int32_t* sri, void* stream) {
+  g_last_error.clear();
+  if (!sri) return fail(FM_ERR_INVALID_ARGUMENT, "startend_row_indices is NULL");
+  if (!aligned16(sri)) return fail(FM_ERR_INVALID_ARGUMENT, "startend_row_indices must be 16-byte aligned");
+  if (batch < 1 || batch > 65535 || seqlen < 1 || seqlen > (1LL << 30) || window < 1 || (causal != 0 && causal != 1))
+    return fail(FM_ERR_INVALID_ARGUMENT, "need batch in [1, 65535], seqlen in [1, 2^30], window >= 1, causal 0/1");
+  const int w = static_cast<int>(window > seqlen ? seqlen : window);
+  cudaError_t e = fm::launch_sliding_window(static_cast<int>(batch), static_cast<int>(seqlen), w, causal, sri,
+                                            static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "sliding window indices");
+  return FM_OK;
+}
+
 fm_status flashmask_timing_enable(int enable) {
   g_timing.on = enable != 0;
   g_timing.mask = (enable & FM_TIMING_SELECT) ? static_cast<uint32_t>(enable & 0xFFFF) : 0xFFFFFFFFu;

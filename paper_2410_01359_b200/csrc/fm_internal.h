@@ -104,6 +104,7 @@ struct F32Args {
 
 // launchers (return cudaError_t of the launch)
 cudaError_t launch_expand(const int32_t* sri, const Dims& d, int bc, int32_t* ext8, int4* vec4, cudaStream_t st);
+cudaError_t launch_sliding_window(int B, int N, int w, int causal, int32_t* sri, cudaStream_t st);
 cudaError_t launch_classify(const int32_t* ext8, const Dims& d, int br, int bc, uint8_t* map, int transposed,
                             int kernel_map, int64_t* counts, cudaStream_t st);
 cudaError_t launch_fwd(const Dims& d, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,

@@ -179,6 +179,28 @@ __global__ void __launch_bounds__(128) k1_classify(const int32_t* __restrict__ e
   }
 }
 
+// Sliding-window startend_row_indices (flashmask_sliding_window_indices): one thread per key.
+__global__ void __launch_bounds__(256) k0_sliding_window(int B, int N, int w, int causal, int32_t* __restrict__ sri) {
+  pdl_wait();
+  pdl_launch();
+  const long idx = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (idx >= static_cast<long>(B) * N) return;
+  const int y = static_cast<int>(idx % N);
+  const int lts = static_cast<int>(min(static_cast<long>(y) + w, static_cast<long>(N)));
+  if (causal) {
+    sri[idx] = lts;
+  } else {
+    sri[2 * idx] = lts;
+    sri[2 * idx + 1] = max(y - w + 1, 0);
+  }
+}
+
+cudaError_t launch_sliding_window(int B, int N, int w, int causal, int32_t* sri, cudaStream_t st) {
+  const long n = static_cast<long>(B) * N;
+  return launch_pdl(k0_sliding_window, dim3(static_cast<unsigned>((n + 255) / 256)), dim3(256), 0, st, B, N, w, causal,
+                    sri);
+}
+
 cudaError_t launch_expand(const int32_t* sri, const Dims& d, int bc, int32_t* ext8, int4* vec4, cudaStream_t st) {
   const int Tc = (d.N + bc - 1) / bc;
   dim3 grid((Tc + 3) / 4, d.B * d.Hm);

@@ -23,7 +23,8 @@ FM_FLAG_DETERMINISTIC = 2
 FM_PASS_FWD, FM_PASS_BWD = 0, 1
 
 EXPORTED = ["flashmask_workspace_size", "flashmask_classify", "flashmask_fwd", "flashmask_bwd",
-            "flashmask_status_string", "flashmask_last_error", "flashmask_timing_enable", "flashmask_timing_collect"]
+            "flashmask_status_string", "flashmask_last_error", "flashmask_timing_enable", "flashmask_timing_collect",
+            "flashmask_sliding_window_indices"]
 KERNEL_NAMES = ["expand", "classify", "fwd", "bwd_pre", "bwd", "dq_convert", "dq"]
 (FM_KERNEL_EXPAND, FM_KERNEL_CLASSIFY, FM_KERNEL_FWD, FM_KERNEL_BWD_PRE, FM_KERNEL_BWD, FM_KERNEL_DQ_CONVERT,
  FM_KERNEL_DQ) = range(7)
@@ -61,6 +62,9 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.flashmask_last_error.argtypes = []
     lib.flashmask_last_error.restype = ctypes.c_char_p
     lib.flashmask_timing_enable.argtypes = [ctypes.c_int]
+    lib.flashmask_sliding_window_indices.argtypes = [ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_int32,
+                                                     vp, vp]
+    lib.flashmask_sliding_window_indices.restype = ctypes.c_int
     lib.flashmask_timing_enable.restype = ctypes.c_int
     lib.flashmask_timing_collect.argtypes = [ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int64)]
     lib.flashmask_timing_collect.restype = ctypes.c_int
@@ -130,6 +134,16 @@ def flashmask_classify(sri: torch.Tensor, causal: bool, br: int = 128, bc: int =
     _check(_lib.flashmask_classify(ctypes.byref(p), _ptr(sri), br, bc, _ptr(minmax), _ptr(cmap), _ptr(counts),
                                    _stream(stream)), "flashmask_classify")
     return minmax, cmap, counts
+
+
+def flashmask_sliding_window_indices(batch: int, seqlen: int, window: int, causal: bool = True, device="cuda",
+                                     stream=None) -> torch.Tensor:
+    """startend_row_indices of a sliding window of `window` keys, generated on the device:
+    causal -> int32 [batch, 1, seqlen, 1]; bidirectional -> int32 [batch, 1, seqlen, 2]."""
+    out = torch.empty(batch, 1, seqlen, 1 if causal else 2, dtype=torch.int32, device=device)
+    _check(_lib.flashmask_sliding_window_indices(batch, seqlen, window, int(bool(causal)), _ptr(out), _stream(stream)),
+           "flashmask_sliding_window_indices")
+    return out
 
 
 def _workspace(params, pass_, workspace, dev):

@@ -552,3 +552,32 @@ def test_random_configurations(fmlib, seed):
         for hk in range(Hkv):
             assert_close(f"dK {fam} [{b},{hk}]", dk[b, :, hk].cpu().numpy(), gk_sum[hk], tol_max=2e-2 * G ** 0.5)
             assert_close(f"dV {fam} [{b},{hk}]", dv[b, :, hk].cpu().numpy(), gv_sum[hk], tol_max=2e-2 * G ** 0.5)
+
+
+@pytest.mark.parametrize("causal", [True, False])
+def test_sliding_window_indices(fmlib, causal):
+    """SURVEY f4 sliding-window shortcut: the device-generated startend_row_indices expand (oracle)
+    to exactly the window predicate — causal: visible iff 0 <= r - y < w; bidirectional: |r - y| < w —
+    and drive the attention kernels to the oracle's result."""
+    N, w, B = 777, 100, 2
+    sri = fmlib.flashmask_sliding_window_indices(B, N, w, causal)
+    torch.cuda.synchronize()
+    s = sri.cpu().numpy()
+    r = np.arange(N)[:, None]
+    y = np.arange(N)[None, :]
+    want = ~((r - y >= 0) & (r - y < w)) if causal else ~(np.abs(r - y) < w)
+    for b in range(B):
+        vec = fo.expand(s[b, 0], causal, N)
+        assert np.array_equal(fo.to_dense(vec), want)
+    if causal:
+        assert np.array_equal(s[0, 0, :, 0], wm.sliding_window(N, w).sri[:, 0])
+    m = wm.MaskInput(N, causal, s.shape[-1], s[0, 0], "sliding_window_api")
+    sri_t, t = build_case([m], 2, 128, base=31)
+    sri_c, tc = to_cuda(sri_t, t)
+    o, lse = fmlib.flashmask_fwd(tc["q"], tc["k"], tc["v"], sri_c, causal, out_dtype=torch.float32)
+    torch.cuda.synchronize()
+    O, L, _ = oracle_head(t, [m], sri_t.numpy(), 0, 1, 1, causal, with_grad=False)
+    assert_close("O", o[0, :, 1].cpu().numpy(), O)
+    assert_lse(lse[0, 1].cpu().numpy(), L)
+    with pytest.raises(fmlib.FlashMaskError):
+        fmlib.flashmask_sliding_window_indices(1, 16, 0, causal)
