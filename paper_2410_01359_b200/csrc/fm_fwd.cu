@@ -60,18 +60,30 @@ namespace fm {
 namespace fwd {
 
 constexpr int NT = 576;   // 16 softmax warps + TMA producer + MMA issuer
-constexpr int KST = 2, VST = 2, MST = 4;
+constexpr int MST = 4;
+#ifndef FM_FWD_KST64
+#define FM_FWD_KST64 3
+#endif
+#ifndef FM_FWD_VST64
+#define FM_FWD_VST64 3
+#endif
+// K / V ring depths (d = 128: 2 each fills shared memory; d = 64 tiles are half the size:
+// 3-deep rings, +1-3 % on the C5 d = 64 sweep)
+template <int D>
+struct Rings {
+  static constexpr int KST = (D == 64) ? FM_FWD_KST64 : 2, VST = (D == 64) ? FM_FWD_VST64 : 2;
+};
 
 template <int D>
 struct Smem {
   static constexpr int TILE = 128 * D * 2;
   uint8_t q[2][TILE];
-  uint8_t k[KST][TILE];
-  uint8_t v[VST][TILE];
+  uint8_t k[Rings<D>::KST][TILE];
+  uint8_t v[Rings<D>::VST][TILE];
   int4 mask[MST][128];
   uint32_t list[kMaxTc];
   uint64_t bar_q;
-  uint64_t k_full[KST], k_empty[KST], v_full[VST], v_empty[VST];
+  uint64_t k_full[Rings<D>::KST], k_empty[Rings<D>::KST], v_full[Rings<D>::VST], v_empty[Rings<D>::VST];
   uint64_t m_full[MST], m_empty[MST];
   uint64_t s_full[2], p_full[2], o_full[2], s_read[2], pv_done[2];
   float xmax[2][2][2][128];  // [tile][parity][column half][row]: row-max exchange between halves
@@ -101,6 +113,7 @@ __global__ void __launch_bounds__(fwd::NT, 1)
                   const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmO, const FwdArgs a) {
   using namespace fwd;
   using S = Smem<D>;
+  constexpr int KST = Rings<D>::KST, VST = Rings<D>::VST;
   extern __shared__ uint8_t smem_raw[];
   S& sm = *smem_align1024<S>(smem_raw);
 
