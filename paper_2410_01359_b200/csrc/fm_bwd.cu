@@ -68,7 +68,6 @@ constexpr int NT = (G_WARP + 1) * 32;
 #ifndef FM_QST
 #define FM_QST 3
 #endif
-constexpr int QST = FM_QST;
 #ifndef FM_DQ_NSTAGE
 #define FM_DQ_NSTAGE 2
 #endif
@@ -96,7 +95,6 @@ constexpr int DQ_CROWS = FM_DQ_CROWS;  // query rows per dQ^T staging chunk (d=1
 #ifndef FM_QST64
 #define FM_QST64 3
 #endif
-constexpr int NDS = FM_BWD_NDS;  // dS shared-memory buffers
 
 template <int D>
 struct Cfg {
@@ -128,7 +126,7 @@ struct Cfg {
   static constexpr int MAXTRB = (D == 128) ? kMaxTrb : kMaxTrb / 2;
   // per-head-dim ring depths: Q/dO stages and dS shared-memory buffers
   static constexpr int QST = (D == 64) ? FM_QST64 : FM_QST;
-  static constexpr int NDS = (D == 64) ? FM_BWD_NDS64 : FM_BWD_NDS;
+  static constexpr int NDS = (D == 64) ? FM_BWD_NDS64 : FM_BWD_NDS;  // dS shared-memory buffers
 };
 
 template <int D>
