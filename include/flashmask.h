@@ -88,7 +88,7 @@ enum {
 
 typedef struct {
   int64_t batch;       /* B >= 1                                                    */
-  int64_t seqlen;      /* N >= 1 (queries = keys)                                  */
+  int64_t seqlen;      /* 1 <= N <= 262144 (queries = keys); larger: UNSUPPORTED     */
   int64_t num_heads;   /* H >= 1                                                    */
   int64_t head_dim;    /* d in {64, 128}                                            */
   int64_t mask_heads;  /* 1 (one mask per batch entry, broadcast) or num_kv_heads   */

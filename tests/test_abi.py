@@ -71,6 +71,11 @@ def test_host_validation_without_gpu(lib_path):
     assert lib.flashmask_fwd(ctypes.byref(p), None, None, None, None, None, None, None, 0, None) == \
         fm.FM_ERR_UNSUPPORTED
     p.batch = 1
+    p.seqlen = 262144 + 1  # beyond the largest supported N (2048 column tiles)
+    assert lib.flashmask_fwd(ctypes.byref(p), None, None, None, None, None, None, None, 0, None) == \
+        fm.FM_ERR_UNSUPPORTED
+    assert b"262144" in lib.flashmask_last_error()
+    p.seqlen = 128
     assert lib.flashmask_status_string(fm.FM_ERR_WORKSPACE_TOO_SMALL) == b"FM_ERR_WORKSPACE_TOO_SMALL"
 
 
