@@ -397,6 +397,32 @@ def test_back_to_back_shared_workspace(fmlib):
                 assert torch.equal(a, b), name
 
 
+def test_chunked_calls_match_full_call(fmlib):
+    """bench.py's e2e leg splits a step into one call per (batch entry, head group) — heads and
+    batch entries are independent.  The chunked calls reproduce the full call: O, lse, dK,
+    dV bitwise (atomic-free), dQ to one bf16 ulp (fp32 reduce-add order)."""
+    masks = [wm.sample_family("document", 900, np.random.default_rng(s), (2, 5)) for s in (7, 8)]
+    causal = masks[0].causal
+    sri, t = build_case(masks, 8, 128, base=31)
+    s, t = to_cuda(sri, t)
+    o, lse = fmlib.flashmask_fwd(t["q"], t["k"], t["v"], s, causal)
+    dq, dk, dv = fmlib.flashmask_bwd(t["q"], t["k"], t["v"], o, t["do"], lse, s, causal)
+    HG = 2
+    for b in range(2):
+        for h0 in range(0, 8, HG):
+            c = {k: v[b:b + 1, :, h0:h0 + HG].contiguous() for k, v in t.items()}
+            sc = s[b:b + 1].contiguous()
+            oc, lc = fmlib.flashmask_fwd(c["q"], c["k"], c["v"], sc, causal)
+            gq, gk, gv = fmlib.flashmask_bwd(c["q"], c["k"], c["v"], oc, c["do"], lc, sc, causal)
+            assert torch.equal(oc, o[b:b + 1, :, h0:h0 + HG])
+            assert torch.equal(lc, lse[b:b + 1, h0:h0 + HG])
+            assert torch.equal(gk, dk[b:b + 1, :, h0:h0 + HG])
+            assert torch.equal(gv, dv[b:b + 1, :, h0:h0 + HG])
+            ref = dq[b:b + 1, :, h0:h0 + HG].float()
+            assert ((gq.float() - ref).abs() <= 2.0 ** -7 * ref.abs() + 1e-3).all()
+    torch.cuda.synchronize()
+
+
 # ------------------------------------------------------------------------- fp16 inputs (SURVEY f4)
 FP16_CASES = [("causal_document", 1000, 128, 1, 2), ("document", 257, 64, 1, 2), ("random_eviction", 384, 128, 1, 1),
               ("global_sliding_window", 700, 64, 1, 1)]
