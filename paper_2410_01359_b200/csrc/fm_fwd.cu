@@ -349,15 +349,26 @@ __global__ void __launch_bounds__(fwd::NT, 1)
             // (unsigned)(r - start_y) < len_y for either interval, or (causal) r < y
             const int4* mk = sm.mask[ms] + hh * 64 + c * 16;
             const int rmy = row - (j * 128 + hh * 64 + c * 16);
+            // causal: below the diagonal tile (j < i) no key of the tile lies after any of its
+            // rows, so the r < y test is dropped there (warp-uniform choice)
+            if (CAUSAL && j < (q == 0 ? i0 : i1)) {
 #pragma unroll
-            for (int t = 0; t < 16; ++t) {
-              const int4 mv = mk[t];
-              bool msk = static_cast<unsigned>(row - mv.x) < static_cast<unsigned>(mv.y);
-              if constexpr (CAUSAL)
-                msk |= rmy < t;
-              else
-                msk |= static_cast<unsigned>(row - mv.z) < static_cast<unsigned>(mv.w);
-              sv[t] = msk ? -INFINITY : sv[t];
+              for (int t = 0; t < 16; ++t) {
+                const int4 mv = mk[t];
+                const bool msk = static_cast<unsigned>(row - mv.x) < static_cast<unsigned>(mv.y);
+                sv[t] = msk ? -INFINITY : sv[t];
+              }
+            } else {
+#pragma unroll
+              for (int t = 0; t < 16; ++t) {
+                const int4 mv = mk[t];
+                bool msk = static_cast<unsigned>(row - mv.x) < static_cast<unsigned>(mv.y);
+                if constexpr (CAUSAL)
+                  msk |= rmy < t;
+                else
+                  msk |= static_cast<unsigned>(row - mv.z) < static_cast<unsigned>(mv.w);
+                sv[t] = msk ? -INFINITY : sv[t];
+              }
             }
             tmem_st16(tSh + c * 16, sr[c & 1]);  // masked S back to TMEM: pass 2 needs no mask work
           }
