@@ -90,3 +90,25 @@ def test_workspace_size_is_linear_in_n(lib_path):
     assert sizes[8192][0] < 2 * 1024 * 1024
     assert 1.9 < sizes[16384][1] / sizes[8192][1] < 2.1
     assert sizes[8192][1] >= 8192 * 32 * 128 * 4
+
+
+def test_binding_fails_loudly_without_the_library(tmp_path):
+    """No CPU or eager fallback: with the shared library absent, importing the binding raises."""
+    code = "import paper_2410_01359_b200.flashmask"
+    env = dict(os.environ, FLASHMASK_LIB=str(tmp_path / "absent" / "libflashmask.so"), PYTHONPATH=ROOT)
+    r = subprocess.run(["python", "-c", code], cwd=str(tmp_path), env=env, capture_output=True, text=True, timeout=300)
+    assert r.returncode != 0, r.stdout
+    assert "libflashmask" in r.stderr or "absent" in r.stderr, r.stderr[-2000:]
+
+
+def test_product_package_never_references_the_oracle():
+    """The oracle is test infrastructure: nothing in the product package imports or calls it."""
+    pkg = os.path.join(ROOT, "paper_2410_01359_b200")
+    hits = []
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
+                src = open(os.path.join(dirpath, f)).read()
+                if re.search(r"^\s*(from|import)\s+oracle\b|oracle[./]", src, re.M):
+                    hits.append(f)
+    assert hits == []
