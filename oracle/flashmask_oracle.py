@@ -215,6 +215,42 @@ def backward_rows(q, k, v, do, vec: Vectors, rows, scale=None):
     return scale * (dS @ k), scale * (dS.T @ q[rr]), dv
 
 
+def backward_cols(q, k, v, do, vec: Vectors, keys, scale=None, row_block: int = 1024):
+    """dK and dV of the key columns ``keys`` only (the column-parallel view of Alg. 2, P:258,
+    P:390-438, restated densely): first the forward over ALL rows (L_r and O_r — every row's
+    softmax spans all keys), D = rowsum(dO o O) (R5); then for the requested columns
+    y: P[:, y] = exp(scale*Q k_y^T - L) on visible cells, 0 on masked cells and on empty rows
+    (L = -inf, R7), dV_y = P[:, y]^T dO, dP[:, y] = dO v_y^T,
+    dS = P o (dP - D), dK_y = scale * dS[:, y]^T Q.  Cost O(N^2 d) for the
+    forward plus O(N |keys| d); used where ``backward`` (O(N^2) memory per block, all
+    columns) is too slow: generic-Q dK/dV checks at N = 32K.  Returns (dK [len(keys), d],
+    dV [len(keys), d])."""
+    q = np.asarray(q, dtype=np.float64)
+    k = np.asarray(k, dtype=np.float64)
+    v_ = np.asarray(v, dtype=np.float64)
+    do = np.asarray(do, dtype=np.float64)
+    N, d = q.shape
+    scale = 1.0 / math.sqrt(d) if scale is None or scale <= 0 else float(scale)
+    keys = np.asarray(keys, dtype=np.int64)
+    O, L = forward(q, k, v_, vec, scale, row_block=row_block)
+    D = (do * O).sum(axis=1)
+    dk = np.zeros((len(keys), d))
+    dv = np.zeros((len(keys), v_.shape[1]))
+    live = np.isfinite(L)
+    for s in range(0, N, row_block):
+        rr = np.arange(s, min(s + row_block, N))
+        S = scale * (q[rr] @ k[keys].T)                       # [rows, |keys|]
+        M = _mask_for_rows(vec, rr)[:, keys]
+        P = np.zeros_like(S)
+        ok = ~M & live[rr, None]
+        P[ok] = np.exp((S - np.where(live[rr], L[rr], 0.0)[:, None])[ok])
+        dv += P.T @ do[rr]
+        dP = do[rr] @ v_[keys].T
+        dS = P * (dP - D[rr, None])
+        dk += scale * (dS.T @ q[rr])
+    return dk, dv
+
+
 # ------------------------------------------------------------------ classification
 def extrema(vec: Vectors, Bc: int) -> np.ndarray:
     """Alg. 1 lines 3-4: per column tile j the min and max of each vector over

@@ -239,3 +239,58 @@ def test_q_zero_linear_forms_match_dense(fam):
     assert np.abs(L[fin] - L2[fin]).max() < 1e-12
     _, _, dv = fo.backward(q, k, v_, do, vv)
     assert np.abs(dv - fo.dv_q_zero(do, vv)).max() < 1e-12
+
+
+@pytest.mark.parametrize("N,d,causal_", [(7, 3, False), (33, 8, True)])
+def test_backward_cols_equals_torch_autograd(N, d, causal_):
+    """backward_cols (dK, dV of chosen key columns) equals torch autograd of fp64 SDPA."""
+    rng = np.random.default_rng(N + 77)
+    q, k, v_, do = rnd(rng, N, d), rnd(rng, N, d), rnd(rng, N, d), rnd(rng, N, d)
+    tq, tk, tv = (torch.tensor(a, dtype=torch.float64, requires_grad=True) for a in (q, k, v_))
+    out = torch.nn.functional.scaled_dot_product_attention(tq[None, None], tk[None, None], tv[None, None],
+                                                           is_causal=causal_)[0, 0]
+    out.backward(torch.tensor(do))
+    keys = np.array([0, N // 2, N - 1])
+    m = wm.causal(N) if causal_ else wm.full(N)
+    dk, dv = fo.backward_cols(q, k, v_, do, vec(m), keys, row_block=5)
+    assert np.abs(dk - tk.grad.numpy()[keys]).max() < 1e-12
+    assert np.abs(dv - tv.grad.numpy()[keys]).max() < 1e-12
+
+
+@pytest.mark.parametrize("fam,N,d", [("share_question", 40, 4), ("global_sliding_window", 24, 3),
+                                     ("qk_sparse", 36, 4), ("random_eviction", 30, 4)])
+def test_backward_cols_finite_differences(fam, N, d):
+    """backward_cols against central differences of the forward loss, including keys
+    masked for every row (zero gradient) and rows masked in every column."""
+    rng = np.random.default_rng(5 + N)
+    m = wm.sample_family(fam, N, rng, (2, 4))
+    vv = vec(m)
+    N = m.N
+    q, k, v_, do = rnd(rng, N, d), rnd(rng, N, d), rnd(rng, N, d), rnd(rng, N, d)
+    scale = 0.6
+    keys = np.unique(rng.integers(0, N, 6))
+    dk, dv = fo.backward_cols(q, k, v_, do, vv, keys, scale, row_block=7)
+    h = 1e-6
+    for which, g in ((1, dk), (2, dv)):
+        for ki, y in enumerate(keys):
+            for c in range(d):
+                args = [q.copy(), k.copy(), v_.copy()]
+                args[which][y, c] += h
+                lp = _loss(*args, do, vv, scale)
+                args[which][y, c] -= 2 * h
+                lm = _loss(*args, do, vv, scale)
+                fd = (lp - lm) / (2 * h)
+                assert abs(fd - g[ki, c]) <= 1e-6 * max(1.0, abs(g[ki, c])), (which, y, c, fd, g[ki, c])
+
+
+@pytest.mark.parametrize("fam", ["causal_document", "document", "prefix_lm_causal", "hash_sparse"])
+def test_backward_cols_matches_backward(fam):
+    rng = np.random.default_rng(41)
+    m = wm.sample_family(fam, 130, rng, (2, 5))
+    vv = vec(m)
+    N, d = m.N, 6
+    q, k, v_, do = (rnd(rng, N, d) for _ in range(4))
+    _, dk, dv = fo.backward(q, k, v_, do, vv)
+    keys = np.arange(0, N, 3)
+    gk, gv = fo.backward_cols(q, k, v_, do, vv, keys, row_block=32)
+    assert np.abs(gk - dk[keys]).max() < 1e-12 and np.abs(gv - dv[keys]).max() < 1e-12
