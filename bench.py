@@ -1,21 +1,27 @@
 """FlashMask hot-path benchmark (one JSON line on rank 0).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3] [--impl flashmask|reference]
+                    [--sweep auto|none|full]
 
 A step = one pass of the whole hot path over one batch: K1 classification + forward
 (K1, K2) + backward (K1, K3, K4, K5) through the C ABI, for every call of the workload.
 Metric (BASELINE.json): effective fwd+bwd TFLOP/s with skipped tiles excluded — FLOPs =
 3.5 x 4 d x (non-SKIP 128x128 tiles) x 128^2 per (batch, head) (R15), the SKIP
-count coming from the library's own K1 classification.  Multi-GPU: one process per GPU
-(torchrun), batch entries sharded across ranks (weak scaling) for C2/C3/C5, heads sharded
-for C4 (strong scaling); NCCL only reduces the per-rank timings.
+count coming from the library's own K1 classification.
+
+Multi-GPU (heads are independent): one process per GPU; `--gpus N`
+without torchrun re-launches itself under torch.distributed.run (and fails loudly when fewer
+than N GPUs are visible).  Every config is HEAD-sharded — rank k computes heads
+[k H/N, (k+1) H/N) of the SAME global problem (strong scaling); inputs are seeded per head so a
+shard holds exactly the 1-GPU run's data.  There is no data-path collective; NCCL all_gathers
+the per-rank timings, effective FLOPs and output checksums after the timed region.
 """
 from __future__ import annotations
 
 import argparse
 import json
-import math
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -33,6 +39,7 @@ from workloads import tensors as wt  # noqa: E402
 
 PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
 FALLBACK_PEAKS = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+METRIC = "effective fwd+bwd TFLOPs/s (skipped tiles excluded) and % of B200 bf16 peak"
 
 
 # ----------------------------------------------------------------------------- workloads
@@ -54,7 +61,7 @@ def rho_gpu(fm):
 
 
 def rho_oracle(m: wm.MaskInput) -> float:
-    """Same quantity from the oracle (used only by the --impl reference arm)."""
+    """Same quantity from the oracle (used only by the --impl reference arm and CPU tests)."""
     from oracle import flashmask_oracle as fo
     _, c, _ = fo.classify(fo.expand(m.sri, m.causal, m.N), 128, 128)
     return fo.block_sparsity(c)
@@ -87,102 +94,148 @@ def sft_mask_in_bucket(N, lo, hi, gidx, rho_fn, base=0, max_tries=4000):
     raise RuntimeError(f"no mask found in bucket [{lo},{hi})")
 
 
+def shard_heads(H: int, rank: int, world: int) -> range:
+    """Rank k's heads [k H/world, (k+1) H/world) (with one mask per batch entry every
+    head has identical tile work, so the shards are balanced exactly)."""
+    if H % world:
+        raise SystemExit(f"{H} heads do not split evenly over {world} ranks")
+    return range(rank * H // world, (rank + 1) * H // world)
+
+
 def build_workload(cfg: str, rank: int, world: int, rho_fn, base=0):
-    """Returns (calls, config_dict, scaling).  A call = dict(masks, causal, B, N, H, d, heads, batch_ids)."""
+    """Returns (calls, config_dict, scaling).  A call = dict(masks, causal, B, N, H, d, heads,
+    batch_ids): the global problem is the same at every world size; `heads` is this rank's shard."""
     if cfg == "C3":
         N, H, d, B = 32768, 32, 128, 4
         buckets = [(0.1, 0.2), (0.3, 0.4), (0.55, 0.65), (0.8, 0.9)]
-        gids = [rank * B + i for i in range(B)]
-        masks = [sft_mask_in_bucket(N, *buckets[i], gids[i], rho_fn, base) for i in range(B)]
-        calls = [dict(masks=masks, causal=False, B=B, N=N, H=H, d=d, heads=range(H), batch_ids=gids)]
-        conf = {"workload": "C3: SFT-style packed documents, B=4 per GPU (one mask per sparsity bucket "
+        masks = [sft_mask_in_bucket(N, *buckets[i], i, rho_fn, base) for i in range(B)]
+        hs = shard_heads(H, rank, world)
+        calls = [dict(masks=masks, causal=False, B=B, N=N, H=H, d=d, heads=hs, batch_ids=list(range(B)))]
+        conf = {"workload": "C3: SFT-style packed documents, B=4 (one mask per sparsity bucket "
                             "10-20/30-40/55-65/80-90%), H=32, N=32768, d=128, bf16 in/out",
-                "global_batch": B * world, "seq_len": N, "heads": H, "head_dim": d,
-                "parallelism": f"batch-sharded x{world}", "l2": "inputs (1 GiB/tensor/GPU) larger than L2"}
-        return calls, conf, "weak"
+                "global_batch": B, "seq_len": N, "heads": H, "head_dim": d,
+                "parallelism": f"head-sharded x{world} ({len(hs)} heads per GPU)",
+                "l2": "no flush; inputs (1 GiB per tensor) larger than L2"}
+        return calls, conf, "strong"
     if cfg == "C2":
         N, H, d = 8192, 32, 128
         calls = []
-        rng = np.random.default_rng(_seed(base, rank, 2))
+        rng = np.random.default_rng(_seed(base, 0, 2))
         lens = wm.sample_doc_lens(N, int(rng.integers(3, 8)), rng, min_len=128)
         docs = []
         for L in lens:
             k = int(rng.integers(2, 7))
             ans = [max(1, int(rng.uniform(0.08, 0.16) * L)) for _ in range(k)]
             docs.append((L - sum(ans), ans))
+        hs = shard_heads(H, rank, world)
         for m in (wm.causal_document(lens), wm.share_question(docs), wm.sliding_window(N, N // 16)):
-            calls.append(dict(masks=[m], causal=True, B=1, N=N, H=H, d=d, heads=range(H), batch_ids=[rank]))
-        conf = {"workload": "C2: B=1 per GPU, H=32, N=8192, d=128, bf16; one call each of causal-document, "
+            calls.append(dict(masks=[m], causal=True, B=1, N=N, H=H, d=d, heads=hs, batch_ids=[0], family=m.family))
+        conf = {"workload": "C2: B=1, H=32, N=8192, d=128, bf16; one call each of causal-document, "
                             "share-question and sliding-window (w=N/16) masks",
-                "global_batch": world, "seq_len": N, "heads": H, "head_dim": d,
-                "parallelism": f"batch-sharded x{world}", "l2": "no flush; 64 MiB/tensor (Q,K,V,dO 256 MiB) > L2"}
-        return calls, conf, "weak"
+                "global_batch": 1, "seq_len": N, "heads": H, "head_dim": d,
+                "parallelism": f"head-sharded x{world}", "l2": "no flush; Q,K,V,dO 256 MiB > L2"}
+        return calls, conf, "strong"
     if cfg == "C4":
         N, H, d = 131072, 64, 128
-        assert H % world == 0
-        hs = range(rank * H // world, (rank + 1) * H // world)
+        hs = shard_heads(H, rank, world)
         calls = []
         for k_ans in (2, 6):   # DPO, RM (App. A.2.1 P:457)
             rng = np.random.default_rng(_seed(base, k_ans, 4))
             m = wm.sample_share_question(N, int(rng.integers(11, 16)), rng, k_range=(k_ans, k_ans), min_len=512)
-            calls.append(dict(masks=[m], causal=True, B=1, N=N, H=H, d=d, heads=hs, batch_ids=[0]))
+            calls.append(dict(masks=[m], causal=True, B=1, N=N, H=H, d=d, heads=hs, batch_ids=[0],
+                              family=f"share_question(k={k_ans})"))
         conf = {"workload": "C4: DPO (k=2) and RM (k=6) share-question masks, B=1, H=64, N=131072, d=128, bf16",
                 "global_batch": 1, "seq_len": N, "heads": H, "head_dim": d,
-                "parallelism": f"head-sharded x{world}", "l2": "inputs larger than L2"}
+                "parallelism": f"head-sharded x{world}", "l2": "no flush; inputs larger than L2"}
         return calls, conf, "strong"
     if cfg.startswith("C5"):
-        # C5:<N>:<d>  kernel sweep of every Figure-1 family, 128K tokens, hidden 4096 (App. A.5.2)
-        _, N, d = cfg.split(":") if ":" in cfg else ("C5", "8192", "128")
-        N, d = int(N), int(d)
+        # C5:<N>:<d>[:family,family]  kernel sweep of the Figure-1 families, 128K tokens, hidden 4096
+        # (App. A.5.2 P:586-588)
+        parts = cfg.split(":")
+        N = int(parts[1]) if len(parts) > 1 else 8192
+        d = int(parts[2]) if len(parts) > 2 else 128
+        fams = parts[3].split(",") if len(parts) > 3 else wm.FAMILIES
         B, H = 131072 // N, 4096 // d
         doc_rng = {8192: (3, 7), 32768: (10, 14), 131072: (11, 15)}.get(N, (3, 7))
+        hs = shard_heads(H, rank, world)
         calls = []
-        for fam in wm.FAMILIES:
-            ms = [wm.sample_family(fam, N, np.random.default_rng(_seed(base, rank * B + b, len(fam))), doc_rng)
-                  for b in range(B)]
-            calls.append(dict(masks=ms, causal=ms[0].causal, B=B, N=N, H=H, d=d, heads=range(H),
-                              batch_ids=[rank * B + b for b in range(B)], family=fam))
-        conf = {"workload": f"C5: all Figure-1 families, N={N}, d={d}, B={B}, H={H} per GPU, bf16",
-                "global_batch": B * world, "seq_len": N, "heads": H, "head_dim": d,
-                "parallelism": f"batch-sharded x{world}", "l2": "inputs larger than L2"}
-        return calls, conf, "weak"
+        for fam in fams:
+            ms = [wm.sample_family(fam, N, np.random.default_rng(_seed(base, b, len(fam))), doc_rng) for b in range(B)]
+            calls.append(dict(masks=ms, causal=ms[0].causal, B=B, N=N, H=H, d=d, heads=hs,
+                              batch_ids=list(range(B)), family=fam))
+        conf = {"workload": f"C5: Figure-1 families {','.join(fams) if len(fams) < 13 else 'all'}, N={N}, d={d}, "
+                            f"B={B}, H={H}, bf16",
+                "global_batch": B, "seq_len": N, "heads": H, "head_dim": d,
+                "parallelism": f"head-sharded x{world}", "l2": "no flush; inputs larger than L2"}
+        return calls, conf, "strong"
     raise SystemExit(f"unknown config {cfg}")
 
 
 # ----------------------------------------------------------------------------- helpers
 def make_inputs(call, device, base=0):
+    """bf16 q, k, v, dO [B, N, heads, d] with one seeded device draw per (tensor, global head):
+    a head shard holds exactly the heads of the 1-GPU run."""
     B, N, d = call["B"], call["N"], call["d"]
-    nh = len(call["heads"])
+    heads = list(call["heads"])
     out = {}
     for name in ("q", "k", "v", "do"):
+        t = torch.empty(B, N, len(heads), d, dtype=torch.bfloat16, device=device)
         g = torch.Generator(device=device)
-        g.manual_seed(_seed(base, wt.TENSOR_IDS[name], call["batch_ids"][0], call["heads"][0], N))
-        out[name] = torch.randn(B, N, nh, d, generator=g, device=device, dtype=torch.float32).to(torch.bfloat16)
+        for i, h in enumerate(heads):
+            g.manual_seed(_seed(base, wt.TENSOR_IDS[name], call["batch_ids"][0], h, N))
+            t[:, :, i, :] = torch.randn(B, N, d, generator=g, device=device, dtype=torch.float32).to(torch.bfloat16)
+        out[name] = t
     out["sri"] = torch.from_numpy(wm.stack(call["masks"], 1)).to(device)
     return out
 
 
 def effective_flops(call, fm):
-    """(fwd, bwd) effective FLOPs of one call from the library's K1 counts at 128x128."""
+    """(fwd, bwd) effective FLOPs of one call from the library's K1 counts at 128x128, the block
+    sparsities, and the tiles the kernels visit at their own granularity: the
+    forward CTA visits the union of two 128-row tiles' non-SKIP column tiles, the backward visits
+    non-SKIP (Brb x 128) tiles, Brb = 64 (d=128) / 128 (d=64)."""
     N, d, nh = call["N"], call["d"], len(call["heads"])
     sri = torch.from_numpy(wm.stack(call["masks"], 1)).cuda()
-    _, _, counts = fm.flashmask_classify(sri, call["causal"], class_map=False)
+    _, cm, counts = fm.flashmask_classify(sri, call["causal"])
     c = counts.cpu().numpy().reshape(-1, 3)
     assert N % 128 == 0
     nonskip = float((c[:, 1] + c[:, 2]).sum())
     rho = [float(x[0]) / float(x.sum()) for x in c]
     fwd = 4.0 * d * nonskip * 128 * 128 * nh
-    return fwd, 2.5 * fwd, rho
+    Tr = cm.shape[2]
+    ns = cm != fm.FM_TILE_SKIP                       # [B, 1, Tr, Tc]
+    if Tr % 2:
+        ns = torch.cat([ns, torch.zeros_like(ns[:, :, :1])], 2)
+    pair = ns.view(ns.shape[0], ns.shape[1], -1, 2, ns.shape[3]).any(3)
+    real = torch.tensor([2] * (Tr // 2) + [1] * (Tr % 2), device=cm.device)
+    vis_fwd = int((pair.sum(-1) * real).sum().item()) * nh
+    brb = 64 if d == 128 else 128
+    _, _, cb = fm.flashmask_classify(sri, call["causal"], br=brb, class_map=False)
+    cb = cb.cpu().numpy().reshape(-1, 3)
+    vis_bwd = int((cb[:, 1] + cb[:, 2]).sum()) * nh
+    visited = {"fwd_128x128_tiles": vis_fwd, "bwd_tiles": vis_bwd, "bwd_tile": f"{brb}x128",
+               "metric_nonskip_128x128_tiles": int(nonskip) * nh}
+    return fwd, 2.5 * fwd, rho, visited
 
 
 def reduce_max_over_ranks(x: float, dist=None, device="cpu") -> float:
-    """Max of a per-rank scalar (timings are reported as the slowest rank).  NCCL on the GPU
-    path, gloo in the CPU tests; the only collective bench.py issues besides barriers."""
+    """Max of a per-rank scalar (timings are reported as the slowest rank)."""
     if dist is None or not dist.is_initialized():
         return x
     t = torch.tensor([x], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
+
+
+def gather_ranks(vals, dist=None, device="cpu"):
+    """all_gather of one float64 vector per rank (NCCL on the GPU path, gloo in the CPU tests):
+    per-rank timings, effective FLOPs and output checksums.  Returns a [world, len(vals)] list."""
+    t = torch.tensor(vals, dtype=torch.float64, device=device)
+    if dist is None or not dist.is_initialized():
+        return [t.tolist()]
+    out = [torch.empty_like(t) for _ in range(dist.get_world_size())]
+    dist.all_gather(out, t)
+    return [o.tolist() for o in out]
 
 
 class ClockSampler:
@@ -200,7 +253,7 @@ class ClockSampler:
             fd, self.path = tempfile.mkstemp(suffix=".csv")
             os.close(fd)
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
                                          stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
         except Exception:
             self.proc = None
@@ -236,42 +289,219 @@ def load_peaks():
     return dict(FALLBACK_PEAKS), "fallback"
 
 
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def self_launch(args) -> int:
+    """`--gpus N` without torchrun: re-launch this script as N ranks (one per GPU) under
+    torch.distributed.run on 127.0.0.1.  Fails loudly when fewer than N GPUs are visible."""
+    n_dev = torch.cuda.device_count()
+    if n_dev < args.gpus:
+        raise SystemExit(f"bench.py --gpus {args.gpus}: only {n_dev} CUDA device(s) visible; refusing to run "
+                         f"{args.gpus} ranks on fewer GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 # ----------------------------------------------------------------------------- CPU oracle
-def oracle_sample_rate(call, budget_s, base=0, rows_per_block=128):
-    """Time the fp64 oracle (forward rows + backward rows) on whole 128-row tiles of one
-    (batch, head) of ``call`` until ``budget_s`` elapses.  Returns (effective TFLOP/s, info)."""
+def _oracle_worker(job):
+    """One process of the CPU oracle pool: forward rows + backward rows of the given 128-row
+    tiles of one (batch, head), until the deadline.  Returns (flops, tiles)."""
+    call_sri, causal, N, d, seeds, tiles, deadline = job
     from oracle import flashmask_oracle as fo
-    try:
-        from threadpoolctl import threadpool_info
-        cores = max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
-    except Exception:
-        cores = os.cpu_count() or 1
-    m = call["masks"][0]
-    N, d = call["N"], call["d"]
     g = torch.Generator()
     tens = {}
-    for name in ("q", "k", "v", "do"):
-        g.manual_seed(_seed(base, wt.TENSOR_IDS[name], 7, 0, N))
+    for name, s in seeds.items():
+        g.manual_seed(s)
         tens[name] = torch.randn(N, d, generator=g).to(torch.bfloat16).double().numpy()
-    vec = fo.expand(m.sri, m.causal, N)
+    vec = fo.expand(call_sri, causal, N)
     cm, _, _ = fo.classify(vec, 128, 128)
-    T = cm.shape[0]
-    order = [int(x) for x in np.random.default_rng(0).permutation(T)]
-    t0 = time.perf_counter()
-    flops = 0.0
-    tiles = 0
-    for i in order:
+    flops, done = 0.0, 0
+    for i in tiles:
+        if time.time() >= deadline:
+            break
         rows = np.arange(i * 128, min((i + 1) * 128, N))
         fo.forward(tens["q"], tens["k"], tens["v"], vec, rows=rows)
         fo.backward_rows(tens["q"], tens["k"], tens["v"], tens["do"], vec, rows)
         flops += 3.5 * 4.0 * d * 128 * 128 * float((cm[i] != fo.SKIP).sum())
-        tiles += 1
-        if time.perf_counter() - t0 >= budget_s:
-            break
-    dt = time.perf_counter() - t0
-    return flops / dt / 1e12, {"cores": cores, "seconds": dt, "row_tiles": tiles,
-                               "sample": f"fp64 NumPy oracle, forward + backward of {tiles} random 128-row tiles "
-                                         f"of one (batch, head) of the {m.family} mask, N={N}, d={d}"}
+        done += 1
+    return flops, done
+
+
+def oracle_sample_rate(call, budget_s, base=0, procs=None):
+    """Time the fp64 oracle (forward rows + backward rows, as it stands) on whole 128-row tiles of
+    one (batch, head) of ``call`` with a process pool over the host cores (SURVEY d.7: the rows
+    are independent; NumPy's elementwise work is single-threaded, so one process per core with
+    one BLAS thread each).  Returns (effective TFLOP/s, info)."""
+    import multiprocessing as mp
+    procs = procs or len(os.sched_getaffinity(0))
+    m = call["masks"][0]
+    N, d = call["N"], call["d"]
+    seeds = {name: _seed(base, wt.TENSOR_IDS[name], 7, 0, N) for name in ("q", "k", "v", "do")}
+    T = -(-N // 128)
+    order = [int(x) for x in np.random.default_rng(0).permutation(T)]
+    env_keys = ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS")
+    old = {k: os.environ.get(k) for k in env_keys}
+    for k in env_keys:
+        os.environ[k] = "1"
+    try:
+        ctx = mp.get_context("spawn")
+        with ctx.Pool(procs) as pool:
+            pool.map(abs, range(procs))             # interpreter start-up outside the timed budget
+            t0 = time.perf_counter()
+            deadline = time.time() + budget_s
+            jobs = [(m.sri, m.causal, N, d, seeds, order[p::procs], deadline) for p in range(procs)]
+            res = pool.map(_oracle_worker, jobs)
+            dt = time.perf_counter() - t0
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+    flops = sum(r[0] for r in res)
+    tiles = sum(r[1] for r in res)
+    return flops / dt / 1e12, {"cores": procs, "seconds": dt, "row_tiles": tiles,
+                               "sample": f"fp64 NumPy oracle in {procs} processes (1 BLAS thread each), forward + "
+                                         f"backward of {tiles} random 128-row tiles of one (batch, head) of the "
+                                         f"{m.family} mask, N={N}, d={d}, {budget_s:.0f} s budget"}
+
+
+# ----------------------------------------------------------------------------- timing
+class Runner:
+    """Inputs, outputs and workspaces of one workload on this rank; `step()` = the whole hot path
+    over every call (fwd + bwd through the C ABI)."""
+
+    def __init__(self, fm, calls, dev):
+        self.fm, self.calls, self.dev = fm, calls, dev
+        self.inputs = [make_inputs(c, dev) for c in calls]
+        fl = [effective_flops(c, fm) for c in calls]
+        self.F_fwd = sum(f[0] for f in fl)
+        self.F_bwd = sum(f[1] for f in fl)
+        self.rhos = [r for f in fl for r in f[2]]
+        self.visited = {k: (sum(f[3][k] for f in fl) if isinstance(fl[0][3][k], int) else fl[0][3][k])
+                        for k in fl[0][3]}
+        self.ws_f, self.ws_b, self.outs = [], [], []
+        for c, x in zip(calls, self.inputs):
+            p = fm.make_params(c["B"], c["N"], len(c["heads"]), c["d"], x["sri"], c["causal"])
+            self.ws_f.append(torch.empty(fm.flashmask_workspace_size(p, fm.FM_PASS_FWD), dtype=torch.uint8, device=dev))
+            self.ws_b.append(torch.empty(fm.flashmask_workspace_size(p, fm.FM_PASS_BWD), dtype=torch.uint8, device=dev))
+            lse = torch.empty(c["B"], len(c["heads"]), c["N"], dtype=torch.float32, device=dev)
+            self.outs.append((torch.empty_like(x["q"]), lse, torch.empty_like(x["q"]), torch.empty_like(x["q"]),
+                              torch.empty_like(x["q"])))
+
+    def step(self):
+        fm = self.fm
+        for c, x, wf, wb, (o, lse, dq, dk, dv) in zip(self.calls, self.inputs, self.ws_f, self.ws_b, self.outs):
+            fm.flashmask_fwd(x["q"], x["k"], x["v"], x["sri"], c["causal"], out=o, lse=lse, workspace=wf)
+            fm.flashmask_bwd(x["q"], x["k"], x["v"], o, x["do"], lse, x["sri"], c["causal"], dq=dq, dk=dk, dv=dv,
+                             workspace=wb)
+
+    def checksums(self):
+        """fp64 sums of the last step's O, finite lse, dQ, dK, dV (cross-rank bookkeeping)."""
+        s = [0.0] * 5
+        for o, lse, dq, dk, dv in self.outs:
+            s[0] += o.double().sum().item()
+            s[1] += lse[torch.isfinite(lse)].double().sum().item()
+            s[2] += dq.double().sum().item()
+            s[3] += dk.double().sum().item()
+            s[4] += dv.double().sum().item()
+        return s
+
+    def free(self):
+        self.inputs = self.outs = self.ws_f = self.ws_b = None
+
+
+def timed_steps(runner, steps, stream, kernels):
+    """K steps between CUDA events on the launch stream, library per-kernel events on `kernels`."""
+    fm = runner.fm
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    fm.flashmask_timing_enable(True, kernels=kernels)
+    torch.cuda.synchronize()
+    ev0.record(stream)
+    for _ in range(steps):
+        runner.step()
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    fm.flashmask_timing_enable(False)
+    return ev0.elapsed_time(ev1), fm.flashmask_timing_collect()
+
+
+def sweep_cells(mode):
+    """The compact Figure-1 sweep of the bench line: C2, C4, and C5 at 8K / 128K,
+    d = 64 / 128, for causal-document, sliding window, QK-sparse and random eviction."""
+    if mode == "none":
+        return []
+    fams = "causal_document,sliding_window,qk_sparse,random_eviction"
+    cells = ["C2", "C4"] + [f"C5:{n}:{d}:{fams}" for n in (8192, 131072) for d in (64, 128)]
+    if mode == "full":
+        cells += [f"C5:{n}:{d}" for n in (8192, 32768, 131072) for d in (64, 128)]
+    return cells
+
+
+def run_sweep(fm, cells, dev, stream, peak, rank, world, dist, steps=3, warmup=2):
+    out = []
+    for cfg in cells:
+        calls, conf, _ = build_workload(cfg, rank, world, rho_gpu(fm))
+        for c in calls:
+            r = Runner(fm, [c], dev)
+            for _ in range(warmup):
+                r.step()
+            clocks = ClockSampler(dev.index)
+            clocks.start()
+            ms, kt = timed_steps(r, steps, stream, [fm.FM_KERNEL_FWD, fm.FM_KERNEL_BWD])
+            clk = clocks.stop()
+            ms = reduce_max_over_ranks(ms / steps, dist, dev)
+            fwd_ms = reduce_max_over_ranks(kt["fwd"][0] / steps, dist, dev)
+            bwd_ms = reduce_max_over_ranks(kt["bwd"][0] / steps, dist, dev)
+            tot = world * (r.F_fwd + r.F_bwd) / (ms * 1e-3) / 1e12
+            out.append({"config": cfg.split(":")[0] + (":" + ":".join(cfg.split(":")[1:3]) if ":" in cfg else ""),
+                        "mask": c.get("family", c["masks"][0].family),
+                        "N": c["N"], "d": c["d"], "B": c["B"], "H": c["H"],
+                        "rho": round(statistics.mean(r.rhos), 4),
+                        "total_tflops": round(tot, 1), "pct_peak": round(100 * tot / world / peak, 1),
+                        "fwd_tflops": round(world * r.F_fwd / (fwd_ms * 1e-3) / 1e12, 1),
+                        "bwd_tflops": round(world * r.F_bwd / (bwd_ms * 1e-3) / 1e12, 1),
+                        "ms_per_step": round(ms, 3),
+                        "clocks": {"sm_mhz": clk and clk["sm_mhz"], "reasons": clk and clk["reasons"]}})
+            r.free()
+            del r
+            torch.cuda.empty_cache()
+    return out
+
+
+def k1_microbench(fm, dev, peak_hbm, reps=20):
+    """K1 on per-head masks (SURVEY d.4: Hm = 64, N = 128K, C = 4 -> 134 MB of
+    startend_row_indices): algorithmic bytes / mean CUDA-event time per kernel."""
+    N, Hm = 131072, 64
+    ms = [wm.sample_family("global_sliding_window", N, np.random.default_rng(Hm + N + h), (11, 15)) for h in range(Hm)]
+    sri = torch.from_numpy(np.stack([m.sri for m in ms])[None]).to(dev)
+    C = ms[0].C
+    for _ in range(3):
+        fm.flashmask_classify(sri, ms[0].causal)
+    torch.cuda.synchronize()
+    fm.flashmask_timing_enable(True)
+    for _ in range(reps):
+        fm.flashmask_classify(sri, ms[0].causal)
+    torch.cuda.synchronize()
+    fm.flashmask_timing_enable(False)
+    t = fm.flashmask_timing_collect()
+    T = N // 128
+    b_exp = Hm * N * C * 4 + Hm * T * 32          # read the vectors, write the extrema
+    b_cls = Hm * T * 32 + Hm * T * T + Hm * 24    # read the extrema, write the u8 map + counts
+    res = {}
+    for name, key, b in (("K1a_expand", "expand", b_exp), ("K1b_classify", "classify", b_cls)):
+        us = t[key][0] / reps * 1e3
+        gbs = b / (us * 1e-6) / 1e9
+        res[name] = {"us": round(us, 2), "bytes": b, "GB/s": round(gbs, 1), "frac": round(gbs / peak_hbm, 3)}
+    del sri
+    return {"workload": "global+sliding-window masks, one per head: B=1, Hm=64, N=131072, C=4", **res}
 
 
 # ----------------------------------------------------------------------------- main
@@ -284,18 +514,22 @@ def main():
     ap.add_argument("--impl", default="flashmask", choices=["flashmask", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=12.0)
+    ap.add_argument("--sweep", default="auto", choices=["auto", "none", "full"],
+                    help="Figure-1 sweep sub-record: auto = the compact sweep at N=1 only")
     ap.add_argument("--time-kernels", default="main", choices=["main", "all"],
                     help="kernels bracketed by CUDA events inside the timed region: main = K2 and K4 only "
                          "(events between kernels remove programmatic-dependent-launch overlap), all = every kernel")
     args = ap.parse_args()
 
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1 and args.impl == "flashmask":
+        sys.exit(self_launch(args))
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    assert world == args.gpus or world == 1, "launch with torchrun --nproc-per-node N for --gpus N"
-
     if args.impl == "reference":
         return run_reference(args, rank, world)
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}: launch one rank per GPU")
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
@@ -307,28 +541,8 @@ def main():
     from paper_2410_01359_b200 import flashmask as fm
 
     calls, conf, scaling = build_workload(args.config, rank, world, rho_gpu(fm))
-    inputs = [make_inputs(c, dev) for c in calls]
-    fl = [effective_flops(c, fm) for c in calls]
-    F_fwd = sum(f[0] for f in fl)
-    F_bwd = sum(f[1] for f in fl)
-    rhos = [r for f in fl for r in f[2]]
-    ws_f = [None] * len(calls)
-    ws_b = [None] * len(calls)
-    outs = [None] * len(calls)
-
-    def step():
-        for ci, (c, x) in enumerate(zip(calls, inputs)):
-            if ws_f[ci] is None:
-                p = fm.make_params(c["B"], c["N"], len(c["heads"]), c["d"], x["sri"], c["causal"])
-                ws_f[ci] = torch.empty(fm.flashmask_workspace_size(p, fm.FM_PASS_FWD), dtype=torch.uint8, device=dev)
-                ws_b[ci] = torch.empty(fm.flashmask_workspace_size(p, fm.FM_PASS_BWD), dtype=torch.uint8, device=dev)
-                o = torch.empty_like(x["q"])
-                lse = torch.empty(c["B"], len(c["heads"]), c["N"], dtype=torch.float32, device=dev)
-                outs[ci] = (o, lse, torch.empty_like(x["q"]), torch.empty_like(x["q"]), torch.empty_like(x["q"]))
-            o, lse, dq, dk, dv = outs[ci]
-            fm.flashmask_fwd(x["q"], x["k"], x["v"], x["sri"], c["causal"], out=o, lse=lse, workspace=ws_f[ci])
-            fm.flashmask_bwd(x["q"], x["k"], x["v"], o, x["do"], lse, x["sri"], c["causal"], dq=dq, dk=dk, dv=dv,
-                             workspace=ws_b[ci])
+    run = Runner(fm, calls, dev)
+    stream = torch.cuda.current_stream()
 
     def barrier():
         if dist is not None:
@@ -339,167 +553,127 @@ def main():
         return reduce_max_over_ranks(x, dist, dev)
 
     for _ in range(args.warmup):
-        step()
+        run.step()
     barrier()
 
     # ---------------- device-timed region ----------------
     clocks = ClockSampler(local)
     clocks.start()
-    stream = torch.cuda.current_stream()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    main_kernels = [fm.FM_KERNEL_FWD, fm.FM_KERNEL_BWD]
-    fm.flashmask_timing_enable(True, kernels=None if args.time_kernels == "all" else main_kernels)
     barrier()
-    ev0.record(stream)
-    for _ in range(args.steps):
-        step()
-    ev1.record(stream)
-    torch.cuda.synchronize()
-    fm.flashmask_timing_enable(False)
-    ktimes = fm.flashmask_timing_collect()
+    main_kernels = None if args.time_kernels == "all" else [fm.FM_KERNEL_FWD, fm.FM_KERNEL_BWD]
+    ms_total, ktimes = timed_steps(run, args.steps, stream, main_kernels)
     barrier()
     clk = clocks.stop()
-    ms_total = ev0.elapsed_time(ev1)
-    ms_step = max_over_ranks(ms_total / args.steps)
-    # kernel split of the small kernels (K1, K3, K5) and the launch count: one extra untimed-for-
-    # value step with every kernel bracketed
+    ms_step_local = ms_total / args.steps
+    ms_step = max_over_ranks(ms_step_local)
+    # kernel split of the small kernels (K1, K3, K5) and the launch count: one extra step with
+    # every kernel bracketed (not part of the timed value)
     fm.flashmask_timing_enable(True)
-    step()
+    run.step()
     torch.cuda.synchronize()
     fm.flashmask_timing_enable(False)
     ksplit = fm.flashmask_timing_collect()
     launches_per_step = int(sum(n for _, n in ksplit.values()))
+    checks = run.checksums()
+    rhos, visited = run.rhos, run.visited
 
     # ---------------- end-to-end through host buffers ----------------
     e2e = None
+    e2e_ms_local = 0.0
     if not args.no_e2e:
-        # End to end through the public API from pinned host buffers: every step copies the
-        # inputs in and dq/dk/dv out.  The step is split into one call per (batch entry, group of
-        # HG heads) — attention heads are independent — so the copies of chunk c+1 (H2D) and c-1
-        # (D2H) overlap the kernels of chunk c on 3 streams and pipeline fill/drain is short.  The
-        # host buffers hold each chunk contiguously ([1, N, HG, d]), chosen at setup.
-        chunks = []
-        for ci, (c, x) in enumerate(zip(calls, inputs)):
-            H = len(c["heads"])
-            HG = int(os.environ.get("FM_E2E_HEADS", "8"))
-            HG = HG if H % HG == 0 else H
-            for bi in range(c["B"]):
-                for h0 in range(0, H, HG):
-                    hx = {k: (v[bi:bi + 1, :, h0:h0 + HG] if k != "sri" else v[bi:bi + 1]).contiguous().cpu()
-                          .pin_memory() for k, v in x.items()}
-                    dx = {k: torch.empty(t.shape, dtype=t.dtype, device=dev) for k, t in hx.items()}
-                    do_ = (torch.empty_like(dx["q"]), torch.empty(1, HG, c["N"], dtype=torch.float32, device=dev),
-                           torch.empty_like(dx["q"]), torch.empty_like(dx["k"]), torch.empty_like(dx["v"]))
-                    ho = tuple(torch.empty(t.shape, dtype=t.dtype).pin_memory() for t in do_[2:])
-                    chunks.append((c, hx, dx, do_, ho))
-        wsf = torch.empty(max(w.numel() for w in ws_f), dtype=torch.uint8, device=dev)
-        wsb = torch.empty(max(w.numel() for w in ws_b), dtype=torch.uint8, device=dev)
-        h2d = sum(t.numel() * t.element_size() for ch in chunks for t in ch[1].values())
-        d2h = sum(t.numel() * t.element_size() for ch in chunks for t in ch[4])
-        s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
+        e2e, e2e_ms_local = run_e2e(fm, run, dev, stream, args.steps, barrier, max_over_ranks, world)
 
-        # Consecutive steps pipeline like a training loop that prefetches its next batch: step
-        # k+1's H2D of chunk c waits only for step k's kernels of chunk c (its device input
-        # buffers), and its kernels of chunk c for step k's D2H of chunk c (its output buffers).
-        done = [None] * len(chunks)  # per chunk: kernels of the last step finished
-        out = [None] * len(chunks)   # per chunk: D2H of the last step finished
-
-        def e2e_step():
-            ev_in = []
-            for i, (c, hx, dx, _, _) in enumerate(chunks):
-                with torch.cuda.stream(s_in):
-                    if done[i] is not None:
-                        s_in.wait_event(done[i])
-                    for k, v in hx.items():
-                        dx[k].copy_(v, non_blocking=True)
-                    e = torch.cuda.Event()
-                    e.record(s_in)
-                    ev_in.append(e)
-            for i, ((c, hx, dx, do_, ho), e) in enumerate(zip(chunks, ev_in)):
-                stream.wait_event(e)
-                if out[i] is not None:
-                    stream.wait_event(out[i])
-                o, lse, dq, dk, dv = do_
-                fm.flashmask_fwd(dx["q"], dx["k"], dx["v"], dx["sri"], c["causal"], out=o, lse=lse, workspace=wsf)
-                fm.flashmask_bwd(dx["q"], dx["k"], dx["v"], o, dx["do"], lse, dx["sri"], c["causal"], dq=dq, dk=dk,
-                                 dv=dv, workspace=wsb)
-                done[i] = torch.cuda.Event()
-                done[i].record(stream)
-                with torch.cuda.stream(s_out):
-                    s_out.wait_event(done[i])
-                    for hdst, dsrc in zip(ho, (dq, dk, dv)):
-                        hdst.copy_(dsrc, non_blocking=True)
-                    out[i] = torch.cuda.Event()
-                    out[i].record(s_out)
-
-        def e2e_drain():  # every D2H issued so far has landed in host memory
-            for ev in out:
-                stream.wait_event(ev)
-
-        e2e_step()
-        e2e_drain()
-        torch.cuda.synchronize()
-        barrier()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        s_in.wait_event(e0)
-        s_out.wait_event(e0)
-        n_e2e = max(1, min(args.steps, 5))
-        for _ in range(n_e2e):
-            e2e_step()
-        e2e_drain()
-        e1.record(stream)
-        torch.cuda.synchronize()
-        e2e_ms = max_over_ranks(e0.elapsed_time(e1) / n_e2e)
-        e2e = {"value": round(world * (F_fwd + F_bwd) / (e2e_ms * 1e-3) / 1e12, 2), "unit": "TFLOP/s",
-               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": round(e2e_ms, 3),
-               "pipeline": f"one call per (batch entry, {HG}-head group), H2D / kernels / D2H on 3 streams; "
-                           "host buffers chunk-contiguous; step k+1's copies overlap step k's kernels (prefetch)"}
+    # ---------------- gather per-rank results (NCCL) ----------------
+    k_bwd_ms, _ = ktimes["bwd"]
+    k_fwd_ms, _ = ktimes["fwd"]
+    per_rank = gather_ranks([ms_step_local, k_fwd_ms / args.steps, k_bwd_ms / args.steps, run.F_fwd, run.F_bwd,
+                             e2e_ms_local] + checks, dist, dev)
+    F_all = sum(r[3] + r[4] for r in per_rank)
+    F_fwd_all = sum(r[3] for r in per_rank)
+    F_bwd_all = sum(r[4] for r in per_rank)
+    fwd_ms_max = max(r[1] for r in per_rank)
+    bwd_ms_max = max(r[2] for r in per_rank)
 
     # ---------------- report ----------------
-    value = world * (F_fwd + F_bwd) / (ms_step * 1e-3) / 1e12
+    value = F_all / (ms_step * 1e-3) / 1e12
     peaks, peak_src = load_peaks()
     peak_sust = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
+    peak_hbm = peaks.get("hbm_gbs", FALLBACK_PEAKS["hbm_gbs"])
     traffic = None
     tpath = os.path.join(ROOT, "profiles", f"traffic_{args.config}.json")
     if os.path.exists(tpath):
-        traffic = json.load(open(tpath)).get("fm_bwd_kernel_bytes_per_launch")
-    k_bwd_ms, k_bwd_n = ktimes["bwd"]
-    k_fwd_ms, k_fwd_n = ktimes["fwd"]
-    bwd_tf = F_bwd * args.steps / (k_bwd_ms * 1e-3) / 1e12 if k_bwd_ms > 0 else None
-    fwd_tf = F_fwd * args.steps / (k_fwd_ms * 1e-3) / 1e12 if k_fwd_ms > 0 else None
+        traffic = json.load(open(tpath))
+    bwd_tf = F_bwd_all / (bwd_ms_max * 1e-3) / 1e12 if bwd_ms_max > 0 else None
+    fwd_tf = F_fwd_all / (fwd_ms_max * 1e-3) / 1e12 if fwd_ms_max > 0 else None
     launches = launches_per_step * args.steps
 
+    sweep, k1 = None, None
+    cells = sweep_cells(args.sweep) if (args.sweep != "auto" or world == 1) else []
+    if cells:
+        run.free()
+        del run
+        torch.cuda.empty_cache()
+        sweep = run_sweep(fm, cells, dev, stream, peak_sust, rank, world, dist)
+        k1 = k1_microbench(fm, dev, peak_hbm)
+
     cpu = None
-    if rank == 0 and world == 1:
+    if rank == 0:
         rate, info = oracle_sample_rate(calls[0], args.cpu_budget)
         cpu = {"value": round(rate, 6), "unit": "TFLOP/s", "cores": info["cores"], "kind": "oracle",
                "sample": info["sample"], "seconds": round(info["seconds"], 2)}
 
     if rank == 0:
+        def kms(k):
+            return round((ktimes[k][0] / args.steps) if ktimes[k][1] else ksplit[k][0], 4)
+
+        def tb_s(bytes_, ms):
+            return round(bytes_ / (ms * 1e-3) / 1e12, 3) if ms else None
+
+        c0 = calls[0]
+        nh = len(c0["heads"])
+        rows_rank = sum(c["B"] * c["N"] * len(c["heads"]) for c in calls)
+        d = c0["d"]
+        k3_bytes = rows_rank * (2 * 2 * d + 4 + 4 + 4 * d + 4)     # read O, dO, lse; write D, lse2, zero dQacc
+        k5_bytes = rows_rank * (4 * d + 2 * d)                     # read dQacc, write bf16 dQ
+        rooflines = [
+            {"kernel": "fm_bwd_kernel (K4)", "bound": "tensor", "achieved": round(bwd_tf, 2) if bwd_tf else None,
+             "peak": peak_sust, "unit": "TFLOP/s", "frac": round(bwd_tf / peak_sust, 4) if bwd_tf else None,
+             "traffic": traffic and traffic.get("fm_bwd_kernel_bytes_per_launch"),
+             "algorithmic": "10*128^2*d FLOPs per non-SKIP 128x128 tile (SURVEY d.5)"},
+            {"kernel": "fm_fwd_kernel (K2)", "bound": "tensor", "achieved": round(fwd_tf, 2) if fwd_tf else None,
+             "peak": peak_sust, "unit": "TFLOP/s", "frac": round(fwd_tf / peak_sust, 4) if fwd_tf else None,
+             "traffic": traffic and traffic.get("fm_fwd_kernel_bytes_per_launch"),
+             "algorithmic": "4*128^2*d FLOPs per non-SKIP 128x128 tile (SURVEY d.5)"},
+            {"kernel": "k3_bwd_pre (K3)", "bound": "hbm", "achieved_TB/s": tb_s(k3_bytes, ksplit["bwd_pre"][0]),
+             "peak_TB/s": round(peak_hbm / 1e3, 3), "algorithmic_bytes": k3_bytes},
+            {"kernel": "k5_dq_convert (K5)", "bound": "hbm", "achieved_TB/s": tb_s(k5_bytes, ksplit["dq_convert"][0]),
+             "peak_TB/s": round(peak_hbm / 1e3, 3), "algorithmic_bytes": k5_bytes},
+        ]
         line = {
-            "metric": "effective fwd+bwd TFLOPs/s (skipped tiles excluded) and % of B200 bf16 peak",
+            "metric": METRIC,
             "value": round(value, 2), "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms_step, 3), "higher_is_better": True,
             "scaling": scaling, "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded N(0,1) "
-            "q/k/v/dO, generated masks)", "config": conf,
+            "q/k/v/dO per head, generated masks)", "config": conf,
             "pct_of_peak": round(100.0 * value / world / peak_sust, 2), "peak_tflops": peak_sust,
             "peak_source": f"{peak_src} bf16_tflops_sustained",
-            "tokens_per_s": round(world * sum(c["B"] * c["N"] for c in calls) / (ms_step * 1e-3), 1),
+            "tokens_per_s": round(sum(c["B"] * c["N"] for c in calls) / (ms_step * 1e-3), 1),
             "fwd_tflops_kernel": round(fwd_tf, 2) if fwd_tf else None,
             "bwd_tflops_kernel": round(bwd_tf, 2) if bwd_tf else None,
             "block_sparsity_128": [round(r, 4) for r in rhos],
-            "kernels_ms_per_step": {k: round((ktimes[k][0] / args.steps) if ktimes[k][1] else v[0], 4)
-                                    for k, v in ksplit.items()},
+            "kernels_ms_per_step": {k: kms(k) for k in ksplit},
             "kernel_timing": "fwd/bwd: CUDA events on the launch stream inside the timed region; others: one "
                              "extra step with every kernel bracketed" if args.time_kernels == "main" else
                              "every kernel bracketed inside the timed region",
-            "roofline": {"kernel": "fm_bwd_kernel (K4)", "bound": "tensor",
-                         "achieved": round(bwd_tf, 2) if bwd_tf else None, "peak": peak_sust, "unit": "TFLOP/s",
-                         "frac": round(bwd_tf / peak_sust, 4) if bwd_tf else None, "traffic": traffic,
-                         "traffic_unit": "bytes per launch (dram read+write, ncu --set full)",
-                         "algorithmic": "10*128^2*d FLOPs per non-SKIP 128x128 tile (SURVEY d.5)"},
-            "e2e": e2e, "gpu_launches": launches, "clocks": clk, "cpu_baseline": cpu,
+            "visited_tiles_per_step_rank0": visited,
+            "roofline": rooflines[0], "rooflines": rooflines, "k1_microbench": k1,
+            "per_rank": [{"rank": i, "ms_per_step": round(r[0], 3), "fwd_ms": round(r[1], 3), "bwd_ms": round(r[2], 3),
+                          "eff_tflop": round((r[3] + r[4]) / 1e12, 3), "e2e_ms": round(r[5], 3),
+                          "checksum": {"o": r[6], "lse": r[7], "dq": r[8], "dk": r[9], "dv": r[10]}}
+                         for i, r in enumerate(per_rank)],
+            "collectives": "NCCL all_gather of per-rank results after the timed region; no data-path collective"
+                           if world > 1 else "none (1 GPU)",
+            "e2e": e2e, "gpu_launches": launches, "clocks": clk, "cpu_baseline": cpu, "sweep": sweep,
         }
         print(json.dumps(line), flush=True)
     if dist is not None:
@@ -507,26 +681,115 @@ def main():
         dist.destroy_process_group()
 
 
+def run_e2e(fm, run, dev, stream, steps, barrier, max_over_ranks, world):
+    """End to end through the public API from pinned host buffers: every step copies the inputs
+    in and dq/dk/dv out.  The step is split into one call per (batch entry, group of HG heads) —
+    attention heads are independent — so the copies of chunk c+1 (H2D) and c-1 (D2H) overlap
+    the kernels of chunk c on 3 streams.  Consecutive steps pipeline like a training loop that
+    prefetches its next batch: step k+1's H2D of chunk c waits only for step k's kernels of chunk
+    c, its kernels of chunk c for step k's D2H of chunk c.  Returns (e2e dict, local ms/step)."""
+    chunks = []
+    HG = 8
+    for ci, (c, x) in enumerate(zip(run.calls, run.inputs)):
+        H = len(c["heads"])
+        HG = int(os.environ.get("FM_E2E_HEADS", "8"))
+        HG = HG if H % HG == 0 else H
+        for bi in range(c["B"]):
+            for h0 in range(0, H, HG):
+                hx = {k: (v[bi:bi + 1, :, h0:h0 + HG] if k != "sri" else v[bi:bi + 1]).contiguous().cpu()
+                      .pin_memory() for k, v in x.items()}
+                dx = {k: torch.empty(t.shape, dtype=t.dtype, device=dev) for k, t in hx.items()}
+                do_ = (torch.empty_like(dx["q"]), torch.empty(1, HG, c["N"], dtype=torch.float32, device=dev),
+                       torch.empty_like(dx["q"]), torch.empty_like(dx["k"]), torch.empty_like(dx["v"]))
+                ho = tuple(torch.empty(t.shape, dtype=t.dtype).pin_memory() for t in do_[2:])
+                chunks.append((c, hx, dx, do_, ho))
+    wsf = torch.empty(max(w.numel() for w in run.ws_f), dtype=torch.uint8, device=dev)
+    wsb = torch.empty(max(w.numel() for w in run.ws_b), dtype=torch.uint8, device=dev)
+    h2d = sum(t.numel() * t.element_size() for ch in chunks for t in ch[1].values())
+    d2h = sum(t.numel() * t.element_size() for ch in chunks for t in ch[4])
+    s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
+    done = [None] * len(chunks)
+    out = [None] * len(chunks)
+
+    def e2e_step():
+        ev_in = []
+        for i, (c, hx, dx, _, _) in enumerate(chunks):
+            with torch.cuda.stream(s_in):
+                if done[i] is not None:
+                    s_in.wait_event(done[i])
+                for k, v in hx.items():
+                    dx[k].copy_(v, non_blocking=True)
+                e = torch.cuda.Event()
+                e.record(s_in)
+                ev_in.append(e)
+        for i, ((c, hx, dx, do_, ho), e) in enumerate(zip(chunks, ev_in)):
+            stream.wait_event(e)
+            if out[i] is not None:
+                stream.wait_event(out[i])
+            o, lse, dq, dk, dv = do_
+            fm.flashmask_fwd(dx["q"], dx["k"], dx["v"], dx["sri"], c["causal"], out=o, lse=lse, workspace=wsf)
+            fm.flashmask_bwd(dx["q"], dx["k"], dx["v"], o, dx["do"], lse, dx["sri"], c["causal"], dq=dq, dk=dk,
+                             dv=dv, workspace=wsb)
+            done[i] = torch.cuda.Event()
+            done[i].record(stream)
+            with torch.cuda.stream(s_out):
+                s_out.wait_event(done[i])
+                for hdst, dsrc in zip(ho, (dq, dk, dv)):
+                    hdst.copy_(dsrc, non_blocking=True)
+                out[i] = torch.cuda.Event()
+                out[i].record(s_out)
+
+    def e2e_drain():
+        for ev in out:
+            stream.wait_event(ev)
+
+    e2e_step()
+    e2e_drain()
+    torch.cuda.synchronize()
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    s_in.wait_event(e0)
+    s_out.wait_event(e0)
+    n_e2e = max(1, min(steps, 5))
+    for _ in range(n_e2e):
+        e2e_step()
+    e2e_drain()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    local_ms = e0.elapsed_time(e1) / n_e2e
+    e2e_ms = max_over_ranks(local_ms)
+    F = run.F_fwd + run.F_bwd
+    e2e = {"value": round(world * F / (e2e_ms * 1e-3) / 1e12, 2), "unit": "TFLOP/s",
+           "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": round(e2e_ms, 3),
+           "pipeline": f"one call per (batch entry, {HG}-head group), H2D / kernels / D2H on 3 streams; "
+                       "host buffers chunk-contiguous; step k+1's copies overlap step k's kernels (prefetch)"}
+    del chunks, wsf, wsb
+    torch.cuda.empty_cache()
+    return e2e, local_ms
+
+
 def run_reference(args, rank, world):
-    """--impl reference: the fp64 oracle as it stands on the host cores, same metric/unit."""
+    """--impl reference: the fp64 oracle as it stands on the host cores, same metric/unit.  Under
+    torchrun (N > 1) rank 0 alone runs and prints; the other ranks exit without work."""
     if rank != 0:
         return
     # same workload (same seeds) as the CUDA arm; buckets picked with the oracle's own
     # classification, which is bit-exact with K1 (tests/test_gpu_parity.py)
-    calls, conf, _ = build_workload(args.config, 0, 1, rho_oracle)
+    calls, conf, scaling = build_workload(args.config, 0, 1, rho_oracle)
     flat = [dict(c, masks=[m]) for c in calls for m in c["masks"]]
     rates = []
     info = None
-    per_step = max(0.5, min(6.0, 150.0 / max(1, args.steps + args.warmup)))
+    per_step = max(1.0, min(8.0, 150.0 / max(1, args.steps + args.warmup)))
     for s in range(args.warmup + args.steps):
         r, info = oracle_sample_rate(flat[s % len(flat)], per_step)
         if s >= args.warmup:
             rates.append(r)
     value = statistics.mean(rates)
     ms_step = per_step * 1e3
-    line = {"impl": "reference", "metric": "effective fwd+bwd TFLOPs/s (skipped tiles excluded) and % of B200 bf16 peak",
+    line = {"impl": "reference", "metric": METRIC,
             "value": round(value, 6), "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": round(ms_step, 1), "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": round(ms_step, 1), "higher_is_better": True, "scaling": scaling,
             "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": conf,
             "cpu_baseline": {"value": round(value, 6), "unit": "TFLOP/s", "cores": info["cores"], "kind": "oracle",
                              "sample": info["sample"] + f"; {per_step:.1f} s per step"},

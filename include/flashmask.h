@@ -91,7 +91,8 @@ typedef struct {
   int64_t seqlen;      /* 1 <= N <= 262144 (queries = keys); larger: UNSUPPORTED     */
   int64_t num_heads;   /* H >= 1                                                    */
   int64_t head_dim;    /* d in {64, 128}                                            */
-  int64_t mask_heads;  /* 1 (one mask per batch entry, broadcast) or num_kv_heads   */
+  int64_t mask_heads;  /* 1 (one mask per batch entry, broadcast) or num_kv_heads;
+                        * batch * mask_heads <= 65535, else FM_ERR_UNSUPPORTED    */
   int64_t mask_cols;   /* C in {1, 2, 4}; must match `causal` per the table above   */
   int32_t causal;      /* 0 or 1                                                    */
   float   scale;       /* softmax scale; <= 0 means 1/sqrt(head_dim) (Eq. 1)        */
@@ -141,7 +142,11 @@ FM_API fm_status flashmask_fwd(const fm_params* p, const void* q, const void* k,
  * ([B, N, H, d], out_dtype).  o and lse must come from flashmask_fwd on the same inputs
  * (o in out_dtype).  dK/dV are accumulated per key tile on chip and written once
  * (column-parallel); dQ is reduced in fp32 in the workspace and
- * converted at the end.  Skipping and masking rules are those of the forward. */
+ * converted at the end.  Skipping and masking rules are those of the forward.
+ * Determinism: by DEFAULT the dQ partial sums of the key tiles are added by fp32 hardware
+ * reduce-adds in completion order, so dq may differ in the last bits from run to run (dk, dv
+ * are always bitwise reproducible).  This deviates from SPEC S:305's ascending-j order on
+ * purpose (speed; R25); set FM_FLAG_DETERMINISTIC for bitwise-reproducible dq. */
 FM_API fm_status flashmask_bwd(const fm_params* p, const void* q, const void* k, const void* v, const void* o,
                         const void* dout, const float* lse, const int32_t* startend_row_indices,
                         void* dq, void* dk, void* dv, void* workspace, size_t workspace_bytes, void* stream);

@@ -100,6 +100,9 @@ fm_status check_params(const fm_params* p, fm::Dims* d, bool need_attention) {
     return fail(FM_ERR_INVALID_ARGUMENT, "num_kv_heads must divide num_heads");
   if (p->mask_heads != 1 && p->mask_heads != hkv)
     return fail(FM_ERR_INVALID_ARGUMENT, "mask_heads must be 1 or num_kv_heads");
+  // K1 puts (batch, mask head) pairs in one grid dimension (limit 65535)
+  if (p->batch * p->mask_heads > 65535)
+    return fail(FM_ERR_UNSUPPORTED, "batch * mask_heads > 65535");
   const int C = static_cast<int>(p->mask_cols);
   const bool ok_c = p->causal ? (C == 1 || C == 2) : (C == 2 || C == 4);
   if ((p->causal != 0 && p->causal != 1) || !ok_c)

@@ -249,6 +249,8 @@ __global__ void __launch_bounds__(bwd::NT, 1)
   {
     const uint8_t* col = a.bmap + (bhm * a.Tc + j) * a.Trb;
     int base = 0;
+    // PARTIAL bit per visit-list entry: zeroed here, set below (ordered by the loop's first barrier)
+    for (int w = tid; w < C::MAXTRB / 32; w += NT) sm.part_bits[w] = 0u;
     for (int i0 = 0; i0 < a.Trb; i0 += NT) {
       const int i = i0 + tid;
       const uint32_t c = (i < a.Trb) ? col[i] : 0u;
@@ -266,7 +268,6 @@ __global__ void __launch_bounds__(bwd::NT, 1)
       if (vis) {
         sm.list[off] = static_cast<uint16_t>(i);
         if (c == 1u) atomicOr(&sm.part_bits[off >> 5], 1u << (off & 31));
-        else atomicAnd(&sm.part_bits[off >> 5], ~(1u << (off & 31)));
       }
       base += tot;
       __syncthreads();

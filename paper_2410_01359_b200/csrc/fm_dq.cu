@@ -77,6 +77,8 @@ __global__ void __launch_bounds__(dqk::NT, 1)
   {
     const uint8_t* row = a.fmap + (bhm * a.Tr + i) * a.Tc;
     int base = 0;
+    // PARTIAL bit per visit-list entry: zeroed here, set below (ordered by the loop's first barrier)
+    for (int w = tid; w < kMaxTc / 32; w += NT) sm.part_bits[w] = 0u;
     for (int j0 = 0; j0 < a.Tc; j0 += NT) {
       const int j = j0 + tid;
       const uint32_t c = (j < a.Tc) ? row[j] : 0u;
@@ -94,7 +96,6 @@ __global__ void __launch_bounds__(dqk::NT, 1)
       if (vis) {
         sm.list[off] = static_cast<uint16_t>(j);
         if (c == 1u) atomicOr(&sm.part_bits[off >> 5], 1u << (off & 31));
-        else atomicAnd(&sm.part_bits[off >> 5], ~(1u << (off & 31)));
       }
       base += tot;
       __syncthreads();

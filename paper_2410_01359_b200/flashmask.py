@@ -84,10 +84,35 @@ def _ptr(t):
     return ctypes.c_void_p(0 if t is None else t.data_ptr())
 
 
-def _stream(stream):
+def _stream(stream, device=None):
+    """The caller's stream, by default the current stream of the tensors' device."""
     if stream is None:
-        stream = torch.cuda.current_stream()
+        stream = torch.cuda.current_stream(device)
     return ctypes.c_void_p(stream.cuda_stream)
+
+
+def _require(cond: bool, what: str, msg: str):
+    if not cond:
+        raise FlashMaskError(FM_ERR_INVALID_ARGUMENT, what, msg)
+
+
+def _check_tensor(t, name: str, what: str, shape, dtypes, device):
+    """The C ABI takes raw pointers to packed row-major tensors: refuse anything else here
+    (non-contiguous views, wrong dtype, wrong device) instead of letting the kernels read the
+    wrong bytes."""
+    _require(isinstance(t, torch.Tensor), what, f"{name} must be a torch.Tensor")
+    _require(t.is_cuda, what, f"{name} must be a CUDA tensor")
+    _require(t.device == device, what, f"{name} is on {t.device}, expected {device}")
+    _require(t.is_contiguous(), what, f"{name} must be contiguous (got strides {tuple(t.stride())})")
+    _require(t.dtype in dtypes, what, f"{name} has dtype {t.dtype}, expected one of {sorted(map(str, dtypes))}")
+    if shape is not None:
+        _require(tuple(t.shape) == tuple(shape), what, f"{name} has shape {tuple(t.shape)}, expected {tuple(shape)}")
+
+
+def _check_sri(sri, B, N, what, device):
+    _check_tensor(sri, "startend_row_indices", what, None, (torch.int32,), device)
+    _require(sri.dim() == 4 and sri.shape[0] == B and sri.shape[2] == N, what,
+             f"startend_row_indices must be [B={B}, Hm, N={N}, C], got {tuple(sri.shape)}")
 
 
 _DTYPES = {torch.bfloat16: FM_BF16, torch.float32: FM_FP32, torch.float16: FM_FP16}
@@ -123,7 +148,10 @@ def flashmask_classify(sri: torch.Tensor, causal: bool, br: int = 128, bc: int =
                        class_map: bool = True, stream=None):
     """Tile classification (K1).  sri: int32 cuda [B, Hm, N, C].  Returns
     (minmax int32 [B,Hm,Tc,8], class_map uint8 [B,Hm,Tr,Tc] or None, counts int64 [B,Hm,3])."""
+    _require(isinstance(sri, torch.Tensor) and sri.dim() == 4, "flashmask_classify",
+             "startend_row_indices must be a 4-D tensor [B, Hm, N, C]")
     B, Hm, N, C = sri.shape
+    _check_sri(sri, B, N, "flashmask_classify", sri.device)
     p = FmParams(batch=B, seqlen=N, num_heads=num_heads or Hm, head_dim=128, mask_heads=Hm, mask_cols=C,
                  causal=int(bool(causal)), scale=0.0, in_dtype=FM_BF16, out_dtype=FM_BF16, flags=0)
     Tr, Tc = -(-N // br), -(-N // bc)
@@ -131,8 +159,9 @@ def flashmask_classify(sri: torch.Tensor, causal: bool, br: int = 128, bc: int =
     minmax = torch.empty(B, Hm, Tc, 8, dtype=torch.int32, device=dev)
     cmap = torch.empty(B, Hm, Tr, Tc, dtype=torch.uint8, device=dev) if class_map else None
     counts = torch.empty(B, Hm, 3, dtype=torch.int64, device=dev)
-    _check(_lib.flashmask_classify(ctypes.byref(p), _ptr(sri), br, bc, _ptr(minmax), _ptr(cmap), _ptr(counts),
-                                   _stream(stream)), "flashmask_classify")
+    with torch.cuda.device(dev):
+        _check(_lib.flashmask_classify(ctypes.byref(p), _ptr(sri), br, bc, _ptr(minmax), _ptr(cmap), _ptr(counts),
+                                       _stream(stream, dev)), "flashmask_classify")
     return minmax, cmap, counts
 
 
@@ -141,13 +170,16 @@ def flashmask_sliding_window_indices(batch: int, seqlen: int, window: int, causa
     """startend_row_indices of a sliding window of `window` keys, generated on the device:
     causal -> int32 [batch, 1, seqlen, 1]; bidirectional -> int32 [batch, 1, seqlen, 2]."""
     out = torch.empty(batch, 1, seqlen, 1 if causal else 2, dtype=torch.int32, device=device)
-    _check(_lib.flashmask_sliding_window_indices(batch, seqlen, window, int(bool(causal)), _ptr(out), _stream(stream)),
-           "flashmask_sliding_window_indices")
+    with torch.cuda.device(out.device):
+        _check(_lib.flashmask_sliding_window_indices(batch, seqlen, window, int(bool(causal)), _ptr(out),
+                                                     _stream(stream, out.device)), "flashmask_sliding_window_indices")
     return out
 
 
 def _workspace(params, pass_, workspace, dev):
     need = flashmask_workspace_size(params, pass_)
+    if workspace is not None:
+        _check_tensor(workspace, "workspace", "workspace", None, (torch.uint8,), dev)
     if workspace is None or workspace.numel() < need:
         workspace = torch.empty(max(need, 256), dtype=torch.uint8, device=dev)
     return workspace, need
@@ -160,36 +192,76 @@ def _out_dtype(q, out_dtype):
     return torch.float16 if q.dtype == torch.float16 else torch.bfloat16
 
 
+def _check_qkv(q, k, v, what):
+    _require(isinstance(q, torch.Tensor) and q.dim() == 4, what, "q must be a 4-D tensor [B, N, H, d]")
+    B, N, H, d = q.shape
+    dev = q.device
+    _check_tensor(q, "q", what, None, tuple(_DTYPES), dev)
+    _require(isinstance(k, torch.Tensor) and k.dim() == 4, what, "k must be a 4-D tensor [B, N, Hkv, d]")
+    Hkv = k.shape[2]
+    _check_tensor(k, "k", what, (B, N, Hkv, d), (q.dtype,), dev)
+    _check_tensor(v, "v", what, (B, N, Hkv, d), (q.dtype,), dev)
+    return B, N, H, d, Hkv, dev
+
+
 def flashmask_fwd(q, k, v, sri, causal: bool, scale=None, out_dtype=None, flags: int = 0,
                   out=None, lse=None, workspace=None, stream=None):
-    """o, lse = FlashMask forward.  q: bf16 (tcgen05 path) or fp32 (fp32 path) cuda [B, N, H, d];
+    """o, lse = FlashMask forward.  q: bf16/fp16 (tcgen05 path) or fp32 (fp32 path) cuda [B, N, H, d];
     k/v: [B, N, Hkv, d] of the same dtype (Hkv divides H, grouped-query attention);
-    sri: int32 [B, Hm, N, C] with Hm in {1, Hkv}."""
-    B, N, H, d = q.shape
+    sri: int32 [B, Hm, N, C] with Hm in {1, Hkv}.  All tensors contiguous on one device."""
+    what = "flashmask_fwd"
+    B, N, H, d, Hkv, dev = _check_qkv(q, k, v, what)
+    _check_sri(sri, B, N, what, dev)
+    if out is not None and out_dtype is None:
+        out_dtype = out.dtype
     out_dtype = _out_dtype(q, out_dtype)
-    p = make_params(B, N, H, d, sri, causal, scale, out_dtype, flags, num_kv_heads=k.shape[2],
-                    in_dtype=_in_dtype(q))
-    o = out if out is not None else torch.empty(B, N, H, d, dtype=out_dtype, device=q.device)
-    lse = lse if lse is not None else torch.empty(B, H, N, dtype=torch.float32, device=q.device)
-    ws, need = _workspace(p, FM_PASS_FWD, workspace, q.device)
-    _check(_lib.flashmask_fwd(ctypes.byref(p), _ptr(q), _ptr(k), _ptr(v), _ptr(sri), _ptr(o), _ptr(lse), _ptr(ws),
-                              ws.numel(), _stream(stream)), "flashmask_fwd")
+    _require(out_dtype in _DTYPES, what, f"unsupported out_dtype {out_dtype}")
+    p = make_params(B, N, H, d, sri, causal, scale, out_dtype, flags, num_kv_heads=Hkv, in_dtype=_in_dtype(q))
+    if out is not None:
+        _check_tensor(out, "out", what, (B, N, H, d), (out_dtype,), dev)
+    if lse is not None:
+        _check_tensor(lse, "lse", what, (B, H, N), (torch.float32,), dev)
+    o = out if out is not None else torch.empty(B, N, H, d, dtype=out_dtype, device=dev)
+    lse = lse if lse is not None else torch.empty(B, H, N, dtype=torch.float32, device=dev)
+    with torch.cuda.device(dev):
+        ws, need = _workspace(p, FM_PASS_FWD, workspace, dev)
+        _check(_lib.flashmask_fwd(ctypes.byref(p), _ptr(q), _ptr(k), _ptr(v), _ptr(sri), _ptr(o), _ptr(lse), _ptr(ws),
+                                  ws.numel(), _stream(stream, dev)), what)
     return o, lse
 
 
 def flashmask_bwd(q, k, v, o, do, lse, sri, causal: bool, scale=None, out_dtype=None, flags: int = 0,
-                  dq=None, dk=None, dv=None, workspace=None, stream=None):
-    """dq, dk, dv = FlashMask backward (o in out_dtype, lse from flashmask_fwd); dk, dv have the
-    key/value head count of k, v."""
-    B, N, H, d = q.shape
-    Hkv = k.shape[2]
-    out_dtype = _out_dtype(q, out_dtype)
+                  dq=None, dk=None, dv=None, workspace=None, stream=None, deterministic: bool = False):
+    """dq, dk, dv = FlashMask backward.  o and lse come from flashmask_fwd on the same inputs; the
+    gradients take o's dtype (out_dtype, if given, must equal it).  dk, dv have the key/value head
+    count of k, v.  dQ is reduced with fp32 hardware reduce-adds whose order is not fixed, so dq may
+    differ in the last bits run to run; `deterministic=True` (FM_FLAG_DETERMINISTIC) computes dq
+    row-parallel in ascending key-tile order instead — bitwise reproducible, ~1.6x the backward time."""
+    what = "flashmask_bwd"
+    B, N, H, d, Hkv, dev = _check_qkv(q, k, v, what)
+    _check_sri(sri, B, N, what, dev)
+    _require(isinstance(o, torch.Tensor), what, "o must be a torch.Tensor")
+    _require(out_dtype is None or out_dtype == o.dtype, what,
+             f"out_dtype {out_dtype} differs from o.dtype {o.dtype}: the gradients take the forward output's dtype")
+    out_dtype = o.dtype
+    _require(out_dtype in (torch.float32, torch.float16 if q.dtype == torch.float16 else torch.bfloat16), what,
+             f"o has dtype {o.dtype}; expected float32 or the 16-bit type of the inputs")
+    _check_tensor(o, "o", what, (B, N, H, d), (out_dtype,), dev)
+    _check_tensor(do, "do", what, (B, N, H, d), (q.dtype,), dev)
+    _check_tensor(lse, "lse", what, (B, H, N), (torch.float32,), dev)
+    if deterministic:
+        flags |= FM_FLAG_DETERMINISTIC
     p = make_params(B, N, H, d, sri, causal, scale, out_dtype, flags, num_kv_heads=Hkv, in_dtype=_in_dtype(q))
-    mk = lambda t, h: t if t is not None else torch.empty(B, N, h, d, dtype=out_dtype, device=q.device)
+    for t, name, h in ((dq, "dq", H), (dk, "dk", Hkv), (dv, "dv", Hkv)):
+        if t is not None:
+            _check_tensor(t, name, what, (B, N, h, d), (out_dtype,), dev)
+    mk = lambda t, h: t if t is not None else torch.empty(B, N, h, d, dtype=out_dtype, device=dev)
     dq, dk, dv = mk(dq, H), mk(dk, Hkv), mk(dv, Hkv)
-    ws, need = _workspace(p, FM_PASS_BWD, workspace, q.device)
-    _check(_lib.flashmask_bwd(ctypes.byref(p), _ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(do), _ptr(lse), _ptr(sri),
-                              _ptr(dq), _ptr(dk), _ptr(dv), _ptr(ws), ws.numel(), _stream(stream)), "flashmask_bwd")
+    with torch.cuda.device(dev):
+        ws, need = _workspace(p, FM_PASS_BWD, workspace, dev)
+        _check(_lib.flashmask_bwd(ctypes.byref(p), _ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(do), _ptr(lse),
+                                  _ptr(sri), _ptr(dq), _ptr(dk), _ptr(dv), _ptr(ws), ws.numel(), _stream(stream, dev)),
+               what)
     return dq, dk, dv
 
 

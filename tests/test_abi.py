@@ -112,3 +112,24 @@ def test_product_package_never_references_the_oracle():
                 if re.search(r"^\s*(from|import)\s+oracle\b|oracle[./]", src, re.M):
                     hits.append(f)
     assert hits == []
+
+
+def test_batch_times_mask_heads_limit(lib_path):
+    """K1 grids hold B * mask_heads in one dimension: > 65535 is refused on the host."""
+    from paper_2410_01359_b200 import flashmask as fm
+    p = fm.FmParams(batch=2048, seqlen=128, num_heads=64, head_dim=128, mask_heads=64, mask_cols=1, causal=1,
+                    scale=0.0, in_dtype=0, out_dtype=0, flags=0, num_kv_heads=0)
+    assert fm._lib.flashmask_workspace_size(ctypes.byref(p), 0) == 0
+    assert b"mask_heads" in fm._lib.flashmask_last_error()
+    p.mask_heads = 1
+    assert fm._lib.flashmask_workspace_size(ctypes.byref(p), 0) > 0
+
+
+def test_binding_rejects_host_tensors(lib_path):
+    """The binding refuses non-CUDA tensors before any call (no CPU fallback exists)."""
+    import torch
+    from paper_2410_01359_b200 import flashmask as fm
+    q = torch.zeros(1, 128, 1, 128, dtype=torch.bfloat16)
+    sri = torch.full((1, 1, 128, 1), 128, dtype=torch.int32)
+    with pytest.raises(fm.FlashMaskError, match="CUDA"):
+        fm.flashmask_fwd(q, q, q, sri, True)

@@ -162,3 +162,24 @@ def test_c5_sampled_rows_and_q_zero(fm, cfg, fams):
             assert_close(f"{cfg} Q=0 dV h{h}", dv[0, :, h].cpu().numpy(), fo.dv_q_zero(_head(x, "do", 0, h), vec))
         del x, xz, o, lse, dq, dk, dv
         torch.cuda.empty_cache()
+
+
+def test_c3_generic_q_dk_dv_sampled_columns(fm):
+    """Generic-Q dK / dV at N = 32K in the C3 bench layout: dK_j, dV_j accumulate in
+    fp32 TMEM over up to 512 visited 64-row tiles, a length the small parity cases never reach.
+    64 sampled key columns of one head in the lowest- and highest-sparsity batch entries against
+    oracle.backward_cols (full forward over all rows, then the columns' gradients)."""
+    calls, _, _ = bench.build_workload("C3", 0, 1, bench.rho_oracle)
+    c = calls[0]
+    x = bench.make_inputs(c, torch.device("cuda", 0))
+    o, lse, dq, dk, dv = _run(fm, c, x, torch.float32)
+    N = c["N"]
+    rng = np.random.default_rng(5)
+    for b, h in ((0, 7), (3, 30)):
+        m = c["masks"][b]
+        vec = fo.expand(m.sri, m.causal, N)
+        keys = np.sort(rng.choice(N, 64, replace=False))
+        q, k, v, do = (_head(x, n, b, h) for n in ("q", "k", "v", "do"))
+        gk, gv = fo.backward_cols(q, k, v, do, vec, keys)
+        assert_close(f"C3 b{b} h{h} dK cols", dk[b, keys, h].cpu().numpy(), gk)
+        assert_close(f"C3 b{b} h{h} dV cols", dv[b, keys, h].cpu().numpy(), gv)

@@ -607,3 +607,74 @@ def test_sliding_window_indices(fmlib, causal):
     assert_lse(lse[0, 1].cpu().numpy(), L)
     with pytest.raises(fmlib.FlashMaskError):
         fmlib.flashmask_sliding_window_indices(1, 16, 0, causal)
+
+
+# ------------------------------------------------------------------ arbitrary int32 intervals (R10)
+INT32_CASES = [(causal, C, N, d) for causal, C in ((True, 1), (True, 2), (False, 2), (False, 4))
+               for N, d in ((333, 128), (700, 64))]
+
+
+@pytest.mark.parametrize("causal,C,N,d", INT32_CASES)
+def test_fwd_bwd_arbitrary_int32_vectors(fmlib, causal, C, N, d):
+    """R10 / flashmask.h: ANY int32 startend_row_indices has defined semantics through the
+    masked(r, y) predicate (Eq. 3): negative, > N, inverted (start >= end),
+    INT_MIN / INT_MAX.  The attention kernels (clamp + (start, length) normalisation in K1a)
+    must give the oracle's O / lse / dQ / dK / dV on such vectors, ragged N, both head dims."""
+    rng = np.random.default_rng(N * 7 + C + 100 * causal)
+    i32 = np.iinfo(np.int32)
+    raw = rng.integers(-N, 2 * N, size=(N, C)).astype(np.int64)
+    # a share of ordinary well-formed columns so most rows keep visible keys
+    ok = rng.random(N) < 0.5
+    raw[ok, 0] = rng.integers(0, N + 1, ok.sum())
+    if C >= 2:
+        raw[ok, 1] = np.maximum(raw[ok, 0], rng.integers(0, N + 1, ok.sum())) if causal or C == 4 else \
+            rng.integers(0, N + 1, ok.sum())
+    special = [i32.max, i32.min, -1, 0, N, N + 1, i32.max - 1, i32.min + 1]
+    for j in range(min(N, 40)):
+        raw[j * (N // 40), int(rng.integers(C))] = special[j % len(special)]
+    raw = raw.astype(np.int32)
+    m = wm.MaskInput(N, causal, C, raw, "arbitrary_int32")
+    sri_t, t = build_case([m], 2, d, base=N + C)
+    sri_c, tc = to_cuda(sri_t, t)
+    o, lse = fmlib.flashmask_fwd(tc["q"], tc["k"], tc["v"], sri_c, causal, out_dtype=torch.float32)
+    dq, dk, dv = fmlib.flashmask_bwd(tc["q"], tc["k"], tc["v"], o, tc["do"], lse, sri_c, causal,
+                                     out_dtype=torch.float32)
+    torch.cuda.synchronize()
+    for h in range(2):
+        O, L, (gq, gk, gv) = oracle_head(t, [m], sri_t.numpy(), 0, h, 1, causal)
+        assert_close(f"O[{h}]", o[0, :, h].cpu().numpy(), O)
+        assert_lse(lse[0, h].cpu().numpy(), L)
+        assert_close(f"dQ[{h}]", dq[0, :, h].cpu().numpy(), gq)
+        assert_close(f"dK[{h}]", dk[0, :, h].cpu().numpy(), gk)
+        assert_close(f"dV[{h}]", dv[0, :, h].cpu().numpy(), gv)
+
+
+# ------------------------------------------------------------------ binding argument checks
+def test_binding_rejects_bad_tensors(fmlib):
+    """The binding passes raw pointers to the C ABI, so it refuses what the kernels would
+    misread: non-contiguous views, non-int32 masks, mixed dtypes, and a backward whose o has a
+    different dtype than the requested gradients."""
+    N, H, d = 256, 2, 128
+    qkv = torch.randn(1, N, 3, H, d, device="cuda").to(torch.bfloat16)
+    q, k, v = qkv.unbind(2)                      # strided views
+    sri = torch.full((1, 1, N, 1), N, dtype=torch.int32, device="cuda")
+    E = fmlib.FlashMaskError
+    with pytest.raises(E, match="contiguous"):
+        fmlib.flashmask_fwd(q, k, v, sri, True)
+    q, k, v = (x.contiguous() for x in (q, k, v))
+    with pytest.raises(E, match="int32"):
+        fmlib.flashmask_fwd(q, k, v, sri.long(), True)
+    with pytest.raises(E, match="dtype"):
+        fmlib.flashmask_fwd(q, k.half(), v, sri, True)
+    o32, lse = fmlib.flashmask_fwd(q, k, v, sri, True, out_dtype=torch.float32)
+    do = torch.randn_like(q)
+    with pytest.raises(E, match="out_dtype"):
+        fmlib.flashmask_bwd(q, k, v, o32, do, lse, sri, True, out_dtype=torch.bfloat16)
+    # o.dtype decides the gradient dtype: the fp32 O of the forward gives fp32 gradients
+    dq, dk, dv = fmlib.flashmask_bwd(q, k, v, o32, do, lse, sri, True)
+    ref = fmlib.flashmask_bwd(q, k, v, o32, do, lse, sri, True, out_dtype=torch.float32)
+    torch.cuda.synchronize()
+    assert dq.dtype == torch.float32 and torch.equal(dk, ref[1]) and torch.equal(dv, ref[2])
+    with pytest.raises(E, match="shape"):
+        fmlib.flashmask_bwd(q, k, v, o32, do, lse[:, :1], sri, True)
+

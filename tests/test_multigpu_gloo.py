@@ -1,17 +1,21 @@
 """Host-side logic of the multi-GPU bench path, run as 2 CPU processes over gloo.
 
-Heads/batch entries are independent, so ranks shard them with no data-path
-collective; the only collective is the max-over-ranks of the timings.  Checks: batch shards
-(C2/C3) are disjoint and seeded per global batch index, head shards (C4) partition the heads,
-and the max reduction returns the slowest rank's time on every rank."""
+Heads are independent, so ranks shard them with no data-path collective (SURVEY
+§8(e)); after the timed region the ranks all_gather their per-rank results.  Checks: every
+config is head-sharded over ONE global problem (same masks on every rank, head ranges
+partition [0, H)), the per-rank gather returns every rank's vector in rank order, the max
+reduction returns the slowest rank's time, and --gpus N without torchrun refuses to run on
+fewer GPUs than requested."""
 import os
 import socket
+import subprocess
+import sys
 
 import numpy as np
-import pytest
-import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 def _free_port():
@@ -28,15 +32,18 @@ def _worker(rank, world, port, q):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         slowest = bench.reduce_max_over_ranks(10.0 + rank, dist, "cpu")
-        c2, conf2, sc2 = bench.build_workload("C2", rank, world, bench.rho_oracle)
-        c4, conf4, sc4 = bench.build_workload("C4", rank, world, bench.rho_oracle)
-        q.put((rank, slowest, [c["batch_ids"] for c in c2], [m.sri.copy() for m in c2[0]["masks"]],
-               list(c4[0]["heads"]), sc2, sc4, conf2["global_batch"]))
+        gathered = bench.gather_ranks([float(rank), 2.5 * rank, -1.0], dist, "cpu")
+        res = {"slowest": slowest, "gathered": gathered}
+        for cfg in ("C2", "C3", "C4", "C5:8192:64:causal_document,random_eviction"):
+            calls, conf, sc = bench.build_workload(cfg, rank, world, bench.rho_oracle)
+            res[cfg] = ([list(c["heads"]) for c in calls], [[m.sri.copy() for m in c["masks"]] for c in calls],
+                        sc, conf["global_batch"], [c["B"] for c in calls])
+        q.put((rank, res))
     finally:
         dist.destroy_process_group()
 
 
-def test_two_rank_sharding_and_max_reduction():
+def test_two_rank_head_sharding_and_gathers():
     world = 2
     port = _free_port()
     ctx = mp.get_context("spawn")
@@ -46,17 +53,30 @@ def test_two_rank_sharding_and_max_reduction():
         p.start()
     res = {}
     for _ in range(world):
-        r = q.get(timeout=600)
-        res[r[0]] = r
+        r, v = q.get(timeout=900)
+        res[r] = v
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    # max over ranks = slowest rank, on every rank
-    assert res[0][1] == res[1][1] == 11.0
-    # C2: batch entries sharded, different seeds -> different masks (weak scaling)
-    assert res[0][2][0] == [0] and res[1][2][0] == [1]
-    assert not np.array_equal(res[0][3][0], res[1][3][0])
-    assert res[0][5] == "weak" and res[0][7] == 2
-    # C4: heads partitioned across ranks (strong scaling)
-    assert res[0][4] == list(range(0, 32)) and res[1][4] == list(range(32, 64))
-    assert res[0][6] == "strong"
+    assert res[0]["slowest"] == res[1]["slowest"] == 11.0
+    assert res[0]["gathered"] == res[1]["gathered"] == [[0.0, 0.0, -1.0], [1.0, 2.5, -1.0]]
+    for cfg, H in (("C2", 32), ("C3", 32), ("C4", 64), ("C5:8192:64:causal_document,random_eviction", 64)):
+        h0, m0, sc0, gb0, b0 = res[0][cfg]
+        h1, m1, sc1, gb1, b1 = res[1][cfg]
+        assert sc0 == sc1 == "strong" and gb0 == gb1 and b0 == b1
+        for a, b in zip(h0, h1):          # head ranges partition [0, H)
+            assert a == list(range(0, H // 2)) and b == list(range(H // 2, H))
+        for ca, cb in zip(m0, m1):        # one global problem: identical masks on both ranks
+            assert all(np.array_equal(x, y) for x, y in zip(ca, cb))
+
+
+def test_gpus_flag_refuses_fewer_gpus():
+    """`bench.py --gpus 2` without torchrun re-launches itself as 2 ranks, or fails loudly when
+    fewer GPUs are visible (here: none) — it never silently runs on 1 GPU."""
+    env = dict(os.environ)
+    env.pop("WORLD_SIZE", None)
+    env["CUDA_VISIBLE_DEVICES"] = ""
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--steps", "1"],
+                       cwd=ROOT, env=env, capture_output=True, text=True, timeout=300)
+    assert r.returncode != 0
+    assert "only 0 CUDA device" in r.stderr, r.stderr[-2000:]
