@@ -453,13 +453,19 @@ def run_sweep(fm, cells, dev, stream, peak, rank, world, dist, steps=3, warmup=2
             r = Runner(fm, [c], dev)
             for _ in range(warmup):
                 r.step()
+            # at least ~1 s of timed steps, so the clock sampler sees the kernels under load
+            t0 = time.perf_counter()
+            r.step()
+            torch.cuda.synchronize()
+            est = max(time.perf_counter() - t0, 1e-4)
+            steps_c = int(min(200, max(steps, 1.0 / est)))
             clocks = ClockSampler(dev.index)
             clocks.start()
-            ms, kt = timed_steps(r, steps, stream, [fm.FM_KERNEL_FWD, fm.FM_KERNEL_BWD])
+            ms, kt = timed_steps(r, steps_c, stream, [fm.FM_KERNEL_FWD, fm.FM_KERNEL_BWD])
             clk = clocks.stop()
-            ms = reduce_max_over_ranks(ms / steps, dist, dev)
-            fwd_ms = reduce_max_over_ranks(kt["fwd"][0] / steps, dist, dev)
-            bwd_ms = reduce_max_over_ranks(kt["bwd"][0] / steps, dist, dev)
+            ms = reduce_max_over_ranks(ms / steps_c, dist, dev)
+            fwd_ms = reduce_max_over_ranks(kt["fwd"][0] / steps_c, dist, dev)
+            bwd_ms = reduce_max_over_ranks(kt["bwd"][0] / steps_c, dist, dev)
             tot = world * (r.F_fwd + r.F_bwd) / (ms * 1e-3) / 1e12
             out.append({"config": cfg.split(":")[0] + (":" + ":".join(cfg.split(":")[1:3]) if ":" in cfg else ""),
                         "mask": c.get("family", c["masks"][0].family),

@@ -123,9 +123,16 @@ FM_API size_t flashmask_workspace_size(const fm_params* p, int pass);
  *              UTSmin, UTSmax, UTEmin, UTEmax), with the table's defaults filled in.
  *   class_map  uint8 [B, Hm, Tr, Tc] fm_tile_class, or NULL.
  *   counts     int64 [B, Hm, 3] = (#SKIP, #PARTIAL, #UNMASKED), or NULL.
- * Tr = ceil(N / br), Tc = ceil(N / bc).  The class map ignores FM_FLAG_NO_SKIP. */
+ *   row_nonskip int32 [B, Hm, Tr]: per row tile the number of non-SKIP tiles in that row, or NULL.
+ *   col_nonskip int32 [B, Hm, Tc]: per column tile the number of non-SKIP tiles in that column,
+ *              or NULL.  These are the per-unit work figures O((1-rho) T_r T_c) of P:262 that
+ *              order the forward's row units and the backward's column units.
+ * Tr = ceil(N / br), Tc = ceil(N / bc).  The class map and all counts use the true Eq. 4
+ * classes (they ignore FM_FLAG_NO_SKIP).  Every output is written in full (no accumulation
+ * into caller data). */
 FM_API fm_status flashmask_classify(const fm_params* p, const int32_t* startend_row_indices, int32_t br, int32_t bc,
-                             int32_t* minmax, uint8_t* class_map, int64_t* counts, void* stream);
+                             int32_t* minmax, uint8_t* class_map, int64_t* counts, int32_t* row_nonskip,
+                             int32_t* col_nonskip, void* stream);
 
 /* Forward pass (Alg. 1): o = Softmax(scale*q k^T + M) v, lse = logsumexp.
  *   q, k, v  [B, N, H, d] in_dtype;  o [B, N, H, d] out_dtype;  lse fp32 [B, H, N].

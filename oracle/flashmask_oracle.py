@@ -303,6 +303,16 @@ def classify(vec: Vectors, Br: int, Bc: int):
     return cm, counts, ext
 
 
+def nonskip_counts(vec: Vectors, Br: int, Bc: int):
+    """Per-unit work of the tiled algorithm: the number of non-SKIP tiles in every
+    row tile (the forward's unit, Alg. 1's inner loop over j) and in every column
+    tile (the backward's unit, Alg. 2's inner loop over i); compute is
+    O((1-rho) T_r T_c).  Returns (rows int64 [Tr], cols int64 [Tc])."""
+    cm, _, _ = classify(vec, Br, Bc)
+    ns = cm != SKIP
+    return ns.sum(axis=1).astype(np.int64), ns.sum(axis=0).astype(np.int64)
+
+
 def alpha_bruteforce(vec: Vectors, Br: int, Bc: int) -> int:
     """alpha of §4.3: number of tiles whose every cell is masked, counted from the
     dense mask (O(N^2): small N only)."""

@@ -249,7 +249,8 @@ size_t flashmask_workspace_size(const fm_params* p, int pass) {
 }
 
 fm_status flashmask_classify(const fm_params* p, const int32_t* sri, int32_t br, int32_t bc, int32_t* minmax,
-                             uint8_t* class_map, int64_t* counts, void* stream) {
+                             uint8_t* class_map, int64_t* counts, int32_t* row_nonskip, int32_t* col_nonskip,
+                             void* stream) {
   g_last_error.clear();
   fm::Dims d{};
   fm_status s = check_params(p, &d, false);
@@ -260,10 +261,12 @@ fm_status flashmask_classify(const fm_params* p, const int32_t* sri, int32_t br,
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   cudaError_t e = timed(FM_KERNEL_EXPAND, st, [&] { return fm::launch_expand(sri, d, bc, minmax, nullptr, st); });
   if (e != cudaSuccess) return cuda_fail(e, "expand");
-  if (class_map || counts) {
+  if (class_map || counts || row_nonskip || col_nonskip) {
     fm::Dims d0 = d;
     d0.flags = 0;
-    e = timed(FM_KERNEL_CLASSIFY, st, [&] { return fm::launch_classify(minmax, d0, br, bc, class_map, 0, 0, counts, st); });
+    e = timed(FM_KERNEL_CLASSIFY, st, [&] {
+      return fm::launch_classify(minmax, d0, br, bc, class_map, 0, 0, counts, st, row_nonskip, col_nonskip);
+    });
     if (e != cudaSuccess) return cuda_fail(e, "classify");
   }
   return FM_OK;

@@ -380,7 +380,9 @@ __global__ void __launch_bounds__(bwd::NT, 1)
           }
           // S^T/dP^T(t) (warp 13) completed before the compute WGs produced P/dS(t)
           mma_commit_w(&sm.q_empty[st]);
-          mma_commit_w(&sm.pds_free[bi]);
+          // pds_free is waited on only when dQ does not share the P/dS columns (else dq_empty
+          // guards the buffer): commit it only then, so no mbarrier phase completes unobserved
+          if (!(C::DQ_ALIAS && a.with_dq)) mma_commit_w(&sm.pds_free[bi]);
           if (lane == 0) FM_T(12, t);
           // dQ(t) overwrites the P/dS columns of buffer t % NB — issued after dV/dK(t) by this
           // thread (in order), and the compute WGs stored P/dS(t) there only after dQ(t-NB) was

@@ -106,7 +106,8 @@ struct F32Args {
 cudaError_t launch_expand(const int32_t* sri, const Dims& d, int bc, int32_t* ext8, int4* vec4, cudaStream_t st);
 cudaError_t launch_sliding_window(int B, int N, int w, int causal, int32_t* sri, cudaStream_t st);
 cudaError_t launch_classify(const int32_t* ext8, const Dims& d, int br, int bc, uint8_t* map, int transposed,
-                            int kernel_map, int64_t* counts, cudaStream_t st);
+                            int kernel_map, int64_t* counts, cudaStream_t st, int32_t* row_cnt = nullptr,
+                            int32_t* col_cnt = nullptr);
 cudaError_t launch_fwd(const Dims& d, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
                        const CUtensorMap& to, const FwdArgs& a, cudaStream_t st);
 cudaError_t launch_bwd_pre(const Dims& d, const void* o, const void* dout, const float* lse, float* dvec, float* l2,

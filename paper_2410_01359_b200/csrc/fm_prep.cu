@@ -98,85 +98,133 @@ __global__ void __launch_bounds__(128) k1_expand(const int32_t* __restrict__ sri
 //   UNMASKED otherwise.
 // kernel_map = 1 writes the map the attention kernels consume: SKIP -> PARTIAL under
 // FM_FLAG_NO_SKIP, and a non-SKIP ragged last column tile -> PARTIAL (bounds mask).
-// Counts always use the true classes.  Grid (ceil(Tc/128), Tr, B*Hm), 128 threads.
+// Counts always use the true classes: per (b, hm) the three class counts, and the
+// number of non-SKIP tiles of every row tile and of every column tile — the per-unit work
+// O((1-rho) T_r T_c) of P:262 that orders the attention kernels' units.
+// Thread = JPT consecutive column tiles (extrema loaded once), looping over rows_per_cta row
+// tiles; row map: one JPT-byte store per row; transposed map (JPT = 1): 16 consecutive row tiles
+// of one column tile per 16-byte store.  Grid (ceil(Tc / (128 JPT)), ceil(Tr / rows_per_cta), B*Hm).
 // ---------------------------------------------------------------------------------------
+__device__ __forceinline__ int tile_class(const int4& a, const int4& b, long r0, long r1, long c0, long c1,
+                                          int causal) {
+  if ((r0 >= a.y && r1 <= a.z) || (r0 >= b.y && r1 <= b.z) || (causal && r1 - 1 < c0)) return 0;
+  if ((r1 > a.x && r0 < a.w) || (r1 > b.x && r0 < b.w) || (causal && r0 < c1 - 1)) return 1;
+  return 2;
+}
+
+template <int JPT>
 __global__ void __launch_bounds__(128) k1_classify(const int32_t* __restrict__ ext8, int N, int causal, int br, int bc,
                                                    int Tr, int Tc, uint8_t* __restrict__ map, int transposed,
                                                    int kernel_map, int no_skip,
-                                                   unsigned long long* __restrict__ counts, int rows_per_cta) {
+                                                   unsigned long long* __restrict__ counts, int* __restrict__ row_cnt,
+                                                   int* __restrict__ col_cnt, int rows_per_cta) {
   pdl_wait();
   pdl_launch();
-  // thread = column tile j (its extrema loaded once), looping over rows_per_cta row tiles: the class
-  // map is written in 16-byte runs (transposed map: 16 consecutive row tiles of one column
-  // tile) and the class counts leave the CTA as 3 atomics instead of one per 128 tiles.
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  __shared__ unsigned int cnt[3];
+  __shared__ int row_acc[64];
+  const int j0 = (blockIdx.x * blockDim.x + threadIdx.x) * JPT;
   const int ib = blockIdx.y * rows_per_cta;
+  const int iend = min(Tr, ib + rows_per_cta);
   const int bh = blockIdx.z;
-  unsigned int c0n = 0, c1n = 0, c2n = 0;
-  if (j < Tc) {
-    const int4* e = reinterpret_cast<const int4*>(ext8 + (static_cast<size_t>(bh) * Tc + j) * 8);
-    const int4 a = e[0], b = e[1];  // (LTSmin, LTSmax, LTEmin, LTEmax), (UTSmin, UTSmax, UTEmin, UTEmax)
-    const long c0 = static_cast<long>(j) * bc, c1 = min(static_cast<long>(N), c0 + bc);
-    const bool ragged_last = kernel_map && (N % bc) != 0 && j == Tc - 1;
-    const int iend = min(Tr, ib + rows_per_cta);
-    for (int i16 = ib; i16 < iend; i16 += 16) {
-      uint32_t packed[4] = {0u, 0u, 0u, 0u};
+  if (threadIdx.x < 3) cnt[threadIdx.x] = 0;
+  if (threadIdx.x < 64) row_acc[threadIdx.x] = 0;
+  __syncthreads();
+  int4 ea[JPT], eb[JPT];
+  long c0[JPT], c1[JPT];
+  bool valid[JPT], ragged[JPT];
 #pragma unroll
-      for (int u = 0; u < 16; ++u) {
-        const int i = i16 + u;
-        if (i >= iend) break;
-        const long r0 = static_cast<long>(i) * br, r1 = min(static_cast<long>(N), r0 + br);
-        int cls;
-        if ((r0 >= a.y && r1 <= a.z) || (r0 >= b.y && r1 <= b.z) || (causal && r1 - 1 < c0))
-          cls = 0;
-        else if ((r1 > a.x && r0 < a.w) || (r1 > b.x && r0 < b.w) || (causal && r0 < c1 - 1))
-          cls = 1;
-        else
-          cls = 2;
+  for (int u = 0; u < JPT; ++u) {
+    const int j = j0 + u;
+    valid[u] = j < Tc;
+    if (valid[u]) {
+      const int4* e = reinterpret_cast<const int4*>(ext8 + (static_cast<size_t>(bh) * Tc + j) * 8);
+      ea[u] = e[0];  // (LTSmin, LTSmax, LTEmin, LTEmax)
+      eb[u] = e[1];  // (UTSmin, UTSmax, UTEmin, UTEmax)
+    } else {
+      ea[u] = eb[u] = make_int4(0, 0, 0, 0);
+    }
+    c0[u] = static_cast<long>(j) * bc;
+    c1[u] = min(static_cast<long>(N), c0[u] + bc);
+    ragged[u] = kernel_map && (N % bc) != 0 && j == Tc - 1;
+  }
+  unsigned int c0n = 0, c1n = 0, c2n = 0;
+  int colns[JPT];
+#pragma unroll
+  for (int u = 0; u < JPT; ++u) colns[u] = 0;
+  const bool row_counts = row_cnt != nullptr && rows_per_cta <= 64;
+  for (int i16 = ib; i16 < iend; i16 += 16) {
+    uint32_t packed[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+    for (int v = 0; v < 16; ++v) {
+      const int i = i16 + v;
+      if (i >= iend) break;
+      const long r0 = static_cast<long>(i) * br, r1 = min(static_cast<long>(N), r0 + br);
+      uint32_t word = 0u;
+      int ns = 0;
+#pragma unroll
+      for (int u = 0; u < JPT; ++u) {
+        if (!valid[u]) continue;
+        const int cls = tile_class(ea[u], eb[u], r0, r1, c0[u], c1[u], causal);
         c0n += cls == 0;
         c1n += cls == 1;
         c2n += cls == 2;
+        ns += cls != 0;
+        colns[u] += cls != 0;
         int out = cls;
         if (kernel_map) {
           if (out == 0 && no_skip) out = 1;
-          if (out == 2 && ragged_last) out = 1;
+          if (out == 2 && ragged[u]) out = 1;
         }
-        if (map) {
-          if (transposed)
-            packed[u >> 2] |= static_cast<uint32_t>(out) << (8 * (u & 3));
-          else
-            map[(static_cast<size_t>(bh) * Tr + i) * Tc + j] = static_cast<uint8_t>(out);
+        word |= static_cast<uint32_t>(out) << (8 * u);
+      }
+      if (row_counts) {
+        const int wsum = __reduce_add_sync(0xffffffffu, ns);
+        if ((threadIdx.x & 31) == 0 && wsum) atomicAdd(&row_acc[i - ib], wsum);
+      }
+      if (map && valid[0]) {
+        if (transposed) {
+          packed[v >> 2] |= (word & 0xffu) << (8 * (v & 3));
+        } else {
+          uint8_t* dst = map + (static_cast<size_t>(bh) * Tr + i) * Tc + j0;
+          if (JPT == 4 && (Tc & 3) == 0) {
+            *reinterpret_cast<uint32_t*>(dst) = word;
+          } else {
+#pragma unroll
+            for (int u = 0; u < JPT; ++u)
+              if (valid[u]) dst[u] = static_cast<uint8_t>(word >> (8 * u));
+          }
         }
       }
-      if (map && transposed) {
-        uint8_t* dst = map + (static_cast<size_t>(bh) * Tc + j) * Tr + i16;
-        if (i16 + 16 <= iend && (Tr & 15) == 0) {
-          *reinterpret_cast<uint4*>(dst) = make_uint4(packed[0], packed[1], packed[2], packed[3]);
-        } else {
-          for (int u = 0; u < 16 && i16 + u < iend; ++u) dst[u] = static_cast<uint8_t>(packed[u >> 2] >> (8 * (u & 3)));
-        }
+    }
+    if (map && transposed && valid[0]) {
+      uint8_t* dst = map + (static_cast<size_t>(bh) * Tc + j0) * Tr + i16;
+      if (i16 + 16 <= iend && (Tr & 15) == 0) {
+        *reinterpret_cast<uint4*>(dst) = make_uint4(packed[0], packed[1], packed[2], packed[3]);
+      } else {
+        for (int v = 0; v < 16 && i16 + v < iend; ++v) dst[v] = static_cast<uint8_t>(packed[v >> 2] >> (8 * (v & 3)));
       }
     }
   }
-  if (counts) {
-    __shared__ unsigned int cnt[3];
-    if (threadIdx.x < 3) cnt[threadIdx.x] = 0;
-    __syncthreads();
+  if (col_cnt) {
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      c0n += __shfl_xor_sync(0xffffffffu, c0n, o);
-      c1n += __shfl_xor_sync(0xffffffffu, c1n, o);
-      c2n += __shfl_xor_sync(0xffffffffu, c2n, o);
-    }
+    for (int u = 0; u < JPT; ++u)
+      if (valid[u] && colns[u]) atomicAdd(&col_cnt[static_cast<size_t>(bh) * Tc + j0 + u], colns[u]);
+  }
+  if (counts) {
+    c0n = __reduce_add_sync(0xffffffffu, c0n);
+    c1n = __reduce_add_sync(0xffffffffu, c1n);
+    c2n = __reduce_add_sync(0xffffffffu, c2n);
     if ((threadIdx.x & 31) == 0) {
       atomicAdd(&cnt[0], c0n);
       atomicAdd(&cnt[1], c1n);
       atomicAdd(&cnt[2], c2n);
     }
-    __syncthreads();
-    if (threadIdx.x < 3 && cnt[threadIdx.x])
-      atomicAdd(&counts[static_cast<size_t>(bh) * 3 + threadIdx.x], static_cast<unsigned long long>(cnt[threadIdx.x]));
   }
+  __syncthreads();
+  if (counts && threadIdx.x < 3 && cnt[threadIdx.x])
+    atomicAdd(&counts[static_cast<size_t>(bh) * 3 + threadIdx.x], static_cast<unsigned long long>(cnt[threadIdx.x]));
+  if (row_counts && threadIdx.x < iend - ib && row_acc[threadIdx.x])
+    atomicAdd(&row_cnt[static_cast<size_t>(bh) * Tr + ib + threadIdx.x], row_acc[threadIdx.x]);
 }
 
 // Sliding-window startend_row_indices (flashmask_sliding_window_indices): one thread per key.
@@ -208,20 +256,28 @@ cudaError_t launch_expand(const int32_t* sri, const Dims& d, int bc, int32_t* ex
 }
 
 cudaError_t launch_classify(const int32_t* ext8, const Dims& d, int br, int bc, uint8_t* map, int transposed,
-                            int kernel_map, int64_t* counts, cudaStream_t st) {
+                            int kernel_map, int64_t* counts, cudaStream_t st, int32_t* row_cnt, int32_t* col_cnt) {
   const int Tr = (d.N + br - 1) / br, Tc = (d.N + bc - 1) / bc;
-  if (counts) {
-    cudaError_t e = cudaMemsetAsync(counts, 0, sizeof(int64_t) * 3 * d.B * d.Hm, st);
-    if (e != cudaSuccess) return e;
-  }
+  const long bhm = static_cast<long>(d.B) * d.Hm;
+  cudaError_t e;
+  if (counts && (e = cudaMemsetAsync(counts, 0, sizeof(int64_t) * 3 * bhm, st)) != cudaSuccess) return e;
+  if (row_cnt && (e = cudaMemsetAsync(row_cnt, 0, sizeof(int32_t) * Tr * bhm, st)) != cudaSuccess) return e;
+  if (col_cnt && (e = cudaMemsetAsync(col_cnt, 0, sizeof(int32_t) * Tc * bhm, st)) != cudaSuccess) return e;
   // Row tiles per CTA: 64 on large maps, where per-CTA count atomics would otherwise contend
   // (measured 4x on Hm = 64 heads at 128K) and the transposed map is written in 16-byte runs;
   // small maps keep one row tile per CTA (parallelism over latency: 2.5x faster at N = 8K)
-  const long tiles = static_cast<long>(d.B) * d.Hm * Tr * Tc;
-  const int rpc = tiles >= (4L << 20) ? 64 : (tiles >= (256L << 10) ? 16 : 1);  // small maps: one row per CTA
-  dim3 grid((Tc + 127) / 128, (Tr + rpc - 1) / rpc, d.B * d.Hm);
-  return launch_pdl(k1_classify, grid, dim3(128), 0, st, ext8, d.N, d.causal, br, bc, Tr, Tc, map, transposed,
-                    kernel_map, (d.flags & 1) ? 1 : 0, reinterpret_cast<unsigned long long*>(counts), rpc);
+  const long tiles = bhm * Tr * Tc;
+  const int rpc = tiles >= (4L << 20) ? 64 : (tiles >= (256L << 10) ? 16 : 1);
+  const int ns = (d.flags & 1) ? 1 : 0;
+  auto cnt64 = reinterpret_cast<unsigned long long*>(counts);
+  if (transposed) {
+    dim3 grid((Tc + 127) / 128, (Tr + rpc - 1) / rpc, static_cast<unsigned>(bhm));
+    return launch_pdl(k1_classify<1>, grid, dim3(128), 0, st, ext8, d.N, d.causal, br, bc, Tr, Tc, map, transposed,
+                      kernel_map, ns, cnt64, row_cnt, col_cnt, rpc);
+  }
+  dim3 grid((Tc + 511) / 512, (Tr + rpc - 1) / rpc, static_cast<unsigned>(bhm));
+  return launch_pdl(k1_classify<4>, grid, dim3(128), 0, st, ext8, d.N, d.causal, br, bc, Tr, Tc, map, transposed,
+                    kernel_map, ns, cnt64, row_cnt, col_cnt, rpc);
 }
 
 // ---------------------------------------------------------------------------------------

@@ -51,7 +51,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     vp, sz, i32 = ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int32
     lib.flashmask_workspace_size.argtypes = [P, ctypes.c_int]
     lib.flashmask_workspace_size.restype = sz
-    lib.flashmask_classify.argtypes = [P, vp, i32, i32, vp, vp, vp, vp]
+    lib.flashmask_classify.argtypes = [P, vp, i32, i32, vp, vp, vp, vp, vp, vp]
     lib.flashmask_classify.restype = ctypes.c_int
     lib.flashmask_fwd.argtypes = [P, vp, vp, vp, vp, vp, vp, vp, sz, vp]
     lib.flashmask_fwd.restype = ctypes.c_int
@@ -145,9 +145,11 @@ def flashmask_workspace_size(params: FmParams, pass_: int) -> int:
 
 
 def flashmask_classify(sri: torch.Tensor, causal: bool, br: int = 128, bc: int = 128, num_heads: int | None = None,
-                       class_map: bool = True, stream=None):
+                       class_map: bool = True, stream=None, nonskip: bool = False):
     """Tile classification (K1).  sri: int32 cuda [B, Hm, N, C].  Returns
-    (minmax int32 [B,Hm,Tc,8], class_map uint8 [B,Hm,Tr,Tc] or None, counts int64 [B,Hm,3])."""
+    (minmax int32 [B,Hm,Tc,8], class_map uint8 [B,Hm,Tr,Tc] or None, counts int64 [B,Hm,3]);
+    with nonskip=True also (row_nonskip int32 [B,Hm,Tr], col_nonskip int32 [B,Hm,Tc]): the
+    number of non-SKIP tiles per row tile / per column tile."""
     _require(isinstance(sri, torch.Tensor) and sri.dim() == 4, "flashmask_classify",
              "startend_row_indices must be a 4-D tensor [B, Hm, N, C]")
     B, Hm, N, C = sri.shape
@@ -159,9 +161,13 @@ def flashmask_classify(sri: torch.Tensor, causal: bool, br: int = 128, bc: int =
     minmax = torch.empty(B, Hm, Tc, 8, dtype=torch.int32, device=dev)
     cmap = torch.empty(B, Hm, Tr, Tc, dtype=torch.uint8, device=dev) if class_map else None
     counts = torch.empty(B, Hm, 3, dtype=torch.int64, device=dev)
+    rows = torch.empty(B, Hm, Tr, dtype=torch.int32, device=dev) if nonskip else None
+    cols = torch.empty(B, Hm, Tc, dtype=torch.int32, device=dev) if nonskip else None
     with torch.cuda.device(dev):
         _check(_lib.flashmask_classify(ctypes.byref(p), _ptr(sri), br, bc, _ptr(minmax), _ptr(cmap), _ptr(counts),
-                                       _stream(stream, dev)), "flashmask_classify")
+                                       _ptr(rows), _ptr(cols), _stream(stream, dev)), "flashmask_classify")
+    if nonskip:
+        return minmax, cmap, counts, rows, cols
     return minmax, cmap, counts
 
 

@@ -36,14 +36,32 @@ def test_classify_bit_exact(fmlib, fam, N):
     m0 = masks[0]
     sri = torch.from_numpy(wm.stack(masks, 1)).cuda()
     for br, bc in ((128, 128), (64, 128), (3, 5), (128, 64)):
-        minmax, cmap, counts = fmlib.flashmask_classify(sri, m0.causal, br, bc)
+        minmax, cmap, counts, rows, cols = fmlib.flashmask_classify(sri, m0.causal, br, bc, nonskip=True)
         torch.cuda.synchronize()
         for b, m in enumerate(masks):
             vec = fo.expand(m.sri, m.causal, N)
             cm_ref, cnt_ref, ext_ref = fo.classify(vec, br, bc)
+            rows_ref, cols_ref = fo.nonskip_counts(vec, br, bc)
             assert np.array_equal(minmax[b, 0].cpu().numpy().astype(np.int64), ext_ref), (br, bc)
             assert np.array_equal(cmap[b, 0].cpu().numpy(), cm_ref), (br, bc)
             assert np.array_equal(counts[b, 0].cpu().numpy(), cnt_ref), (br, bc)
+            assert np.array_equal(rows[b, 0].cpu().numpy(), rows_ref), (br, bc)   # a2 per-row-tile work
+            assert np.array_equal(cols[b, 0].cpu().numpy(), cols_ref), (br, bc)   # a2 per-column-tile work
+    # large per-head maps (64 heads x 256 x 256 tiles) take the 64-row-tiles-per-CTA path
+    if N == 8192 and fam in ("causal_document", "global_sliding_window"):
+        big = [wm.sample_family(fam, 32768, rng, (3, 7)) for _ in range(64)]
+        sb = torch.from_numpy(np.stack([m.sri for m in big])[None]).cuda()
+        _, cmap, counts, rows, cols = fmlib.flashmask_classify(sb, big[0].causal, 128, 128, nonskip=True)
+        torch.cuda.synchronize()
+        for h in (0, 21, 42, 63):
+            m = big[h]
+            vec = fo.expand(m.sri, m.causal, 32768)
+            cm_ref, cnt_ref, _ = fo.classify(vec, 128, 128)
+            rows_ref, cols_ref = fo.nonskip_counts(vec, 128, 128)
+            assert np.array_equal(cmap[0, h].cpu().numpy(), cm_ref)
+            assert np.array_equal(counts[0, h].cpu().numpy(), cnt_ref)
+            assert np.array_equal(rows[0, h].cpu().numpy(), rows_ref)
+            assert np.array_equal(cols[0, h].cpu().numpy(), cols_ref)
 
 
 def test_classify_arbitrary_int32_vectors(fmlib):

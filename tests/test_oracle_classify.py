@@ -227,3 +227,24 @@ def test_rule_r_matches_exact_skip_on_families(fam):
         none_masked = int((~dense.any(-1)).sum())
         assert cnt[0] == all_masked, (fam, cnt, all_masked)
         assert none_masked - cnt[2] <= 0.03 * T * T, (fam, cnt, none_masked)
+
+
+@pytest.mark.parametrize("N", [1024, 4096, 8192])
+def test_nonskip_counts_closed_forms(N):
+    """a2 per-unit work: causal -> row tile i has i+1 non-SKIP tiles, column tile j has T-j;
+    sliding window w (multiple of 128, W = w/128) -> row i has min(i, W) + 1; full -> T each;
+    both sums equal the non-SKIP count."""
+    T = N // 128
+    rows, cols = fo.nonskip_counts(vec(wm.causal(N)), 128, 128)
+    assert list(rows) == [i + 1 for i in range(T)] and list(cols) == [T - j for j in range(T)]
+    w = max(128, N // 16)
+    W = w // 128
+    rows, cols = fo.nonskip_counts(vec(wm.sliding_window(N, w)), 128, 128)
+    assert list(rows) == [min(i, W) + 1 for i in range(T)]
+    assert list(cols) == [min(T - j, W + 1) for j in range(T)]
+    rows, cols = fo.nonskip_counts(vec(wm.full(N)), 128, 128)
+    assert (rows == T).all() and (cols == T).all()
+    m = wm.sample_family("causal_document", N, np.random.default_rng(N), (3, 7))
+    rows, cols = fo.nonskip_counts(vec(m), 128, 128)
+    _, c, _ = fo.classify(vec(m), 128, 128)
+    assert rows.sum() == cols.sum() == c[1] + c[2]
