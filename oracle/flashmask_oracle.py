@@ -313,6 +313,44 @@ def nonskip_counts(vec: Vectors, Br: int, Bc: int):
     return ns.sum(axis=1).astype(np.int64), ns.sum(axis=0).astype(np.int64)
 
 
+CHUNK_ROWS, CHUNK_COLS = 32, 16   # refinement sub-blocks of a 128 x 128 tile: 4 x 8 = 32 bits
+
+
+def refine_chunks(vec: Vectors):
+    """Tighter-than-Eq.-4 refinement (R31), rule version 1.
+
+    Eq. 4 classifies a tile from hulls (min/max) of its columns' intervals, so a
+    PARTIAL tile may hold large regions with no masked cell (P:232-240 then masks every element
+    of it).  Refinement: each 128 x 128 tile (the forward's tile, R14) is cut into 4 row groups
+    of 32 rows x 8 column chunks of 16 columns; bit (8 g + c) of the tile's 32-bit word is 1 iff
+    the sub-block [r0 + 32 g, r0 + 32 g + 32) x [c0 + 16 c, c0 + 16 c + 16) — real rows and
+    columns only (R3) — contains a masked cell: masked(r, y) of Eq. 3 / §4.1 (P:100-104,
+    P:127) with the causal triangle (R8).  Written out per column and row group: column y has a
+    masked cell in rows [a, b) iff one of its intervals [LTS, LTE), [UTS, UTE) intersects [a, b)
+    or (causal) a < y.  Returns uint32 [Tr, Tc]."""
+    N = vec.N
+    T = -(-N // 128)
+    out = np.zeros((T, T), dtype=np.uint32)
+    y = np.arange(N, dtype=np.int64)
+    for i in range(T):
+        for g in range(4):
+            a = i * 128 + g * CHUNK_ROWS
+            b = min(a + CHUNK_ROWS, N)
+            if a >= N:
+                continue
+            hit = ((vec.lts < vec.lte) & (vec.lts < b) & (vec.lte > a)) | \
+                  ((vec.uts < vec.ute) & (vec.uts < b) & (vec.ute > a))
+            if vec.causal:
+                hit |= a < y
+            for j in range(T):
+                for c in range(8):
+                    c0 = j * 128 + c * CHUNK_COLS
+                    c1 = min(c0 + CHUNK_COLS, N)
+                    if c0 < N and hit[c0:c1].any():
+                        out[i, j] |= np.uint32(1 << (8 * g + c))
+    return out
+
+
 def alpha_bruteforce(vec: Vectors, Br: int, Bc: int) -> int:
     """alpha of §4.3: number of tiles whose every cell is masked, counted from the
     dense mask (O(N^2): small N only)."""

@@ -248,3 +248,53 @@ def test_nonskip_counts_closed_forms(N):
     rows, cols = fo.nonskip_counts(vec(m), 128, 128)
     _, c, _ = fo.classify(vec(m), 128, 128)
     assert rows.sum() == cols.sum() == c[1] + c[2]
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_refine_chunks_bruteforce(seed):
+    """f3 refinement words against brute force on the dense mask (every 32 x 16 sub-block of
+    every 128 x 128 tile: bit set iff it holds a masked cell), ragged N, all families, plus the
+    class consistency Eq. 4 implies: UNMASKED tiles have word 0, SKIP tiles every real sub-block
+    dirty."""
+    rng = np.random.default_rng(100 + seed)
+    for fam in wm.FAMILIES:
+        N = int(rng.integers(1, 420))
+        m = wm.sample_family(fam, N, rng, (1, 5))
+        v = vec(m)
+        words = fo.refine_chunks(v)
+        M = fo.to_dense(v)
+        cm, _, _ = fo.classify(v, 128, 128)
+        T = -(-N // 128)
+        for i in range(T):
+            for j in range(T):
+                want = 0
+                full = 0
+                for g in range(4):
+                    for c in range(8):
+                        a, b = i * 128 + 32 * g, min(i * 128 + 32 * g + 32, N)
+                        c0, c1 = j * 128 + 16 * c, min(j * 128 + 16 * c + 16, N)
+                        if a < N and c0 < N:
+                            full |= 1 << (8 * g + c)
+                            if M[a:b, c0:c1].any():
+                                want |= 1 << (8 * g + c)
+                assert int(words[i, j]) == want, (fam, N, i, j)
+                if cm[i, j] == fo.UNMASKED:
+                    assert want == 0
+                if cm[i, j] == fo.SKIP:
+                    assert want == full
+
+
+def test_refine_chunks_qk_sparse_clean_blocks():
+    """The case f3 targets: a QK-sparse tile below the diagonal with one dropped key is PARTIAL
+    under Eq. 4 but has exactly one dirty column chunk per row group."""
+    m = wm.qk_sparse(512, [300], (500, 510))
+    v = vec(m)
+    cm, _, _ = fo.classify(v, 128, 128)
+    w = fo.refine_chunks(v)
+    assert cm[3, 2] == fo.PARTIAL           # rows 384..511, keys 256..383 (key 300 dropped)
+    chunk = (300 - 256) // 16               # = 2
+    rows_hit = 0
+    for g in range(4):
+        rows_hit |= 1 << (8 * g + chunk)
+    # rows 500..509 (dropped query range) are masked for every key: row group 3 is all dirty
+    assert int(w[3, 2]) == rows_hit | (0xFF << 24)
