@@ -83,7 +83,11 @@ enum {
   /* flashmask_bwd: compute dQ row-parallel in a separate kernel that accumulates over the key
    * tiles in ascending order on chip (no fp32 atomics), so dq is bitwise reproducible run to
    * run ("deterministic control").  Costs two extra GEMMs per visited tile. */
-  FM_FLAG_DETERMINISTIC = 2
+  FM_FLAG_DETERMINISTIC = 2,
+  /* flashmask_fwd: do not run the f3 refinement (K1c, flashmask_refine below); every element of
+   * a PARTIAL tile is then masked element-wise as in Alg. 1 lines 15-21.  Outputs are bitwise
+   * identical either way (masking a sub-block with no masked cell changes nothing). */
+  FM_FLAG_NO_REFINE = 4
 };
 
 typedef struct {
@@ -134,6 +138,22 @@ FM_API fm_status flashmask_classify(const fm_params* p, const int32_t* startend_
                              int32_t* minmax, uint8_t* class_map, int64_t* counts, int32_t* row_nonskip,
                              int32_t* col_nonskip, void* stream);
 
+/* Tighter-than-Eq.-4 refinement (R31).  Eq. 4 classifies a tile from
+ * the hulls of its columns' intervals, so a PARTIAL tile may contain large regions without any
+ * masked cell.  For every 128 x 128 tile, the 32-bit word whose bit (8 g + c) is 1 iff the
+ * sub-block of rows [128 i + 32 g, +32) x columns [128 j + 16 c, +16) (real rows / columns
+ * only) holds a masked cell (masked(r, y) as in the header comment).  Inputs:
+ *   startend_row_indices  as for flashmask_classify;
+ *   class_map  uint8 [B, Hm, Tr, Tc] at 128 x 128 from flashmask_classify (br = bc = 128).
+ * Outputs (device pointers):
+ *   words      uint32 [B, Hm, Tr, Tc], required.
+ *   counts     int64 [B, Hm, 2] = (#PARTIAL tiles without any masked cell, #dirty sub-blocks
+ *              of PARTIAL tiles), or NULL.
+ * flashmask_fwd runs the same refinement internally (unless FM_FLAG_NO_REFINE) and applies the
+ * element mask only on the dirty sub-blocks of PARTIAL tiles. */
+FM_API fm_status flashmask_refine(const fm_params* p, const int32_t* startend_row_indices, const uint8_t* class_map,
+                                  uint32_t* words, int64_t* counts, void* stream);
+
 /* Forward pass (Alg. 1): o = Softmax(scale*q k^T + M) v, lse = logsumexp.
  *   q, k, v  [B, N, H, d] in_dtype;  o [B, N, H, d] out_dtype;  lse fp32 [B, H, N].
  * in_dtype FM_BF16 / FM_FP16 runs the tcgen05 kernels (16-bit operands, fp32 accumulation);
@@ -167,7 +187,8 @@ enum {
   FM_KERNEL_BWD = 4,         /* K4   backward main loop (Alg. 2)                             */
   FM_KERNEL_DQ_CONVERT = 5,  /* K5   dQ = scale * dQacc -> out dtype                         */
   FM_KERNEL_DQ = 6,          /* K6   deterministic dQ (FM_FLAG_DETERMINISTIC)                */
-  FM_NUM_KERNELS = 7
+  FM_KERNEL_REFINE = 7,      /* K1c  f3 refinement words of PARTIAL tiles                    */
+  FM_NUM_KERNELS = 8
 };
 
 /* Optional per-kernel timing for roofline reporting (off by default).  enable = 0: off;

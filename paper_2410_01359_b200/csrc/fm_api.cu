@@ -157,8 +157,10 @@ size_t carve(const fm::Dims& d, int pass, void* base, fm::Workspace* w) {
   w->fmap = nullptr;
   w->bmap = nullptr;
   w->dvec = w->l2 = w->dqacc = nullptr;
+  w->cw = nullptr;
   if (pass == FM_PASS_FWD) {
     w->fmap = take(bhm * d.Tr * d.Tc);
+    w->cw = reinterpret_cast<uint32_t*>(take(bhm * d.Tr * d.Tc * sizeof(uint32_t)));
   } else {
     w->fmap = take(bhm * d.Tr * d.Tc);  // used by the deterministic dQ kernel (K6)
     w->bmap = take(bhm * d.Tc * d.Trb);
@@ -272,6 +274,20 @@ fm_status flashmask_classify(const fm_params* p, const int32_t* sri, int32_t br,
   return FM_OK;
 }
 
+fm_status flashmask_refine(const fm_params* p, const int32_t* sri, const uint8_t* class_map, uint32_t* words,
+                           int64_t* counts, void* stream) {
+  g_last_error.clear();
+  fm::Dims d{};
+  fm_status s = check_params(p, &d, false);
+  if (s != FM_OK) return s;
+  if (!sri || !class_map || !words) return fail(FM_ERR_INVALID_ARGUMENT, "startend_row_indices, class_map, words required");
+  if (!aligned16(sri)) return fail(FM_ERR_INVALID_ARGUMENT, "startend_row_indices must be 16-byte aligned");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  cudaError_t e = timed(FM_KERNEL_REFINE, st, [&] { return fm::launch_refine(sri, class_map, d, words, counts, st); });
+  if (e != cudaSuccess) return cuda_fail(e, "refine");
+  return FM_OK;
+}
+
 fm_status flashmask_fwd(const fm_params* p, const void* q, const void* k, const void* v, const int32_t* sri, void* o,
                         float* lse, void* workspace, size_t workspace_bytes, void* stream) {
   g_last_error.clear();
@@ -314,10 +330,16 @@ fm_status flashmask_fwd(const fm_params* p, const void* q, const void* k, const 
   if (e != cudaSuccess) return cuda_fail(e, "expand");
   e = timed(FM_KERNEL_CLASSIFY, st, [&] { return fm::launch_classify(w.ext8, d, fm::kTile, fm::kTile, w.fmap, 0, 1, nullptr, st); });
   if (e != cudaSuccess) return cuda_fail(e, "classify");
+  const bool refine = (p->flags & FM_FLAG_NO_REFINE) == 0;
+  if (refine) {
+    e = timed(FM_KERNEL_REFINE, st, [&] { return fm::launch_refine(sri, w.fmap, d, w.cw, nullptr, st); });
+    if (e != cudaSuccess) return cuda_fail(e, "refine");
+  }
   fm::FwdArgs a{};
   a.B = d.B; a.N = d.N; a.H = d.H; a.Hm = d.Hm; a.Tr = d.Tr; a.Tc = d.Tc; a.G = d.G;
   a.scale_log2 = d.scale * 1.4426950408889634f;
   a.fmap = w.fmap;
+  a.cw = refine ? w.cw : nullptr;
   a.vec4 = w.vec4;
   a.o = o;
   a.lse = lse;

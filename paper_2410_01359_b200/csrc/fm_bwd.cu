@@ -283,7 +283,6 @@ __global__ void __launch_bounds__(bwd::NT, 1)
   tc_fence_after();
   // work items t = (query head of the group, visited row tile): t / nE1 selects the head
   const int nE1 = sm.n_entries;
-  auto lidx = [&](int t) { return t % nE1; };
   const int nE = nE1 * G;
   const uint32_t tbase = sm.tmem_base;
 
@@ -293,9 +292,11 @@ __global__ void __launch_bounds__(bwd::NT, 1)
     if (lane == 0 && nE > 0) {
       tma_prefetch_desc(&tmQ);
       tma_prefetch_desc(&tmdO);
-      for (int t = 0; t < nE; ++t) {
-        const int i = sm.list[lidx(t)];
-        const int hq = hk * G + t / nE1;
+      // t = g * nE1 + t1 walked with counters (a runtime division per item measured ~3 % of
+      // the backward's stall samples)
+      for (int t = 0, t1 = 0, g = 0; t < nE; ++t, (++t1 == nE1) ? (t1 = 0, ++g) : 0) {
+        const int i = sm.list[t1];
+        const int hq = hk * G + g;
         const size_t bh = static_cast<size_t>(b) * a.H + hq;
         const int st = t % C::QST;
         mbar_wait(&sm.q_empty[st], ((t / C::QST) & 1) ^ 1);
@@ -419,8 +420,7 @@ __global__ void __launch_bounds__(bwd::NT, 1)
     const int4 mv = a.vec4[(bhm * a.Tc) * 128 + key];  // this key's (LTS, len, UTS, len), normalised
     const float sl2 = a.scale_log2;
     constexpr int CH = C::CH_PER_WG;
-    for (int t = 0; t < nE; ++t) {
-      const int t1 = lidx(t);
+    for (int t = 0, t1 = 0; t < nE; ++t, t1 = (t1 + 1 == nE1) ? 0 : t1 + 1) {
       const int i = sm.list[t1];
       const bool partial = (sm.part_bits[t1 >> 5] >> (t1 & 31)) & 1u;
       const int st = t % C::QST;
@@ -587,9 +587,9 @@ __global__ void __launch_bounds__(bwd::NT, 1)
     const int t_id = wl * 32 + lane;  // TMEM lane: d index (d=128) or query (d=64)
     const uint32_t lane_off = static_cast<uint32_t>(wl * 32) << 16;
     uint32_t stage_n = 0;  // dQ staging chunks issued so far (DQT)
-    for (int t = 0; t < (a.with_dq ? nE : 0); ++t) {
-      const int i = sm.list[lidx(t)];
-      const size_t bh = static_cast<size_t>(b) * a.H + hk * G + t / nE1;
+    for (int t = 0, t1 = 0, g = 0; t < (a.with_dq ? nE : 0); ++t, (++t1 == nE1) ? (t1 = 0, ++g) : 0) {
+      const int i = sm.list[t1];
+      const size_t bh = static_cast<size_t>(b) * a.H + hk * G + g;
       const int bi = C::DQ_ALIAS ? t % C::NB : 0;
       const uint32_t boff = bi * C::BUF_STRIDE;
       mbar_wait(&sm.dq_full[bi], (t / (C::DQ_ALIAS ? C::NB : 1)) & 1);

@@ -81,6 +81,7 @@ struct Smem {
   uint8_t k[Rings<D>::KST][TILE];
   uint8_t v[Rings<D>::VST][TILE];
   int4 mask[MST][128];
+  uint32_t cw[MST][2];  // f3 refinement words of the stage's tile for Q0 / Q1 (PARTIAL only)
   uint32_t list[kMaxTc];
   uint64_t bar_q;
   uint64_t k_full[Rings<D>::KST], k_empty[Rings<D>::KST], v_full[Rings<D>::VST], v_empty[Rings<D>::VST];
@@ -152,7 +153,7 @@ __global__ void __launch_bounds__(fwd::NT, 1)
     }
   }
   if (warp == MMA_WARP) tmem_alloc<512>(&sm.tmem_base);
-  pdl_wait();  // the class map (K1b, the stream predecessor) is complete from here on
+  pdl_wait();  // the class map (K1b) and refinement words (K1c, the stream predecessor) are complete
   pdl_launch();
 
   // ---- visit list: union of the non-SKIP column tiles of Q0 and Q1 (K1 class map) ----
@@ -211,7 +212,16 @@ __global__ void __launch_bounds__(fwd::NT, 1)
         FT(11, e);
         mbar_wait(&sm.m_empty[ms], ((e / MST) & 1) ^ 1);
         if (ent_cls(ent, 0) == 1 || ent_cls(ent, 1) == 1) {
-          mbar_expect_tx(&sm.m_full[ms], 128 * 16);
+          // f3: which 32-row x 16-column sub-blocks hold a masked cell (K1c); the ragged last
+          // column tile keeps every sub-block masked (its padded keys need the bounds mask)
+#pragma unroll
+          for (int qq = 0; qq < 2; ++qq) {
+            uint32_t wq = 0xFFFFFFFFu;
+            if (a.cw != nullptr && ent_cls(ent, qq) == 1 && !(j == a.Tc - 1 && (a.N & 127) != 0))
+              wq = a.cw[(bhm * a.Tr + (qq == 0 ? i0 : i1)) * a.Tc + j];
+            sm.cw[ms][qq] = wq;
+          }
+          mbar_expect_tx(&sm.m_full[ms], 128 * 16);  // arrive (release): the words above are visible
           bulk_g2s(sm.mask[ms], vec_bh + static_cast<size_t>(j) * 128, 128 * 16, &sm.m_full[ms]);
         } else {
           mbar_arrive(&sm.m_full[ms]);
@@ -296,6 +306,9 @@ __global__ void __launch_bounds__(fwd::NT, 1)
       }
 #pragma unroll
       for (int q = 0; q < 2; ++q) {  // O_q complete: its epilogue need not wait for the other tile
+        // SEP_P: consume the last s_read phase too (already complete: P follows the read), so
+        // every mbarrier phase is observed
+        if (Layout<D>::SEP_P && pend[q] >= 0) mbar_wait(&sm.s_read[q], pv_cnt[q] & 1);
         if (pend[q] >= 0) issue_pv(q);
         mma_commit_w(&sm.o_full[q]);
       }
@@ -338,13 +351,15 @@ __global__ void __launch_bounds__(fwd::NT, 1)
         // written back to TMEM, so pass 2 is identical for PARTIAL and UNMASKED tiles.
         float mx0 = -INFINITY, mx1 = -INFINITY, mx2 = -INFINITY, mx3 = -INFINITY;
         uint32_t sr[2][16];
+        // f3: the 16-column chunks of this warp's 32 rows x 64 columns that hold a masked cell
+        const uint32_t pm = (cls == 1) ? (sm.cw[ms][q] >> (wl * 8 + hh * 4)) & 0xFu : 0u;
         tmem_ld16(tSh, sr[0]);
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
           tmem_wait_ld();
           if (c + 1 < 4) tmem_ld16(tSh + (c + 1) * 16, sr[(c + 1) & 1]);
           float* sv = reinterpret_cast<float*>(sr[c & 1]);
-          if (cls == 1) {
+          if (pm & (1u << c)) {
             // element mask of Alg. 1 lines 15-21: row r is masked for key y iff
             // (unsigned)(r - start_y) < len_y for either interval, or (causal) r < y
             const int4* mk = sm.mask[ms] + hh * 64 + c * 16;
@@ -380,7 +395,7 @@ __global__ void __launch_bounds__(fwd::NT, 1)
             mx3 = fmax3(mx3, sv[t + 6], sv[t + 7]);
           }
         }
-        if (cls == 1) tmem_wait_st();
+        if (pm) tmem_wait_st();
         const float mh = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3));
         if (row_t == 0 && q == 0 && hh == 0) FT(10, e);
         sm.xmax[q][cnt & 1][hh][row_t] = mh;

@@ -37,6 +37,7 @@ struct Workspace {
   int32_t* ext8;    // [B, Hm, Tc, 8] raw extrema (Alg. 1 line 4)
   int4* vec4;       // [B, Hm, Tc*128] normalised (LTS, LTE, UTS, UTE) per column, padded columns masked
   uint8_t* fmap;    // [B, Hm, Tr, Tc] forward kernel map (128 x 128)
+  uint32_t* cw;     // [B, Hm, Tr, Tc] f3 refinement words of the forward map (K1c; PARTIAL tiles)
   uint8_t* bmap;    // [B, Hm, Tc, Trb] backward kernel map, transposed (Brb x 128)
   float* dvec;      // [B, H, Npb] D = rowsum(dO o O)
   float* l2;        // [B, H, Npb] lse * log2(e) (+inf for empty / padded rows)
@@ -59,6 +60,7 @@ struct FwdArgs {
   int B, N, H, Hm, Tr, Tc, G;
   float scale_log2;
   const uint8_t* fmap;
+  const uint32_t* cw;  // f3 refinement words (nullptr: every sub-block of a PARTIAL tile is masked)
   const int4* vec4;
   void* o;
   float* lse;
@@ -108,6 +110,8 @@ cudaError_t launch_sliding_window(int B, int N, int w, int causal, int32_t* sri,
 cudaError_t launch_classify(const int32_t* ext8, const Dims& d, int br, int bc, uint8_t* map, int transposed,
                             int kernel_map, int64_t* counts, cudaStream_t st, int32_t* row_cnt = nullptr,
                             int32_t* col_cnt = nullptr);
+cudaError_t launch_refine(const int32_t* sri, const uint8_t* cmap, const Dims& d, uint32_t* words, int64_t* rcounts,
+                          cudaStream_t st);
 cudaError_t launch_fwd(const Dims& d, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
                        const CUtensorMap& to, const FwdArgs& a, cudaStream_t st);
 cudaError_t launch_bwd_pre(const Dims& d, const void* o, const void* dout, const float* lse, float* dvec, float* l2,

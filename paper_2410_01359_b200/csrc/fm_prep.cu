@@ -105,8 +105,9 @@ __global__ void __launch_bounds__(128) k1_expand(const int32_t* __restrict__ sri
 // tiles; row map: one JPT-byte store per row; transposed map (JPT = 1): 16 consecutive row tiles
 // of one column tile per 16-byte store.  Grid (ceil(Tc / (128 JPT)), ceil(Tr / rows_per_cta), B*Hm).
 // ---------------------------------------------------------------------------------------
-__device__ __forceinline__ int tile_class(const int4& a, const int4& b, long r0, long r1, long c0, long c1,
-                                          int causal) {
+// 32-bit arithmetic: N <= 2^30 and br, bc are clamped to [1, N] on the host, so r0 < N + br
+// and c0 < N + bc never overflow.
+__device__ __forceinline__ int tile_class(const int4& a, const int4& b, int r0, int r1, int c0, int c1, int causal) {
   if ((r0 >= a.y && r1 <= a.z) || (r0 >= b.y && r1 <= b.z) || (causal && r1 - 1 < c0)) return 0;
   if ((r1 > a.x && r0 < a.w) || (r1 > b.x && r0 < b.w) || (causal && r0 < c1 - 1)) return 1;
   return 2;
@@ -130,7 +131,7 @@ __global__ void __launch_bounds__(128) k1_classify(const int32_t* __restrict__ e
   if (threadIdx.x < 64) row_acc[threadIdx.x] = 0;
   __syncthreads();
   int4 ea[JPT], eb[JPT];
-  long c0[JPT], c1[JPT];
+  int c0[JPT], c1[JPT];
   bool valid[JPT], ragged[JPT];
 #pragma unroll
   for (int u = 0; u < JPT; ++u) {
@@ -143,8 +144,8 @@ __global__ void __launch_bounds__(128) k1_classify(const int32_t* __restrict__ e
     } else {
       ea[u] = eb[u] = make_int4(0, 0, 0, 0);
     }
-    c0[u] = static_cast<long>(j) * bc;
-    c1[u] = min(static_cast<long>(N), c0[u] + bc);
+    c0[u] = valid[u] ? j * bc : N;
+    c1[u] = c0[u] + min(bc, N - c0[u]);
     ragged[u] = kernel_map && (N % bc) != 0 && j == Tc - 1;
   }
   unsigned int c0n = 0, c1n = 0, c2n = 0;
@@ -158,7 +159,7 @@ __global__ void __launch_bounds__(128) k1_classify(const int32_t* __restrict__ e
     for (int v = 0; v < 16; ++v) {
       const int i = i16 + v;
       if (i >= iend) break;
-      const long r0 = static_cast<long>(i) * br, r1 = min(static_cast<long>(N), r0 + br);
+      const int r0 = i * br, r1 = r0 + min(br, N - r0);
       uint32_t word = 0u;
       int ns = 0;
 #pragma unroll
@@ -227,6 +228,90 @@ __global__ void __launch_bounds__(128) k1_classify(const int32_t* __restrict__ e
     atomicAdd(&row_cnt[static_cast<size_t>(bh) * Tr + ib + threadIdx.x], row_acc[threadIdx.x]);
 }
 
+// ---------------------------------------------------------------------------------------
+// K1c: f3 refinement (R31, oracle refine_chunks): for every PARTIAL 128 x 128 tile
+// the 32-bit word whose bit (8 g + c) says whether the 32-row group g x 16-column chunk c holds
+// a masked cell (real rows and columns only).  UNMASKED tiles get 0 and SKIP tiles every real
+// sub-block (rule R is sound: no / every cell masked).  One warp per (b, hm, column tile j);
+// lane = 4 consecutive columns whose expanded intervals stay in registers while the warp walks
+// the column's row tiles; one ballot per row group turns the per-column tests into chunk bits.
+// Optional counts per (b, hm): PARTIAL tiles whose word is 0 (no masked cell at all), and dirty
+// sub-blocks over all PARTIAL tiles.  Grid (ceil(Tc / 4), B*Hm), 128 threads.
+// ---------------------------------------------------------------------------------------
+__device__ __forceinline__ bool ivl_hits(int s, int e, int a, int b) { return s < e && s < b && e > a; }
+
+__global__ void __launch_bounds__(128) k1_refine(const int32_t* __restrict__ sri, const uint8_t* __restrict__ cmap,
+                                                 int N, int C, int causal, int Tr, int Tc, uint32_t* __restrict__ words,
+                                                 unsigned long long* __restrict__ rcounts) {
+  pdl_wait();
+  pdl_launch();
+  const int lane = threadIdx.x & 31;
+  const int j = blockIdx.x * 4 + (threadIdx.x >> 5);
+  const int bh = blockIdx.y;
+  if (j >= Tc) return;
+  const int32_t* base = sri + static_cast<size_t>(bh) * N * C;
+  int ls[4], le[4], us[4], ue[4], yy[4];
+  bool ok[4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    yy[u] = j * 128 + lane * 4 + u;
+    ok[u] = yy[u] < N;
+    if (ok[u]) {
+      expand_col(base + static_cast<size_t>(yy[u]) * C, C, causal, N, ls[u], le[u], us[u], ue[u]);
+    } else {
+      ls[u] = le[u] = us[u] = ue[u] = 0;
+    }
+  }
+  // real sub-blocks of this column tile (a SKIP tile has all of them dirty)
+  uint32_t colbits = 0u;
+#pragma unroll
+  for (int c = 0; c < 8; ++c)
+    if (j * 128 + c * 16 < N) colbits |= 1u << c;
+  unsigned long long n_clean = 0, n_dirty = 0;
+  for (int i = 0; i < Tr; ++i) {
+    const uint32_t cls = cmap[(static_cast<size_t>(bh) * Tr + i) * Tc + j];
+    uint32_t w = 0u;
+    if (cls == 0u) {
+#pragma unroll
+      for (int g = 0; g < 4; ++g)
+        if (i * 128 + g * 32 < N) w |= colbits << (8 * g);
+    } else if (cls == 1u) {
+#pragma unroll
+      for (int g = 0; g < 4; ++g) {
+        const int a = i * 128 + g * 32;
+        const int b = min(a + 32, N);
+        bool d = false;
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          d |= ok[u] && a < N && (ivl_hits(ls[u], le[u], a, b) || ivl_hits(us[u], ue[u], a, b) || (causal && a < yy[u]));
+        const uint32_t bal = __ballot_sync(0xffffffffu, d);
+        uint32_t byte = 0u;
+#pragma unroll
+        for (int c = 0; c < 8; ++c) byte |= ((bal >> (4 * c)) & 0xFu) ? (1u << c) : 0u;
+        w |= byte << (8 * g);
+      }
+      n_clean += (w == 0u);
+      n_dirty += __popc(w);
+    }
+    if (lane == 0) words[(static_cast<size_t>(bh) * Tr + i) * Tc + j] = w;
+  }
+  if (rcounts && lane == 0) {
+    if (n_clean) atomicAdd(&rcounts[static_cast<size_t>(bh) * 2], n_clean);
+    if (n_dirty) atomicAdd(&rcounts[static_cast<size_t>(bh) * 2 + 1], n_dirty);
+  }
+}
+
+cudaError_t launch_refine(const int32_t* sri, const uint8_t* cmap, const Dims& d, uint32_t* words, int64_t* rcounts,
+                          cudaStream_t st) {
+  if (rcounts) {
+    cudaError_t e = cudaMemsetAsync(rcounts, 0, sizeof(int64_t) * 2 * d.B * d.Hm, st);
+    if (e != cudaSuccess) return e;
+  }
+  dim3 grid((d.Tc + 3) / 4, d.B * d.Hm);
+  return launch_pdl(k1_refine, grid, dim3(128), 0, st, sri, cmap, d.N, d.C, d.causal, d.Tr, d.Tc, words,
+                    reinterpret_cast<unsigned long long*>(rcounts));
+}
+
 // Sliding-window startend_row_indices (flashmask_sliding_window_indices): one thread per key.
 __global__ void __launch_bounds__(256) k0_sliding_window(int B, int N, int w, int causal, int32_t* __restrict__ sri) {
   pdl_wait();
@@ -257,27 +342,29 @@ cudaError_t launch_expand(const int32_t* sri, const Dims& d, int bc, int32_t* ex
 
 cudaError_t launch_classify(const int32_t* ext8, const Dims& d, int br, int bc, uint8_t* map, int transposed,
                             int kernel_map, int64_t* counts, cudaStream_t st, int32_t* row_cnt, int32_t* col_cnt) {
+  br = br < d.N ? br : d.N;  // a tile taller / wider than N is the whole extent (same classes)
+  bc = bc < d.N ? bc : d.N;
   const int Tr = (d.N + br - 1) / br, Tc = (d.N + bc - 1) / bc;
   const long bhm = static_cast<long>(d.B) * d.Hm;
   cudaError_t e;
   if (counts && (e = cudaMemsetAsync(counts, 0, sizeof(int64_t) * 3 * bhm, st)) != cudaSuccess) return e;
   if (row_cnt && (e = cudaMemsetAsync(row_cnt, 0, sizeof(int32_t) * Tr * bhm, st)) != cudaSuccess) return e;
   if (col_cnt && (e = cudaMemsetAsync(col_cnt, 0, sizeof(int32_t) * Tc * bhm, st)) != cudaSuccess) return e;
-  // Row tiles per CTA: 64 on large maps, where per-CTA count atomics would otherwise contend
-  // (measured 4x on Hm = 64 heads at 128K) and the transposed map is written in 16-byte runs;
-  // small maps keep one row tile per CTA (parallelism over latency: 2.5x faster at N = 8K)
-  const long tiles = bhm * Tr * Tc;
-  const int rpc = tiles >= (4L << 20) ? 64 : (tiles >= (256L << 10) ? 16 : 1);
+  // Row tiles per CTA: enough CTAs for ~8 per SM (148 SMs), at most 64 row tiles each (the
+  // counts leave each CTA as a few atomics; the transposed map is written in 16-row runs)
+  const int jpt = transposed ? 1 : 4;
+  const long gx = (Tc + 128L * jpt - 1) / (128L * jpt);
+  long rpc = (gx * Tr * bhm + 1183) / 1184;
+  rpc = rpc < 1 ? 1 : (rpc > 64 ? 64 : rpc);
+  if (transposed && rpc > 8) rpc = (rpc + 15) / 16 * 16;
   const int ns = (d.flags & 1) ? 1 : 0;
   auto cnt64 = reinterpret_cast<unsigned long long*>(counts);
-  if (transposed) {
-    dim3 grid((Tc + 127) / 128, (Tr + rpc - 1) / rpc, static_cast<unsigned>(bhm));
+  dim3 grid(static_cast<unsigned>(gx), static_cast<unsigned>((Tr + rpc - 1) / rpc), static_cast<unsigned>(bhm));
+  if (transposed)
     return launch_pdl(k1_classify<1>, grid, dim3(128), 0, st, ext8, d.N, d.causal, br, bc, Tr, Tc, map, transposed,
-                      kernel_map, ns, cnt64, row_cnt, col_cnt, rpc);
-  }
-  dim3 grid((Tc + 511) / 512, (Tr + rpc - 1) / rpc, static_cast<unsigned>(bhm));
+                      kernel_map, ns, cnt64, row_cnt, col_cnt, static_cast<int>(rpc));
   return launch_pdl(k1_classify<4>, grid, dim3(128), 0, st, ext8, d.N, d.causal, br, bc, Tr, Tc, map, transposed,
-                    kernel_map, ns, cnt64, row_cnt, col_cnt, rpc);
+                    kernel_map, ns, cnt64, row_cnt, col_cnt, static_cast<int>(rpc));
 }
 
 // ---------------------------------------------------------------------------------------

@@ -20,14 +20,15 @@ FM_BF16, FM_FP32, FM_FP16 = 0, 1, 2
 FM_TILE_SKIP, FM_TILE_PARTIAL, FM_TILE_UNMASKED = 0, 1, 2
 FM_FLAG_NO_SKIP = 1
 FM_FLAG_DETERMINISTIC = 2
+FM_FLAG_NO_REFINE = 4
 FM_PASS_FWD, FM_PASS_BWD = 0, 1
 
-EXPORTED = ["flashmask_workspace_size", "flashmask_classify", "flashmask_fwd", "flashmask_bwd",
+EXPORTED = ["flashmask_workspace_size", "flashmask_classify", "flashmask_refine", "flashmask_fwd", "flashmask_bwd",
             "flashmask_status_string", "flashmask_last_error", "flashmask_timing_enable", "flashmask_timing_collect",
             "flashmask_sliding_window_indices"]
-KERNEL_NAMES = ["expand", "classify", "fwd", "bwd_pre", "bwd", "dq_convert", "dq"]
+KERNEL_NAMES = ["expand", "classify", "fwd", "bwd_pre", "bwd", "dq_convert", "dq", "refine"]
 (FM_KERNEL_EXPAND, FM_KERNEL_CLASSIFY, FM_KERNEL_FWD, FM_KERNEL_BWD_PRE, FM_KERNEL_BWD, FM_KERNEL_DQ_CONVERT,
- FM_KERNEL_DQ) = range(7)
+ FM_KERNEL_DQ, FM_KERNEL_REFINE) = range(8)
 
 
 class FmParams(ctypes.Structure):
@@ -53,6 +54,8 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.flashmask_workspace_size.restype = sz
     lib.flashmask_classify.argtypes = [P, vp, i32, i32, vp, vp, vp, vp, vp, vp]
     lib.flashmask_classify.restype = ctypes.c_int
+    lib.flashmask_refine.argtypes = [P, vp, vp, vp, vp, vp]
+    lib.flashmask_refine.restype = ctypes.c_int
     lib.flashmask_fwd.argtypes = [P, vp, vp, vp, vp, vp, vp, vp, sz, vp]
     lib.flashmask_fwd.restype = ctypes.c_int
     lib.flashmask_bwd.argtypes = [P, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp]
@@ -169,6 +172,27 @@ def flashmask_classify(sri: torch.Tensor, causal: bool, br: int = 128, bc: int =
     if nonskip:
         return minmax, cmap, counts, rows, cols
     return minmax, cmap, counts
+
+
+def flashmask_refine(sri: torch.Tensor, causal: bool, class_map: torch.Tensor | None = None, stream=None):
+    """f3 refinement (K1c): uint32 [B, Hm, Tr, Tc] words, bit 8g+c set iff the 32-row group g x
+    16-column chunk c of the 128 x 128 tile holds a masked cell; and int64 [B, Hm, 2] counts
+    (PARTIAL tiles without any masked cell, dirty sub-blocks of PARTIAL tiles).  class_map: the
+    128 x 128 map of flashmask_classify (computed here when None)."""
+    B, Hm, N, C = sri.shape
+    _check_sri(sri, B, N, "flashmask_refine", sri.device)
+    if class_map is None:
+        _, class_map, _ = flashmask_classify(sri, causal, 128, 128, stream=stream)
+    T = -(-N // 128)
+    _check_tensor(class_map, "class_map", "flashmask_refine", (B, Hm, T, T), (torch.uint8,), sri.device)
+    p = FmParams(batch=B, seqlen=N, num_heads=Hm, head_dim=128, mask_heads=Hm, mask_cols=C,
+                 causal=int(bool(causal)), scale=0.0, in_dtype=FM_BF16, out_dtype=FM_BF16, flags=0)
+    words = torch.empty(B, Hm, T, T, dtype=torch.int32, device=sri.device)   # uint32 bit patterns
+    counts = torch.empty(B, Hm, 2, dtype=torch.int64, device=sri.device)
+    with torch.cuda.device(sri.device):
+        _check(_lib.flashmask_refine(ctypes.byref(p), _ptr(sri), _ptr(class_map), _ptr(words), _ptr(counts),
+                                     _stream(stream, sri.device)), "flashmask_refine")
+    return words, counts
 
 
 def flashmask_sliding_window_indices(batch: int, seqlen: int, window: int, causal: bool = True, device="cuda",

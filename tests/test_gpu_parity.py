@@ -696,3 +696,43 @@ def test_binding_rejects_bad_tensors(fmlib):
     with pytest.raises(E, match="shape"):
         fmlib.flashmask_bwd(q, k, v, o32, do, lse[:, :1], sri, True)
 
+
+
+# ------------------------------------------------------------------ f3 refinement (K1c)
+REFINE_CASES = [(fam, N) for fam in wm.FAMILIES for N in (129, 700)] + \
+               [("qk_sparse", 4096), ("random_eviction", 4096), ("causal_blockwise", 4096), ("document", 4096)]
+
+
+@pytest.mark.parametrize("fam,N", REFINE_CASES)
+def test_refine_words_bit_exact(fmlib, fam, N):
+    """f3 (R31): the refinement words of every tile equal the oracle's refine_chunks bit for
+    bit, and the counts (PARTIAL tiles without a masked cell, dirty sub-blocks) follow."""
+    rng = np.random.default_rng(N + 7 * len(fam))
+    masks = [wm.sample_family(fam, N, rng, (2, 6)) for _ in range(2)]
+    sri = torch.from_numpy(wm.stack(masks, 1)).cuda()
+    words, counts = fmlib.flashmask_refine(sri, masks[0].causal)
+    torch.cuda.synchronize()
+    for b, m in enumerate(masks):
+        vec = fo.expand(m.sri, m.causal, N)
+        ref = fo.refine_chunks(vec)
+        cm, _, _ = fo.classify(vec, 128, 128)
+        got = words[b, 0].cpu().numpy().view(np.uint32)
+        assert np.array_equal(got, ref), np.argwhere(got != ref)[:5]
+        part = cm == fo.PARTIAL
+        clean = int((ref[part] == 0).sum())
+        dirty = int(sum(bin(int(w)).count("1") for w in ref[part]))
+        assert counts[b, 0].tolist() == [clean, dirty]
+
+
+@pytest.mark.parametrize("fam,N,d", [("qk_sparse", 1000, 128), ("random_eviction", 777, 64), ("causal_document", 900, 128),
+                                     ("global_sliding_window", 640, 64), ("hash_sparse", 513, 128)])
+def test_refine_forward_bitwise(fmlib, fam, N, d):
+    """Masking only the dirty sub-blocks of PARTIAL tiles is exact: O and lse are bitwise those
+    of the unrefined forward (FM_FLAG_NO_REFINE), both vs the oracle."""
+    _, _, _, r0 = _run(fmlib, fam, N, d, 1, 2, seed=9)
+    masks, sri, t, r1 = _run(fmlib, fam, N, d, 1, 2, seed=9, flags=fmlib.FM_FLAG_NO_REFINE)
+    assert torch.equal(r0[0], r1[0]) and torch.equal(r0[1], r1[1])
+    for h in range(2):
+        O, L, _ = oracle_head(t, masks, sri.numpy(), 0, h, 1, masks[0].causal, with_grad=False)
+        assert_close(f"O[{h}]", r0[0][0, :, h].cpu().numpy(), O)
+        assert_lse(r0[1][0, h].cpu().numpy(), L)
