@@ -55,6 +55,10 @@ namespace fm { __device__ long long g_fm_trace_fwd[64 * 16]; __device__ long lon
 #define FM_POLY_PAIRS 3  // of every 8 column pairs, how many use the FMA-pipe exp2 (rest: MUFU)
 #endif
 
+#ifndef FM_FWD_REFINE
+#define FM_FWD_REFINE 1  // f3: mask only the dirty 32 x 16 sub-blocks of PARTIAL tiles (K1c words)
+#endif
+
 namespace fm {
 
 namespace fwd {
@@ -217,7 +221,7 @@ __global__ void __launch_bounds__(fwd::NT, 1)
 #pragma unroll
           for (int qq = 0; qq < 2; ++qq) {
             uint32_t wq = 0xFFFFFFFFu;
-            if (a.cw != nullptr && ent_cls(ent, qq) == 1 && !(j == a.Tc - 1 && (a.N & 127) != 0))
+            if (FM_FWD_REFINE && a.cw != nullptr && ent_cls(ent, qq) == 1 && !(j == a.Tc - 1 && (a.N & 127) != 0))
               wq = a.cw[(bhm * a.Tr + (qq == 0 ? i0 : i1)) * a.Tc + j];
             sm.cw[ms][qq] = wq;
           }
@@ -299,7 +303,11 @@ __global__ void __launch_bounds__(fwd::NT, 1)
             mma_commit_w(&sm.s_full[q]);
             if (lane == 0) FT(6 + q, e);
           }
-          if (Layout<D>::SEP_P && pend[q] >= 0) issue_pv(q);
+          if (Layout<D>::SEP_P && pend[q] >= 0) {
+            // every s_read phase is observed, also when no S_q(e) follows (tile SKIP for q)
+            if (ent_cls(ent, q) == 0) mbar_wait(&sm.s_read[q], pv_cnt[q] & 1);
+            issue_pv(q);
+          }
           if (ent_cls(ent, q) != 0) pend[q] = e;
         }
         mma_commit_w(&sm.k_empty[ks]);
@@ -352,7 +360,7 @@ __global__ void __launch_bounds__(fwd::NT, 1)
         float mx0 = -INFINITY, mx1 = -INFINITY, mx2 = -INFINITY, mx3 = -INFINITY;
         uint32_t sr[2][16];
         // f3: the 16-column chunks of this warp's 32 rows x 64 columns that hold a masked cell
-        const uint32_t pm = (cls == 1) ? (sm.cw[ms][q] >> (wl * 8 + hh * 4)) & 0xFu : 0u;
+        const uint32_t pm = (cls != 1) ? 0u : (FM_FWD_REFINE ? (sm.cw[ms][q] >> (wl * 8 + hh * 4)) & 0xFu : 0xFu);
         tmem_ld16(tSh, sr[0]);
 #pragma unroll
         for (int c = 0; c < 4; ++c) {

@@ -146,7 +146,7 @@ __global__ void __launch_bounds__(128) k1_classify(const int32_t* __restrict__ e
     }
     c0[u] = valid[u] ? j * bc : N;
     c1[u] = c0[u] + min(bc, N - c0[u]);
-    ragged[u] = kernel_map && (N % bc) != 0 && j == Tc - 1;
+    ragged[u] = kernel_map == 2 && j == Tc - 1;  // kernel_map = 2: N is not a multiple of bc
   }
   unsigned int c0n = 0, c1n = 0, c2n = 0;
   int colns[JPT];
@@ -268,8 +268,13 @@ __global__ void __launch_bounds__(128) k1_refine(const int32_t* __restrict__ sri
   for (int c = 0; c < 8; ++c)
     if (j * 128 + c * 16 < N) colbits |= 1u << c;
   unsigned long long n_clean = 0, n_dirty = 0;
+  uint32_t cls32 = 0u;  // classes of row tiles [i & ~31, +32): lane l holds row (i & ~31) + l
   for (int i = 0; i < Tr; ++i) {
-    const uint32_t cls = cmap[(static_cast<size_t>(bh) * Tr + i) * Tc + j];
+    if ((i & 31) == 0) {  // one strided load per lane instead of a dependent load per row tile
+      const int il = i + lane;
+      cls32 = il < Tr ? cmap[(static_cast<size_t>(bh) * Tr + il) * Tc + j] : 0u;
+    }
+    const uint32_t cls = __shfl_sync(0xffffffffu, cls32, i & 31);
     uint32_t w = 0u;
     if (cls == 0u) {
 #pragma unroll
@@ -342,6 +347,8 @@ cudaError_t launch_expand(const int32_t* sri, const Dims& d, int bc, int32_t* ex
 
 cudaError_t launch_classify(const int32_t* ext8, const Dims& d, int br, int bc, uint8_t* map, int transposed,
                             int kernel_map, int64_t* counts, cudaStream_t st, int32_t* row_cnt, int32_t* col_cnt) {
+  // the kernels' maps mark a ragged last column tile PARTIAL (bounds mask): decided on the tile size
+  const int km = kernel_map ? ((d.N % bc) != 0 ? 2 : 1) : 0;
   br = br < d.N ? br : d.N;  // a tile taller / wider than N is the whole extent (same classes)
   bc = bc < d.N ? bc : d.N;
   const int Tr = (d.N + br - 1) / br, Tc = (d.N + bc - 1) / bc;
@@ -352,19 +359,16 @@ cudaError_t launch_classify(const int32_t* ext8, const Dims& d, int br, int bc, 
   if (col_cnt && (e = cudaMemsetAsync(col_cnt, 0, sizeof(int32_t) * Tc * bhm, st)) != cudaSuccess) return e;
   // Row tiles per CTA: enough CTAs for ~8 per SM (148 SMs), at most 64 row tiles each (the
   // counts leave each CTA as a few atomics; the transposed map is written in 16-row runs)
-  const int jpt = transposed ? 1 : 4;
-  const long gx = (Tc + 128L * jpt - 1) / (128L * jpt);
+  // (one column tile per thread: 4 per thread halved the CTA count and measured 1.3-1.9x slower)
+  const long gx = (Tc + 127) / 128;
   long rpc = (gx * Tr * bhm + 1183) / 1184;
   rpc = rpc < 1 ? 1 : (rpc > 64 ? 64 : rpc);
   if (transposed && rpc > 8) rpc = (rpc + 15) / 16 * 16;
   const int ns = (d.flags & 1) ? 1 : 0;
   auto cnt64 = reinterpret_cast<unsigned long long*>(counts);
   dim3 grid(static_cast<unsigned>(gx), static_cast<unsigned>((Tr + rpc - 1) / rpc), static_cast<unsigned>(bhm));
-  if (transposed)
-    return launch_pdl(k1_classify<1>, grid, dim3(128), 0, st, ext8, d.N, d.causal, br, bc, Tr, Tc, map, transposed,
-                      kernel_map, ns, cnt64, row_cnt, col_cnt, static_cast<int>(rpc));
-  return launch_pdl(k1_classify<4>, grid, dim3(128), 0, st, ext8, d.N, d.causal, br, bc, Tr, Tc, map, transposed,
-                    kernel_map, ns, cnt64, row_cnt, col_cnt, static_cast<int>(rpc));
+  return launch_pdl(k1_classify<1>, grid, dim3(128), 0, st, ext8, d.N, d.causal, br, bc, Tr, Tc, map, transposed, km,
+                    ns, cnt64, row_cnt, col_cnt, static_cast<int>(rpc));
 }
 
 // ---------------------------------------------------------------------------------------

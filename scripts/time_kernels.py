@@ -17,7 +17,7 @@ tot = {}
 F = 0.0
 for c in calls:
     x = bench.make_inputs(c, dev)
-    ff, fb, _ = bench.effective_flops(c, fm)
+    ff, fb = bench.effective_flops(c, fm)[:2]
     o, lse = fm.flashmask_fwd(x["q"], x["k"], x["v"], x["sri"], c["causal"])
     fm.flashmask_bwd(x["q"], x["k"], x["v"], o, x["do"], lse, x["sri"], c["causal"], flags=flags)
     torch.cuda.synchronize()
