@@ -28,7 +28,7 @@ for N in (8192, 32768, 131072):
         k = torch.randn(1, N, Hkv, d, generator=g, device=dev).to(torch.bfloat16)
         v = torch.randn(1, N, Hkv, d, generator=g, device=dev).to(torch.bfloat16)
         call = dict(masks=[m], causal=m.causal, B=1, N=N, H=H, d=d, heads=range(H), batch_ids=[0])
-        ff, _, rho = bench.effective_flops(call, fm)
+        ff, _, rho = bench.effective_flops(call, fm)[:3]
         for _ in range(3):
             fm.flashmask_fwd(q, k, v, sri, m.causal)
         torch.cuda.synchronize()

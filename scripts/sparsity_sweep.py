@@ -28,7 +28,7 @@ for bk in buckets:
         m = bench.sft_mask_in_bucket(N, bk[0], bk[1], 7, rho_fn)
     call = dict(masks=[m], causal=m.causal, B=1, N=N, H=H, d=d, heads=range(H), batch_ids=[0])
     x = bench.make_inputs(call, dev)
-    ff, fb, rho = bench.effective_flops(call, fm)
+    ff, fb, rho = bench.effective_flops(call, fm)[:3]
     for _ in range(2):
         o, lse = fm.flashmask_fwd(x["q"], x["k"], x["v"], x["sri"], m.causal)
         fm.flashmask_bwd(x["q"], x["k"], x["v"], o, x["do"], lse, x["sri"], m.causal)

@@ -14,7 +14,7 @@ calls, conf, _ = bench.build_workload(cfg, 0, 1, bench.rho_gpu(fm))
 dev = torch.device("cuda", 0)
 for c in calls[:1]:
     x = bench.make_inputs(c, dev)
-    ff, fb, _ = bench.effective_flops(c, fm)
+    ff, fb, _ = bench.effective_flops(c, fm)[:3]
     o, lse = fm.flashmask_fwd(x["q"], x["k"], x["v"], x["sri"], c["causal"])
     fm.flashmask_bwd(x["q"], x["k"], x["v"], o, x["do"], lse, x["sri"], c["causal"])
     torch.cuda.synchronize()
