@@ -1,6 +1,6 @@
 """Interleaved A/B of library builds in ONE process (same clocks, same inputs):
 
-    python scripts/ab_libs.py CFG[,CFG...] libA.so libB.so [...] [--rounds R] [--flags F] [--fwd-only]
+    python scripts/ab_libs.py "CFG[;CFG...]" libA.so libB.so[@FLAGS] [...] [--rounds R] [--fwd-only]
 
 Every library is loaded as its own instance of the ctypes binding; the rounds alternate
 A, B, A, B, ... and each round times K2 and K4 of every call with the library's CUDA-event timing
@@ -36,11 +36,13 @@ def main():
     ap.add_argument("--flags", type=int, default=0)
     ap.add_argument("--fwd-only", action="store_true")
     args = ap.parse_args()
-    libs = [p if os.path.isabs(p) else os.path.join(ROOT, "paper_2410_01359_b200", p) for p in args.libs]
+    flags = [int(p.split("@")[1]) if "@" in p else args.flags for p in args.libs]
+    libs = [p.split("@")[0] for p in args.libs]
+    libs = [p if os.path.isabs(p) else os.path.join(ROOT, "paper_2410_01359_b200", p) for p in libs]
     mods = [load_binding(p, i) for i, p in enumerate(libs)]
     dev = torch.device("cuda", 0)
     ref = mods[0]
-    for cfg in args.cfgs.split(","):
+    for cfg in args.cfgs.split(";"):
         calls, _, _ = bench.build_workload(cfg, 0, 1, bench.rho_gpu(ref))
         for c in calls:
             r = bench.Runner(ref, [c], dev)
@@ -48,21 +50,22 @@ def main():
             o, lse, dq, dk, dv = r.outs[0]
             res = {i: {"fwd": [], "bwd": []} for i in range(len(mods))}
 
-            def run(m):
+            def run(i):
+                m = mods[i]
                 m.flashmask_fwd(x["q"], x["k"], x["v"], x["sri"], c["causal"], out=o, lse=lse, workspace=r.ws_f[0],
-                                flags=args.flags)
+                                flags=flags[i])
                 if not args.fwd_only:
                     m.flashmask_bwd(x["q"], x["k"], x["v"], o, x["do"], lse, x["sri"], c["causal"], dq=dq, dk=dk,
-                                    dv=dv, workspace=r.ws_b[0], flags=args.flags)
+                                    dv=dv, workspace=r.ws_b[0], flags=flags[i])
 
-            for m in mods:
-                run(m)
+            for i in range(len(mods)):
+                run(i)
             torch.cuda.synchronize()
             for _ in range(args.rounds):
                 for i, m in enumerate(mods):
                     m.flashmask_timing_enable(True, kernels=[m.FM_KERNEL_FWD, m.FM_KERNEL_BWD])
                     for _ in range(args.reps):
-                        run(m)
+                        run(i)
                     torch.cuda.synchronize()
                     m.flashmask_timing_enable(False)
                     t = m.flashmask_timing_collect()
