@@ -330,7 +330,8 @@ fm_status flashmask_fwd(const fm_params* p, const void* q, const void* k, const 
   if (e != cudaSuccess) return cuda_fail(e, "expand");
   e = timed(FM_KERNEL_CLASSIFY, st, [&] { return fm::launch_classify(w.ext8, d, fm::kTile, fm::kTile, w.fmap, 0, 1, nullptr, st); });
   if (e != cudaSuccess) return cuda_fail(e, "classify");
-  const bool refine = (p->flags & FM_FLAG_NO_REFINE) == 0;
+  // f3 refinement: consumed by the causal forward kernels (fm_fwd.cu FM_FWD_REFINE)
+  const bool refine = d.causal && (p->flags & FM_FLAG_NO_REFINE) == 0;
   if (refine) {
     e = timed(FM_KERNEL_REFINE, st, [&] { return fm::launch_refine(sri, w.fmap, d, w.cw, nullptr, st); });
     if (e != cudaSuccess) return cuda_fail(e, "refine");

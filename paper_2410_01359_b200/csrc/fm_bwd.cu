@@ -55,11 +55,6 @@ namespace fm { __device__ long long g_fm_trace[64 * 16]; __device__ long long g_
 #ifndef FM_BWD_KA
 #define FM_BWD_KA 1  // K_j as TMEM A operand of S^T (single P/dS TMEM buffer): +2-3 % since the dQ stages moved
 #endif
-
-#ifndef FM_BWD_DQ_IN_S
-#define FM_BWD_DQ_IN_S 0  // d=128: dQ^T accumulates in the S^T columns (see Cfg::DQ_IN_S)
-#endif
-
 namespace fm {
 
 namespace bwd {
@@ -111,18 +106,13 @@ struct Cfg {
   // d=128: two P/dS column buffers, so the compute WGs write P/dS(t+1) while dV/dK/dQ(t) still
   // read buffer t; dQ^T(t) reuses the 64 columns of its own buffer (written after dV/dK(t)).
   static constexpr int NB = (D == 128 && !KA_TMEM) ? 2 : 1;
-  // d=128 option: dQ^T(t) lands in the S^T columns (free once the compute WGs hold S^T(t+1) in
-  // registers) instead of the P/dS columns, so the compute WGs store P/dS(t+1) as soon as
-  // dV/dK(t) have read P/dS(t), without waiting for the dQ WG to drain dQ^T(t); S^T/dP^T(t+2)
-  // then waits for that drain instead.
-  static constexpr bool DQ_IN_S = (D == 128) && KA_TMEM && (FM_BWD_DQ_IN_S != 0);
-  static constexpr bool DQ_ALIAS = !DQ_IN_S && ((D == 64) || KA_TMEM || NB == 2);  // dQ shares the P/dS columns
+  static constexpr bool DQ_ALIAS = (D == 64) || KA_TMEM || NB == 2;  // dQ shares the P/dS columns
   static constexpr int KV_TILE = 128 * D * 2;      // bytes
   static constexpr int Q_TILE = BR * D * 2;
   static constexpr int DS_BYTES = 128 * BR * 2;
   static constexpr int CH_PER_WG = BR / 64;        // 32-query chunks per compute WG
   static constexpr int S_COL = 0, DP_COL = BR, P_COL = 2 * BR, DS_COL = 2 * BR + BR / 2;
-  static constexpr int DQ_COL = DQ_IN_S ? S_COL : (DQ_ALIAS ? P_COL : 192);
+  static constexpr int DQ_COL = DQ_ALIAS ? P_COL : 192;
   static constexpr int BUF_STRIDE = BR;  // column offset of P/dS/dQ buffer 1 (NB == 2)
   // Option: dK += dS^T Q reads dS^T from the shared-memory buffer the dQ GEMM uses anyway (SS,
   // N = 128) instead of a TMEM copy.  It balances the sub-partitions (TS operand reads slow the
@@ -344,10 +334,7 @@ __global__ void __launch_bounds__(bwd::NT, 1)
         }
         for (int t = 0; t < nE; ++t) {
           const int st = t % C::QST;
-          if (t > 0) FM_BWD_ISSUER_WAIT(&sm.sdp_free, (t - 1) & 1);  // compute WGs hold S^T/dP^T(t-1) in registers
-          // DQ_IN_S: dQ^T(t-2) (written into the S^T columns after S^T(t-1) was read) is drained
-          if (C::DQ_IN_S && a.with_dq && t > 1) FM_BWD_ISSUER_WAIT(&sm.dq_empty[0], t & 1);
-          if (lane == 0) FM_T(1, t);
+          if (t > 0) FM_BWD_ISSUER_WAIT(&sm.sdp_free, (t - 1) & 1);  // compute WGs hold S^T/dP^T(t-1) in registers          if (lane == 0) FM_T(1, t);
           FM_BWD_ISSUER_WAIT(&sm.q_full[st], (t / C::QST) & 1);
           if (lane == 0) FM_T(14, t);
           tc_fence_after();
@@ -403,10 +390,7 @@ __global__ void __launch_bounds__(bwd::NT, 1)
             if constexpr (C::DK_SS) mma_commit_w(&sm.ds_empty[t % C::NDS]);  // dK(t) read dS^T(t)
             continue;
           }
-          if constexpr (!C::DQ_ALIAS) FM_BWD_ISSUER_WAIT(&sm.dq_empty[0], (t & 1) ^ 1);
-          // DQ_IN_S: dQ^T(t) overwrites the S^T columns once the compute WGs hold S^T(t+1)
-          if (C::DQ_IN_S && t + 1 < nE) FM_BWD_ISSUER_WAIT(&sm.sdp_free, (t + 1) & 1);
-          tc_fence_after();
+          if constexpr (!C::DQ_ALIAS) FM_BWD_ISSUER_WAIT(&sm.dq_empty[0], (t & 1) ^ 1);          tc_fence_after();
           const uint32_t ds_addr = smem_u32(sm.ds[t % C::NDS]);
 #pragma unroll
           for (int kk = 0; kk < 8; ++kk) {
