@@ -7,7 +7,7 @@ import subprocess
 import sys
 
 R = sys.argv[1] if len(sys.argv) > 1 else "profiles/r01"
-G = "gpurun_out"
+G = sys.argv[2] if len(sys.argv) > 2 else "gpurun_out"
 for f in ("bench_C3", "bench_C2", "bench_C4", "bench_C3_reference"):
     lines = [l for l in open(f"{G}/{f}.json").read().splitlines() if l.strip().startswith("{")]
     open(f"{R}/{f}.json", "w").write(lines[-1] + "\n")
@@ -24,10 +24,11 @@ for name, rep, note in [
         ("ncu_k1_summary.md", "prof_k1", "K1a expand / K1b classify, C3"),
         ("ncu_k35_summary.md", "prof_k35", "K3 backward preprocess and K5 dQ convert, C3 (HBM-bound: compare dram bytes / duration with MEASURED_PEAKS hbm_gbs)")]:
     open(f"{R}/{name}", "w").write(note + "\n\n" + run("report", f"{G}/{rep}.ncu-rep"))
-sweep = subprocess.run(["python", "scripts/sweep_table.py", f"{G}/c5_sweep.txt"], capture_output=True, text=True).stdout
-open(f"{R}/c5_sweep.md", "w").write(
-    "C5 kernel sweep (App. A.5.2 shapes: 128K tokens, hidden 4096), `scripts/time_kernels.py C5:<N>:<d> 3`,\n"
-    "CUDA events per kernel; fwd = K2, bwd = K4 (K1/K3/K5 excluded here, included in bench.py lines).\n\n" + sweep)
+if os.path.exists(f"{G}/c5_sweep.txt"):
+    sweep = subprocess.run(["python", "scripts/sweep_table.py", f"{G}/c5_sweep.txt"], capture_output=True, text=True).stdout
+    open(f"{R}/c5_sweep.md", "w").write(
+        "C5 kernel sweep (App. A.5.2 shapes: 128K tokens, hidden 4096), `scripts/time_kernels.py C5:<N>:<d> 3`,\n"
+        "CUDA events per kernel; fwd = K2, bwd = K4 (K1/K3/K5 excluded here, included in bench.py lines).\n\n" + sweep)
 
 
 def metric(path, key):
