@@ -87,7 +87,12 @@ enum {
   /* flashmask_fwd: do not run the f3 refinement (K1c, flashmask_refine below); every element of
    * a PARTIAL tile is then masked element-wise as in Alg. 1 lines 15-21.  Outputs are bitwise
    * identical either way (masking a sub-block with no masked cell changes nothing). */
-  FM_FLAG_NO_REFINE = 4
+  FM_FLAG_NO_REFINE = 4,
+  /* flashmask_fwd, head_dim 128: run the forward on CTA pairs (K2b, tcgen05 cta_group::2: each
+   * SM holds one query tile and half of every K/V tile, three S accumulators in TMEM) instead of
+   * the single-SM kernel K2a.  Same results to rounding order (every output within the parity
+   * tolerances of the single-SM kernel). */
+  FM_FLAG_FWD_PAIR = 8
 };
 
 typedef struct {

@@ -10,7 +10,7 @@ import sys
 PKG = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libflashmask.so")
-SOURCES = ["fm_api.cu", "fm_prep.cu", "fm_fwd.cu", "fm_bwd.cu", "fm_dq.cu", "fm_f32.cu"]
+SOURCES = ["fm_api.cu", "fm_prep.cu", "fm_fwd.cu", "fm_fwd2.cu", "fm_bwd.cu", "fm_dq.cu", "fm_f32.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-std=c++17", "-O3", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
          "--expt-relaxed-constexpr"]

@@ -344,7 +344,13 @@ fm_status flashmask_fwd(const fm_params* p, const void* q, const void* k, const 
   a.vec4 = w.vec4;
   a.o = o;
   a.lse = lse;
-  e = timed(FM_KERNEL_FWD, st, [&] { return fm::launch_fwd(d, tq, tk, tv, to, a, st); });
+  if ((p->flags & FM_FLAG_FWD_PAIR) && d.D == 128) {
+    CUtensorMap tk64;
+    if (!make_map(&tk64, k, d, d.Hkv, 64, &err)) return fail(FM_ERR_CUDA, err);
+    e = timed(FM_KERNEL_FWD, st, [&] { return fm::launch_fwd2(d, tq, tk64, tv, to, a, st); });
+  } else {
+    e = timed(FM_KERNEL_FWD, st, [&] { return fm::launch_fwd(d, tq, tk, tv, to, a, st); });
+  }
   if (e != cudaSuccess) return cuda_fail(e, "forward kernel");
   return FM_OK;
 }

@@ -114,6 +114,8 @@ cudaError_t launch_refine(const int32_t* sri, const uint8_t* cmap, const Dims& d
                           cudaStream_t st);
 cudaError_t launch_fwd(const Dims& d, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
                        const CUtensorMap& to, const FwdArgs& a, cudaStream_t st);
+cudaError_t launch_fwd2(const Dims& d, const CUtensorMap& tq, const CUtensorMap& tk64, const CUtensorMap& tv,
+                        const CUtensorMap& to, const FwdArgs& a, cudaStream_t st);
 cudaError_t launch_bwd_pre(const Dims& d, const void* o, const void* dout, const float* lse, float* dvec, float* l2,
                            float* dqacc, cudaStream_t st);
 cudaError_t launch_bwd(const Dims& d, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,

@@ -93,6 +93,13 @@ FM_DEV void mbar_wait_spin(uint64_t* bar, uint32_t parity) {
   while (!mbar_test_wait(bar, parity)) {
   }
 }
+// Poll with a short sleep between tests: wakes within ~the sleep time of the phase completing
+// (a suspended try_wait was measured to wake hundreds of ns late when the phase is completed by
+// tcgen05.commit or by arrivals from another CTA) without spending issue slots on a tight spin.
+template <int NS>
+FM_DEV void mbar_wait_nap(uint64_t* bar, uint32_t parity) {
+  while (!mbar_test_wait(bar, parity)) __nanosleep(NS);
+}
 
 // ------------------------------------------------------------------ named barriers
 FM_DEV void named_bar_sync(uint32_t id, uint32_t nthreads) {
@@ -294,6 +301,92 @@ __host__ __device__ constexpr uint32_t idesc_bf16(int M, int N, int a_mn, int b_
 template <bool F16>
 __host__ __device__ constexpr uint32_t idesc16(int M, int N, int a_mn, int b_mn) {
   return F16 ? (idesc_bf16(M, N, a_mn, b_mn) & ~((7u << 7) | (7u << 10))) : idesc_bf16(M, N, a_mn, b_mn);
+}
+
+// ------------------------------------------------------------------ CTA pairs (cta_group::2)
+// A 2-CTA cluster whose two SMs execute tcgen05.mma.cta_group::2 together: M = 256 rows, each
+// CTA holding its 128 rows of A and D (TMEM) and half of the N columns of B (shared memory);
+// the leader (rank 0) issues every MMA and commit.
+FM_DEV uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+FM_DEV void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// shared::cluster address of the same shared variable in CTA `rank` of the cluster
+FM_DEV uint32_t mapa_shared(const void* p, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
+  return r;
+}
+// arrive on an mbarrier given by its shared::cluster address (possibly the peer CTA's).  Default
+// (.release.cta) semantics: what the arrival publishes is TMEM written by tcgen05.st, ordered by
+// tcgen05.wait::st + fence::before_thread_sync on this side and fence::after_thread_sync on the
+// MMA-issuing side.  A .release.cluster arrive was measured to cost ~1-2 K clk per arrival
+// (the thread waits for a cluster-scope fence).
+FM_DEV void mbar_arrive_cluster(uint32_t cl_addr) {
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cl_addr) : "memory");
+}
+// 4-D TMA tile load into this CTA's shared memory whose completion (bytes) is signalled on the
+// mbarrier at shared::cluster address `cl_bar` (the leader CTA's barrier).
+FM_DEV void tma_load_4d_pair(void* smem_dst, const CUtensorMap* m, uint32_t cl_bar, int c0, int c1, int c2, int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(cl_bar), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
+template <int NCOLS>
+FM_DEV void tmem_alloc_pair(uint32_t* dst_smem) {
+  asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst_smem)),
+               "n"(NCOLS)
+               : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+}
+template <int NCOLS>
+FM_DEV void tmem_dealloc_pair(uint32_t taddr) {
+  asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "n"(NCOLS) : "memory");
+}
+FM_DEV void mma2_ss_w(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+FM_DEV void mma2_ts_w(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// commit of the pair's MMAs: arrive on the mbarrier at the same offset in both CTAs (mask 0b11)
+FM_DEV void mma2_commit_mc_w(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      ".reg .b16 m;\n\t"
+      "mov.b16 m, 3;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], m;\n\t}" ::"r"(
+          smem_u32(bar))
+      : "memory");
+}
+
+// commit of the pair's MMAs to the barrier at the same offset in the CTAs of `mask` (bit = rank)
+FM_DEV void mma2_commit_w(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}" ::"r"(
+          smem_u32(bar)), "h"(mask)
+      : "memory");
 }
 
 // ------------------------------------------------------------------ math

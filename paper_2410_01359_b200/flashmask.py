@@ -21,6 +21,7 @@ FM_TILE_SKIP, FM_TILE_PARTIAL, FM_TILE_UNMASKED = 0, 1, 2
 FM_FLAG_NO_SKIP = 1
 FM_FLAG_DETERMINISTIC = 2
 FM_FLAG_NO_REFINE = 4
+FM_FLAG_FWD_PAIR = 8
 FM_PASS_FWD, FM_PASS_BWD = 0, 1
 
 EXPORTED = ["flashmask_workspace_size", "flashmask_classify", "flashmask_refine", "flashmask_fwd", "flashmask_bwd",
