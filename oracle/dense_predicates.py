@@ -111,3 +111,12 @@ def random_eviction(N, starts, span):
     r, y = _grid(N)
     s = np.asarray([N if x is None else x for x in starts])
     return (r < y) | ((s[None, :] <= r) & (r < s[None, :] + span))
+
+
+def key_window(a, b):
+    """Row r attends exactly to keys a[r] <= y < b[r] (a per-query key window; row-wise family)."""
+    a = np.asarray(a)[:, None]
+    b = np.asarray(b)[:, None]
+    N = a.shape[0]
+    y = np.arange(N)[None, :]
+    return ~((a <= y) & (y < b))

@@ -37,6 +37,9 @@ class Vectors:
     ute: np.ndarray
     causal: bool
     N: int
+    # False: column-wise (§4.1): index = key column y, values = masked ROW intervals.
+    # True: row-wise (R32): index = query row r, values = masked KEY intervals.
+    rowwise: bool = False
 
 
 def expand(sri: np.ndarray, causal: bool, N: int) -> Vectors:
@@ -61,18 +64,39 @@ def expand(sri: np.ndarray, causal: bool, N: int) -> Vectors:
     raise ValueError(f"unsupported (causal={causal}, C={C})")
 
 
+def expand_rowwise(sri: np.ndarray, causal: bool, N: int) -> Vectors:
+    """Row-wise representation ("by transposing the attention matrix, we can obtain a
+    row-wise representation using column index intervals"; R32): row r of
+    ``sri [N, C]`` holds the masked KEY intervals of query row r.  The triangles keep their
+    meaning — lower = keys left of the diagonal (y <= r), upper = right of it — and the C-table
+    is the mirror of the column-wise one: an implicit end extends to the far edge of its
+    triangle (column 0 for the lower, column N for the upper):
+    causal C=1 -> (LTE; LTS=0), causal C=2 -> (LTS, LTE), non-causal C=2 -> (LTE, UTS;
+    LTS=0, UTE=N), non-causal C=4 -> all four.  Causal adds the implicit {y > r} (R8)."""
+    sri = np.asarray(sri, dtype=np.int64).reshape(N, -1)
+    C = sri.shape[1]
+    zeros = np.zeros(N, dtype=np.int64)
+    full_n = np.full(N, N, dtype=np.int64)
+    if causal and C == 1:
+        return Vectors(zeros, sri[:, 0], zeros, zeros, True, N, True)
+    if causal and C == 2:
+        return Vectors(sri[:, 0], sri[:, 1], zeros, zeros, True, N, True)
+    if not causal and C == 2:
+        return Vectors(zeros, sri[:, 0], sri[:, 1], full_n, False, N, True)
+    if not causal and C == 4:
+        return Vectors(sri[:, 0], sri[:, 1], sri[:, 2], sri[:, 3], False, N, True)
+    raise ValueError(f"unsupported (causal={causal}, C={C})")
+
+
 def mask_rows(v: Vectors, r0: int, r1: int) -> np.ndarray:
     """Dense boolean mask rows [r0, r1) x all N columns; True = masked (M = -inf).
 
-    masked(r, y) = LTS_y <= r < LTE_y  or  UTS_y <= r < UTE_y  or  (causal and r < y)
-    — Eq. 3 per interval, §4.1 union of both intervals, Eq. 2's
-    additive -inf mask, causal as the implicit upper triangle (R8)."""
-    r = np.arange(r0, r1, dtype=np.int64)[:, None]
-    y = np.arange(v.N, dtype=np.int64)[None, :]
-    m = ((v.lts[None, :] <= r) & (r < v.lte[None, :])) | ((v.uts[None, :] <= r) & (r < v.ute[None, :]))
-    if v.causal:
-        m |= r < y
-    return m
+    Column-wise: masked(r, y) = LTS_y <= r < LTE_y  or  UTS_y <= r < UTE_y  or  (causal and
+    r < y) — Eq. 3 per interval, §4.1 union of both intervals, Eq. 2's
+    additive -inf mask, causal as the implicit upper triangle (R8).
+    Row-wise (P:108, R32): masked(r, y) = LTS_r <= y < LTE_r  or  UTS_r <= y < UTE_r  or
+    (causal and r < y)."""
+    return _mask_for_rows(v, np.arange(r0, r1, dtype=np.int64))
 
 
 def to_dense(v: Vectors) -> np.ndarray:
@@ -142,9 +166,13 @@ def forward(q, k, v, vec: Vectors, scale: float | None = None, rows=None, row_bl
 
 
 def _mask_for_rows(vec: Vectors, rows: np.ndarray) -> np.ndarray:
-    r = rows[:, None]
-    y = np.arange(vec.N)[None, :]
-    m = ((vec.lts[None, :] <= r) & (r < vec.lte[None, :])) | ((vec.uts[None, :] <= r) & (r < vec.ute[None, :]))
+    r = np.asarray(rows, dtype=np.int64)[:, None]
+    y = np.arange(vec.N, dtype=np.int64)[None, :]
+    if vec.rowwise:
+        rr = r[:, 0]
+        m = ((vec.lts[rr, None] <= y) & (y < vec.lte[rr, None])) | ((vec.uts[rr, None] <= y) & (y < vec.ute[rr, None]))
+    else:
+        m = ((vec.lts[None, :] <= r) & (r < vec.lte[None, :])) | ((vec.uts[None, :] <= r) & (r < vec.ute[None, :]))
     if vec.causal:
         m |= r < y
     return m
@@ -268,6 +296,11 @@ def extrema(vec: Vectors, Bc: int) -> np.ndarray:
 
 
 def classify(vec: Vectors, Br: int, Bc: int):
+    """Dispatch: column-wise vectors -> ``classify_colwise``; row-wise -> ``classify_rowwise``."""
+    return classify_rowwise(vec, Br, Bc) if vec.rowwise else classify_colwise(vec, Br, Bc)
+
+
+def classify_colwise(vec: Vectors, Br: int, Bc: int):
     """Eq. 4 per tile, in Alg. 1's order, 0-based (R2), ragged
     tiles by their real extents (R3), causal region as its own triangle (R13):
 
@@ -303,6 +336,73 @@ def classify(vec: Vectors, Br: int, Bc: int):
     return cm, counts, ext
 
 
+def classify_rowwise(vec: Vectors, Br: int, Bc: int):
+    """Eq. 4 for the row-wise representation (P:108 "by transposing the attention matrix";
+    DESIGN.md R32): the intervals are KEY ranges of each query row, so Alg. 1 lines 3-4's
+    min/max are taken over the real rows of row tile i (R3) and compared with the column
+    range [c0, c1) of tile j — Eq. 4 with the roles of rows and columns exchanged; the causal
+    triangle (a property of the (r, y) position, not of the vectors) is unchanged:
+
+      SKIP     iff (c0 >= LTS^max and c1 <= LTE^min)
+               or  (c0 >= UTS^max and c1 <= UTE^min)
+               or  (causal and r1-1 < c0)
+      PARTIAL  iff (c1 > LTS^min and c0 < LTE^max)
+               or  (c1 > UTS^min and c0 < UTE^max)
+               or  (causal and r0 < c1-1)
+      UNMASKED otherwise.
+
+    Returns (class_map uint8 [Tr, Tc], counts int64 [3], extrema int64 [Tr, 8] (per row tile))."""
+    assert vec.rowwise
+    N = vec.N
+    Tr, Tc = -(-N // Br), -(-N // Bc)
+    ext = extrema(vec, Br)          # index = row: min/max over each row tile's real rows
+    cm = np.zeros((Tr, Tc), dtype=np.uint8)
+    c0 = np.arange(Tc, dtype=np.int64) * Bc
+    c1 = np.minimum(c0 + Bc, N)
+    for i in range(Tr):
+        r0, r1 = i * Br, min((i + 1) * Br, N)
+        ltsmin, ltsmax, ltemin, ltemax, utsmin, utsmax, utemin, utemax = ext[i]
+        skip = ((c0 >= ltsmax) & (c1 <= ltemin)) | ((c0 >= utsmax) & (c1 <= utemin))
+        if vec.causal:
+            skip |= r1 - 1 < c0
+        part = ((c1 > ltsmin) & (c0 < ltemax)) | ((c1 > utsmin) & (c0 < utemax))
+        if vec.causal:
+            part |= r0 < c1 - 1
+        cm[i, :] = np.where(skip, SKIP, np.where(part, PARTIAL, UNMASKED))
+    counts = np.array([(cm == SKIP).sum(), (cm == PARTIAL).sum(), (cm == UNMASKED).sum()], dtype=np.int64)
+    return cm, counts, ext
+
+
+def from_dense_rowwise(dense: np.ndarray, causal: bool) -> np.ndarray:
+    """Dense mask -> row-wise startend indices (R32): the masked keys of row r left of or
+    on the diagonal (y <= r) must be one interval, those right of it (y > r) another (for a
+    causal mask: all of them).  Returns [N, C] int32: causal -> C=2 (LTS, LTE), bidirectional
+    -> C=4 (LTS, LTE, UTS, UTE); empty intervals as [0, 0) / [N, N).  Raises ValueError when
+    a row's masked keys within a triangle are not contiguous."""
+    dense = np.asarray(dense, dtype=bool)
+    N = dense.shape[0]
+    lo = np.zeros((N, 2), dtype=np.int64)
+    up = np.full((N, 2), N, dtype=np.int64)
+    for r in range(N):
+        row = dense[r]
+        if causal and not row[r + 1:].all():
+            raise ValueError(f"causal mask must mask every y>r (row {r})")
+        ys = np.nonzero(row[:r + 1])[0]
+        if len(ys):
+            if ys[-1] - ys[0] + 1 != len(ys):
+                raise ValueError(f"row {r} lower triangle not contiguous")
+            lo[r] = (ys[0], ys[-1] + 1)
+        if not causal:
+            ys = np.nonzero(row[r + 1:])[0] + r + 1
+            if len(ys):
+                if ys[-1] - ys[0] + 1 != len(ys):
+                    raise ValueError(f"row {r} upper triangle not contiguous")
+                up[r] = (ys[0], ys[-1] + 1)
+    if causal:
+        return np.stack([lo[:, 0], lo[:, 1]], 1).astype(np.int32)
+    return np.stack([lo[:, 0], lo[:, 1], up[:, 0], up[:, 1]], 1).astype(np.int32)
+
+
 def nonskip_counts(vec: Vectors, Br: int, Bc: int):
     """Per-unit work of the tiled algorithm: the number of non-SKIP tiles in every
     row tile (the forward's unit, Alg. 1's inner loop over j) and in every column
@@ -328,6 +428,7 @@ def refine_chunks(vec: Vectors):
     P:127) with the causal triangle (R8).  Written out per column and row group: column y has a
     masked cell in rows [a, b) iff one of its intervals [LTS, LTE), [UTS, UTE) intersects [a, b)
     or (causal) a < y.  Returns uint32 [Tr, Tc]."""
+    assert not vec.rowwise, "column-wise representation only"
     N = vec.N
     T = -(-N // 128)
     out = np.zeros((T, T), dtype=np.uint32)
@@ -390,6 +491,7 @@ def visible_counts(vec: Vectors) -> np.ndarray:
     r<y triangle, with inclusion-exclusion done per column on the row axis via difference
     arrays.  Exact for any vectors (each column's masked row set is the union of at most
     three row intervals: [LTS, LTE), [UTS, UTE), and [0, y) if causal)."""
+    assert not vec.rowwise, "column-wise representation only"
     N = vec.N
     diff = np.zeros(N + 1, dtype=np.int64)
     y = np.arange(N, dtype=np.int64)

@@ -41,6 +41,7 @@ class MaskInput:
     sri: np.ndarray  # int32 [N, C]
     family: str
     params: dict = field(default_factory=dict)
+    rowwise: bool = False  # True: sri rows are query rows holding masked KEY intervals
 
     def __post_init__(self):
         self.sri = np.ascontiguousarray(self.sri, dtype=np.int32).reshape(self.N, self.C)
@@ -208,6 +209,132 @@ def empty_rows_padding(doc_lens: Sequence[int], pad: int) -> MaskInput:
     lts = base.sri[:, 0].astype(np.int64).copy()
     lts[N - pad:] = np.arange(N - pad, N)
     return _mk(N, True, [lts], "padding_empty_rows", doc_lens=list(doc_lens), pad=pad)
+
+
+# ---------------------------------------------------------------- row-wise builders
+# The row-wise representation (R32): row r of sri holds the masked KEY
+# columns of query row r.  C-table (mirror of the column-wise one; an implicit end extends to the
+# far edge of its triangle):
+#
+#     causal  C   col0  col1  col2  col3   implicit
+#     1       1   LTE   -     -     -      LTS = 0, upper = {y > r}
+#     1       2   LTS   LTE   -     -      upper = {y > r}
+#     0       2   LTE   UTS   -     -      LTS = 0, UTE = N
+#     0       4   LTS   LTE   UTS   UTE    -
+def _mkr(N, causal, cols, family, **params):
+    m = _mk(N, causal, cols, family, **params)
+    m.rowwise = True
+    return m
+
+
+def rw_full(N: int) -> MaskInput:
+    """No masking: LTE = 0, UTS = N (both key intervals empty)."""
+    return _mkr(N, False, [np.zeros(N), np.full(N, N)], "rw_full")
+
+
+def rw_causal(N: int) -> MaskInput:
+    """Causal: only the implicit y > r triangle; LTE = 0."""
+    return _mkr(N, True, [np.zeros(N)], "rw_causal")
+
+
+def rw_sliding_window(N: int, w: int) -> MaskInput:
+    """Sliding window: row r sees keys r-w+1..r; LTE = max(r-w+1, 0)."""
+    r = np.arange(N)
+    return _mkr(N, True, [np.maximum(r - w + 1, 0)], "rw_sliding_window", w=w)
+
+
+def rw_causal_document(doc_lens: Sequence[int]) -> MaskInput:
+    """Causal document: row r sees its document's keys up to r; LTE = document start."""
+    N, starts, ends, doc_of = _doc_bounds(doc_lens)
+    return _mkr(N, True, [starts[doc_of]], "rw_causal_document", doc_lens=list(map(int, doc_lens)))
+
+
+def rw_document(doc_lens: Sequence[int]) -> MaskInput:
+    """Document: row r sees its whole document; LTE = doc start, UTS = doc end."""
+    N, starts, ends, doc_of = _doc_bounds(doc_lens)
+    return _mkr(N, False, [starts[doc_of], ends[doc_of]], "rw_document", doc_lens=list(map(int, doc_lens)))
+
+
+def rw_global_sliding_window(N: int, g: int, w: int) -> MaskInput:
+    """Global + sliding window (reading R19 as in the column-wise builder): rows r < g see
+    every key; a row r >= g sees the global keys y < g and the window y in (r-w, r].
+    Masked keys of a row r >= g: [g, max(g, r-w+1)) and [r+1, N)."""
+    r = np.arange(N)
+    glob = r < g
+    lts = np.where(glob, 0, g)
+    lte = np.where(glob, 0, np.maximum(g, r - w + 1))
+    uts = np.where(glob, N, r + 1)
+    ute = np.full(N, N)
+    return _mkr(N, False, [lts, lte, uts, ute], "rw_global_sliding_window", g=g, w=w)
+
+
+def rw_causal_blockwise(block_lens: Sequence[int]) -> MaskInput:
+    """Causal blockwise: a row of a demonstration block sees its own block causally; a
+    row of the last block sees every earlier key.  LTE = block start (0 in the last block)."""
+    N, starts, ends, blk = _doc_bounds(block_lens)
+    last = len(block_lens) - 1
+    return _mkr(N, True, [np.where(blk == last, 0, starts[blk])], "rw_causal_blockwise",
+                block_lens=list(map(int, block_lens)))
+
+
+def rw_prefix_lm_document(docs: Sequence[tuple[int, int]]) -> MaskInput:
+    """Prefix-LM document: row r of document [s, e) with prefix p sees [s, max(s+p, r+1)).
+    LTE = s, UTS = max(s + p, r + 1)."""
+    lens = [int(l) for l, _ in docs]
+    N, starts, ends, doc_of = _doc_bounds(lens)
+    pre = np.asarray([int(p) for _, p in docs])
+    r = np.arange(N)
+    uts = np.maximum(starts[doc_of] + pre[doc_of], r + 1)
+    return _mkr(N, False, [starts[doc_of], uts], "rw_prefix_lm_document",
+                docs=[(l, int(p)) for l, (_, p) in zip(lens, docs)])
+
+
+def rw_prefix_lm_causal(N: int, p: int) -> MaskInput:
+    """Prefix-LM causal / T5: row r sees [0, max(p, r+1)).  LTE = 0, UTS = max(p, r+1)."""
+    r = np.arange(N)
+    return _mkr(N, False, [np.zeros(N), np.maximum(p, r + 1)], "rw_prefix_lm_causal", p=p)
+
+
+def rw_key_window(N: int, rng: np.random.Generator, max_len: int) -> MaskInput:
+    """A mask natural only in the row-wise form: every query row r attends to one random key
+    window [a_r, b_r) (a per-query retrieval span; b_r - a_r <= max_len).  A column's visible
+    rows are then an arbitrary set, so the column-wise form cannot represent it.
+    Masked keys [0, a_r) and [b_r, N): LTE = a_r, UTS = b_r."""
+    a = rng.integers(0, N, size=N)
+    b = np.minimum(a + rng.integers(1, max(2, max_len + 1), size=N), N)
+    return _mkr(N, False, [a, b], "rw_key_window", max_len=max_len)
+
+
+def rw_sample_family(family: str, N: int, rng: np.random.Generator, doc_range=(3, 7)) -> MaskInput:
+    """One row-wise instance of a Figure-1 family (those whose masked keys per row form one
+    interval per triangle) at the kernel-sweep parameters, or of rw_key_window."""
+    lo, hi = doc_range
+    if family == "full":
+        return rw_full(N)
+    if family == "causal":
+        return rw_causal(N)
+    if family == "sliding_window":
+        return rw_sliding_window(N, max(1, N // 16))
+    if family == "causal_document":
+        return rw_causal_document(sample_doc_lens(N, int(rng.integers(lo, hi + 1)), rng))
+    if family == "document":
+        return rw_document(sample_doc_lens(N, int(rng.integers(lo, hi + 1)), rng))
+    if family == "global_sliding_window":
+        return rw_global_sliding_window(N, max(1, N // 16), min(256, N))
+    if family == "causal_blockwise":
+        return rw_causal_blockwise(sample_doc_lens(N, int(rng.integers(lo, hi + 1)), rng))
+    if family == "prefix_lm_document":
+        lens = sample_doc_lens(N, int(rng.integers(lo, hi + 1)), rng)
+        return rw_prefix_lm_document([(l, max(0, int(round(0.1 * l)))) for l in lens])
+    if family == "prefix_lm_causal":
+        return rw_prefix_lm_causal(N, N // 2)
+    if family == "key_window":
+        return rw_key_window(N, rng, max(1, N // 8))
+    raise KeyError(family)
+
+
+ROWWISE_FAMILIES = ["full", "causal", "sliding_window", "causal_document", "document", "global_sliding_window",
+                    "causal_blockwise", "prefix_lm_document", "prefix_lm_causal", "key_window"]
 
 
 # ------------------------------------------------------------- sampling
