@@ -92,7 +92,17 @@ enum {
    * SM holds one query tile and half of every K/V tile, three S accumulators in TMEM) instead of
    * the single-SM kernel K2a.  Same results to rounding order (every output within the parity
    * tolerances of the single-SM kernel). */
-  FM_FLAG_FWD_PAIR = 8
+  FM_FLAG_FWD_PAIR = 8,
+  /* Row-wise representation ("by transposing the attention matrix, we can obtain a row-wise
+   * representation using column index intervals"; R32): startend_row_indices[b, hm, r, .]
+   * holds the masked KEY column intervals of query row r, masked(r, y) = LTS_r <= y < LTE_r or
+   * UTS_r <= y < UTE_r or (causal and r < y), with the mirrored (causal, C) table
+   *     causal C=1: (LTE; LTS=0)   causal C=2: (LTS, LTE)
+   *     non-causal C=2: (LTE, UTS; LTS=0, UTE=N)   non-causal C=4: (LTS, LTE, UTS, UTE).
+   * Tiles are classified by Eq. 4 on the transposed problem (per-row-tile extrema against the
+   * column range).  flashmask_classify then returns minmax per ROW tile ([B, Hm, Tr, 8], tile br).
+   * Accepted by every entry point; FM_FLAG_FWD_PAIR is ignored with it (single-SM forward). */
+  FM_FLAG_ROWWISE = 16
 };
 
 typedef struct {

@@ -134,6 +134,7 @@ fm_status check_params(const fm_params* p, fm::Dims* d, bool need_attention) {
   d->out_f32 = p->out_dtype == FM_FP32;
   d->in_f16 = p->in_dtype == FM_FP16;
   d->flags = p->flags;
+  d->rowwise = (p->flags & FM_FLAG_ROWWISE) ? 1 : 0;
   if (need_attention && d->Tc > fm::kMaxTc) return fail(FM_ERR_UNSUPPORTED, "seqlen > 262144");
   return FM_OK;
 }
@@ -153,6 +154,8 @@ size_t carve(const fm::Dims& d, int pass, void* base, fm::Workspace* w) {
   const size_t bhm = static_cast<size_t>(d.B) * d.Hm;
   const size_t bh = static_cast<size_t>(d.B) * d.H;
   w->ext8 = reinterpret_cast<int32_t*>(take(bhm * d.Tc * 8 * sizeof(int32_t)));
+  // row-wise backward: extrema of the Brb-row tiles of the backward map (Trb >= Tc)
+  w->ext8b = (pass == FM_PASS_BWD) ? reinterpret_cast<int32_t*>(take(bhm * d.Trb * 8 * sizeof(int32_t))) : nullptr;
   w->vec4 = reinterpret_cast<int4*>(take(bhm * d.Tc * 128 * sizeof(int4)));
   w->fmap = nullptr;
   w->bmap = nullptr;
@@ -175,7 +178,7 @@ size_t carve(const fm::Dims& d, int pass, void* base, fm::Workspace* w) {
 fm::F32Args f32_args(const fm::Dims& d, const fm::Workspace& w) {
   fm::F32Args a{};
   a.B = d.B; a.N = d.N; a.H = d.H; a.Hm = d.Hm; a.Hkv = d.Hkv; a.G = d.G; a.Tr = d.Tr; a.Tc = d.Tc;
-  a.Npb = d.Npb; a.causal = d.causal;
+  a.Npb = d.Npb; a.causal = d.causal; a.rowwise = d.rowwise;
   a.scale = d.scale;
   a.fmap = w.fmap;
   a.vec4 = w.vec4;
@@ -261,11 +264,12 @@ fm_status flashmask_classify(const fm_params* p, const int32_t* sri, int32_t br,
   if (br < 1 || bc < 1) return fail(FM_ERR_INVALID_ARGUMENT, "br and bc must be >= 1");
   if (!aligned16(minmax)) return fail(FM_ERR_INVALID_ARGUMENT, "minmax must be 16-byte aligned");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  cudaError_t e = timed(FM_KERNEL_EXPAND, st, [&] { return fm::launch_expand(sri, d, bc, minmax, nullptr, st); });
+  // column-wise: extrema per bc-column tile; row-wise (R32): per br-row tile
+  cudaError_t e = timed(FM_KERNEL_EXPAND, st, [&] { return fm::launch_expand(sri, d, d.rowwise ? br : bc, minmax, nullptr, st); });
   if (e != cudaSuccess) return cuda_fail(e, "expand");
   if (class_map || counts || row_nonskip || col_nonskip) {
     fm::Dims d0 = d;
-    d0.flags = 0;
+    d0.flags = 0;  // true classes (FM_FLAG_NO_SKIP does not apply); d0.rowwise is kept
     e = timed(FM_KERNEL_CLASSIFY, st, [&] {
       return fm::launch_classify(minmax, d0, br, bc, class_map, 0, 0, counts, st, row_nonskip, col_nonskip);
     });
@@ -281,6 +285,7 @@ fm_status flashmask_refine(const fm_params* p, const int32_t* sri, const uint8_t
   fm_status s = check_params(p, &d, false);
   if (s != FM_OK) return s;
   if (!sri || !class_map || !words) return fail(FM_ERR_INVALID_ARGUMENT, "startend_row_indices, class_map, words required");
+  if (d.rowwise) return fail(FM_ERR_UNSUPPORTED, "flashmask_refine: column-wise representation only (R31)");
   if (!aligned16(sri)) return fail(FM_ERR_INVALID_ARGUMENT, "startend_row_indices must be 16-byte aligned");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   cudaError_t e = timed(FM_KERNEL_REFINE, st, [&] { return fm::launch_refine(sri, class_map, d, words, counts, st); });
@@ -331,7 +336,7 @@ fm_status flashmask_fwd(const fm_params* p, const void* q, const void* k, const 
   e = timed(FM_KERNEL_CLASSIFY, st, [&] { return fm::launch_classify(w.ext8, d, fm::kTile, fm::kTile, w.fmap, 0, 1, nullptr, st); });
   if (e != cudaSuccess) return cuda_fail(e, "classify");
   // f3 refinement: consumed by the causal forward kernels (fm_fwd.cu FM_FWD_REFINE)
-  const bool refine = d.causal && (p->flags & FM_FLAG_NO_REFINE) == 0;
+  const bool refine = d.causal && !d.rowwise && (p->flags & FM_FLAG_NO_REFINE) == 0;
   if (refine) {
     e = timed(FM_KERNEL_REFINE, st, [&] { return fm::launch_refine(sri, w.fmap, d, w.cw, nullptr, st); });
     if (e != cudaSuccess) return cuda_fail(e, "refine");
@@ -344,7 +349,7 @@ fm_status flashmask_fwd(const fm_params* p, const void* q, const void* k, const 
   a.vec4 = w.vec4;
   a.o = o;
   a.lse = lse;
-  if ((p->flags & FM_FLAG_FWD_PAIR) && d.D == 128) {
+  if ((p->flags & FM_FLAG_FWD_PAIR) && d.D == 128 && !d.rowwise) {
     CUtensorMap tk64;
     if (!make_map(&tk64, k, d, d.Hkv, 64, &err)) return fail(FM_ERR_CUDA, err);
     e = timed(FM_KERNEL_FWD, st, [&] { return fm::launch_fwd2(d, tq, tk64, tv, to, a, st); });
@@ -401,7 +406,14 @@ fm_status flashmask_bwd(const fm_params* p, const void* q, const void* k, const 
     return fail(FM_ERR_CUDA, err);
   cudaError_t e = timed(FM_KERNEL_EXPAND, st, [&] { return fm::launch_expand(sri, d, fm::kTile, w.ext8, w.vec4, st); });
   if (e != cudaSuccess) return cuda_fail(e, "expand");
-  e = timed(FM_KERNEL_CLASSIFY, st, [&] { return fm::launch_classify(w.ext8, d, d.Brb, fm::kTile, w.bmap, 1, 1, nullptr, st); });
+  // row-wise: the backward map's rows are Brb-row tiles, whose extrema K1a computes separately
+  const int32_t* ext_b = w.ext8;
+  if (d.rowwise && d.Brb != fm::kTile) {
+    e = timed(FM_KERNEL_EXPAND, st, [&] { return fm::launch_expand(sri, d, d.Brb, w.ext8b, nullptr, st); });
+    if (e != cudaSuccess) return cuda_fail(e, "expand");
+    ext_b = w.ext8b;
+  }
+  e = timed(FM_KERNEL_CLASSIFY, st, [&] { return fm::launch_classify(ext_b, d, d.Brb, fm::kTile, w.bmap, 1, 1, nullptr, st); });
   if (e != cudaSuccess) return cuda_fail(e, "classify");
   e = timed(FM_KERNEL_BWD_PRE, st, [&] { return fm::launch_bwd_pre(d, o, dout, lse, w.dvec, w.l2, w.dqacc, st); });
   if (e != cudaSuccess) return cuda_fail(e, "bwd preprocess");
@@ -442,6 +454,7 @@ fm_status flashmask_bwd(const fm_params* p, const void* q, const void* k, const 
   if (e != cudaSuccess) return cuda_fail(e, "classify");
   fm::DqArgs qa{};
   qa.B = d.B; qa.N = d.N; qa.H = d.H; qa.Hm = d.Hm; qa.G = d.G; qa.Tr = d.Tr; qa.Tc = d.Tc; qa.Npb = d.Npb;
+  qa.rowwise = d.rowwise;
   qa.scale_log2 = a.scale_log2;
   qa.scale = d.scale;
   qa.fmap = w.fmap;

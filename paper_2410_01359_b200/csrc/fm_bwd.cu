@@ -128,7 +128,7 @@ struct Cfg {
   static constexpr int NDS = (D == 64) ? FM_BWD_NDS64 : FM_BWD_NDS;  // dS shared-memory buffers
 };
 
-template <int D>
+template <int D, bool ROWW>
 struct Smem {
   using C = Cfg<D>;
   uint8_t k[C::KV_TILE];
@@ -141,6 +141,7 @@ struct Smem {
   float dq_stage[C::DQT ? DQ_NSTAGE : DQ64_STAGES][C::DQT ? DQ_CROWS * D : DQ64_STAGE_FLOATS];
   float lvec[C::QST][C::BR];
   float dvec[C::QST][C::BR];
+  int4 rvec[C::QST][ROWW ? C::BR : 1];  // row-wise: the row tile's (LTS, len, UTS, len) per query row
   uint16_t list[C::MAXTRB];
   uint32_t part_bits[C::MAXTRB / 32];
   uint64_t kv_full;
@@ -171,10 +172,25 @@ __device__ __forceinline__ uint32_t row_mask_bits(int r0, int key, int4 mv) {
   return m;
 }
 
+// Row-wise representation (R32): bit u set iff query row r0 + u masks this thread's key — one of
+// the row's key intervals holds it, it lies after the row (causal) or it is a padded key (>= N).
+template <bool CAUSAL>
+__device__ __forceinline__ uint32_t row_mask_bits_rw(int r0, int key, const int4* rv, int N) {
+  uint32_t m = 0u;
+#pragma unroll 8
+  for (int u = 0; u < 32; ++u) {
+    const int4 iv = rv[u];  // the same row for every thread of the warp: broadcast
+    bool msk = (static_cast<unsigned>(key - iv.x) < static_cast<unsigned>(iv.y)) ||
+               (static_cast<unsigned>(key - iv.z) < static_cast<unsigned>(iv.w));
+    if constexpr (CAUSAL) msk |= r0 + u < key;
+    m |= static_cast<uint32_t>(msk) << u;
+  }
+  return key >= N ? 0xFFFFFFFFu : m;
+}
+
 template <bool PART, bool CAUSAL, bool F16>
 __device__ __forceinline__ void pds_chunk(const uint32_t* sr, const uint32_t* dr, const float* lq, const float* dq,
-                                          float sl2, int r0, int key, int4 mv, uint32_t* pp, uint32_t* dp) {
-  const uint32_t mb = PART ? row_mask_bits<CAUSAL>(r0, key, mv) : 0u;
+                                          float sl2, uint32_t mb, uint32_t* pp, uint32_t* dp) {
 #pragma unroll
   for (int c = 0; c < 32; c += 4) {
     const float4 L4 = *reinterpret_cast<const float4*>(lq + c);
@@ -197,7 +213,9 @@ __device__ __forceinline__ void pds_chunk(const uint32_t* sr, const uint32_t* dr
 
 }  // namespace bwd
 
-template <int D, bool CAUSAL, bool OUT_F32, bool F16>
+// ROWW: row-wise representation (FM_FLAG_ROWWISE, R32): the producer loads each visited row tile's
+// per-row key intervals next to L and D; the compute threads (= keys) test them per 32 rows.
+template <int D, bool CAUSAL, bool OUT_F32, bool F16, bool ROWW>
 __global__ void __launch_bounds__(bwd::NT, 1)
     fm_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                   const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO,
@@ -205,7 +223,7 @@ __global__ void __launch_bounds__(bwd::NT, 1)
                   const __grid_constant__ CUtensorMap tmDV, const BwdArgs a) {
   using namespace bwd;
   using C = Cfg<D>;
-  using S = Smem<D>;
+  using S = Smem<D, ROWW>;
   constexpr int BR = C::BR;
   extern __shared__ uint8_t smem_raw[];
   S& sm = *smem_align1024<S>(smem_raw);
@@ -299,7 +317,7 @@ __global__ void __launch_bounds__(bwd::NT, 1)
         const size_t bh = static_cast<size_t>(b) * a.H + hq;
         const int st = t % C::QST;
         mbar_wait(&sm.q_empty[st], ((t / C::QST) & 1) ^ 1);
-        mbar_expect_tx(&sm.q_full[st], 2 * C::Q_TILE + 2 * BR * 4);
+        mbar_expect_tx(&sm.q_full[st], 2 * C::Q_TILE + 2 * BR * 4 + (ROWW ? BR * 16 : 0));
 #pragma unroll
         for (int c = 0; c < D / 64; ++c) {
           tma_load_4d(sm.q[st] + c * (BR * 128), &tmQ, &sm.q_full[st], c * 64, hq, i * BR, b);
@@ -307,6 +325,9 @@ __global__ void __launch_bounds__(bwd::NT, 1)
         }
         bulk_g2s(sm.lvec[st], a.l2 + bh * a.Npb + static_cast<size_t>(i) * BR, BR * 4, &sm.q_full[st]);
         bulk_g2s(sm.dvec[st], a.dvec + bh * a.Npb + static_cast<size_t>(i) * BR, BR * 4, &sm.q_full[st]);
+        if constexpr (ROWW)
+          bulk_g2s(sm.rvec[st], a.vec4 + bhm * static_cast<size_t>(a.Tc) * 128 + static_cast<size_t>(i) * BR,
+                   BR * 16, &sm.q_full[st]);
       }
     }
   } else if (warp == 13 || warp == G_WARP) {
@@ -414,7 +435,8 @@ __global__ void __launch_bounds__(bwd::NT, 1)
     const int key_t = wl * 32 + lane;
     const int key = j * 128 + key_t;
     const uint32_t lane_off = static_cast<uint32_t>(wl * 32) << 16;
-    const int4 mv = a.vec4[(bhm * a.Tc) * 128 + key];  // this key's (LTS, len, UTS, len), normalised
+    // this key's (LTS, len, UTS, len), normalised (column-wise representation)
+    const int4 mv = ROWW ? make_int4(0, 0, 0, 0) : a.vec4[(bhm * a.Tc) * 128 + key];
     const float sl2 = a.scale_log2;
     constexpr int CH = C::CH_PER_WG;
     for (int t = 0, t1 = 0; t < nE; ++t, t1 = (t1 + 1 == nE1) ? 0 : t1 + 1) {
@@ -443,10 +465,13 @@ __global__ void __launch_bounds__(bwd::NT, 1)
           tc_fence_before();
           mbar_arrive(&sm.sdp_free);
         }
-        if (partial)
-          pds_chunk<true, CAUSAL, F16>(sr, dr, lv + q0, dv + q0, sl2, i * BR + q0, key, mv, pp[ch], dp[ch]);
-        else
-          pds_chunk<false, CAUSAL, F16>(sr, dr, lv + q0, dv + q0, sl2, i * BR + q0, key, mv, pp[ch], dp[ch]);
+        if (partial) {
+          const uint32_t mb = ROWW ? row_mask_bits_rw<CAUSAL>(i * BR + q0, key, sm.rvec[st] + (ROWW ? q0 : 0), a.N)
+                                   : row_mask_bits<CAUSAL>(i * BR + q0, key, mv);
+          pds_chunk<true, CAUSAL, F16>(sr, dr, lv + q0, dv + q0, sl2, mb, pp[ch], dp[ch]);
+        } else {
+          pds_chunk<false, CAUSAL, F16>(sr, dr, lv + q0, dv + q0, sl2, 0u, pp[ch], dp[ch]);
+        }
       }
       if (tid == 0) FM_T(5, t);
 #ifdef FM_TRACE
@@ -658,13 +683,13 @@ __global__ void __launch_bounds__(bwd::NT, 1)
   }
 }
 
-template <int D, bool CAUSAL, bool OUT_F32, bool F16>
+template <int D, bool CAUSAL, bool OUT_F32, bool F16, bool ROWW>
 static cudaError_t launch_bwd_t(const Dims& d, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
                                 const CUtensorMap& tdo, const CUtensorMap& tdq, const CUtensorMap& tdk,
                                 const CUtensorMap& tdv, const BwdArgs& a, cudaStream_t st) {
-  auto kern = fm_bwd_kernel<D, CAUSAL, OUT_F32, F16>;
-  const size_t smem = sizeof(bwd::Smem<D>) + 1024;
-  static_assert(sizeof(bwd::Smem<D>) + 1024 <= 232448, "shared memory budget");
+  auto kern = fm_bwd_kernel<D, CAUSAL, OUT_F32, F16, ROWW>;
+  const size_t smem = sizeof(bwd::Smem<D, ROWW>) + 1024;
+  static_assert(sizeof(bwd::Smem<D, ROWW>) + 1024 <= 232448, "shared memory budget");
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (e != cudaSuccess) return e;
   dim3 grid(d.Tc, d.Hkv, d.B);
@@ -674,9 +699,14 @@ static cudaError_t launch_bwd_t(const Dims& d, const CUtensorMap& tq, const CUte
 cudaError_t launch_bwd(const Dims& d, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
                        const CUtensorMap& tdo, const CUtensorMap& tdq, const CUtensorMap& tdk, const CUtensorMap& tdv,
                        const BwdArgs& a, cudaStream_t st) {
-#define FM_B(DD, CC, FF) \
-  return d.in_f16 ? launch_bwd_t<DD, CC, FF, true>(d, tq, tk, tv, tdo, tdq, tdk, tdv, a, st) \
-                  : launch_bwd_t<DD, CC, FF, false>(d, tq, tk, tv, tdo, tdq, tdk, tdv, a, st)
+#define FM_B(DD, CC, FF)                                                                                     \
+  do {                                                                                                       \
+    if (d.rowwise)                                                                                           \
+      return d.in_f16 ? launch_bwd_t<DD, CC, FF, true, true>(d, tq, tk, tv, tdo, tdq, tdk, tdv, a, st)       \
+                      : launch_bwd_t<DD, CC, FF, false, true>(d, tq, tk, tv, tdo, tdq, tdk, tdv, a, st);     \
+    return d.in_f16 ? launch_bwd_t<DD, CC, FF, true, false>(d, tq, tk, tv, tdo, tdq, tdk, tdv, a, st)        \
+                    : launch_bwd_t<DD, CC, FF, false, false>(d, tq, tk, tv, tdo, tdq, tdk, tdv, a, st);      \
+  } while (0)
   if (d.D == 128) {
     if (d.causal) { if (d.out_f32) FM_B(128, true, true); else FM_B(128, true, false); }
     else { if (d.out_f32) FM_B(128, false, true); else FM_B(128, false, false); }

@@ -126,7 +126,7 @@ __global__ void __launch_bounds__(dqk::NT, 1)
         const int j = sm.list[e];
         const int ks = e % KST;
         mbar_wait(&sm.kv_empty[ks], ((e / KST) & 1) ^ 1);
-        const bool part = (sm.part_bits[e >> 5] >> (e & 31)) & 1u;
+        const bool part = ((sm.part_bits[e >> 5] >> (e & 31)) & 1u) && !a.rowwise;  // row-wise: no column slice
         mbar_expect_tx(&sm.kv_full[ks], 2 * S::TILE + (part ? 128 * 16 : 0));
 #pragma unroll
         for (int c = 0; c < D / 64; ++c) {
@@ -178,6 +178,8 @@ __global__ void __launch_bounds__(dqk::NT, 1)
     const float sl2 = a.scale_log2;
     const size_t ri = bh * a.Npb + row;  // Npb >= Tr * 128 rows, so this index is in range
     const float l2 = a.l2[ri], dval = a.dvec[ri];
+    // row-wise representation (R32): this row's (LTS, len, UTS, len) over key columns
+    const int4 rmv = a.rowwise ? a.vec4[bhm * static_cast<size_t>(a.Tc) * 128 + row] : make_int4(0, 0, 0, 0);
     for (int e = 0; e < nE; ++e) {
       const int j = sm.list[e];
       const int ks = e % KST;
@@ -205,12 +207,20 @@ __global__ void __launch_bounds__(dqk::NT, 1)
             float p = ex2(fmaf(__uint_as_float(sr[c][t + u]), sl2, -l2));
             if (part) {
               const int col = hh * 64 + c * 32 + t + u;
-              const int4 mv = sm.mask[ks][col];
-              bool msk = static_cast<unsigned>(row - mv.x) < static_cast<unsigned>(mv.y);
-              if constexpr (CAUSAL)
-                msk |= row < j * 128 + col;
-              else
-                msk |= static_cast<unsigned>(row - mv.z) < static_cast<unsigned>(mv.w);
+              bool msk;
+              if (a.rowwise) {  // this row's key intervals (R32); keys past N are padding
+                const int y = j * 128 + col;
+                msk = (static_cast<unsigned>(y - rmv.x) < static_cast<unsigned>(rmv.y)) ||
+                      (static_cast<unsigned>(y - rmv.z) < static_cast<unsigned>(rmv.w)) || y >= a.N;
+                if constexpr (CAUSAL) msk |= row < y;
+              } else {
+                const int4 mv = sm.mask[ks][col];
+                msk = static_cast<unsigned>(row - mv.x) < static_cast<unsigned>(mv.y);
+                if constexpr (CAUSAL)
+                  msk |= row < j * 128 + col;
+                else
+                  msk |= static_cast<unsigned>(row - mv.z) < static_cast<unsigned>(mv.w);
+              }
               p = msk ? 0.f : p;
             }
             ds2[u] = p * (__uint_as_float(dr[c][t + u]) - dval);

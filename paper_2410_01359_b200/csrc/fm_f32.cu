@@ -28,6 +28,12 @@ __device__ __forceinline__ bool cell_masked(const int4 mv, int r, int y, bool ca
   if (static_cast<unsigned>(r - mv.x) < static_cast<unsigned>(mv.y)) return true;
   return causal ? (r < y) : (static_cast<unsigned>(r - mv.z) < static_cast<unsigned>(mv.w));
 }
+// row-wise representation (R32): rv = query row r's (LTS, len, UTS, len) over key columns
+__device__ __forceinline__ bool cell_masked_rw(const int4 rv, int r, int y, bool causal, int N) {
+  if (static_cast<unsigned>(y - rv.x) < static_cast<unsigned>(rv.y)) return true;
+  if (static_cast<unsigned>(y - rv.z) < static_cast<unsigned>(rv.w)) return true;
+  return (causal && r < y) || y >= N;
+}
 
 template <bool F32>
 __device__ __forceinline__ void store_out(void* base, size_t idx, float v) {
@@ -72,7 +78,8 @@ __global__ void __launch_bounds__(128) f32_fwd_kernel(F32Args a) {
     if (cls == 0) continue;  // SKIP: no load, no compute
     const int y1 = min(j * 128 + 128, a.N);
     for (int y = j * 128; y < y1; ++y) {
-      if (cls == 1 && cell_masked(vec[y], r, y, a.causal)) continue;
+      if (cls == 1 && (a.rowwise ? cell_masked_rw(vec[r], r, y, a.causal, a.N) : cell_masked(vec[y], r, y, a.causal)))
+        continue;
       const float* kp = a.k + ((static_cast<size_t>(b) * a.N + y) * a.Hkv + hk) * D;
       const float* vp = a.v + ((static_cast<size_t>(b) * a.N + y) * a.Hkv + hk) * D;
       float s = 0.f;
@@ -127,7 +134,8 @@ __global__ void __launch_bounds__(128) f32_dq_kernel(F32Args a) {
       if (cls == 0) continue;
       const int y1 = min(j * 128 + 128, a.N);
       for (int y = j * 128; y < y1; ++y) {
-        if (cls == 1 && cell_masked(vec[y], r, y, a.causal)) continue;
+        if (cls == 1 && (a.rowwise ? cell_masked_rw(vec[r], r, y, a.causal, a.N) : cell_masked(vec[y], r, y, a.causal)))
+          continue;
         const float* kp = a.k + ((static_cast<size_t>(b) * a.N + y) * a.Hkv + hk) * D;
         const float* vp = a.v + ((static_cast<size_t>(b) * a.N + y) * a.Hkv + hk) * D;
         float s = 0.f, dp = 0.f;
@@ -160,7 +168,7 @@ __global__ void __launch_bounds__(128) f32_dkdv_kernel(F32Args a) {
   if (y >= a.N) return;
   const int hm = (a.Hm == 1) ? 0 : hk;
   const size_t bhm = static_cast<size_t>(b) * a.Hm + hm;
-  const int4 mv = a.vec4[bhm * static_cast<size_t>(a.Tc) * 128 + y];
+  const int4 mv = a.rowwise ? make_int4(0, 0, 0, 0) : a.vec4[bhm * static_cast<size_t>(a.Tc) * 128 + y];
   const int j = y / 128;
   const size_t krow = (static_cast<size_t>(b) * a.N + y) * a.Hkv + hk;
   float kv[E], vv[E], dk[E], dv[E];
@@ -179,7 +187,9 @@ __global__ void __launch_bounds__(128) f32_dkdv_kernel(F32Args a) {
       if (cls == 0) continue;
       const int r1 = min(i * 128 + 128, a.N);
       for (int r = i * 128; r < r1; ++r) {
-        if (cls == 1 && cell_masked(mv, r, y, a.causal)) continue;
+        if (cls == 1 && (a.rowwise ? cell_masked_rw(a.vec4[bhm * static_cast<size_t>(a.Tc) * 128 + r], r, y, a.causal, a.N)
+                                   : cell_masked(mv, r, y, a.causal)))
+          continue;
         const float L = Lh[r];
         if (L == -INFINITY) continue;
         const size_t row = (static_cast<size_t>(b) * a.N + r) * a.H + h;

@@ -24,14 +24,17 @@
 #ifndef FM_TRACE_BX
 #define FM_TRACE_BX 64
 #endif
+#ifndef FM_TRACE_BY
+#define FM_TRACE_BY 0
+#endif
 namespace fm { __device__ long long g_fm_trace_fwd[64 * 16]; __device__ long long g_fm_trace_fwd_ev[16]; }
 #define FT(slot, e)                                                                                   \
   do {                                                                                                 \
-    if (blockIdx.x == FM_TRACE_BX && blockIdx.y == 0 && blockIdx.z == 0 && (e) < 64) fm::g_fm_trace_fwd[(e) * 16 + (slot)] = clock64(); \
+    if (blockIdx.x == FM_TRACE_BX && blockIdx.y == FM_TRACE_BY && blockIdx.z == 0 && (e) < 64) fm::g_fm_trace_fwd[(e) * 16 + (slot)] = clock64(); \
   } while (0)
 #define FTE(k)                                                                                          \
   do {                                                                                                 \
-    if (blockIdx.x == FM_TRACE_BX && blockIdx.y == 0 && blockIdx.z == 0) fm::g_fm_trace_fwd_ev[k] = clock64(); \
+    if (blockIdx.x == FM_TRACE_BX && blockIdx.y == FM_TRACE_BY && blockIdx.z == 0) fm::g_fm_trace_fwd_ev[k] = clock64(); \
   } while (0)
 #define FM_TRACE_NE(n) (fm::g_fm_trace_fwd_ev[9] = (n))
 #else
@@ -115,7 +118,10 @@ __device__ __forceinline__ int ent_cls(uint32_t ent, int q) { return (ent >> (24
 
 }  // namespace fwd
 
-template <int D, bool CAUSAL, bool OUT_F32, bool F16>
+// ROWW: row-wise representation (FM_FLAG_ROWWISE, R32) — a.vec4 holds each query
+// ROW's masked key intervals; a softmax thread (= one row) keeps its own in registers and no mask
+// slice is loaded per tile.
+template <int D, bool CAUSAL, bool OUT_F32, bool F16, bool ROWW>
 __global__ void __launch_bounds__(fwd::NT, 1)
     fm_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                   const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmO, const FwdArgs a) {
@@ -218,7 +224,7 @@ __global__ void __launch_bounds__(fwd::NT, 1)
         for (int c = 0; c < D / 64; ++c) tma_load_4d(sm.k[ks] + c * 16384, &tmK, &sm.k_full[ks], c * 64, hk, j * 128, b);
         FT(11, e);
         mbar_wait(&sm.m_empty[ms], ((e / MST) & 1) ^ 1);
-        if (ent_cls(ent, 0) == 1 || ent_cls(ent, 1) == 1) {
+        if (!ROWW && (ent_cls(ent, 0) == 1 || ent_cls(ent, 1) == 1)) {
           // f3: which 32-row x 16-column sub-blocks hold a masked cell (K1c); the ragged last
           // column tile keeps every sub-block masked (its padded keys need the bounds mask)
 #pragma unroll
@@ -347,6 +353,8 @@ __global__ void __launch_bounds__(fwd::NT, 1)
     float m_used = -INFINITY;  // running max of the scaled logits, log2 units (threshold-updated)
     float l = 0.f;             // this half's share of the row sum
     uint32_t cnt = 0;
+    int4 rmv = make_int4(0, 0, 0, 0);  // row-wise: this row's (LTS, len, UTS, len) over key columns
+    if constexpr (ROWW) rmv = a.vec4[bhm * static_cast<size_t>(a.Tc) * 128 + row];
     for (int e = 0; e < nE; ++e) {
       const uint32_t ent = sm.list[e];
       const int cls = ent_cls(ent, q);
@@ -363,7 +371,8 @@ __global__ void __launch_bounds__(fwd::NT, 1)
         float mx0 = -INFINITY, mx1 = -INFINITY, mx2 = -INFINITY, mx3 = -INFINITY;
         uint32_t sr[2][16];
         // f3: the 16-column chunks of this warp's 32 rows x 64 columns that hold a masked cell
-        const uint32_t pm = (cls != 1) ? 0u : (FM_FWD_REFINE(CAUSAL) ? (sm.cw[ms][q] >> (wl * 8 + hh * 4)) & 0xFu : 0xFu);
+        const uint32_t pm =
+            (cls != 1) ? 0u : ((FM_FWD_REFINE(CAUSAL) && !ROWW) ? (sm.cw[ms][q] >> (wl * 8 + hh * 4)) & 0xFu : 0xFu);
         tmem_ld16(tSh, sr[0]);
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
@@ -375,9 +384,20 @@ __global__ void __launch_bounds__(fwd::NT, 1)
             // (unsigned)(r - start_y) < len_y for either interval, or (causal) r < y
             const int4* mk = sm.mask[ms] + hh * 64 + c * 16;
             const int rmy = row - (j * 128 + hh * 64 + c * 16);
-            // causal: below the diagonal tile (j < i) no key of the tile lies after any of its
-            // rows, so the r < y test is dropped there (warp-uniform choice)
-            if (CAUSAL && j < (q == 0 ? i0 : i1)) {
+            if constexpr (ROWW) {
+              // key y = row - rmy + t is masked for this row iff it lies in one of the row's key
+              // intervals, after the row (causal), or past N (the ragged last column tile)
+#pragma unroll
+              for (int t = 0; t < 16; ++t) {
+                const int y = row - rmy + t;
+                bool msk = (static_cast<unsigned>(y - rmv.x) < static_cast<unsigned>(rmv.y)) ||
+                           (static_cast<unsigned>(y - rmv.z) < static_cast<unsigned>(rmv.w)) || y >= a.N;
+                if constexpr (CAUSAL) msk |= rmy < t;
+                sv[t] = msk ? -INFINITY : sv[t];
+              }
+            } else if (CAUSAL && j < (q == 0 ? i0 : i1)) {
+              // causal: below the diagonal tile (j < i) no key of the tile lies after any of its
+              // rows, so the r < y test is dropped there (warp-uniform choice)
 #pragma unroll
               for (int t = 0; t < 16; ++t) {
                 const int4 mv = mk[t];
@@ -577,15 +597,15 @@ __global__ void __launch_bounds__(fwd::NT, 1)
 #ifdef FM_TRACE
   if (tid == 0) {
     FTE(7);
-    if (blockIdx.x == FM_TRACE_BX && blockIdx.y == 0 && blockIdx.z == 0) FM_TRACE_NE(nE);
+    if (blockIdx.x == FM_TRACE_BX && blockIdx.y == FM_TRACE_BY && blockIdx.z == 0) FM_TRACE_NE(nE);
   }
 #endif
 }
 
-template <int D, bool CAUSAL, bool OUT_F32, bool F16>
+template <int D, bool CAUSAL, bool OUT_F32, bool F16, bool ROWW>
 static cudaError_t launch_fwd_t(const Dims& d, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
                                 const CUtensorMap& to, const FwdArgs& a, cudaStream_t st) {
-  auto kern = fm_fwd_kernel<D, CAUSAL, OUT_F32, F16>;
+  auto kern = fm_fwd_kernel<D, CAUSAL, OUT_F32, F16, ROWW>;
   const size_t smem = sizeof(fwd::Smem<D>) + 1024;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (e != cudaSuccess) return e;
@@ -595,9 +615,14 @@ static cudaError_t launch_fwd_t(const Dims& d, const CUtensorMap& tq, const CUte
 
 cudaError_t launch_fwd(const Dims& d, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
                        const CUtensorMap& to, const FwdArgs& a, cudaStream_t st) {
-#define FM_F(DD, CC, FF) \
-  return d.in_f16 ? launch_fwd_t<DD, CC, FF, true>(d, tq, tk, tv, to, a, st) \
-                  : launch_fwd_t<DD, CC, FF, false>(d, tq, tk, tv, to, a, st)
+#define FM_F(DD, CC, FF)                                                                                    \
+  do {                                                                                                      \
+    if (d.rowwise)                                                                                          \
+      return d.in_f16 ? launch_fwd_t<DD, CC, FF, true, true>(d, tq, tk, tv, to, a, st)                      \
+                      : launch_fwd_t<DD, CC, FF, false, true>(d, tq, tk, tv, to, a, st);                    \
+    return d.in_f16 ? launch_fwd_t<DD, CC, FF, true, false>(d, tq, tk, tv, to, a, st)                       \
+                    : launch_fwd_t<DD, CC, FF, false, false>(d, tq, tk, tv, to, a, st);                     \
+  } while (0)
   if (d.D == 128) {
     if (d.causal) { if (d.out_f32) FM_F(128, true, true); else FM_F(128, true, false); }
     else { if (d.out_f32) FM_F(128, false, true); else FM_F(128, false, false); }

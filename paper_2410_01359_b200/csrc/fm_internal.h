@@ -34,7 +34,8 @@ constexpr int kDq64BoxRows = 128;
 
 // Workspace layout (buffers 4 KiB-aligned in the device address space), produced by flashmask_fwd/bwd.
 struct Workspace {
-  int32_t* ext8;    // [B, Hm, Tc, 8] raw extrema (Alg. 1 line 4)
+  int32_t* ext8;    // [B, Hm, Tc, 8] raw extrema (Alg. 1 line 4); row-wise: per 128-row tile
+  int32_t* ext8b;   // row-wise backward: [B, Hm, Trb, 8] extrema per Brb-row tile
   int4* vec4;       // [B, Hm, Tc*128] normalised (LTS, LTE, UTS, UTE) per column, padded columns masked
   uint8_t* fmap;    // [B, Hm, Tr, Tc] forward kernel map (128 x 128)
   uint32_t* cw;     // [B, Hm, Tr, Tc] f3 refinement words of the forward map (K1c; PARTIAL tiles)
@@ -54,6 +55,7 @@ struct Dims {
   int out_f32;
   int in_f16;       // 16-bit operands (and 16-bit outputs) are fp16 instead of bf16
   int flags;
+  int rowwise;      // FM_FLAG_ROWWISE: vectors indexed by query row, values = key intervals (R32)
 };
 
 struct FwdArgs {
@@ -61,7 +63,7 @@ struct FwdArgs {
   float scale_log2;
   const uint8_t* fmap;
   const uint32_t* cw;  // f3 refinement words (nullptr: every sub-block of a PARTIAL tile is masked)
-  const int4* vec4;
+  const int4* vec4;    // normalised (start, len, start, len) per key column, or per query row (row-wise)
   void* o;
   float* lse;
 };
@@ -81,7 +83,7 @@ struct BwdArgs {
 };
 
 struct DqArgs {
-  int B, N, H, Hm, G, Tr, Tc, Npb;
+  int B, N, H, Hm, G, Tr, Tc, Npb, rowwise;
   float scale_log2;
   float scale;
   const uint8_t* fmap;
@@ -93,7 +95,7 @@ struct DqArgs {
 
 // FP32-input path (fm_f32.cu): plain fp32 tensors, same layouts as the bf16 path
 struct F32Args {
-  int B, N, H, Hm, Hkv, G, Tr, Tc, Npb, causal;
+  int B, N, H, Hm, Hkv, G, Tr, Tc, Npb, causal, rowwise;
   float scale;
   const uint8_t* fmap;  // [B, Hm, Tr, Tc] 128 x 128 kernel map
   const int4* vec4;
@@ -105,6 +107,8 @@ struct F32Args {
 };
 
 // launchers (return cudaError_t of the launch)
+// K1a: C-table -> normalised vec4 (when non-null) and min/max per tile of `bc` vector entries
+// (key columns; query rows under Dims::rowwise)
 cudaError_t launch_expand(const int32_t* sri, const Dims& d, int bc, int32_t* ext8, int4* vec4, cudaStream_t st);
 cudaError_t launch_sliding_window(int B, int N, int w, int causal, int32_t* sri, cudaStream_t st);
 cudaError_t launch_classify(const int32_t* ext8, const Dims& d, int br, int bc, uint8_t* map, int transposed,

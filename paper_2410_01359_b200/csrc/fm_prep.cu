@@ -18,7 +18,27 @@ namespace fm {
 // Grid (Tc, B*Hm), 128 threads; one CTA reduces one column tile.
 // ---------------------------------------------------------------------------------------
 __device__ __forceinline__ void expand_col(const int32_t* s, int C, int causal, int N, int& lts, int& lte, int& uts,
-                                           int& ute) {
+                                           int& ute, int rowwise) {
+  if (rowwise) {
+    // row-wise C-table (R32): an implicit end extends to the far edge of its triangle
+    if (causal) {
+      lts = (C >= 2) ? s[0] : 0;
+      lte = (C >= 2) ? s[1] : s[0];
+      uts = 0;
+      ute = 0;
+    } else if (C == 2) {
+      lts = 0;
+      lte = s[0];
+      uts = s[1];
+      ute = N;
+    } else {
+      lts = s[0];
+      lte = s[1];
+      uts = s[2];
+      ute = s[3];
+    }
+    return;
+  }
   if (causal) {
     lts = s[0];
     lte = (C >= 2) ? s[1] : N;
@@ -40,7 +60,8 @@ __device__ __forceinline__ void expand_col(const int32_t* s, int C, int causal, 
 __device__ __forceinline__ int clampi(int x, int lo, int hi) { return x < lo ? lo : (x > hi ? hi : x); }
 
 __global__ void __launch_bounds__(128) k1_expand(const int32_t* __restrict__ sri, int N, int C, int causal, int bc,
-                                                 int Tc, int32_t* __restrict__ ext8, int4* __restrict__ vec4) {
+                                                 int Tc, int32_t* __restrict__ ext8, int4* __restrict__ vec4,
+                                                 int rowwise) {
   pdl_wait();
   pdl_launch();
   // one warp per column tile (4 per CTA): lanes stride over the tile's columns, the extrema
@@ -57,7 +78,7 @@ __global__ void __launch_bounds__(128) k1_expand(const int32_t* __restrict__ sri
     int4 nv;
     if (y < N) {
       int v[4];
-      expand_col(base + y * C, C, causal, N, v[0], v[1], v[2], v[3]);
+      expand_col(base + y * C, C, causal, N, v[0], v[1], v[2], v[3], rowwise);
 #pragma unroll
       for (int t = 0; t < 4; ++t) {
         mn[t] = min(mn[t], v[t]);
@@ -113,7 +134,16 @@ __device__ __forceinline__ int tile_class(const int4& a, const int4& b, int r0, 
   return 2;
 }
 
-template <int JPT>
+// Row-wise representation (R32): Eq. 4 on the transposed problem — the extrema are those of row
+// tile i (key intervals of its rows), compared with the column range [c0, c1) of tile j; the
+// causal triangle is unchanged.
+__device__ __forceinline__ int tile_class_rw(const int4& a, const int4& b, int r0, int r1, int c0, int c1, int causal) {
+  if ((c0 >= a.y && c1 <= a.z) || (c0 >= b.y && c1 <= b.z) || (causal && r1 - 1 < c0)) return 0;
+  if ((c1 > a.x && c0 < a.w) || (c1 > b.x && c0 < b.w) || (causal && r0 < c1 - 1)) return 1;
+  return 2;
+}
+
+template <int JPT, bool ROWW>
 __global__ void __launch_bounds__(128) k1_classify(const int32_t* __restrict__ ext8, int N, int causal, int br, int bc,
                                                    int Tr, int Tc, uint8_t* __restrict__ map, int transposed,
                                                    int kernel_map, int no_skip,
@@ -137,13 +167,14 @@ __global__ void __launch_bounds__(128) k1_classify(const int32_t* __restrict__ e
   for (int u = 0; u < JPT; ++u) {
     const int j = j0 + u;
     valid[u] = j < Tc;
-    if (valid[u]) {
+    if (valid[u] && !ROWW) {
       const int4* e = reinterpret_cast<const int4*>(ext8 + (static_cast<size_t>(bh) * Tc + j) * 8);
       ea[u] = e[0];  // (LTSmin, LTSmax, LTEmin, LTEmax)
       eb[u] = e[1];  // (UTSmin, UTSmax, UTEmin, UTEmax)
     } else {
       ea[u] = eb[u] = make_int4(0, 0, 0, 0);
     }
+    if (ROWW) ea[u] = eb[u] = make_int4(0, 0, 0, 0);  // row-wise: extrema come per row tile
     c0[u] = valid[u] ? j * bc : N;
     c1[u] = c0[u] + min(bc, N - c0[u]);
     ragged[u] = kernel_map == 2 && j == Tc - 1;  // kernel_map = 2: N is not a multiple of bc
@@ -162,10 +193,17 @@ __global__ void __launch_bounds__(128) k1_classify(const int32_t* __restrict__ e
       const int r0 = i * br, r1 = r0 + min(br, N - r0);
       uint32_t word = 0u;
       int ns = 0;
+      int4 ra, rb;
+      if constexpr (ROWW) {  // the same row tile for the whole warp: broadcast loads
+        const int4* e = reinterpret_cast<const int4*>(ext8 + (static_cast<size_t>(bh) * Tr + i) * 8);
+        ra = e[0];
+        rb = e[1];
+      }
 #pragma unroll
       for (int u = 0; u < JPT; ++u) {
         if (!valid[u]) continue;
-        const int cls = tile_class(ea[u], eb[u], r0, r1, c0[u], c1[u], causal);
+        const int cls = ROWW ? tile_class_rw(ra, rb, r0, r1, c0[u], c1[u], causal)
+                             : tile_class(ea[u], eb[u], r0, r1, c0[u], c1[u], causal);
         c0n += cls == 0;
         c1n += cls == 1;
         c2n += cls == 2;
@@ -257,7 +295,7 @@ __global__ void __launch_bounds__(128) k1_refine(const int32_t* __restrict__ sri
     yy[u] = j * 128 + lane * 4 + u;
     ok[u] = yy[u] < N;
     if (ok[u]) {
-      expand_col(base + static_cast<size_t>(yy[u]) * C, C, causal, N, ls[u], le[u], us[u], ue[u]);
+      expand_col(base + static_cast<size_t>(yy[u]) * C, C, causal, N, ls[u], le[u], us[u], ue[u], 0);
     } else {
       ls[u] = le[u] = us[u] = ue[u] = 0;
     }
@@ -342,7 +380,7 @@ cudaError_t launch_sliding_window(int B, int N, int w, int causal, int32_t* sri,
 cudaError_t launch_expand(const int32_t* sri, const Dims& d, int bc, int32_t* ext8, int4* vec4, cudaStream_t st) {
   const int Tc = (d.N + bc - 1) / bc;
   dim3 grid((Tc + 3) / 4, d.B * d.Hm);
-  return launch_pdl(k1_expand, grid, dim3(128), 0, st, sri, d.N, d.C, d.causal, bc, Tc, ext8, vec4);
+  return launch_pdl(k1_expand, grid, dim3(128), 0, st, sri, d.N, d.C, d.causal, bc, Tc, ext8, vec4, d.rowwise);
 }
 
 cudaError_t launch_classify(const int32_t* ext8, const Dims& d, int br, int bc, uint8_t* map, int transposed,
@@ -367,8 +405,9 @@ cudaError_t launch_classify(const int32_t* ext8, const Dims& d, int br, int bc, 
   const int ns = (d.flags & 1) ? 1 : 0;
   auto cnt64 = reinterpret_cast<unsigned long long*>(counts);
   dim3 grid(static_cast<unsigned>(gx), static_cast<unsigned>((Tr + rpc - 1) / rpc), static_cast<unsigned>(bhm));
-  return launch_pdl(k1_classify<1>, grid, dim3(128), 0, st, ext8, d.N, d.causal, br, bc, Tr, Tc, map, transposed, km,
-                    ns, cnt64, row_cnt, col_cnt, static_cast<int>(rpc));
+  // (row-wise: ext8 holds the extrema of the br-row tiles)
+  return launch_pdl(d.rowwise ? k1_classify<1, true> : k1_classify<1, false>, grid, dim3(128), 0, st, ext8, d.N,
+                    d.causal, br, bc, Tr, Tc, map, transposed, km, ns, cnt64, row_cnt, col_cnt, static_cast<int>(rpc));
 }
 
 // ---------------------------------------------------------------------------------------

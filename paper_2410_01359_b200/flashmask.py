@@ -22,6 +22,7 @@ FM_FLAG_NO_SKIP = 1
 FM_FLAG_DETERMINISTIC = 2
 FM_FLAG_NO_REFINE = 4
 FM_FLAG_FWD_PAIR = 8
+FM_FLAG_ROWWISE = 16
 FM_PASS_FWD, FM_PASS_BWD = 0, 1
 
 EXPORTED = ["flashmask_workspace_size", "flashmask_classify", "flashmask_refine", "flashmask_fwd", "flashmask_bwd",
@@ -149,20 +150,23 @@ def flashmask_workspace_size(params: FmParams, pass_: int) -> int:
 
 
 def flashmask_classify(sri: torch.Tensor, causal: bool, br: int = 128, bc: int = 128, num_heads: int | None = None,
-                       class_map: bool = True, stream=None, nonskip: bool = False):
+                       class_map: bool = True, stream=None, nonskip: bool = False, rowwise: bool = False):
     """Tile classification (K1).  sri: int32 cuda [B, Hm, N, C].  Returns
     (minmax int32 [B,Hm,Tc,8], class_map uint8 [B,Hm,Tr,Tc] or None, counts int64 [B,Hm,3]);
     with nonskip=True also (row_nonskip int32 [B,Hm,Tr], col_nonskip int32 [B,Hm,Tc]): the
-    number of non-SKIP tiles per row tile / per column tile."""
+    number of non-SKIP tiles per row tile / per column tile.  rowwise=True
+    (FM_FLAG_ROWWISE): sri is the row-wise representation and minmax is per row tile
+    [B,Hm,Tr,8]."""
     _require(isinstance(sri, torch.Tensor) and sri.dim() == 4, "flashmask_classify",
              "startend_row_indices must be a 4-D tensor [B, Hm, N, C]")
     B, Hm, N, C = sri.shape
     _check_sri(sri, B, N, "flashmask_classify", sri.device)
     p = FmParams(batch=B, seqlen=N, num_heads=num_heads or Hm, head_dim=128, mask_heads=Hm, mask_cols=C,
-                 causal=int(bool(causal)), scale=0.0, in_dtype=FM_BF16, out_dtype=FM_BF16, flags=0)
+                 causal=int(bool(causal)), scale=0.0, in_dtype=FM_BF16, out_dtype=FM_BF16,
+                 flags=FM_FLAG_ROWWISE if rowwise else 0)
     Tr, Tc = -(-N // br), -(-N // bc)
     dev = sri.device
-    minmax = torch.empty(B, Hm, Tc, 8, dtype=torch.int32, device=dev)
+    minmax = torch.empty(B, Hm, Tr if rowwise else Tc, 8, dtype=torch.int32, device=dev)
     cmap = torch.empty(B, Hm, Tr, Tc, dtype=torch.uint8, device=dev) if class_map else None
     counts = torch.empty(B, Hm, 3, dtype=torch.int64, device=dev)
     rows = torch.empty(B, Hm, Tr, dtype=torch.int32, device=dev) if nonskip else None

@@ -45,12 +45,12 @@ def test_pair_forward_vs_oracle_and_single(fmlib, fam, N):
                                  flags=fmlib.FM_FLAG_FWD_PAIR)
     o1, l1 = fmlib.flashmask_fwd(tc["q"], tc["k"], tc["v"], sri_c, causal, out_dtype=torch.float32)
     torch.cuda.synchronize()
-    # same P (same running-max decisions, same bf16 rounding), same PV order: O agrees to the
-    # rounding of the row-sum reduction order
-    assert torch.allclose(o2, o1, atol=1e-5, rtol=1e-4), (o2 - o1).abs().max().item()
+    # same running-max decisions and PV order; the two kernels split exp2 differently between MUFU
+    # and the polynomial (1 vs 3 pairs of 8), so a few P values round to a neighbouring bf16
+    assert torch.allclose(o2, o1, atol=2e-3, rtol=0), (o2 - o1).abs().max().item()
     fin = torch.isfinite(l1)
     assert torch.equal(fin, torch.isfinite(l2))
-    assert torch.allclose(l2[fin], l1[fin], atol=1e-5, rtol=0)
+    assert torch.allclose(l2[fin], l1[fin], atol=1e-4, rtol=0)
     f = lambda x, b, h: x[b, :, h, :].double().numpy()
     for b in range(B):
         vec = fo.expand(masks[b].sri, causal, N)
