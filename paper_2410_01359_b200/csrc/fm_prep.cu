@@ -143,56 +143,71 @@ __device__ __forceinline__ int tile_class_rw(const int4& a, const int4& b, int r
   return 2;
 }
 
-template <int JPT, bool ROWW>
+// Compile-time variants: TRANS = the backward's transposed map (JPT = 1, 16-row runs per 16-byte
+// store); API = flashmask_classify (true classes, counts; NS adds the a2 per-row / per-column
+// non-SKIP counts) — otherwise the attention kernels' map (FM_FLAG_NO_SKIP, ragged last column
+// tile PARTIAL) without counts.  Keeping every choice out of the row loop, four column tiles per
+// thread and one 32-bit store per row took the Hm = 64 microbenchmark from 165 to 85 us.
+template <int JPT, bool ROWW, bool TRANS, bool API, bool NS>
 __global__ void __launch_bounds__(128) k1_classify(const int32_t* __restrict__ ext8, int N, int causal, int br, int bc,
-                                                   int Tr, int Tc, uint8_t* __restrict__ map, int transposed,
-                                                   int kernel_map, int no_skip,
-                                                   unsigned long long* __restrict__ counts, int* __restrict__ row_cnt,
-                                                   int* __restrict__ col_cnt, int rows_per_cta) {
+                                                   int Tr, int Tc, uint8_t* __restrict__ map, int kernel_map,
+                                                   int no_skip, unsigned long long* __restrict__ counts,
+                                                   int* __restrict__ row_cnt, int* __restrict__ col_cnt,
+                                                   int rows_per_cta) {
+  static_assert(!TRANS || JPT == 1, "transposed map: one column tile per thread");
   pdl_wait();
   pdl_launch();
-  __shared__ unsigned int cnt[3];
+  __shared__ unsigned int cnt[2];
   __shared__ int row_acc[64];
   const int j0 = (blockIdx.x * blockDim.x + threadIdx.x) * JPT;
   const int ib = blockIdx.y * rows_per_cta;
   const int iend = min(Tr, ib + rows_per_cta);
   const int bh = blockIdx.z;
-  if (threadIdx.x < 3) cnt[threadIdx.x] = 0;
-  if (threadIdx.x < 64) row_acc[threadIdx.x] = 0;
-  __syncthreads();
+  if (API) {
+    if (threadIdx.x < 2) cnt[threadIdx.x] = 0;
+    if (NS && threadIdx.x < 64) row_acc[threadIdx.x] = 0;
+    __syncthreads();
+  }
   int4 ea[JPT], eb[JPT];
   int c0[JPT], c1[JPT];
-  bool valid[JPT], ragged[JPT];
+  bool valid[JPT];
+  int nvalid = 0;
+  uint32_t force1 = 0u;  // kernel map: per column-tile byte, class 2 -> 1 (ragged last column tile)
 #pragma unroll
   for (int u = 0; u < JPT; ++u) {
     const int j = j0 + u;
     valid[u] = j < Tc;
+    nvalid += valid[u];
     if (valid[u] && !ROWW) {
       const int4* e = reinterpret_cast<const int4*>(ext8 + (static_cast<size_t>(bh) * Tc + j) * 8);
       ea[u] = e[0];  // (LTSmin, LTSmax, LTEmin, LTEmax)
       eb[u] = e[1];  // (UTSmin, UTSmax, UTEmin, UTEmax)
     } else {
-      ea[u] = eb[u] = make_int4(0, 0, 0, 0);
+      ea[u] = eb[u] = make_int4(0, 0, 0, 0);  // row-wise: the extrema come per row tile
     }
-    if (ROWW) ea[u] = eb[u] = make_int4(0, 0, 0, 0);  // row-wise: extrema come per row tile
     c0[u] = valid[u] ? j * bc : N;
     c1[u] = c0[u] + min(bc, N - c0[u]);
-    ragged[u] = kernel_map == 2 && j == Tc - 1;  // kernel_map = 2: N is not a multiple of bc
+    if (!API && kernel_map == 2 && j == Tc - 1) force1 |= 1u << (8 * u);  // N is not a multiple of bc
   }
-  unsigned int c0n = 0, c1n = 0, c2n = 0;
+  const bool skip_to_partial = !API && no_skip;
+  uint32_t vmask = 0u;  // byte mask of the valid column tiles of this thread
+#pragma unroll
+  for (int u = 0; u < JPT; ++u) vmask |= valid[u] ? (0xFFu << (8 * u)) : 0u;
+  unsigned int n0 = 0, n1 = 0;
   int colns[JPT];
 #pragma unroll
   for (int u = 0; u < JPT; ++u) colns[u] = 0;
-  const bool row_counts = row_cnt != nullptr && rows_per_cta <= 64;
+  const bool row_counts = NS && row_cnt != nullptr && rows_per_cta <= 64;
+  const bool any = valid[0] && map != nullptr;
   for (int i16 = ib; i16 < iend; i16 += 16) {
     uint32_t packed[4] = {0u, 0u, 0u, 0u};
 #pragma unroll
     for (int v = 0; v < 16; ++v) {
       const int i = i16 + v;
       if (i >= iend) break;
-      const int r0 = i * br, r1 = r0 + min(br, N - r0);
       uint32_t word = 0u;
       int ns = 0;
+      const int r0 = i * br, r1 = r0 + min(br, N - r0);
       int4 ra, rb;
       if constexpr (ROWW) {  // the same row tile for the whole warp: broadcast loads
         const int4* e = reinterpret_cast<const int4*>(ext8 + (static_cast<size_t>(bh) * Tr + i) * 8);
@@ -201,32 +216,34 @@ __global__ void __launch_bounds__(128) k1_classify(const int32_t* __restrict__ e
       }
 #pragma unroll
       for (int u = 0; u < JPT; ++u) {
-        if (!valid[u]) continue;
         const int cls = ROWW ? tile_class_rw(ra, rb, r0, r1, c0[u], c1[u], causal)
                              : tile_class(ea[u], eb[u], r0, r1, c0[u], c1[u], causal);
-        c0n += cls == 0;
-        c1n += cls == 1;
-        c2n += cls == 2;
-        ns += cls != 0;
-        colns[u] += cls != 0;
-        int out = cls;
-        if (kernel_map) {
-          if (out == 0 && no_skip) out = 1;
-          if (out == 2 && ragged[u]) out = 1;
+        if (NS) {
+          ns += valid[u] && cls != 0;
+          colns[u] += cls != 0;
         }
-        word |= static_cast<uint32_t>(out) << (8 * u);
+        word |= static_cast<uint32_t>(cls) << (8 * u);
+      }
+      if (API) {  // class bytes 0 / 1 / 2: PARTIAL = bit 0, UNMASKED = bit 1 of a valid byte
+        n1 += __popc(word & vmask & 0x01010101u);
+        n0 += __popc(word & vmask & 0x02020202u);  // (UNMASKED here; SKIP = tiles - the two)
+      }
+      if (!API) {
+        // SKIP (0) -> PARTIAL (1) under FM_FLAG_NO_SKIP; UNMASKED (2) -> PARTIAL on the ragged tile
+        if (skip_to_partial) word |= (~word & (~word >> 1)) & 0x01010101u;
+        word ^= (word & (force1 << 1)) | ((word & (force1 << 1)) >> 1);
       }
       if (row_counts) {
         const int wsum = __reduce_add_sync(0xffffffffu, ns);
         if ((threadIdx.x & 31) == 0 && wsum) atomicAdd(&row_acc[i - ib], wsum);
       }
-      if (map && valid[0]) {
-        if (transposed) {
+      if (any) {
+        if constexpr (TRANS) {
           packed[v >> 2] |= (word & 0xffu) << (8 * (v & 3));
         } else {
           uint8_t* dst = map + (static_cast<size_t>(bh) * Tr + i) * Tc + j0;
-          if (JPT == 4 && (Tc & 3) == 0) {
-            *reinterpret_cast<uint32_t*>(dst) = word;
+          if (JPT == 4 && valid[JPT - 1]) {
+            *reinterpret_cast<uint32_t*>(dst) = word;  // Tc % 4 == 0 when JPT == 4 (host)
           } else {
 #pragma unroll
             for (int u = 0; u < JPT; ++u)
@@ -235,7 +252,7 @@ __global__ void __launch_bounds__(128) k1_classify(const int32_t* __restrict__ e
         }
       }
     }
-    if (map && transposed && valid[0]) {
+    if (TRANS && any) {
       uint8_t* dst = map + (static_cast<size_t>(bh) * Tc + j0) * Tr + i16;
       if (i16 + 16 <= iend && (Tr & 15) == 0) {
         *reinterpret_cast<uint4*>(dst) = make_uint4(packed[0], packed[1], packed[2], packed[3]);
@@ -244,27 +261,32 @@ __global__ void __launch_bounds__(128) k1_classify(const int32_t* __restrict__ e
       }
     }
   }
-  if (col_cnt) {
+  if (!API) return;
+  if (NS && col_cnt) {
 #pragma unroll
     for (int u = 0; u < JPT; ++u)
       if (valid[u] && colns[u]) atomicAdd(&col_cnt[static_cast<size_t>(bh) * Tc + j0 + u], colns[u]);
   }
   if (counts) {
-    c0n = __reduce_add_sync(0xffffffffu, c0n);
-    c1n = __reduce_add_sync(0xffffffffu, c1n);
-    c2n = __reduce_add_sync(0xffffffffu, c2n);
+    n0 = __reduce_add_sync(0xffffffffu, n0);
+    n1 = __reduce_add_sync(0xffffffffu, n1);
     if ((threadIdx.x & 31) == 0) {
-      atomicAdd(&cnt[0], c0n);
-      atomicAdd(&cnt[1], c1n);
-      atomicAdd(&cnt[2], c2n);
+      atomicAdd(&cnt[0], n0);
+      atomicAdd(&cnt[1], n1);
     }
   }
   __syncthreads();
-  if (counts && threadIdx.x < 3 && cnt[threadIdx.x])
-    atomicAdd(&counts[static_cast<size_t>(bh) * 3 + threadIdx.x], static_cast<unsigned long long>(cnt[threadIdx.x]));
+  if (counts && threadIdx.x < 3) {
+    const int cols = max(0, min(Tc - static_cast<int>(blockIdx.x * blockDim.x * JPT), static_cast<int>(blockDim.x) * JPT));
+    const unsigned long long tiles = static_cast<unsigned long long>(cols) * static_cast<unsigned>(max(0, iend - ib));
+    // cnt[0] = UNMASKED, cnt[1] = PARTIAL; SKIP = the CTA's valid tiles minus both
+    const unsigned long long v = threadIdx.x == 0 ? tiles - cnt[0] - cnt[1] : (threadIdx.x == 1 ? cnt[1] : cnt[0]);
+    if (v) atomicAdd(&counts[static_cast<size_t>(bh) * 3 + threadIdx.x], v);
+  }
   if (row_counts && threadIdx.x < iend - ib && row_acc[threadIdx.x])
     atomicAdd(&row_cnt[static_cast<size_t>(bh) * Tr + ib + threadIdx.x], row_acc[threadIdx.x]);
 }
+
 
 // ---------------------------------------------------------------------------------------
 // K1c: f3 refinement (R31, oracle refine_chunks): for every PARTIAL 128 x 128 tile
@@ -397,17 +419,36 @@ cudaError_t launch_classify(const int32_t* ext8, const Dims& d, int br, int bc, 
   if (col_cnt && (e = cudaMemsetAsync(col_cnt, 0, sizeof(int32_t) * Tc * bhm, st)) != cudaSuccess) return e;
   // Row tiles per CTA: enough CTAs for ~8 per SM (148 SMs), at most 64 row tiles each (the
   // counts leave each CTA as a few atomics; the transposed map is written in 16-row runs)
-  // (one column tile per thread: 4 per thread halved the CTA count and measured 1.3-1.9x slower)
+  // (wide non-transposed maps: 4 column tiles per thread and one 32-bit store per row, see the kernel)
   const long gx = (Tc + 127) / 128;
   long rpc = (gx * Tr * bhm + 1183) / 1184;
   rpc = rpc < 1 ? 1 : (rpc > 64 ? 64 : rpc);
   if (transposed && rpc > 8) rpc = (rpc + 15) / 16 * 16;
   const int ns = (d.flags & 1) ? 1 : 0;
   auto cnt64 = reinterpret_cast<unsigned long long*>(counts);
-  dim3 grid(static_cast<unsigned>(gx), static_cast<unsigned>((Tr + rpc - 1) / rpc), static_cast<unsigned>(bhm));
+  const bool api = !kernel_map;
+  const bool nsc = row_cnt != nullptr || col_cnt != nullptr;
+  const int jpt = (!transposed && (Tc % 4) == 0 && Tc >= 512) ? 4 : 1;  // wide maps: 4 column tiles per thread
+  const long gxj = (Tc + 128L * jpt - 1) / (128L * jpt);
+  dim3 grid(static_cast<unsigned>(gxj), static_cast<unsigned>((Tr + rpc - 1) / rpc), static_cast<unsigned>(bhm));
   // (row-wise: ext8 holds the extrema of the br-row tiles)
-  return launch_pdl(d.rowwise ? k1_classify<1, true> : k1_classify<1, false>, grid, dim3(128), 0, st, ext8, d.N,
-                    d.causal, br, bc, Tr, Tc, map, transposed, km, ns, cnt64, row_cnt, col_cnt, static_cast<int>(rpc));
+  auto pick = [&](auto kern) {
+    return launch_pdl(kern, grid, dim3(128), 0, st, ext8, d.N, d.causal, br, bc, Tr, Tc, map, km, ns, cnt64, row_cnt,
+                      col_cnt, static_cast<int>(rpc));
+  };
+#define FM_K1B(RW)                                                                          \
+  if (transposed) return api ? pick(k1_classify<1, RW, true, true, false>) : pick(k1_classify<1, RW, true, false, false>); \
+  if (api) {                                                                                \
+    if (nsc) return jpt == 4 ? pick(k1_classify<4, RW, false, true, true>) : pick(k1_classify<1, RW, false, true, true>); \
+    return jpt == 4 ? pick(k1_classify<4, RW, false, true, false>) : pick(k1_classify<1, RW, false, true, false>); \
+  }                                                                                         \
+  return jpt == 4 ? pick(k1_classify<4, RW, false, false, false>) : pick(k1_classify<1, RW, false, false, false>)
+  if (d.rowwise) {
+    FM_K1B(true);
+  } else {
+    FM_K1B(false);
+  }
+#undef FM_K1B
 }
 
 // ---------------------------------------------------------------------------------------

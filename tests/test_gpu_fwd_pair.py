@@ -46,8 +46,9 @@ def test_pair_forward_vs_oracle_and_single(fmlib, fam, N):
     o1, l1 = fmlib.flashmask_fwd(tc["q"], tc["k"], tc["v"], sri_c, causal, out_dtype=torch.float32)
     torch.cuda.synchronize()
     # same running-max decisions and PV order; the two kernels split exp2 differently between MUFU
-    # and the polynomial (1 vs 3 pairs of 8), so a few P values round to a neighbouring bf16
-    assert torch.allclose(o2, o1, atol=2e-3, rtol=0), (o2 - o1).abs().max().item()
+    # and the polynomial (1 vs 3 pairs of 8), so some P values round to a neighbouring bf16 — up to
+    # ~5e-3 in O where few keys are visible (P near 1); both are checked against the oracle below
+    assert torch.allclose(o2, o1, atol=1e-2, rtol=0), (o2 - o1).abs().max().item()
     fin = torch.isfinite(l1)
     assert torch.equal(fin, torch.isfinite(l2))
     assert torch.allclose(l2[fin], l1[fin], atol=1e-4, rtol=0)
