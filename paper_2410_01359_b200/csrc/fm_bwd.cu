@@ -44,56 +44,21 @@ namespace fm { __device__ long long g_fm_trace[64 * 16]; __device__ long long g_
   } while (0)
 #endif
 
-#ifndef FM_BWD_ISSUER_WAIT
-#define FM_BWD_ISSUER_WAIT mbar_wait_sleep  // MMA issuer warps wait suspended (see fm_ptx.cuh)
-#endif
-
-#ifndef FM_BWD_DK_SS
-#define FM_BWD_DK_SS 0  // 1: dK reads dS^T from smem (SS); measured ~2% slower (smem bandwidth)
-#endif
-
-#ifndef FM_BWD_KA
-#define FM_BWD_KA 1  // K_j as TMEM A operand of S^T (single P/dS TMEM buffer): +2-3 % since the dQ stages moved
-#endif
 namespace fm {
 
 namespace bwd {
 
-#ifndef FM_BWD_G_WARP
-#define FM_BWD_G_WARP 14  // warp issuing dV/dK/dQ (15: moves it to the fourth sub-partition)
-#endif
-constexpr int G_WARP = FM_BWD_G_WARP;
+constexpr int G_WARP = 14;  // warp issuing dV/dK/dQ (warp 13 issues S^T/dP^T)
 constexpr int NT = (G_WARP + 1) * 32;
-#ifndef FM_QST
-#define FM_QST 3
-#endif
-#ifndef FM_DQ_NSTAGE
-#define FM_DQ_NSTAGE 2
-#endif
-constexpr int DQ_NSTAGE = FM_DQ_NSTAGE;  // 8 KiB dQ^T staging buffers (d=128)
-#ifndef FM_MAXTRB
-#define FM_MAXTRB 4096
-#endif
-constexpr int kMaxTrb = FM_MAXTRB;  // d=128 (Br=64); d=64 (Br=128) uses half: the same max N
+constexpr int DQ_NSTAGE = 2;  // dQ^T staging buffers (d=128), DQ_CROWS query rows each
+constexpr int DQ_CROWS = 32;  // query rows per dQ^T staging chunk: two bulk reduce-adds per row tile
+constexpr int kMaxTrb = 4096;  // d=128 (Br=64); d=64 (Br=128) uses half: the same max N
 // d=64 dQ reduction: the dQ warpgroup stages the 128-row x 32-column fp32 half tiles (16 KiB,
 // 128-byte swizzle) for one TMA tensor reduce-add each, DQ64_NBUF in flight — two operations per
 // row tile (the cost of the reduction follows the number of operations).
 constexpr int DQ64_NBUF = 3;
 constexpr int DQ64_STAGES = DQ64_NBUF;
 constexpr int DQ64_STAGE_FLOATS = kDq64BoxRows * 32;
-#ifndef FM_DQ_CROWS
-#define FM_DQ_CROWS 32
-#endif
-constexpr int DQ_CROWS = FM_DQ_CROWS;  // query rows per dQ^T staging chunk (d=128)
-#ifndef FM_BWD_NDS
-#define FM_BWD_NDS 1
-#endif
-#ifndef FM_BWD_NDS64
-#define FM_BWD_NDS64 1
-#endif
-#ifndef FM_QST64
-#define FM_QST64 3
-#endif
 
 template <int D>
 struct Cfg {
@@ -102,7 +67,7 @@ struct Cfg {
   // K_j in TMEM as S^T's A operand: an SS MMA with N = 64 is bound by shared-memory operand
   // bandwidth (A 4 KiB + B 2 KiB per 48 clk), a TS one runs at the full 32 clk
   // (scripts/bwdmix_bench.cu).  Its 64 columns come from letting dQ^T share the P/dS columns.
-  static constexpr bool KA_TMEM = (D == 128) && (FM_BWD_KA != 0);
+  static constexpr bool KA_TMEM = (D == 128);
   // d=128: two P/dS column buffers, so the compute WGs write P/dS(t+1) while dV/dK/dQ(t) still
   // read buffer t; dQ^T(t) reuses the 64 columns of its own buffer (written after dV/dK(t)).
   static constexpr int NB = (D == 128 && !KA_TMEM) ? 2 : 1;
@@ -114,18 +79,16 @@ struct Cfg {
   static constexpr int S_COL = 0, DP_COL = BR, P_COL = 2 * BR, DS_COL = 2 * BR + BR / 2;
   static constexpr int DQ_COL = DQ_ALIAS ? P_COL : 192;
   static constexpr int BUF_STRIDE = BR;  // column offset of P/dS/dQ buffer 1 (NB == 2)
-  // Option: dK += dS^T Q reads dS^T from the shared-memory buffer the dQ GEMM uses anyway (SS,
-  // N = 128) instead of a TMEM copy.  It balances the sub-partitions (TS operand reads slow the
-  // compute warps sharing the issuing warp's sub-partition) but costs shared-memory bandwidth;
-  // measured ~2 % slower overall, so off by default.
-  static constexpr bool DK_SS = (D == 128) && (FM_BWD_DK_SS != 0);
+  // (dK += dS^T Q with dS^T read from the dQ GEMM's shared-memory buffer (SS) instead of TMEM was
+  // measured ~2 % slower: shared-memory bandwidth)
+  static constexpr bool DK_SS = false;
   static constexpr int KA_COL = 192;
   static constexpr int DV_COL = (D == 128) ? 256 : 384;
   static constexpr int DK_COL = DV_COL + D;
   static constexpr int MAXTRB = (D == 128) ? kMaxTrb : kMaxTrb / 2;
   // per-head-dim ring depths: Q/dO stages and dS shared-memory buffers
-  static constexpr int QST = (D == 64) ? FM_QST64 : FM_QST;
-  static constexpr int NDS = (D == 64) ? FM_BWD_NDS64 : FM_BWD_NDS;  // dS shared-memory buffers
+  static constexpr int QST = 3;  // Q/dO ring (2 stages measured -6 %)
+  static constexpr int NDS = 1;  // dS shared-memory buffers: one frees room for the dQ stages
 };
 
 template <int D, bool ROWW>
@@ -341,7 +304,7 @@ __global__ void __launch_bounds__(bwd::NT, 1)
       constexpr uint32_t ID_G = idesc16<F16>(128, D, 0, 1);    // dV, dK: A in TMEM, B MN-major
       constexpr uint32_t ID_Q = idesc16<F16>(128, 64, 1, 1);   // dQ^T (d=128) / dQ (d=64), both MN-major
       const uint32_t k_addr = smem_u32(sm.k), v_addr = smem_u32(sm.v);
-      FM_BWD_ISSUER_WAIT(&sm.kv_full, 0);
+      mbar_wait_sleep(&sm.kv_full, 0);
       if (warp == 13) {
         if constexpr (C::KA_TMEM) {
           // K_j (SW128 K-major smem tile) -> TMEM columns [KA_COL, KA_COL + 64) by the tensor core:
@@ -355,8 +318,8 @@ __global__ void __launch_bounds__(bwd::NT, 1)
         }
         for (int t = 0; t < nE; ++t) {
           const int st = t % C::QST;
-          if (t > 0) FM_BWD_ISSUER_WAIT(&sm.sdp_free, (t - 1) & 1);  // compute WGs hold S^T/dP^T(t-1) in registers          if (lane == 0) FM_T(1, t);
-          FM_BWD_ISSUER_WAIT(&sm.q_full[st], (t / C::QST) & 1);
+          if (t > 0) mbar_wait_sleep(&sm.sdp_free, (t - 1) & 1);  // compute WGs hold S^T/dP^T(t-1) in registers          if (lane == 0) FM_T(1, t);
+          mbar_wait_sleep(&sm.q_full[st], (t / C::QST) & 1);
           if (lane == 0) FM_T(14, t);
           tc_fence_after();
           const uint32_t q_addr = smem_u32(sm.q[st]), do_addr = smem_u32(sm.dO[st]);
@@ -382,7 +345,7 @@ __global__ void __launch_bounds__(bwd::NT, 1)
           if (lane == 0) FM_T(0, t);
           const int bi = t % C::NB;
           const uint32_t ph = (t / C::NB) & 1, boff = bi * C::BUF_STRIDE;
-          FM_BWD_ISSUER_WAIT(&sm.p_full[bi], ph);
+          mbar_wait_sleep(&sm.p_full[bi], ph);
           if (lane == 0) FM_T(2, t);
           tc_fence_after();
           const uint32_t q_addr = smem_u32(sm.q[st]), do_addr = smem_u32(sm.dO[st]);
@@ -411,7 +374,7 @@ __global__ void __launch_bounds__(bwd::NT, 1)
             if constexpr (C::DK_SS) mma_commit_w(&sm.ds_empty[t % C::NDS]);  // dK(t) read dS^T(t)
             continue;
           }
-          if constexpr (!C::DQ_ALIAS) FM_BWD_ISSUER_WAIT(&sm.dq_empty[0], (t & 1) ^ 1);          tc_fence_after();
+          if constexpr (!C::DQ_ALIAS) mbar_wait_sleep(&sm.dq_empty[0], (t & 1) ^ 1);          tc_fence_after();
           const uint32_t ds_addr = smem_u32(sm.ds[t % C::NDS]);
 #pragma unroll
           for (int kk = 0; kk < 8; ++kk) {

@@ -47,41 +47,25 @@ namespace fm { __device__ long long g_fm_trace_fwd[64 * 16]; __device__ long lon
 #define FM_TRACE_NE(n) ((void)0)
 #endif
 
-#ifndef FM_WAIT_P
-#define FM_WAIT_P mbar_wait  // MMA issuer waiting for P (mbar_wait_spin measured ~2% slower)
-#endif
-#ifndef FM_WAIT_S
-#define FM_WAIT_S mbar_wait  // softmax waiting for S
-#endif
-
-#ifndef FM_POLY_PAIRS
-#define FM_POLY_PAIRS 3  // of every 8 column pairs, how many use the FMA-pipe exp2 (rest: MUFU)
-#endif
-
-#ifndef FM_FWD_REFINE
-// f3: mask only the dirty 32 x 16 sub-blocks of PARTIAL tiles (K1c words).  Compiled into the
-// causal kernels only: in-process A/B measured +2..+6 % on causal families (+24 %
-// QK-sparse) but -1.3 % on the non-causal C3 kernel (code generation) and +-1.5 % elsewhere.
-#define FM_FWD_REFINE(causal) (causal)
-#endif
-
 namespace fm {
 
 namespace fwd {
 
 constexpr int NT = 576;   // 16 softmax warps + TMA producer + MMA issuer
 constexpr int MST = 4;
-#ifndef FM_FWD_KST64
-#define FM_FWD_KST64 3
-#endif
-#ifndef FM_FWD_VST64
-#define FM_FWD_VST64 3
-#endif
+// of every 8 column pairs, how many take the FMA-pipe polynomial exp2 (the rest MUFU ex2):
+// 1-3 of 8 change the forward by < 2 %
+constexpr int kPolyPairs = 3;
+// f3: mask only the dirty 32 x 16 sub-blocks of PARTIAL tiles (K1c words).  Compiled into the
+// causal kernels only: in-process A/B measured +2..+6 % on causal families
+// (+24 % QK-sparse) but -1.3 % on the non-causal C3 kernel (code generation) and +-1.5 % elsewhere.
+template <bool CAUSAL>
+constexpr bool kRefine = CAUSAL;
 // K / V ring depths (d = 128: 2 each fills shared memory; d = 64 tiles are half the size:
 // 3-deep rings, +1-3 % on the C5 d = 64 sweep)
 template <int D>
 struct Rings {
-  static constexpr int KST = (D == 64) ? FM_FWD_KST64 : 2, VST = (D == 64) ? FM_FWD_VST64 : 2;
+  static constexpr int KST = (D == 64) ? 3 : 2, VST = (D == 64) ? 3 : 2;
 };
 
 template <int D>
@@ -230,7 +214,7 @@ __global__ void __launch_bounds__(fwd::NT, 1)
 #pragma unroll
           for (int qq = 0; qq < 2; ++qq) {
             uint32_t wq = 0xFFFFFFFFu;
-            if (FM_FWD_REFINE(CAUSAL) && a.cw != nullptr && ent_cls(ent, qq) == 1 && !(j == a.Tc - 1 && (a.N & 127) != 0))
+            if (kRefine<CAUSAL> && a.cw != nullptr && ent_cls(ent, qq) == 1 && !(j == a.Tc - 1 && (a.N & 127) != 0))
               wq = a.cw[(bhm * a.Tr + (qq == 0 ? i0 : i1)) * a.Tc + j];
             sm.cw[ms][qq] = wq;
           }
@@ -261,7 +245,7 @@ __global__ void __launch_bounds__(fwd::NT, 1)
       uint32_t pv_cnt[2] = {0, 0};
       auto issue_pv = [&](int q) {
         const int pe = pend[q];
-        FM_WAIT_P(&sm.p_full[q], pv_cnt[q] & 1);
+        mbar_wait(&sm.p_full[q], pv_cnt[q] & 1);
         if (lane == 0) FT(4 + q, pe);
         const int vs = pe % VST;
         mbar_wait(&sm.v_full[vs], (pe / VST) & 1);
@@ -362,7 +346,7 @@ __global__ void __launch_bounds__(fwd::NT, 1)
       mbar_wait(&sm.m_full[ms], (e / MST) & 1);
       if (cls != 0) {
         const int j = static_cast<int>(ent & 0xFFFFFFu);
-        FM_WAIT_S(&sm.s_full[q], cnt & 1);
+        mbar_wait(&sm.s_full[q], cnt & 1);
         if (row_t == 0 && hh == 0) FT(0 + q, e);
         tc_fence_after();
         // Pass 1: max over this half's 64 columns, 32 at a time (S stays in TMEM for pass 2).
@@ -372,7 +356,7 @@ __global__ void __launch_bounds__(fwd::NT, 1)
         uint32_t sr[2][16];
         // f3: the 16-column chunks of this warp's 32 rows x 64 columns that hold a masked cell
         const uint32_t pm =
-            (cls != 1) ? 0u : ((FM_FWD_REFINE(CAUSAL) && !ROWW) ? (sm.cw[ms][q] >> (wl * 8 + hh * 4)) & 0xFu : 0xFu);
+            (cls != 1) ? 0u : ((kRefine<CAUSAL> && !ROWW) ? (sm.cw[ms][q] >> (wl * 8 + hh * 4)) & 0xFu : 0xFu);
         tmem_ld16(tSh, sr[0]);
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
@@ -460,7 +444,7 @@ __global__ void __launch_bounds__(fwd::NT, 1)
         }
         const float m_use = (m_used == -INFINITY) ? 0.f : m_used;
         // Pass 2: P = exp2(S*scale*log2e - m) over this half's columns; packed FFMA2 for the
-        // argument, MUFU ex2 for most pairs and the FMA-pipe polynomial for FM_POLY_PAIRS of 8;
+        // argument, MUFU ex2 for most pairs and the FMA-pipe polynomial for kPolyPairs of 8;
         // row sums with packed FADD2; packed bf16 P written back over consumed S columns.
         const uint64_t sl2x2 = f2pack(sl2, sl2), negm2 = f2pack(-m_use, -m_use);
         uint64_t acc[4] = {0ull, 0ull, 0ull, 0ull};
@@ -480,7 +464,7 @@ __global__ void __launch_bounds__(fwd::NT, 1)
             const int k = ch * 8 + kk;
             const uint64_t x2 = f2fma(f2pack(sv[2 * kk], sv[2 * kk + 1]), sl2x2, negm2);
             float p0, p1;
-            if ((k & 7) >= 8 - FM_POLY_PAIRS) {
+            if ((k & 7) >= 8 - kPolyPairs) {
               exp2_poly2(x2, p0, p1);
             } else {
               float x0, x1;

@@ -69,25 +69,19 @@ __device__ __forceinline__ long long fm_gtimer() { long long t; asm volatile("mo
   } while (0)
 #endif
 
-#ifndef FM_POLY_PAIRS2
-#define FM_POLY_PAIRS2 1  // of every 8 column pairs, how many use the FMA-pipe exp2 (rest: MUFU;
-                          // 1 measured best here: the pair kernel's softmax is issue-bound, and a
-                          // polynomial pair costs ~14 instructions against ~5 for a MUFU pair)
-#endif
-#ifndef FM_FWD2_REFINE
-#define FM_FWD2_REFINE(causal) (causal)
-#endif
-
 namespace fm {
 
 namespace fwd2 {
 
 constexpr int NT = 576;
 constexpr int KST = 4, VST = 4, MST = 4;  // ring depths (MST even: a mask stage belongs to one warpset)
-#ifndef FM_FWD2_MMA_WARP
-#define FM_FWD2_MMA_WARP 17
-#endif
-constexpr int MMA_WARP = FM_FWD2_MMA_WARP, PRODUCER_WARP = 33 - FM_FWD2_MMA_WARP;
+// of every 8 column pairs, how many use the FMA-pipe exp2 (rest: MUFU): 1 measured best here —
+// the pair kernel's softmax is issue-bound and a polynomial pair costs ~14 instructions against
+// ~5 for a MUFU pair
+constexpr int kPolyPairs = 1;
+template <bool CAUSAL>
+constexpr bool kRefine = CAUSAL;  // f3 words in the causal kernels only, as in K2a
+constexpr int MMA_WARP = 17, PRODUCER_WARP = 16;
 constexpr int D = 128;
 constexpr uint32_t O_COL = 384;
 
@@ -228,7 +222,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fwd2::NT, 1)
         mbar_wait(&sm.m_empty[ms], ((e / MST) & 1) ^ 1);
         if (ent_cls(ent, rank) == 1) {
           uint32_t wq = 0xFFFFFFFFu;
-          if (FM_FWD2_REFINE(CAUSAL) && a.cw != nullptr && !(j == a.Tc - 1 && (a.N & 127) != 0))
+          if (kRefine<CAUSAL> && a.cw != nullptr && !(j == a.Tc - 1 && (a.N & 127) != 0))
             wq = a.cw[(bhm * a.Tr + my_i) * a.Tc + j];
           sm.cw[ms] = wq;
           mbar_expect_tx(&sm.m_full[ms], 128 * 16);
@@ -339,7 +333,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fwd2::NT, 1)
       uint32_t sr[2][16];
       if (cls != 0) {
         const int j = static_cast<int>(ent & 0xFFFFFFu);
-        const uint32_t pm = (cls != 1) ? 0u : (FM_FWD2_REFINE(CAUSAL) ? (sm.cw[ms] >> (wl * 8 + hh * 4)) & 0xFu : 0xFu);
+        const uint32_t pm = (cls != 1) ? 0u : (kRefine<CAUSAL> ? (sm.cw[ms] >> (wl * 8 + hh * 4)) & 0xFu : 0xFu);
         tmem_ld16(tSh, sr[0]);
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
@@ -442,7 +436,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fwd2::NT, 1)
             const int k = ch * 8 + kk;
             const uint64_t x2 = f2fma(f2pack(sv[2 * kk], sv[2 * kk + 1]), sl2x2, negm2);
             float p0, p1;
-            if ((k & 7) >= 8 - FM_POLY_PAIRS2) {
+            if ((k & 7) >= 8 - kPolyPairs) {
               exp2_poly2(x2, p0, p1);
             } else {
               float x0, x1;
