@@ -151,22 +151,52 @@ __device__ __forceinline__ uint32_t row_mask_bits_rw(int r0, int key, const int4
   return key >= N ? 0xFFFFFFFFu : m;
 }
 
-template <bool PART, bool CAUSAL, bool F16>
+// lq = -l2 and dq = -D of the chunk's 32 queries (K3 stores them negated).  PACKED (d = 64, where
+// the compute warpgroups are the critical resource): the argument
+// S*scale*log2e - l2, dP - D and P*(dP - D) as packed FFMA2 / FADD2 / FMUL2 per query pair
+// (backward +2..+5 % at d = 64; neutral within noise at d = 128, which keeps the scalar form).
+template <bool PART, bool CAUSAL, bool F16, bool PACKED>
 __device__ __forceinline__ void pds_chunk(const uint32_t* sr, const uint32_t* dr, const float* lq, const float* dq,
                                           float sl2, uint32_t mb, uint32_t* pp, uint32_t* dp) {
+  if constexpr (!PACKED) {
+#pragma unroll
+    for (int c = 0; c < 32; c += 4) {
+      const float4 L4 = *reinterpret_cast<const float4*>(lq + c);
+      const float4 D4 = *reinterpret_cast<const float4*>(dq + c);
+      const float l4[4] = {L4.x, L4.y, L4.z, L4.w};
+      const float d4[4] = {D4.x, D4.y, D4.z, D4.w};
+      float p[4], ds[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        p[u] = ex2(fmaf(__uint_as_float(sr[c + u]), sl2, l4[u]));
+        if constexpr (PART) p[u] = ((mb >> (c + u)) & 1u) ? 0.f : p[u];
+        ds[u] = p[u] * (__uint_as_float(dr[c + u]) + d4[u]);
+      }
+      pp[c / 2] = pack16<F16>(p[0], p[1]);
+      pp[c / 2 + 1] = pack16<F16>(p[2], p[3]);
+      dp[c / 2] = pack16<F16>(ds[0], ds[1]);
+      dp[c / 2 + 1] = pack16<F16>(ds[2], ds[3]);
+    }
+    return;
+  }
+  const uint64_t sl2x2 = f2pack(sl2, sl2);
 #pragma unroll
   for (int c = 0; c < 32; c += 4) {
     const float4 L4 = *reinterpret_cast<const float4*>(lq + c);
     const float4 D4 = *reinterpret_cast<const float4*>(dq + c);
-    const float l4[4] = {L4.x, L4.y, L4.z, L4.w};
-    const float d4[4] = {D4.x, D4.y, D4.z, D4.w};
-    float p[4], ds[4];
+    float x[4], p[4], ds[4];
+    f2unpack(f2fma(f2pack(__uint_as_float(sr[c]), __uint_as_float(sr[c + 1])), sl2x2, f2pack(L4.x, L4.y)), x[0], x[1]);
+    f2unpack(f2fma(f2pack(__uint_as_float(sr[c + 2]), __uint_as_float(sr[c + 3])), sl2x2, f2pack(L4.z, L4.w)), x[2],
+             x[3]);
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      p[u] = ex2(fmaf(__uint_as_float(sr[c + u]), sl2, -l4[u]));
+      p[u] = ex2(x[u]);
       if constexpr (PART) p[u] = ((mb >> (c + u)) & 1u) ? 0.f : p[u];
-      ds[u] = p[u] * (__uint_as_float(dr[c + u]) - d4[u]);
     }
+    const uint64_t d01 = f2add(f2pack(__uint_as_float(dr[c]), __uint_as_float(dr[c + 1])), f2pack(D4.x, D4.y));
+    const uint64_t d23 = f2add(f2pack(__uint_as_float(dr[c + 2]), __uint_as_float(dr[c + 3])), f2pack(D4.z, D4.w));
+    f2unpack(f2mul(f2pack(p[0], p[1]), d01), ds[0], ds[1]);
+    f2unpack(f2mul(f2pack(p[2], p[3]), d23), ds[2], ds[3]);
     pp[c / 2] = pack16<F16>(p[0], p[1]);
     pp[c / 2 + 1] = pack16<F16>(p[2], p[3]);
     dp[c / 2] = pack16<F16>(ds[0], ds[1]);
@@ -431,9 +461,9 @@ __global__ void __launch_bounds__(bwd::NT, 1)
         if (partial) {
           const uint32_t mb = ROWW ? row_mask_bits_rw<CAUSAL>(i * BR + q0, key, sm.rvec[st] + (ROWW ? q0 : 0), a.N)
                                    : row_mask_bits<CAUSAL>(i * BR + q0, key, mv);
-          pds_chunk<true, CAUSAL, F16>(sr, dr, lv + q0, dv + q0, sl2, mb, pp[ch], dp[ch]);
+          pds_chunk<true, CAUSAL, F16, D == 64>(sr, dr, lv + q0, dv + q0, sl2, mb, pp[ch], dp[ch]);
         } else {
-          pds_chunk<false, CAUSAL, F16>(sr, dr, lv + q0, dv + q0, sl2, 0u, pp[ch], dp[ch]);
+          pds_chunk<false, CAUSAL, F16, D == 64>(sr, dr, lv + q0, dv + q0, sl2, 0u, pp[ch], dp[ch]);
         }
       }
       if (tid == 0) FM_T(5, t);

@@ -177,7 +177,7 @@ __global__ void __launch_bounds__(dqk::NT, 1)
     const uint32_t lane_off = static_cast<uint32_t>(wl * 32) << 16;
     const float sl2 = a.scale_log2;
     const size_t ri = bh * a.Npb + row;  // Npb >= Tr * 128 rows, so this index is in range
-    const float l2 = a.l2[ri], dval = a.dvec[ri];
+    const float nl2 = a.l2[ri], ndval = a.dvec[ri];  // -lse*log2e and -D (K3 stores them negated)
     // row-wise representation (R32): this row's (LTS, len, UTS, len) over key columns
     const int4 rmv = a.rowwise ? a.vec4[bhm * static_cast<size_t>(a.Tc) * 128 + row] : make_int4(0, 0, 0, 0);
     for (int e = 0; e < nE; ++e) {
@@ -204,7 +204,7 @@ __global__ void __launch_bounds__(dqk::NT, 1)
           float ds2[2];
 #pragma unroll
           for (int u = 0; u < 2; ++u) {
-            float p = ex2(fmaf(__uint_as_float(sr[c][t + u]), sl2, -l2));
+            float p = ex2(fmaf(__uint_as_float(sr[c][t + u]), sl2, nl2));
             if (part) {
               const int col = hh * 64 + c * 32 + t + u;
               bool msk;
@@ -223,7 +223,7 @@ __global__ void __launch_bounds__(dqk::NT, 1)
               }
               p = msk ? 0.f : p;
             }
-            ds2[u] = p * (__uint_as_float(dr[c][t + u]) - dval);
+            ds2[u] = p * (__uint_as_float(dr[c][t + u]) + ndval);
           }
           pk[c * 16 + t / 2] = pack16<F16>(ds2[0], ds2[1]);
         }

@@ -40,8 +40,8 @@ struct Workspace {
   uint8_t* fmap;    // [B, Hm, Tr, Tc] forward kernel map (128 x 128)
   uint32_t* cw;     // [B, Hm, Tr, Tc] f3 refinement words of the forward map (K1c; PARTIAL tiles)
   uint8_t* bmap;    // [B, Hm, Tc, Trb] backward kernel map, transposed (Brb x 128)
-  float* dvec;      // [B, H, Npb] D = rowsum(dO o O)
-  float* l2;        // [B, H, Npb] lse * log2(e) (+inf for empty / padded rows)
+  float* dvec;      // [B, H, Npb] -D, D = rowsum(dO o O) (negated: consumers add it)
+  float* l2;        // [B, H, Npb] -lse * log2(e) (-inf for empty / padded rows)
   float* dqacc;     // [B, H, Npb, d] fp32 dQ accumulator
   size_t bytes;
 };

@@ -455,6 +455,8 @@ cudaError_t launch_classify(const int32_t* ext8, const Dims& d, int br, int bc, 
 // K3: backward preprocess (Alg. 2 line 4, D per row — DESIGN.md R5).  A group of D/8
 // threads per (b, h, r), r < Npb, each owning 8 consecutive columns (16-byte loads):
 // D = sum_c dO[r,c] * O[r,c]; l2 = lse * log2(e), or +inf when the row is empty (lse = -inf)
+// (both written NEGATED — -D and -l2, -l2 = -inf for empty / padded rows — so K4 and K6 form
+// scale*S*log2e - l2 and dP - D as one packed fma / add)
 // or padded (r >= N) so that exp2(S - l2) = 0 exactly; zero the row of dQacc.
 // ---------------------------------------------------------------------------------------
 template <int D, bool OUT_F32, bool F16>
@@ -494,9 +496,9 @@ __global__ void __launch_bounds__(256) k3_bwd_pre(const void* __restrict__ o, co
   if (!active) return;
   if (part == 0) {
     const size_t ri = static_cast<size_t>(bh) * Npb + r;
-    dvec[ri] = (r < N) ? acc : 0.f;
+    dvec[ri] = (r < N) ? -acc : 0.f;  // stored negated: the consumers add it (packed FFMA2 / FADD2)
     const float lv = (r < N) ? lse[static_cast<size_t>(bh) * N + r] : -INFINITY;
-    l2[ri] = (lv == -INFINITY) ? INFINITY : lv * 1.4426950408889634f;
+    l2[ri] = (lv == -INFINITY) ? -INFINITY : -lv * 1.4426950408889634f;  // negated, as D
   }
   float4* dq = reinterpret_cast<float4*>(dqacc + (static_cast<size_t>(bh) * Npb + r) * D + part * 8);
   dq[0] = make_float4(0.f, 0.f, 0.f, 0.f);
