@@ -171,8 +171,27 @@ size_t carve(const fm::Dims& d, int pass, void* base, fm::Workspace* w) {
     w->l2 = reinterpret_cast<float*>(take(bh * d.Npb * sizeof(float)));
     w->dqacc = reinterpret_cast<float*>(take(bh * d.Npb * d.D * sizeof(float)));
   }
+  // LPT orders (>= ceil(Tr/2) pairs or Tc key tiles per (b, hm)) followed by one flag per (b, hm)
+  w->order = reinterpret_cast<uint16_t*>(take(bhm * (d.Tc + 1) * sizeof(uint16_t)));
   w->bytes = off;
   return off;
+}
+
+// LPT scheduling (K1d) for small problems: the attention kernels' grid spans only a few waves of
+// 148 SMs, so unequal unit costs leave SMs idle at the end (a list-scheduling simulation of C2
+// put the default order at 0.87-0.90 of ideal, LPT by groups of heads at 0.95-0.97).  Returns the
+// heads per group (a divisor of `heads`) sized so that the group's K/V (and for the backward
+// Q/dO) stay in L2 while its units run, or 0 when LPT is not used.
+int lpt_group(const fm::Dims& d, long units, int heads, size_t bytes_per_head) {
+  if (units > 16L * 148 || units < 148) return 0;
+  constexpr size_t kBudget = size_t(40) << 20;
+  int g = 1;
+  for (int c = heads; c >= 1; --c)
+    if (heads % c == 0 && static_cast<size_t>(c) * bytes_per_head <= kBudget) {
+      g = c;
+      break;
+    }
+  return g;
 }
 
 fm::F32Args f32_args(const fm::Dims& d, const fm::Workspace& w) {
@@ -343,6 +362,15 @@ fm_status flashmask_fwd(const fm_params* p, const void* q, const void* k, const 
   }
   fm::FwdArgs a{};
   a.B = d.B; a.N = d.N; a.H = d.H; a.Hm = d.Hm; a.Tr = d.Tr; a.Tc = d.Tc; a.G = d.G;
+  // LPT order of (head, pair) units for small grids (K1d); K/V bytes per query head ~ 2 N d 2 / G
+  a.hgrp = lpt_group(d, static_cast<long>((d.Tr + 1) / 2) * d.H * d.B, d.H,
+                     static_cast<size_t>(4) * d.N * d.D / static_cast<size_t>(d.G));
+  a.order = nullptr;
+  if (a.hgrp > 0 && !((p->flags & FM_FLAG_FWD_PAIR) && d.D == 128 && !d.rowwise)) {
+    e = timed(FM_KERNEL_CLASSIFY, st, [&] { return fm::launch_order(w.fmap, d, 1, w.order, st); });
+    if (e != cudaSuccess) return cuda_fail(e, "order");
+    a.order = w.order;
+  }
   a.scale_log2 = d.scale * 1.4426950408889634f;
   a.fmap = w.fmap;
   a.cw = refine ? w.cw : nullptr;
@@ -415,6 +443,15 @@ fm_status flashmask_bwd(const fm_params* p, const void* q, const void* k, const 
   }
   e = timed(FM_KERNEL_CLASSIFY, st, [&] { return fm::launch_classify(ext_b, d, d.Brb, fm::kTile, w.bmap, 1, 1, nullptr, st); });
   if (e != cudaSuccess) return cuda_fail(e, "classify");
+  // LPT order of (kv head, key tile) units for small grids (K1d); per kv head: K, V and the
+  // group's Q, dO ~ 2 N d 2 (1 + G).  Launched before K3 so that K4, which reads it before its
+  // griddepcontrol.wait, finds it complete (two launches back, fm_ptx.cuh)
+  const int lpt_hgrp = lpt_group(d, static_cast<long>(d.Tc) * d.Hkv * d.B, d.Hkv,
+                                 static_cast<size_t>(4) * d.N * d.D * static_cast<size_t>(1 + d.G));
+  if (lpt_hgrp > 0) {
+    e = timed(FM_KERNEL_CLASSIFY, st, [&] { return fm::launch_order(w.bmap, d, 0, w.order, st); });
+    if (e != cudaSuccess) return cuda_fail(e, "order");
+  }
   e = timed(FM_KERNEL_BWD_PRE, st, [&] { return fm::launch_bwd_pre(d, o, dout, lse, w.dvec, w.l2, w.dqacc, st); });
   if (e != cudaSuccess) return cuda_fail(e, "bwd preprocess");
   fm::BwdArgs a{};
@@ -429,6 +466,8 @@ fm_status flashmask_bwd(const fm_params* p, const void* q, const void* k, const 
   a.dqacc = w.dqacc;
   a.dk = dk;
   a.dv = dv;
+  a.hgrp = lpt_hgrp;
+  a.order = lpt_hgrp > 0 ? w.order : nullptr;
   const bool deterministic = (p->flags & FM_FLAG_DETERMINISTIC) != 0;
   a.with_dq = deterministic ? 0 : 1;
   CUtensorMap tdq, tdk, tdv;

@@ -222,8 +222,22 @@ __global__ void __launch_bounds__(bwd::NT, 1)
   S& sm = *smem_align1024<S>(smem_raw);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int j = static_cast<int>(blockIdx.x);
-  const int hk = blockIdx.y, b = blockIdx.z;  // key/value head; its G query heads are looped over
+  const int b = blockIdx.z;
+  // unit: key tile j of key/value head hk (its G query heads are looped over).  With an LPT order
+  // (K1d, small problems) the CTAs of a batch entry take groups of a.hgrp kv heads, in each group
+  // the key tiles by descending work, heads innermost; else j = x, hk = y.
+  int j, hk;
+  if (a.order != nullptr && (a.Hm > 1 || a.order[static_cast<size_t>(a.B) * a.Tc + b] != 0)) {
+    const int L = static_cast<int>(blockIdx.x) + a.Tc * static_cast<int>(blockIdx.y);
+    const int per_g = a.Tc * a.hgrp;
+    const int g = L / per_g, rem = L - g * per_g;
+    const int jrank = rem / a.hgrp;
+    hk = g * a.hgrp + (rem - jrank * a.hgrp);
+    j = a.order[(static_cast<size_t>(b) * a.Hm + ((a.Hm == 1) ? 0 : hk)) * a.Tc + jrank];
+  } else {
+    j = static_cast<int>(blockIdx.x);
+    hk = blockIdx.y;
+  }
   const int hm = (a.Hm == 1) ? 0 : hk;
   const size_t bhm = static_cast<size_t>(b) * a.Hm + hm;
   const int G = a.G;

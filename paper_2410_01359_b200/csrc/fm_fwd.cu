@@ -117,8 +117,25 @@ __global__ void __launch_bounds__(fwd::NT, 1)
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int npairs = (a.Tr + 1) >> 1;
-  const int pair = npairs - 1 - static_cast<int>(blockIdx.x);  // heaviest (last) row tiles first
-  const int h = blockIdx.y, b = blockIdx.z;
+  const int b = blockIdx.z;
+  // unit of this CTA: without an LPT order, pair npairs-1-x of head y (last row tiles first: the
+  // heaviest under causal-like masks); with one (K1d, small problems), the CTAs of a batch entry
+  // take groups of a.hgrp heads, in each group the pairs by descending work, heads innermost
+  int pair, h;
+  // the order comes from the stream predecessor (K1d): wait for it before the (early) Q load
+  if (a.order != nullptr) pdl_wait();
+  if (a.order != nullptr && (a.Hm > 1 || a.order[static_cast<size_t>(a.B) * npairs + b] != 0)) {
+    const int L = static_cast<int>(blockIdx.x) + npairs * static_cast<int>(blockIdx.y);
+    const int per_g = npairs * a.hgrp;
+    const int g = L / per_g, rem = L - g * per_g;
+    const int prank = rem / a.hgrp;
+    h = g * a.hgrp + (rem - prank * a.hgrp);
+    const int hmo = (a.Hm == 1) ? 0 : h / a.G;
+    pair = a.order[(static_cast<size_t>(b) * a.Hm + hmo) * npairs + prank];
+  } else {
+    pair = npairs - 1 - static_cast<int>(blockIdx.x);
+    h = blockIdx.y;
+  }
   const int hk = h / a.G;                      // key/value head of this query head (GQA)
   const int hm = (a.Hm == 1) ? 0 : hk;
   const int i0 = 2 * pair, i1 = 2 * pair + 1;

@@ -43,6 +43,8 @@ struct Workspace {
   float* dvec;      // [B, H, Npb] -D, D = rowsum(dO o O) (negated: consumers add it)
   float* l2;        // [B, H, Npb] -lse * log2(e) (-inf for empty / padded rows)
   float* dqacc;     // [B, H, Npb, d] fp32 dQ accumulator
+  uint16_t* order;  // LPT unit order (K1d): forward [B, Hm, ceil(Tr/2)] pairs, backward [B, Hm, Tc] key
+                    // tiles, then one flag per (b, hm) (0: near-uniform work, keep the default order)
   size_t bytes;
 };
 
@@ -66,6 +68,10 @@ struct FwdArgs {
   const int4* vec4;    // normalised (start, len, start, len) per key column, or per query row (row-wise)
   void* o;
   float* lse;
+  // LPT schedule (small problems): query-tile pairs of each (b, hm) by descending work (K1d), the
+  // CTA -> (head, pair) map taking `hgrp` heads at a time; nullptr: last pairs first per head
+  const uint16_t* order;
+  int hgrp;
 };
 
 struct BwdArgs {
@@ -80,6 +86,8 @@ struct BwdArgs {
   void* dk;
   void* dv;
   int with_dq;  // 0 under FM_FLAG_DETERMINISTIC: dQ comes from K6 instead
+  const uint16_t* order;  // LPT schedule: key tiles of each (b, hm) by descending work (K1d); nullptr: j order
+  int hgrp;               // key/value heads taken together by the LPT map
 };
 
 struct DqArgs {
@@ -116,6 +124,9 @@ cudaError_t launch_classify(const int32_t* ext8, const Dims& d, int br, int bc, 
                             int32_t* col_cnt = nullptr);
 cudaError_t launch_refine(const int32_t* sri, const uint8_t* cmap, const Dims& d, uint32_t* words, int64_t* rcounts,
                           cudaStream_t st);
+// K1d: LPT order of the attention kernels' units from a kernel map (fwd: row map, pairs of row
+// tiles; bwd: transposed map, key tiles)
+cudaError_t launch_order(const uint8_t* map, const Dims& d, int fwd, uint16_t* order, cudaStream_t st);
 cudaError_t launch_fwd(const Dims& d, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
                        const CUtensorMap& to, const FwdArgs& a, cudaStream_t st);
 cudaError_t launch_fwd2(const Dims& d, const CUtensorMap& tq, const CUtensorMap& tk64, const CUtensorMap& tv,

@@ -1,0 +1,61 @@
+"""LPT scheduling (K1d, small grids: a few waves of 148 SMs) — the attention kernels read the
+unit order before griddepcontrol.wait, so back-to-back calls under programmatic dependent launch
+are the case to cover.  SURVEY a2 (per-unit work O((1-rho) T_r T_c))."""
+import numpy as np
+import pytest
+import torch
+
+from oracle import flashmask_oracle as fo
+from workloads import masks as wm
+from workloads import tensors as wt
+
+from gpu_util import assert_close, assert_lse
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def fmlib():
+    from paper_2410_01359_b200 import flashmask
+    return flashmask
+
+
+# (family, N, H, Hkv): forward grids of 256-1024 CTAs, backward 512-2048 (LPT on)
+CASES = [("causal_document", 8192, 32, 32), ("share_question", 8192, 16, 16), ("document", 4096, 64, 64),
+         ("causal_document", 4096, 64, 16)]
+
+
+@pytest.mark.parametrize("fam,N,H,Hkv", CASES)
+def test_lpt_back_to_back(fmlib, fam, N, H, Hkv):
+    rng = np.random.default_rng(N + H + len(fam))
+    m = wm.sample_family(fam, N, rng, (3, 7))
+    sri = torch.from_numpy(wm.stack([m])).cuda()
+    x = {}
+    for n, heads in (("q", H), ("do", H), ("k", Hkv), ("v", Hkv)):
+        x[n] = wt.make_tensor(n, 1, N, heads, 128, base=5).cuda()
+    runs = []
+    for _ in range(3):   # no synchronisation between the calls: PDL chains across them
+        o, lse = fmlib.flashmask_fwd(x["q"], x["k"], x["v"], sri, m.causal, out_dtype=torch.float32)
+        g = fmlib.flashmask_bwd(x["q"], x["k"], x["v"], o, x["do"], lse, sri, m.causal, out_dtype=torch.float32)
+        runs.append((o, lse) + tuple(g))
+    torch.cuda.synchronize()
+    for r in runs[1:]:
+        for name, a, b in zip(("o", "lse", "dq", "dk", "dv"), runs[0], r):
+            if name == "dq":   # fp32 hardware reduce-add order (R25)
+                assert torch.allclose(a, b, atol=1e-5, rtol=0), name
+            else:
+                assert torch.equal(a, b), name
+    o, lse, dq, dk, dv = runs[0]
+    vec = fo.expand(m.sri, m.causal, N)
+    G = H // Hkv
+    f = lambda t, h: t[0, :, h, :].double().cpu().numpy()
+    for h in (0, H - 1):
+        hk = h // G
+        O, L = fo.forward(f(x["q"], h), f(x["k"], hk), f(x["v"], hk), vec)
+        assert_close(f"O[{h}]", o[0, :, h].cpu().numpy(), O)
+        assert_lse(lse[0, h].cpu().numpy(), L)
+        if G == 1:
+            gq, gk, gv = fo.backward(f(x["q"], h), f(x["k"], h), f(x["v"], h), f(x["do"], h), vec)
+            assert_close(f"dQ[{h}]", dq[0, :, h].cpu().numpy(), gq)
+            assert_close(f"dK[{h}]", dk[0, :, h].cpu().numpy(), gk)
+            assert_close(f"dV[{h}]", dv[0, :, h].cpu().numpy(), gv)
