@@ -355,7 +355,10 @@ __global__ void __launch_bounds__(fwd::NT, 1)
     float l = 0.f;             // this half's share of the row sum
     uint32_t cnt = 0;
     int4 rmv = make_int4(0, 0, 0, 0);  // row-wise: this row's (LTS, len, UTS, len) over key columns
-    if constexpr (ROWW) rmv = a.vec4[bhm * static_cast<size_t>(a.Tc) * 128 + row];
+    // (rows past N — the ragged last tile, or the absent second tile of an odd tile count — take
+    // K1a's padding value: every key masked)
+    if constexpr (ROWW)
+      rmv = row < a.N ? a.vec4[bhm * static_cast<size_t>(a.Tc) * 128 + row] : make_int4(0, INT_MAX, 0, 0);
     for (int e = 0; e < nE; ++e) {
       const uint32_t ent = sm.list[e];
       const int cls = ent_cls(ent, q);

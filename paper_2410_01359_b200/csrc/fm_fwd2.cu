@@ -99,7 +99,7 @@ struct Smem {
   uint64_t k_full[KST], k_empty[KST], v_full[VST], v_empty[VST];
   uint64_t m_full[MST], m_empty[MST];
   uint64_t s_full[4], p_full[4], pv_done[4], o_full;  // indexed by tile e % 4
-  uint64_t mchain[4][2];                              // [lane quadrant][tile parity]
+  uint64_t mchain[4][2];                              // [lane quadrant][tile parity], 64 arrivals
   float xmax[2][2][2][128];                           // [warpset][local tile parity][half][row]
   float mval[2][128];                                 // running max after tile e, by e parity
   float xl[2][2][128], xm[2][2][128];                 // final row-sum combine [warpset][half][row]
@@ -143,7 +143,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fwd2::NT, 1)
       mbar_init(&sm.s_full[x], 1);
       mbar_init(&sm.p_full[x], 16);  // 8 softmax warps of each CTA
       mbar_init(&sm.pv_done[x], 1);
-      for (int p = 0; p < 2; ++p) mbar_init(&sm.mchain[x][p], 2);
+      for (int p = 0; p < 2; ++p) mbar_init(&sm.mchain[x][p], 64);  // every thread of the two warps
     }
     mbar_init(&sm.o_full, 1);
     fence_barrier_init();
@@ -392,9 +392,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fwd2::NT, 1)
       const bool need = m_tile > m_prev + 8.0f;
       const float m_cur = need ? m_tile : m_prev;
       if (e + 1 < nE) {
+        // each thread publishes (hh = 0) / releases (hh = 1) its own row: its arrive orders its own
+        // accesses (also for compute-sanitizer racecheck, which does not follow warp-sync chains)
         if (hh == 0) sm.mval[e & 1][row_t] = m_cur;
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&sm.mchain[wl][e & 1]);
+        mbar_arrive(&sm.mchain[wl][e & 1]);
       }
       // O holds sum_{e' < e} P_e' V_e' relative to m_prev: rescale it between PV_{e-1} and PV_e
       // (PV_e cannot start before this warpset's P_e is released below)

@@ -3,7 +3,7 @@
 # of the bench command and --set full captures of K4 / K2 (C3), K4 d=64, K1, K3/K5.
 cd $GRAFT_REPO_ROOT
 export PYTHONUNBUFFERED=1
-O=gpurun_out/r02
+O=gpurun_out/r02final
 mkdir -p $O
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw,power.limit --format=csv > $O/gpu_state.txt 2>&1
 timeout -s KILL 1500 python -m pytest tests -m gpu -x -q -p no:cacheprovider --durations=10 > $O/pytest_gpu.txt 2>&1

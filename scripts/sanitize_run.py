@@ -16,6 +16,8 @@ from workloads import tensors as wt  # noqa: E402
 
 def run(m, H, d, dtype=torch.bfloat16, Hkv=None, flags=0, ws=None):
     Hkv = Hkv or H
+    if getattr(m, "rowwise", False):
+        flags |= fm.FM_FLAG_ROWWISE
     sri = torch.from_numpy(wm.stack([m])).cuda()
     q = wt.make_tensor("q", 1, m.N, H, d, dtype=dtype).cuda()
     do = wt.make_tensor("do", 1, m.N, H, d, dtype=dtype).cuda()
@@ -39,6 +41,13 @@ cases = [
     ("random_eviction d128 det", lambda: run(wm.sample_family("random_eviction", 513, rng, (2, 5)), 2, 128,
                                              flags=fm.FM_FLAG_DETERMINISTIC)),
     ("gqa share_question d64", lambda: run(wm.sample_family("share_question", 640, rng, (2, 5)), 4, 64, Hkv=2)),
+    ("rowwise key_window d128", lambda: run(wm.rw_sample_family("key_window", 700, rng, (2, 5)), 2, 128)),
+    ("rowwise causal_document d64 det", lambda: run(wm.rw_sample_family("causal_document", 515, rng, (2, 5)), 2, 64,
+                                                    flags=fm.FM_FLAG_DETERMINISTIC)),
+    ("pair forward causal_document", lambda: run(wm.sample_family("causal_document", 900, rng, (2, 5)), 2, 128,
+                                                 flags=fm.FM_FLAG_FWD_PAIR)),
+    # 256 forward / 512 backward CTAs: the LPT order (K1d) is used
+    ("lpt causal_document 4K x 16 heads", lambda: run(wm.sample_family("causal_document", 4096, rng, (3, 7)), 16, 128)),
 ]
 for name, f in cases:
     if which in ("all", "cases"):
