@@ -199,7 +199,7 @@ enum {
   FM_KERNEL_CLASSIFY = 1,    /* K1b  tile classification (Eq. 4)                             */
   FM_KERNEL_FWD = 2,         /* K2   forward (Alg. 1)                                        */
   FM_KERNEL_BWD_PRE = 3,     /* K3   D = rowsum(dO o O), zero dQ accumulator (Alg. 2 l.3-4)  */
-  FM_KERNEL_BWD = 4,         /* K4   backward main loop (Alg. 2)                             */
+  FM_KERNEL_BWD = 4,         /* K4   backward main loop (Alg. 2); + K7 under split-G         */
   FM_KERNEL_DQ_CONVERT = 5,  /* K5   dQ = scale * dQacc -> out dtype                         */
   FM_KERNEL_DQ = 6,          /* K6   deterministic dQ (FM_FLAG_DETERMINISTIC)                */
   FM_KERNEL_REFINE = 7,      /* K1c  f3 refinement words of PARTIAL tiles                    */

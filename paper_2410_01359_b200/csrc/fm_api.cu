@@ -139,6 +139,19 @@ fm_status check_params(const fm_params* p, fm::Dims* d, bool need_attention) {
   return FM_OK;
 }
 
+// Split-G backward: when the key-tile units (Tc * Hkv * B) do not fill the 148 SMs and each CTA
+// would loop over G > 1 query heads (MQA / GQA), the G heads are split over gsplit CTAs (the
+// largest divisor of G up to two waves' worth), whose fp32 dK / dV partials K7 sums.
+int gsplit_for(const fm::Dims& d) {
+  const long units = static_cast<long>(d.Tc) * d.Hkv * d.B;
+  if (d.G < 2 || units >= 148) return 1;
+  const long target = (296 + units - 1) / units;
+  int s = 1;
+  for (int c = 2; c <= d.G; ++c)
+    if (d.G % c == 0 && c <= target) s = c;
+  return s;
+}
+
 // Carve the workspace.  Returns the total size; pointers valid only when base != nullptr.
 // Every buffer starts on a 4 KiB boundary of the device address space (the caller's base is
 // first rounded up to 64 KiB; the size bound includes that slack): the backward's 8 KiB bulk
@@ -159,7 +172,7 @@ size_t carve(const fm::Dims& d, int pass, void* base, fm::Workspace* w) {
   w->vec4 = reinterpret_cast<int4*>(take(bhm * d.Tc * 128 * sizeof(int4)));
   w->fmap = nullptr;
   w->bmap = nullptr;
-  w->dvec = w->l2 = w->dqacc = nullptr;
+  w->dvec = w->l2 = w->dqacc = w->dkv_part = nullptr;
   w->cw = nullptr;
   if (pass == FM_PASS_FWD) {
     w->fmap = take(bhm * d.Tr * d.Tc);
@@ -170,6 +183,10 @@ size_t carve(const fm::Dims& d, int pass, void* base, fm::Workspace* w) {
     w->dvec = reinterpret_cast<float*>(take(bh * d.Npb * sizeof(float)));
     w->l2 = reinterpret_cast<float*>(take(bh * d.Npb * sizeof(float)));
     w->dqacc = reinterpret_cast<float*>(take(bh * d.Npb * d.D * sizeof(float)));
+    const int gs = gsplit_for(d);
+    w->dkv_part = gs > 1 ? reinterpret_cast<float*>(take(static_cast<size_t>(2) * gs * d.B * d.N * d.Hkv * d.D *
+                                                         sizeof(float)))
+                         : nullptr;
   }
   // LPT orders (>= ceil(Tr/2) pairs or Tc key tiles per (b, hm)) followed by one flag per (b, hm)
   w->order = reinterpret_cast<uint16_t*>(take(bhm * (d.Tc + 1) * sizeof(uint16_t)));
@@ -446,8 +463,9 @@ fm_status flashmask_bwd(const fm_params* p, const void* q, const void* k, const 
   // LPT order of (kv head, key tile) units for small grids (K1d); per kv head: K, V and the
   // group's Q, dO ~ 2 N d 2 (1 + G).  Launched before K3 so that K4, which reads it before its
   // griddepcontrol.wait, finds it complete (two launches back, fm_ptx.cuh)
-  const int lpt_hgrp = lpt_group(d, static_cast<long>(d.Tc) * d.Hkv * d.B, d.Hkv,
-                                 static_cast<size_t>(4) * d.N * d.D * static_cast<size_t>(1 + d.G));
+  const int gsplit = gsplit_for(d);
+  const int lpt_hgrp = gsplit > 1 ? 0 : lpt_group(d, static_cast<long>(d.Tc) * d.Hkv * d.B, d.Hkv,
+                                                  static_cast<size_t>(4) * d.N * d.D * static_cast<size_t>(1 + d.G));
   if (lpt_hgrp > 0) {
     e = timed(FM_KERNEL_CLASSIFY, st, [&] { return fm::launch_order(w.bmap, d, 0, w.order, st); });
     if (e != cudaSuccess) return cuda_fail(e, "order");
@@ -468,6 +486,8 @@ fm_status flashmask_bwd(const fm_params* p, const void* q, const void* k, const 
   a.dv = dv;
   a.hgrp = lpt_hgrp;
   a.order = lpt_hgrp > 0 ? w.order : nullptr;
+  a.gsplit = gsplit;
+  a.dkv_part = w.dkv_part;
   const bool deterministic = (p->flags & FM_FLAG_DETERMINISTIC) != 0;
   a.with_dq = deterministic ? 0 : 1;
   CUtensorMap tdq, tdk, tdv;
@@ -480,6 +500,10 @@ fm_status flashmask_bwd(const fm_params* p, const void* q, const void* k, const 
   }
   e = timed(FM_KERNEL_BWD, st, [&] { return fm::launch_bwd(d, tq, tk, tv, tdo, tdq, tdk, tdv, a, st); });
   if (e != cudaSuccess) return cuda_fail(e, "backward kernel");
+  if (gsplit > 1) {
+    e = timed(FM_KERNEL_BWD, st, [&] { return fm::launch_dkv_reduce(d, gsplit, w.dkv_part, dk, dv, st); });
+    if (e != cudaSuccess) return cuda_fail(e, "dk/dv reduce");
+  }
   if (!deterministic) {
     e = timed(FM_KERNEL_DQ_CONVERT, st, [&] { return fm::launch_dq_convert(d, w.dqacc, dq, st); });
     if (e != cudaSuccess) return cuda_fail(e, "dq convert");

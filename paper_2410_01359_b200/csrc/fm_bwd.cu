@@ -227,7 +227,14 @@ __global__ void __launch_bounds__(bwd::NT, 1)
   // (K1d, small problems) the CTAs of a batch entry take groups of a.hgrp kv heads, in each group
   // the key tiles by descending work, heads innermost; else j = x, hk = y.
   int j, hk;
-  if (a.order != nullptr && (a.Hm > 1 || a.order[static_cast<size_t>(a.B) * a.Tc + b] != 0)) {
+  // split-G (MQA / GQA grids under one wave): blockIdx.y = hk * gsplit + slice; the CTA takes the
+  // slice's G / gsplit query heads of the group and writes fp32 dK / dV partials (K7 sums them)
+  const int gsplit = a.gsplit > 1 ? a.gsplit : 1;
+  const int slice = static_cast<int>(blockIdx.y) % gsplit;
+  if (gsplit > 1) {
+    j = static_cast<int>(blockIdx.x);
+    hk = static_cast<int>(blockIdx.y) / gsplit;
+  } else if (a.order != nullptr && (a.Hm > 1 || a.order[static_cast<size_t>(a.B) * a.Tc + b] != 0)) {
     const int L = static_cast<int>(blockIdx.x) + a.Tc * static_cast<int>(blockIdx.y);
     const int per_g = a.Tc * a.hgrp;
     const int g = L / per_g, rem = L - g * per_g;
@@ -240,7 +247,7 @@ __global__ void __launch_bounds__(bwd::NT, 1)
   }
   const int hm = (a.Hm == 1) ? 0 : hk;
   const size_t bhm = static_cast<size_t>(b) * a.Hm + hm;
-  const int G = a.G;
+  const int Gs = a.G / (a.gsplit > 1 ? a.gsplit : 1);  // query heads of this CTA (all G unless split)
 
   if (warp == 12 && lane == 0) {
     mbar_init(&sm.kv_full, 1);
@@ -307,7 +314,8 @@ __global__ void __launch_bounds__(bwd::NT, 1)
   tc_fence_after();
   // work items t = (query head of the group, visited row tile): t / nE1 selects the head
   const int nE1 = sm.n_entries;
-  const int nE = nE1 * G;
+  const int nE = nE1 * Gs;
+  const int hq0 = hk * a.G + slice * Gs;  // first query head of this CTA
   const uint32_t tbase = sm.tmem_base;
 
   if (warp == 12) {
@@ -320,7 +328,7 @@ __global__ void __launch_bounds__(bwd::NT, 1)
       // the backward's stall samples)
       for (int t = 0, t1 = 0, g = 0; t < nE; ++t, (++t1 == nE1) ? (t1 = 0, ++g) : 0) {
         const int i = sm.list[t1];
-        const int hq = hk * G + g;
+        const int hq = hq0 + g;
         const size_t bh = static_cast<size_t>(b) * a.H + hq;
         const int st = t % C::QST;
         mbar_wait(&sm.q_empty[st], ((t / C::QST) & 1) ^ 1);
@@ -552,7 +560,27 @@ __global__ void __launch_bounds__(bwd::NT, 1)
     const uint32_t col = wg == 0 ? C::DV_COL : C::DK_COL;
     const float mul = wg == 0 ? 1.0f : a.scale;
     void* outp = wg == 0 ? a.dv : a.dk;
-    if constexpr (!OUT_F32) {
+    if (gsplit > 1) {
+      // split-G: this slice's unscaled fp32 partial, part[slice][dV | dK][b][key][hk][d]; K7 sums
+      // the slices in order, scales dK and converts (deterministic, atomic-free)
+      float* part = a.dkv_part + ((static_cast<size_t>(slice) * 2 + wg) * a.B * a.N) * a.Hkv * D;
+#pragma unroll 1
+      for (int c = 0; c < D / 32; ++c) {
+        uint32_t r[32];
+        if (nE > 0) {
+          tmem_ld32(tbase + lane_off + col + c * 32, r);
+          tmem_wait_ld();
+        }
+        if (key < a.N) {
+          float4* dst = reinterpret_cast<float4*>(part + orow + c * 32);
+#pragma unroll
+          for (int t = 0; t < 8; ++t)
+            dst[t] = nE > 0 ? make_float4(__uint_as_float(r[4 * t]), __uint_as_float(r[4 * t + 1]),
+                                          __uint_as_float(r[4 * t + 2]), __uint_as_float(r[4 * t + 3]))
+                            : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+      }
+    } else if constexpr (!OUT_F32) {
       // bf16 dV / dK go out through shared memory (the V / K tile buffers: every MMA that read
       // them completed before `done`) and TMA stores — a thread holds one key row, so direct
       // 16-byte stores would scatter each warp instruction over 32 rows.  Keys >= N are clipped.
@@ -587,7 +615,7 @@ __global__ void __launch_bounds__(bwd::NT, 1)
       }
     }
 #pragma unroll 1
-    for (int c = 0; c < (OUT_F32 ? D / 32 : 0); ++c) {
+    for (int c = 0; c < ((OUT_F32 && gsplit == 1) ? D / 32 : 0); ++c) {
       uint32_t r[32];
       if (nE > 0) {
         tmem_ld32(tbase + lane_off + col + c * 32, r);
@@ -618,7 +646,7 @@ __global__ void __launch_bounds__(bwd::NT, 1)
     uint32_t stage_n = 0;  // dQ staging chunks issued so far (DQT)
     for (int t = 0, t1 = 0, g = 0; t < (a.with_dq ? nE : 0); ++t, (++t1 == nE1) ? (t1 = 0, ++g) : 0) {
       const int i = sm.list[t1];
-      const size_t bh = static_cast<size_t>(b) * a.H + hk * G + g;
+      const size_t bh = static_cast<size_t>(b) * a.H + hq0 + g;
       const int bi = C::DQ_ALIAS ? t % C::NB : 0;
       const uint32_t boff = bi * C::BUF_STRIDE;
       mbar_wait(&sm.dq_full[bi], (t / (C::DQ_ALIAS ? C::NB : 1)) & 1);
@@ -699,7 +727,7 @@ static cudaError_t launch_bwd_t(const Dims& d, const CUtensorMap& tq, const CUte
   static_assert(sizeof(bwd::Smem<D, ROWW>) + 1024 <= 232448, "shared memory budget");
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (e != cudaSuccess) return e;
-  dim3 grid(d.Tc, d.Hkv, d.B);
+  dim3 grid(d.Tc, d.Hkv * (a.gsplit > 1 ? a.gsplit : 1), d.B);
   return launch_pdl(kern, grid, dim3(bwd::NT), smem, st, tq, tk, tv, tdo, tdq, tdk, tdv, a);
 }
 

@@ -43,6 +43,7 @@ struct Workspace {
   float* dvec;      // [B, H, Npb] -D, D = rowsum(dO o O) (negated: consumers add it)
   float* l2;        // [B, H, Npb] -lse * log2(e) (-inf for empty / padded rows)
   float* dqacc;     // [B, H, Npb, d] fp32 dQ accumulator
+  float* dkv_part;  // split-G backward: [gsplit][2][B, N, Hkv, d] fp32 dV / dK partials
   uint16_t* order;  // LPT unit order (K1d): forward [B, Hm, ceil(Tr/2)] pairs, backward [B, Hm, Tc] key
                     // tiles, then one flag per (b, hm) (0: near-uniform work, keep the default order)
   size_t bytes;
@@ -88,6 +89,8 @@ struct BwdArgs {
   int with_dq;  // 0 under FM_FLAG_DETERMINISTIC: dQ comes from K6 instead
   const uint16_t* order;  // LPT schedule: key tiles of each (b, hm) by descending work (K1d); nullptr: j order
   int hgrp;               // key/value heads taken together by the LPT map
+  int gsplit;             // > 1: query heads of a group split over gsplit CTAs (fp32 partials, K7)
+  float* dkv_part;        // [gsplit][2 (dV, dK)][B, N, Hkv, d] fp32 partials when gsplit > 1
 };
 
 struct DqArgs {
@@ -137,6 +140,8 @@ cudaError_t launch_bwd(const Dims& d, const CUtensorMap& tq, const CUtensorMap& 
                        const CUtensorMap& tdo, const CUtensorMap& tdq, const CUtensorMap& tdk, const CUtensorMap& tdv,
                        const BwdArgs& a, cudaStream_t st);
 cudaError_t launch_dq_convert(const Dims& d, const float* dqacc, void* dq, cudaStream_t st);
+// K7: dK = scale * sum_s dK_s, dV = sum_s dV_s over the split-G partials, converted to the out dtype
+cudaError_t launch_dkv_reduce(const Dims& d, int gsplit, const float* part, void* dk, void* dv, cudaStream_t st);
 cudaError_t launch_dq(const Dims& d, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
                       const CUtensorMap& tdo, const DqArgs& a, cudaStream_t st);
 

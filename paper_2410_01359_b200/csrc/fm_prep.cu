@@ -624,6 +624,48 @@ __global__ void __launch_bounds__(256) k5_dq_convert(const float* __restrict__ d
   }
 }
 
+// ---------------------------------------------------------------------------------------
+// K7 (split-G backward, MQA / GQA with fewer key-tile units than SMs): dV = sum_s dV_s and
+// dK = scale * sum_s dK_s over the slices' fp32 partials, in slice order (deterministic), to the
+// out dtype.  One thread per 8 elements of [B, N, Hkv, d] (both tensors).
+// ---------------------------------------------------------------------------------------
+template <bool OUT_F32, bool F16>
+__global__ void __launch_bounds__(256) k7_dkv_reduce(const float* __restrict__ part, int gsplit, long total8,
+                                                     float scale, void* __restrict__ dk, void* __restrict__ dv) {
+  pdl_wait();
+  pdl_launch();
+  const long idx8 = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (idx8 >= 2 * total8) return;
+  const int kind = idx8 >= total8 ? 1 : 0;  // 0: dV, 1: dK
+  const long e8 = idx8 - kind * total8;
+  float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  for (int s = 0; s < gsplit; ++s) {
+    const float4* src = reinterpret_cast<const float4*>(part + ((static_cast<size_t>(s) * 2 + kind) * total8 + e8) * 8);
+    const float4 a = src[0], b = src[1];
+    acc[0] += a.x; acc[1] += a.y; acc[2] += a.z; acc[3] += a.w;
+    acc[4] += b.x; acc[5] += b.y; acc[6] += b.z; acc[7] += b.w;
+  }
+  const float mul = kind ? scale : 1.0f;
+  void* out = kind ? dk : dv;
+  if constexpr (OUT_F32) {
+    float4* dst = reinterpret_cast<float4*>(static_cast<float*>(out) + e8 * 8);
+    dst[0] = make_float4(acc[0] * mul, acc[1] * mul, acc[2] * mul, acc[3] * mul);
+    dst[1] = make_float4(acc[4] * mul, acc[5] * mul, acc[6] * mul, acc[7] * mul);
+  } else {
+    *reinterpret_cast<uint4*>(static_cast<uint16_t*>(out) + e8 * 8) =
+        make_uint4(pack16<F16>(acc[0] * mul, acc[1] * mul), pack16<F16>(acc[2] * mul, acc[3] * mul),
+                   pack16<F16>(acc[4] * mul, acc[5] * mul), pack16<F16>(acc[6] * mul, acc[7] * mul));
+  }
+}
+
+cudaError_t launch_dkv_reduce(const Dims& d, int gsplit, const float* part, void* dk, void* dv, cudaStream_t st) {
+  const long total8 = static_cast<long>(d.B) * d.N * d.Hkv * d.D / 8;
+  const unsigned blocks = static_cast<unsigned>((2 * total8 + 255) / 256);
+  if (d.out_f32) return launch_pdl(k7_dkv_reduce<true, false>, dim3(blocks), dim3(256), 0, st, part, gsplit, total8, d.scale, dk, dv);
+  if (d.in_f16) return launch_pdl(k7_dkv_reduce<false, true>, dim3(blocks), dim3(256), 0, st, part, gsplit, total8, d.scale, dk, dv);
+  return launch_pdl(k7_dkv_reduce<false, false>, dim3(blocks), dim3(256), 0, st, part, gsplit, total8, d.scale, dk, dv);
+}
+
 cudaError_t launch_dq_convert(const Dims& d, const float* dqacc, void* dq, cudaStream_t st) {
   const long total8 = static_cast<long>(d.B) * d.N * d.H * d.D / 8;
   const long blocks = (total8 + 255) / 256;
