@@ -27,7 +27,8 @@
 #ifndef FM_TRACE_BY
 #define FM_TRACE_BY 0
 #endif
-namespace fm { __device__ long long g_fm_trace_fwd[64 * 16]; __device__ long long g_fm_trace_fwd_ev[16]; }
+namespace fm { __device__ long long g_fm_trace_fwd[64 * 16]; __device__ long long g_fm_trace_fwd_ev[16];
+__device__ long long g_fm_trace_fwd_w[8 * 32]; }
 #define FT(slot, e)                                                                                   \
   do {                                                                                                 \
     if (blockIdx.x == FM_TRACE_BX && blockIdx.y == FM_TRACE_BY && blockIdx.z == 0 && (e) < 64) fm::g_fm_trace_fwd[(e) * 16 + (slot)] = clock64(); \
@@ -509,6 +510,11 @@ __global__ void __launch_bounds__(fwd::NT, 1)
         tc_fence_before();
         mbar_arrive(&sm.p_full[q]);
         if (row_t == 0 && hh == 0) FT(2 + q, e);
+#ifdef FM_TRACE
+        // per-warp P-ready time of visited entries 20..27 (all 16 softmax warps)
+        if (lane == 0 && e >= 20 && e < 28 && blockIdx.x == FM_TRACE_BX && blockIdx.y == FM_TRACE_BY && blockIdx.z == 0)
+          g_fm_trace_fwd_w[(e - 20) * 32 + warp] = clock64();
+#endif
         ++cnt;
       }
       __syncwarp();
@@ -642,6 +648,9 @@ cudaError_t launch_fwd(const Dims& d, const CUtensorMap& tq, const CUtensorMap& 
 #ifdef FM_TRACE
 extern "C" __attribute__((visibility("default"))) int flashmask_debug_trace_fwd(long long* host) {
   return cudaMemcpyFromSymbol(host, fm::g_fm_trace_fwd, sizeof(long long) * 64 * 16) == cudaSuccess ? 0 : 1;
+}
+extern "C" __attribute__((visibility("default"))) int flashmask_debug_trace_fwd_w(long long* host) {
+  return cudaMemcpyFromSymbol(host, fm::g_fm_trace_fwd_w, sizeof(long long) * 8 * 32) == cudaSuccess ? 0 : 1;
 }
 extern "C" __attribute__((visibility("default"))) int flashmask_debug_trace_fwd_ev(long long* host) {
   return cudaMemcpyFromSymbol(host, fm::g_fm_trace_fwd_ev, sizeof(long long) * 16) == cudaSuccess ? 0 : 1;

@@ -31,3 +31,13 @@ names = ["s0full", "s1full", "p0full", "p1full", "mma_p0", "mma_p1", "mma_s0", "
 print("e  " + " ".join(f"{n[:8]:>8s}" for n in names))
 for i in range(min(nE, 40)):
     print(f"{i:2d} " + " ".join(f"{a[i, s] - t0 if a[i, s] else -1:8d}" for s in range(len(names))))
+
+bw = (ctypes.c_longlong * (8 * 32))()
+if hasattr(fm._lib, "flashmask_debug_trace_fwd_w") and fm._lib.flashmask_debug_trace_fwd_w(bw) == 0:
+    w = np.array(bw).reshape(8, 32)
+    print("per-warp P-ready (clk, relative to the earliest warp of the tile), entries 20..27; warp w sits on SMSP w % 4")
+    for k in range(8):
+        for q in range(2):
+            ws = w[k, q * 8:(q + 1) * 8]
+            if ws.min() > 0:
+                print(f"e={20 + k} tile q{q}: " + " ".join(f"w{q * 8 + i}(s{(q * 8 + i) % 4}):{int(ws[i] - ws.min())}" for i in range(8)))
