@@ -460,16 +460,7 @@ fm_status flashmask_bwd(const fm_params* p, const void* q, const void* k, const 
   }
   e = timed(FM_KERNEL_CLASSIFY, st, [&] { return fm::launch_classify(ext_b, d, d.Brb, fm::kTile, w.bmap, 1, 1, nullptr, st); });
   if (e != cudaSuccess) return cuda_fail(e, "classify");
-  // LPT order of (kv head, key tile) units for small grids (K1d); per kv head: K, V and the
-  // group's Q, dO ~ 2 N d 2 (1 + G).  Launched before K3 so that K4, which reads it before its
-  // griddepcontrol.wait, finds it complete (two launches back, fm_ptx.cuh)
   const int gsplit = gsplit_for(d);
-  const int lpt_hgrp = gsplit > 1 ? 0 : lpt_group(d, static_cast<long>(d.Tc) * d.Hkv * d.B, d.Hkv,
-                                                  static_cast<size_t>(4) * d.N * d.D * static_cast<size_t>(1 + d.G));
-  if (lpt_hgrp > 0) {
-    e = timed(FM_KERNEL_CLASSIFY, st, [&] { return fm::launch_order(w.bmap, d, 0, w.order, st); });
-    if (e != cudaSuccess) return cuda_fail(e, "order");
-  }
   e = timed(FM_KERNEL_BWD_PRE, st, [&] { return fm::launch_bwd_pre(d, o, dout, lse, w.dvec, w.l2, w.dqacc, st); });
   if (e != cudaSuccess) return cuda_fail(e, "bwd preprocess");
   fm::BwdArgs a{};
@@ -484,8 +475,6 @@ fm_status flashmask_bwd(const fm_params* p, const void* q, const void* k, const 
   a.dqacc = w.dqacc;
   a.dk = dk;
   a.dv = dv;
-  a.hgrp = lpt_hgrp;
-  a.order = lpt_hgrp > 0 ? w.order : nullptr;
   a.gsplit = gsplit;
   a.dkv_part = w.dkv_part;
   const bool deterministic = (p->flags & FM_FLAG_DETERMINISTIC) != 0;

@@ -223,28 +223,13 @@ __global__ void __launch_bounds__(bwd::NT, 1)
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int b = blockIdx.z;
-  // unit: key tile j of key/value head hk (its G query heads are looped over).  With an LPT order
-  // (K1d, small problems) the CTAs of a batch entry take groups of a.hgrp kv heads, in each group
-  // the key tiles by descending work, heads innermost; else j = x, hk = y.
-  int j, hk;
-  // split-G (MQA / GQA grids under one wave): blockIdx.y = hk * gsplit + slice; the CTA takes the
-  // slice's G / gsplit query heads of the group and writes fp32 dK / dV partials (K7 sums them)
+  // unit: key tile j of key/value head hk (its G query heads are looped over).  Split-G (MQA / GQA
+  // grids under one wave): blockIdx.y = hk * gsplit + slice; the CTA takes the slice's G / gsplit
+  // query heads of the group and writes fp32 dK / dV partials (K7 sums them).
   const int gsplit = a.gsplit > 1 ? a.gsplit : 1;
   const int slice = static_cast<int>(blockIdx.y) % gsplit;
-  if (gsplit > 1) {
-    j = static_cast<int>(blockIdx.x);
-    hk = static_cast<int>(blockIdx.y) / gsplit;
-  } else if (a.order != nullptr && (a.Hm > 1 || a.order[static_cast<size_t>(a.B) * a.Tc + b] != 0)) {
-    const int L = static_cast<int>(blockIdx.x) + a.Tc * static_cast<int>(blockIdx.y);
-    const int per_g = a.Tc * a.hgrp;
-    const int g = L / per_g, rem = L - g * per_g;
-    const int jrank = rem / a.hgrp;
-    hk = g * a.hgrp + (rem - jrank * a.hgrp);
-    j = a.order[(static_cast<size_t>(b) * a.Hm + ((a.Hm == 1) ? 0 : hk)) * a.Tc + jrank];
-  } else {
-    j = static_cast<int>(blockIdx.x);
-    hk = blockIdx.y;
-  }
+  const int j = static_cast<int>(blockIdx.x);
+  const int hk = static_cast<int>(blockIdx.y) / gsplit;
   const int hm = (a.Hm == 1) ? 0 : hk;
   const size_t bhm = static_cast<size_t>(b) * a.Hm + hm;
   const int Gs = a.G / (a.gsplit > 1 ? a.gsplit : 1);  // query heads of this CTA (all G unless split)

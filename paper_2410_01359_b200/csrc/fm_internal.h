@@ -87,8 +87,6 @@ struct BwdArgs {
   void* dk;
   void* dv;
   int with_dq;  // 0 under FM_FLAG_DETERMINISTIC: dQ comes from K6 instead
-  const uint16_t* order;  // LPT schedule: key tiles of each (b, hm) by descending work (K1d); nullptr: j order
-  int hgrp;               // key/value heads taken together by the LPT map
   int gsplit;             // > 1: query heads of a group split over gsplit CTAs (fp32 partials, K7)
   float* dkv_part;        // [gsplit][2 (dV, dK)][B, N, Hkv, d] fp32 partials when gsplit > 1
 };
@@ -127,8 +125,7 @@ cudaError_t launch_classify(const int32_t* ext8, const Dims& d, int br, int bc, 
                             int32_t* col_cnt = nullptr);
 cudaError_t launch_refine(const int32_t* sri, const uint8_t* cmap, const Dims& d, uint32_t* words, int64_t* rcounts,
                           cudaStream_t st);
-// K1d: LPT order of the attention kernels' units from a kernel map (fwd: row map, pairs of row
-// tiles; bwd: transposed map, key tiles)
+// K1d: LPT order of the forward's units (pairs of row tiles) from its class map
 cudaError_t launch_order(const uint8_t* map, const Dims& d, int fwd, uint16_t* order, cudaStream_t st);
 cudaError_t launch_fwd(const Dims& d, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
                        const CUtensorMap& to, const FwdArgs& a, cudaStream_t st);

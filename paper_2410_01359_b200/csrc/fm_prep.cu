@@ -452,12 +452,14 @@ cudaError_t launch_classify(const int32_t* ext8, const Dims& d, int br, int bc, 
 }
 
 // ---------------------------------------------------------------------------------------
-// K1d: longest-processing-time-first order of the attention kernels' units (the work
-// of a unit is its number of non-SKIP tiles, O((1-rho) T_r T_c) overall).  One CTA per
-// (b, hm): the forward's unit is a pair of 128-row query tiles (work = non-SKIP column tiles of
-// their union, as K2a visits), the backward's a key tile (work = its non-SKIP row tiles); a
-// bitonic sort in shared memory orders them by descending work (ties: lower index first).
-// Used for small problems only (launch_fwd / launch_bwd take it when the grid is a few waves).
+// K1d: longest-processing-time-first order of the forward's units (the work of a unit
+// is its number of non-SKIP tiles, O((1-rho) T_r T_c) overall).  One CTA per (b, hm): a
+// unit is a pair of 128-row query tiles (work = non-SKIP column tiles of their union, as K2a
+// visits); a bitonic sort in shared memory orders them by descending work (ties: lower index
+// first).  Used for small problems only (the forward's grid a few waves).  (The FWD = false
+// variant orders key tiles by non-SKIP row tiles; measured neutral for the backward — its
+// default order is already heaviest-first under causal-like masks — so flashmask_bwd does not
+// launch it.)
 // ---------------------------------------------------------------------------------------
 template <bool FWD>
 __global__ void __launch_bounds__(1024) k1_order(const uint8_t* __restrict__ map, int Tr, int Tc, int Trb,
