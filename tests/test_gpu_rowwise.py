@@ -180,3 +180,30 @@ def test_rowwise_and_colwise_agree(fmlib):
     torch.cuda.synchronize()
     for a, b in zip(*res):
         assert torch.allclose(a, b, atol=2e-3, rtol=0)
+
+
+@pytest.mark.parametrize("fam", ["causal_document", "key_window"])
+def test_rowwise_full_size_sampled(fmlib, fam):
+    """Row-wise masks at N = 32K (256 x 256 tiles, H = 4): O / lse of sampled rows and dK / dV of
+    sampled key columns against the oracle (forward rows and backward_cols)."""
+    N, H, d = 32768, 4, 128
+    rng = np.random.default_rng(len(fam) * 11)
+    m = wm.rw_sample_family(fam, N, rng, (10, 14))
+    sri = _stack([m]).cuda()
+    x = {n: wt.make_tensor(n, 1, N, H, d, base=21).cuda() for n in ("q", "k", "v", "do")}
+    F = fmlib.FM_FLAG_ROWWISE
+    o, lse = fmlib.flashmask_fwd(x["q"], x["k"], x["v"], sri, m.causal, out_dtype=torch.float32, flags=F)
+    dq, dk, dv = fmlib.flashmask_bwd(x["q"], x["k"], x["v"], o, x["do"], lse, sri, m.causal,
+                                     out_dtype=torch.float32, flags=F)
+    torch.cuda.synchronize()
+    vec = fo.expand_rowwise(m.sri, m.causal, N)
+    rows = np.sort(rng.choice(N, 48, replace=False))
+    keys = np.sort(rng.choice(N, 24, replace=False))
+    f = lambda t, h: t[0, :, h, :].double().cpu().numpy()
+    for h in (0, H - 1):
+        O, L = fo.forward(f(x["q"], h), f(x["k"], h), f(x["v"], h), vec, rows=rows)
+        assert_close(f"O {fam}[{h}]", o[0, rows, h].cpu().numpy(), O)
+        assert_lse(lse[0, h, rows].cpu().numpy(), L)
+        gk, gv = fo.backward_cols(f(x["q"], h), f(x["k"], h), f(x["v"], h), f(x["do"], h), vec, keys)
+        assert_close(f"dK {fam}[{h}]", dk[0, keys, h].cpu().numpy(), gk)
+        assert_close(f"dV {fam}[{h}]", dv[0, keys, h].cpu().numpy(), gv)
