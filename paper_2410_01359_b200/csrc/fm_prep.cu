@@ -129,9 +129,10 @@ __global__ void __launch_bounds__(128) k1_expand(const int32_t* __restrict__ sri
 // 32-bit arithmetic: N <= 2^30 and br, bc are clamped to [1, N] on the host, so r0 < N + br
 // and c0 < N + bc never overflow.
 __device__ __forceinline__ int tile_class(const int4& a, const int4& b, int r0, int r1, int c0, int c1, int causal) {
-  if ((r0 >= a.y && r1 <= a.z) || (r0 >= b.y && r1 <= b.z) || (causal && r1 - 1 < c0)) return 0;
-  if ((r1 > a.x && r0 < a.w) || (r1 > b.x && r0 < b.w) || (causal && r0 < c1 - 1)) return 1;
-  return 2;
+  // branch-free (predicate logic only): the per-row loop of K1b is latency-bound on branches
+  const bool s = ((r0 >= a.y) & (r1 <= a.z)) | ((r0 >= b.y) & (r1 <= b.z)) | ((causal != 0) & (r1 - 1 < c0));
+  const bool p = ((r1 > a.x) & (r0 < a.w)) | ((r1 > b.x) & (r0 < b.w)) | ((causal != 0) & (r0 < c1 - 1));
+  return s ? 0 : (p ? 1 : 2);
 }
 
 // Row-wise representation (R32): Eq. 4 on the transposed problem — the extrema are those of row
@@ -148,8 +149,17 @@ __device__ __forceinline__ int tile_class_rw(const int4& a, const int4& b, int r
 // non-SKIP counts) — otherwise the attention kernels' map (FM_FLAG_NO_SKIP, ragged last column
 // tile PARTIAL) without counts.  Keeping every choice out of the row loop, four column tiles per
 // thread and one 32-bit store per row took the Hm = 64 microbenchmark from 165 to 85 us.
+#ifndef FM_K1_THREADS
+#define FM_K1_THREADS 32
+#endif
+#ifndef FM_K1_MINB
+#define FM_K1_MINB 24
+#endif
+#ifndef FM_K1_KB
+#define FM_K1_KB 16
+#endif
 template <int JPT, bool ROWW, bool TRANS, bool API, bool NS>
-__global__ void __launch_bounds__(128) k1_classify(const int32_t* __restrict__ ext8, int N, int causal, int br, int bc,
+__global__ void __launch_bounds__(FM_K1_THREADS, FM_K1_MINB) k1_classify(const int32_t* __restrict__ ext8, int N, int causal, int br, int bc,
                                                    int Tr, int Tc, uint8_t* __restrict__ map, int kernel_map,
                                                    int no_skip, unsigned long long* __restrict__ counts,
                                                    int* __restrict__ row_cnt, int* __restrict__ col_cnt,
@@ -165,7 +175,8 @@ __global__ void __launch_bounds__(128) k1_classify(const int32_t* __restrict__ e
   const int bh = blockIdx.z;
   if (API) {
     if (threadIdx.x < 2) cnt[threadIdx.x] = 0;
-    if (NS && threadIdx.x < 64) row_acc[threadIdx.x] = 0;
+    if (NS)
+      for (int t = threadIdx.x; t < 64; t += blockDim.x) row_acc[t] = 0;
     __syncthreads();
   }
   int4 ea[JPT], eb[JPT];
@@ -189,6 +200,15 @@ __global__ void __launch_bounds__(128) k1_classify(const int32_t* __restrict__ e
     c1[u] = c0[u] + min(bc, N - c0[u]);
     if (!API && kernel_map == 2 && j == Tc - 1) force1 |= 1u << (8 * u);  // N is not a multiple of bc
   }
+  // extrema of every lane of the warp, for the rows of non-uniform lanes (see the block loop)
+  __shared__ int4 ext_s[ROWW || TRANS ? 1 : FM_K1_THREADS / 32][ROWW || TRANS ? 1 : 32][ROWW || TRANS ? 1 : JPT][2];
+  if constexpr (!ROWW && !TRANS) {
+#pragma unroll
+    for (int u = 0; u < JPT; ++u) {
+      ext_s[threadIdx.x >> 5][threadIdx.x & 31][u][0] = ea[u];
+      ext_s[threadIdx.x >> 5][threadIdx.x & 31][u][1] = eb[u];
+    }
+  }
   const bool skip_to_partial = !API && no_skip;
   uint32_t vmask = 0u;  // byte mask of the valid column tiles of this thread
 #pragma unroll
@@ -199,12 +219,194 @@ __global__ void __launch_bounds__(128) k1_classify(const int32_t* __restrict__ e
   for (int u = 0; u < JPT; ++u) colns[u] = 0;
   const bool row_counts = NS && row_cnt != nullptr && rows_per_cta <= 64;
   const bool any = valid[0] && map != nullptr;
-  for (int i16 = ib; i16 < iend; i16 += 16) {
-    uint32_t packed[4] = {0u, 0u, 0u, 0u};
+  constexpr int KB = (TRANS || ROWW) ? 16 : FM_K1_KB;  // rows per block
+  for (int i16 = ib; i16 < iend; i16 += KB) {
+    // Uniform block: every comparison of Eq. 4 / the causal test is between r0 or r1 (both in
+    // [lo, hi] for the 16 row tiles, hi = min((i16+16) br, N)) and a column-tile value v; when no v
+    // lies in [lo, hi] all 16 rows have the class of the first one (evaluated once, stored 16x).
+    if constexpr (!ROWW) {
+      if (i16 + KB <= iend) {
+        const int lo = i16 * br;
+        const unsigned span = static_cast<unsigned>(min(static_cast<long long>(i16 + KB) * br, static_cast<long long>(N)) - lo);
+        bool ok = true;
 #pragma unroll
-    for (int v = 0; v < 16; ++v) {
+        for (int u = 0; u < JPT; ++u) {
+          const int vs[10] = {ea[u].x, ea[u].y, ea[u].z, ea[u].w, eb[u].x, eb[u].y, eb[u].z, eb[u].w, c0[u], c1[u] - 1};
+#pragma unroll
+          for (int k = 0; k < 10; ++k)
+            ok = ok && (!valid[u] || (k >= 8 && !causal) || static_cast<unsigned>(vs[k]) - static_cast<unsigned>(lo) > span);
+        }
+        const uint32_t rest0 = __ballot_sync(0xffffffffu, !ok);
+        if constexpr (!TRANS) {
+         if (__popc(rest0) <= 16) {
+          // Row map: the uniform lanes store their class word 16x; the 16 rows of each non-uniform
+          // lane are spread over a half-warp (two lanes per round), which reloads that lane's
+          // extrema and evaluates one row each — the band of a mask edge costs ~k/2 rounds
+          // instead of 16 full-warp row evaluations.
+          const int lane = threadIdx.x & 31;
+          const int r0 = lo, r1 = r0 + min(br, N - r0);
+          uint32_t word = 0u;
+          int ns = 0, cz[JPT];
+#pragma unroll
+          for (int u = 0; u < JPT; ++u) {
+            const int cls = tile_class(ea[u], eb[u], r0, r1, c0[u], c1[u], causal);
+            cz[u] = cls != 0;
+            ns += valid[u] && cls != 0;
+            word |= static_cast<uint32_t>(cls) << (8 * u);
+          }
+          if (ok) {
+            if (API) {
+              n1 += KB * __popc(word & vmask & 0x01010101u);
+              n0 += KB * __popc(word & vmask & 0x02020202u);
+            }
+            if (NS) {
+#pragma unroll
+              for (int u = 0; u < JPT; ++u) colns[u] += KB * cz[u];
+            }
+          }
+          if (!API) {
+            if (skip_to_partial) word |= (~word & (~word >> 1)) & 0x01010101u;
+            word ^= (word & (force1 << 1)) | ((word & (force1 << 1)) >> 1);
+          }
+          if (row_counts) {
+            const int wsum = __reduce_add_sync(0xffffffffu, ok ? ns : 0);
+            if (lane < KB && wsum) atomicAdd(&row_acc[i16 - ib + lane], wsum);
+          }
+          if (ok && any) {
+            uint8_t* dst = map + (static_cast<size_t>(bh) * Tr + i16) * Tc + j0;
+            if (JPT == 4 && valid[JPT - 1]) {
+#pragma unroll 4
+              for (int v = 0; v < KB; ++v, dst += Tc) *reinterpret_cast<uint32_t*>(dst) = word;
+            } else {
+              for (int v = 0; v < KB; ++v, dst += Tc) {
+#pragma unroll
+                for (int u = 0; u < JPT; ++u)
+                  if (valid[u]) dst[u] = static_cast<uint8_t>(word >> (8 * u));
+              }
+            }
+          }
+          uint32_t rest = rest0;
+          __syncwarp();  // ext_s of this warp (written at the start) visible to every lane
+          while (rest) {  // warp-uniform
+            const int la = __ffs(rest) - 1;
+            rest &= rest - 1;
+            int lb = -1;
+            if (KB == 16) {  // two lanes per round (a half-warp each); KB = 32: one lane per round
+              lb = rest ? __ffs(rest) - 1 : -1;
+              rest &= rest ? rest - 1 : 0u;
+            }
+            const int src = (KB == 32 || lane < 16) ? la : lb;
+            int pk = 0;  // NS: per-u non-SKIP flags of this row (8-bit fields)
+            if (src >= 0) {
+              const int i = i16 + (lane & (KB - 1));
+              const int js = (blockIdx.x * blockDim.x + (threadIdx.x & ~31) + src) * JPT;
+              const int q0 = i * br, q1 = q0 + min(br, N - q0);
+              uint32_t w = 0u, vm = 0u, f1 = 0u;
+              int nsr = 0;
+#pragma unroll
+              for (int u = 0; u < JPT; ++u) {
+                const int j = js + u;
+                const bool vld = j < Tc;
+                const int4 a4 = ext_s[threadIdx.x >> 5][src][u][0], b4 = ext_s[threadIdx.x >> 5][src][u][1];
+                const int cc0 = vld ? j * bc : N;
+                const int cls = tile_class(a4, b4, q0, q1, cc0, cc0 + min(bc, N - cc0), causal);
+                w |= static_cast<uint32_t>(cls) << (8 * u);
+                vm |= vld ? (0xFFu << (8 * u)) : 0u;
+                if (!API && kernel_map == 2 && j == Tc - 1) f1 |= 1u << (8 * u);
+                if (NS) {
+                  nsr += vld && cls != 0;
+                  pk += (cls != 0 ? 1 : 0) << (8 * u);
+                }
+              }
+              if (API) {
+                n1 += __popc(w & vm & 0x01010101u);
+                n0 += __popc(w & vm & 0x02020202u);
+              }
+              if (!API) {
+                if (skip_to_partial) w |= (~w & (~w >> 1)) & 0x01010101u;
+                w ^= (w & (f1 << 1)) | ((w & (f1 << 1)) >> 1);
+              }
+              if (row_counts && nsr) atomicAdd(&row_acc[i - ib], nsr);
+              if (map != nullptr && js < Tc) {
+                uint8_t* dst = map + (static_cast<size_t>(bh) * Tr + i) * Tc + js;
+                if (JPT == 4 && js + JPT <= Tc) {
+                  *reinterpret_cast<uint32_t*>(dst) = w;
+                } else {
+#pragma unroll
+                  for (int u = 0; u < JPT; ++u)
+                    if (js + u < Tc) dst[u] = static_cast<uint8_t>(w >> (8 * u));
+                }
+              }
+            }
+            if (NS) {  // column counts of lanes la / lb: sums over their half-warp
+#pragma unroll
+              for (int o = KB / 2; o; o >>= 1) pk += __shfl_xor_sync(0xffffffffu, pk, o);
+              const int pa = __shfl_sync(0xffffffffu, pk, 0), pb = KB == 16 ? __shfl_sync(0xffffffffu, pk, 16) : 0;
+              const int mine = lane == la ? pa : (lane == lb ? pb : 0);
+#pragma unroll
+              for (int u = 0; u < JPT; ++u) colns[u] += (mine >> (8 * u)) & 0xFF;
+            }
+          }
+          continue;
+         }
+        }
+        if (__all_sync(0xffffffffu, ok)) {
+          const int r0 = lo, r1 = r0 + min(br, N - r0);
+          uint32_t word = 0u;
+          int ns = 0;
+#pragma unroll
+          for (int u = 0; u < JPT; ++u) {
+            const int cls = tile_class(ea[u], eb[u], r0, r1, c0[u], c1[u], causal);
+            if (NS) {
+              ns += valid[u] && cls != 0;
+              colns[u] += cls != 0 ? 16 : 0;
+            }
+            word |= static_cast<uint32_t>(cls) << (8 * u);
+          }
+          if (API) {
+            n1 += 16 * __popc(word & vmask & 0x01010101u);
+            n0 += 16 * __popc(word & vmask & 0x02020202u);
+          }
+          if (!API) {
+            if (skip_to_partial) word |= (~word & (~word >> 1)) & 0x01010101u;
+            word ^= (word & (force1 << 1)) | ((word & (force1 << 1)) >> 1);
+          }
+          if (row_counts) {
+            const int wsum = __reduce_add_sync(0xffffffffu, ns);
+            if ((threadIdx.x & 31) < 16 && wsum) atomicAdd(&row_acc[i16 - ib + (threadIdx.x & 31)], wsum);
+          }
+          if (any) {
+            if constexpr (TRANS) {
+              uint8_t* dst = map + (static_cast<size_t>(bh) * Tc + j0) * Tr + i16;
+              const uint32_t w4 = (word & 0xffu) * 0x01010101u;
+              if ((Tr & 15) == 0) {
+                *reinterpret_cast<uint4*>(dst) = make_uint4(w4, w4, w4, w4);
+              } else {
+                for (int v = 0; v < 16; ++v) dst[v] = static_cast<uint8_t>(w4);
+              }
+            } else {
+              uint8_t* dst = map + (static_cast<size_t>(bh) * Tr + i16) * Tc + j0;
+#pragma unroll 4
+              for (int v = 0; v < 16; ++v, dst += Tc) {
+                if (JPT == 4 && valid[JPT - 1]) {
+                  *reinterpret_cast<uint32_t*>(dst) = word;
+                } else {
+#pragma unroll
+                  for (int u = 0; u < JPT; ++u)
+                    if (valid[u]) dst[u] = static_cast<uint8_t>(word >> (8 * u));
+                }
+              }
+            }
+          }
+          continue;
+        }
+      }
+    }
+    uint32_t packed[4] = {0u, 0u, 0u, 0u};
+#pragma unroll (TRANS ? 16 : 2)
+    for (int v = 0; v < KB; ++v) {
       const int i = i16 + v;
-      if (i >= iend) break;
+      if (i16 + KB > iend && i >= iend) break;
       uint32_t word = 0u;
       int ns = 0;
       const int r0 = i * br, r1 = r0 + min(br, N - r0);
@@ -283,8 +485,9 @@ __global__ void __launch_bounds__(128) k1_classify(const int32_t* __restrict__ e
     const unsigned long long v = threadIdx.x == 0 ? tiles - cnt[0] - cnt[1] : (threadIdx.x == 1 ? cnt[1] : cnt[0]);
     if (v) atomicAdd(&counts[static_cast<size_t>(bh) * 3 + threadIdx.x], v);
   }
-  if (row_counts && threadIdx.x < iend - ib && row_acc[threadIdx.x])
-    atomicAdd(&row_cnt[static_cast<size_t>(bh) * Tr + ib + threadIdx.x], row_acc[threadIdx.x]);
+  if (row_counts)
+    for (int t = threadIdx.x; t < iend - ib; t += blockDim.x)
+      if (row_acc[t]) atomicAdd(&row_cnt[static_cast<size_t>(bh) * Tr + ib + t], row_acc[t]);
 }
 
 
@@ -420,20 +623,20 @@ cudaError_t launch_classify(const int32_t* ext8, const Dims& d, int br, int bc, 
   // Row tiles per CTA: enough CTAs for ~8 per SM (148 SMs), at most 64 row tiles each (the
   // counts leave each CTA as a few atomics; the transposed map is written in 16-row runs)
   // (wide non-transposed maps: 4 column tiles per thread and one 32-bit store per row, see the kernel)
-  const long gx = (Tc + 127) / 128;
-  long rpc = (gx * Tr * bhm + 1183) / 1184;
+  const long gx = (Tc + FM_K1_THREADS - 1) / FM_K1_THREADS;
+  long rpc = (gx * Tr * bhm * FM_K1_THREADS / 128 + 1183) / 1184;
   rpc = rpc < 1 ? 1 : (rpc > 64 ? 64 : rpc);
-  if (transposed && rpc > 8) rpc = (rpc + 15) / 16 * 16;
+  if (rpc > 8) rpc = (rpc + 15) / 16 * 16;  // 16-row blocks (uniform-block fast path, 16-row runs)
   const int ns = (d.flags & 1) ? 1 : 0;
   auto cnt64 = reinterpret_cast<unsigned long long*>(counts);
   const bool api = !kernel_map;
   const bool nsc = row_cnt != nullptr || col_cnt != nullptr;
   const int jpt = (!transposed && (Tc % 4) == 0 && Tc >= 512) ? 4 : 1;  // wide maps: 4 column tiles per thread
-  const long gxj = (Tc + 128L * jpt - 1) / (128L * jpt);
+  const long gxj = (Tc + static_cast<long>(FM_K1_THREADS) * jpt - 1) / (static_cast<long>(FM_K1_THREADS) * jpt);
   dim3 grid(static_cast<unsigned>(gxj), static_cast<unsigned>((Tr + rpc - 1) / rpc), static_cast<unsigned>(bhm));
   // (row-wise: ext8 holds the extrema of the br-row tiles)
   auto pick = [&](auto kern) {
-    return launch_pdl(kern, grid, dim3(128), 0, st, ext8, d.N, d.causal, br, bc, Tr, Tc, map, km, ns, cnt64, row_cnt,
+    return launch_pdl(kern, grid, dim3(FM_K1_THREADS), 0, st, ext8, d.N, d.causal, br, bc, Tr, Tc, map, km, ns, cnt64, row_cnt,
                       col_cnt, static_cast<int>(rpc));
   };
 #define FM_K1B(RW)                                                                          \

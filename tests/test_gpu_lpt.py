@@ -101,3 +101,32 @@ def test_split_g_backward(fmlib, fam, N, H, Hkv, d, dtype, flags):
                 assert_close(f"dQ[{h}]", dq[0, :, h].cpu().numpy(), gq)
         assert_close(f"dK[{hk}]", dk[0, :, hk].cpu().numpy(), gk, tol_max=2e-2 * G ** 0.5)
         assert_close(f"dV[{hk}]", dv[0, :, hk].cpu().numpy(), gv, tol_max=2e-2 * G ** 0.5)
+
+
+def test_per_head_masks_uniform_blocks(fmlib):
+    """32 distinct masks (Hm = H = 32) at N = 32K: the class maps take K1b's 16-row-tile uniform
+    blocks (forward row map and the backward's transposed map).  Each head must equal the same
+    head run alone (Hm = 1, per-row path) — bitwise for O / lse / dK / dV, dQ to fp32 reduce order."""
+    N, H = 32768, 32
+    rng = np.random.default_rng(7)
+    fams = ("causal_document", "share_question", "causal", "causal_blockwise")
+    ms = [wm.sample_family(fams[h % 4], N, rng, (3, 9)) for h in range(H)]
+    C = max(m.C for m in ms)
+    raw = np.stack([np.pad(m.sri, ((0, 0), (0, C - m.C)), constant_values=0) if m.C < C else m.sri for m in ms])
+    # causal masks of C = 1 (LTS) and C = 2 (LTS, LTE): pad C = 1 with LTE = N (R-causal layout)
+    for h, m in enumerate(ms):
+        if m.C < C:
+            raw[h, :, 1] = N
+    sri = torch.from_numpy(raw[None].astype(np.int32)).cuda()
+    x = {n: wt.make_tensor(n, 1, N, H, 128, base=11).cuda() for n in ("q", "k", "v", "do")}
+    o, lse = fmlib.flashmask_fwd(x["q"], x["k"], x["v"], sri, True, out_dtype=torch.float32)
+    dq, dk, dv = fmlib.flashmask_bwd(x["q"], x["k"], x["v"], o, x["do"], lse, sri, True, out_dtype=torch.float32)
+    for h in (0, 5, 18, 31):
+        xs = {n: t[:, :, h:h + 1].contiguous() for n, t in x.items()}
+        s1 = sri[:, h:h + 1].contiguous()
+        o1, l1 = fmlib.flashmask_fwd(xs["q"], xs["k"], xs["v"], s1, True, out_dtype=torch.float32)
+        g1 = fmlib.flashmask_bwd(xs["q"], xs["k"], xs["v"], o1, xs["do"], l1, s1, True, out_dtype=torch.float32)
+        torch.cuda.synchronize()
+        assert torch.equal(o[:, :, h:h + 1], o1) and torch.equal(lse[:, h:h + 1], l1), h
+        assert torch.allclose(dq[:, :, h:h + 1], g1[0], atol=1e-5, rtol=0), h
+        assert torch.equal(dk[:, :, h:h + 1], g1[1]) and torch.equal(dv[:, :, h:h + 1], g1[2]), h

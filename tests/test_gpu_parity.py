@@ -64,6 +64,35 @@ def test_classify_bit_exact(fmlib, fam, N):
             assert np.array_equal(cols[0, h].cpu().numpy(), cols_ref)
 
 
+@pytest.mark.parametrize("fam,N", [("global_sliding_window", 8192), ("causal_document", 8190), ("share_question", 8192),
+                                   ("random_eviction", 8192), ("causal", 8192), ("qk_sparse", 8176)])
+def test_classify_uniform_blocks(fmlib, fam, N):
+    """K1b's 16-row-tile blocks whose classes are constant (one evaluation, 16 stores): small tiles
+    and 8 heads give 16 row tiles per CTA; four column tiles per thread (Tc = 512); structured
+    masks with a few columns set to INT_MIN / INT_MAX / out-of-range values (R10)."""
+    rng = np.random.default_rng(N + len(fam))
+    ms = [wm.sample_family(fam, N, rng, (2, 6)) for _ in range(8)]
+    raw = np.stack([m.sri for m in ms])[None].copy()
+    for h in range(1, 8, 2):
+        cols = rng.choice(N, size=8, replace=False)
+        raw[0, h, cols[:3]] = np.iinfo(np.int32).max
+        raw[0, h, cols[3:6]] = np.iinfo(np.int32).min
+        raw[0, h, cols[6:]] = rng.integers(-N, 2 * N, size=(2, raw.shape[-1]))
+    causal = ms[0].causal
+    sri = torch.from_numpy(raw).cuda()
+    for br, bc in ((16, 16), (64, 16), (16, 64)):
+        _, cmap, counts, rows, cols = fmlib.flashmask_classify(sri, causal, br, bc, nonskip=True)
+        torch.cuda.synchronize()
+        for h in range(8):
+            vec = fo.expand(raw[0, h], causal, N)
+            cm_ref, cnt_ref, _ = fo.classify(vec, br, bc)
+            rows_ref, cols_ref = fo.nonskip_counts(vec, br, bc)
+            assert np.array_equal(cmap[0, h].cpu().numpy(), cm_ref), (br, bc, h)
+            assert np.array_equal(counts[0, h].cpu().numpy(), cnt_ref), (br, bc, h)
+            assert np.array_equal(rows[0, h].cpu().numpy(), rows_ref), (br, bc, h)
+            assert np.array_equal(cols[0, h].cpu().numpy(), cols_ref), (br, bc, h)
+
+
 def test_classify_arbitrary_int32_vectors(fmlib):
     """R10: any int32 values (inverted / out-of-range intervals) classify like the oracle."""
     rng = np.random.default_rng(0)
