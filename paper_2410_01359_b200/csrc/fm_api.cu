@@ -297,6 +297,7 @@ fm_status flashmask_classify(const fm_params* p, const int32_t* sri, int32_t br,
   fm_status s = check_params(p, &d, false);
   if (s != FM_OK) return s;
   if (!sri || !minmax) return fail(FM_ERR_INVALID_ARGUMENT, "startend_row_indices and minmax are required");
+  if (!aligned16(sri)) return fail(FM_ERR_INVALID_ARGUMENT, "startend_row_indices must be 16-byte aligned");
   if (br < 1 || bc < 1) return fail(FM_ERR_INVALID_ARGUMENT, "br and bc must be >= 1");
   if (!aligned16(minmax)) return fail(FM_ERR_INVALID_ARGUMENT, "minmax must be 16-byte aligned");
   cudaStream_t st = static_cast<cudaStream_t>(stream);

@@ -59,55 +59,81 @@ __device__ __forceinline__ void expand_col(const int32_t* s, int C, int causal, 
 
 __device__ __forceinline__ int clampi(int x, int lo, int hi) { return x < lo ? lo : (x > hi ? hi : x); }
 
-__global__ void __launch_bounds__(128) k1_expand(const int32_t* __restrict__ sri, int N, int C, int causal, int bc,
+// C is a template parameter (1, 2, 4) so that a column's C values come in one 4/8/16-byte load and
+// the column loop unrolls (several loads in flight per lane)
+template <int C>
+__global__ void __launch_bounds__(128) k1_expand(const int32_t* __restrict__ sri, int N, int causal, int bc,
                                                  int Tc, int32_t* __restrict__ ext8, int4* __restrict__ vec4,
                                                  int rowwise) {
   pdl_wait();
   pdl_launch();
   // one warp per column tile (4 per CTA): lanes stride over the tile's columns, the extrema
   // are reduced with warp shuffles only
+  // (grid-stride over column tiles; the launch sizes the grid at one warp per column tile)
   const int lane = threadIdx.x & 31;
-  const int j = blockIdx.x * 4 + (threadIdx.x >> 5);
   const int bh = blockIdx.y;
-  if (j >= Tc) return;
   const int32_t* base = sri + static_cast<size_t>(bh) * N * C;
-  int mn[4] = {INT_MAX, INT_MAX, INT_MAX, INT_MAX};
-  int mx[4] = {INT_MIN, INT_MIN, INT_MIN, INT_MIN};
-  for (int c = lane; c < bc; c += 32) {
-    const long y = static_cast<long>(j) * bc + c;
-    int4 nv;
-    if (y < N) {
-      int v[4];
-      expand_col(base + y * C, C, causal, N, v[0], v[1], v[2], v[3], rowwise);
+  for (int j = blockIdx.x * 4 + (threadIdx.x >> 5); j < Tc; j += gridDim.x * 4) {
+    int mn[4] = {INT_MAX, INT_MAX, INT_MAX, INT_MAX};
+    int mx[4] = {INT_MIN, INT_MIN, INT_MIN, INT_MIN};
+    // four columns per lane per round, all four loads issued before any is used
+    for (int cb = lane; cb < bc; cb += 128) {
+      int raw[4][4];
 #pragma unroll
-      for (int t = 0; t < 4; ++t) {
-        mn[t] = min(mn[t], v[t]);
-        mx[t] = max(mx[t], v[t]);
+      for (int k = 0; k < 4; ++k) {
+        const long y = static_cast<long>(j) * bc + cb + 32 * k;
+        raw[k][0] = raw[k][1] = raw[k][2] = raw[k][3] = 0;
+        if (cb + 32 * k < bc && y < N) {
+          if constexpr (C == 4) {
+            const int4 t = __ldg(reinterpret_cast<const int4*>(base + y * 4));
+            raw[k][0] = t.x; raw[k][1] = t.y; raw[k][2] = t.z; raw[k][3] = t.w;
+          } else if constexpr (C == 2) {
+            const int2 t = __ldg(reinterpret_cast<const int2*>(base + y * 2));
+            raw[k][0] = t.x; raw[k][1] = t.y;
+          } else {
+            raw[k][0] = __ldg(base + y);
+          }
+        }
       }
-      int a = clampi(v[0], 0, N), b = clampi(v[1], 0, N), u = clampi(v[2], 0, N), w = clampi(v[3], 0, N);
-      if (a >= b) a = b = 0;
-      if (u >= w) u = w = 0;
-      nv = make_int4(a, b - a, u, w - u);  // (start, length) per interval
-    } else {
-      nv = make_int4(0, INT_MAX, 0, 0);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        if (cb + 32 * k >= bc) break;
+        const long y = static_cast<long>(j) * bc + cb + 32 * k;
+        int4 nv;
+        if (y < N) {
+          int v[4];
+          expand_col(raw[k], C, causal, N, v[0], v[1], v[2], v[3], rowwise);
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            mn[t] = min(mn[t], v[t]);
+            mx[t] = max(mx[t], v[t]);
+          }
+          int a = clampi(v[0], 0, N), b = clampi(v[1], 0, N), u = clampi(v[2], 0, N), w = clampi(v[3], 0, N);
+          if (a >= b) a = b = 0;
+          if (u >= w) u = w = 0;
+          nv = make_int4(a, b - a, u, w - u);  // (start, length) per interval
+        } else {
+          nv = make_int4(0, INT_MAX, 0, 0);
+        }
+        if (vec4) vec4[static_cast<size_t>(bh) * Tc * bc + y] = nv;
+      }
     }
-    if (vec4) vec4[static_cast<size_t>(bh) * Tc * bc + y] = nv;
-  }
 #pragma unroll
-  for (int t = 0; t < 4; ++t) {
+    for (int t = 0; t < 4; ++t) {
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      mn[t] = min(mn[t], __shfl_xor_sync(0xffffffffu, mn[t], o));
-      mx[t] = max(mx[t], __shfl_xor_sync(0xffffffffu, mx[t], o));
+      for (int o = 16; o > 0; o >>= 1) {
+        mn[t] = min(mn[t], __shfl_xor_sync(0xffffffffu, mn[t], o));
+        mx[t] = max(mx[t], __shfl_xor_sync(0xffffffffu, mx[t], o));
+      }
     }
-  }
-  if (lane < 8) {
-    const int t = lane >> 1;
-    int r = (lane & 1) ? mx[0] : mn[0];
+    if (lane < 8) {
+      const int t = lane >> 1;
+      int r = (lane & 1) ? mx[0] : mn[0];
 #pragma unroll
-    for (int k = 1; k < 4; ++k)
-      if (t == k) r = (lane & 1) ? mx[k] : mn[k];
-    ext8[(static_cast<size_t>(bh) * Tc + j) * 8 + lane] = r;
+      for (int k = 1; k < 4; ++k)
+        if (t == k) r = (lane & 1) ? mx[k] : mn[k];
+      ext8[(static_cast<size_t>(bh) * Tc + j) * 8 + lane] = r;
+    }
   }
 }
 
@@ -605,7 +631,8 @@ cudaError_t launch_sliding_window(int B, int N, int w, int causal, int32_t* sri,
 cudaError_t launch_expand(const int32_t* sri, const Dims& d, int bc, int32_t* ext8, int4* vec4, cudaStream_t st) {
   const int Tc = (d.N + bc - 1) / bc;
   dim3 grid((Tc + 3) / 4, d.B * d.Hm);
-  return launch_pdl(k1_expand, grid, dim3(128), 0, st, sri, d.N, d.C, d.causal, bc, Tc, ext8, vec4, d.rowwise);
+  auto kern = d.C == 4 ? k1_expand<4> : (d.C == 2 ? k1_expand<2> : k1_expand<1>);
+  return launch_pdl(kern, grid, dim3(128), 0, st, sri, d.N, d.causal, bc, Tc, ext8, vec4, d.rowwise);
 }
 
 cudaError_t launch_classify(const int32_t* ext8, const Dims& d, int br, int bc, uint8_t* map, int transposed,
