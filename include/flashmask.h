@@ -107,7 +107,9 @@ enum {
 
 typedef struct {
   int64_t batch;       /* B >= 1                                                    */
-  int64_t seqlen;      /* 1 <= N <= 262144 (queries = keys); larger: UNSUPPORTED     */
+  int64_t seqlen;      /* 1 <= N (queries = keys): N <= 262144 for the attention calls,
+                        * N <= 2^30 and ceil(N / br) <= 4194240 for flashmask_classify;
+                        * larger: FM_ERR_UNSUPPORTED                                 */
   int64_t num_heads;   /* H >= 1                                                    */
   int64_t head_dim;    /* d in {64, 128}                                            */
   int64_t mask_heads;  /* 1 (one mask per batch entry, broadcast) or num_kv_heads;

@@ -7,6 +7,7 @@
 
 #include <cmath>
 #include <cstdio>
+#include <algorithm>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -299,6 +300,9 @@ fm_status flashmask_classify(const fm_params* p, const int32_t* sri, int32_t br,
   if (!sri || !minmax) return fail(FM_ERR_INVALID_ARGUMENT, "startend_row_indices and minmax are required");
   if (!aligned16(sri)) return fail(FM_ERR_INVALID_ARGUMENT, "startend_row_indices must be 16-byte aligned");
   if (br < 1 || bc < 1) return fail(FM_ERR_INVALID_ARGUMENT, "br and bc must be >= 1");
+  // K1b: at most 64 row tiles per CTA and 65535 CTAs along the row-tile grid dimension
+  if ((p->seqlen + std::min<int64_t>(br, p->seqlen) - 1) / std::min<int64_t>(br, p->seqlen) > 65535LL * 64)
+    return fail(FM_ERR_UNSUPPORTED, "ceil(seqlen / br) > 4194240 row tiles");
   if (!aligned16(minmax)) return fail(FM_ERR_INVALID_ARGUMENT, "minmax must be 16-byte aligned");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   // column-wise: extrema per bc-column tile; row-wise (R32): per br-row tile

@@ -133,3 +133,15 @@ def test_binding_rejects_host_tensors(lib_path):
     sri = torch.full((1, 1, 128, 1), 128, dtype=torch.int32)
     with pytest.raises(fm.FlashMaskError, match="CUDA"):
         fm.flashmask_fwd(q, q, q, sri, True)
+
+
+def test_classify_row_tile_grid_limit(lib_path):
+    """K1b holds <= 64 row tiles per CTA and <= 65535 CTAs along that grid dimension: a classify
+    call with more than 4194240 row tiles is refused on the host, before any launch."""
+    from paper_2410_01359_b200 import flashmask as fm
+    p = fm.FmParams(batch=1, seqlen=1 << 27, num_heads=1, head_dim=128, mask_heads=1, mask_cols=1, causal=1,
+                    scale=0.0, in_dtype=0, out_dtype=0, flags=0, num_kv_heads=0)
+    dummy = ctypes.c_void_p(256)   # aligned, never dereferenced: the call fails in host validation
+    st = fm._lib.flashmask_classify(ctypes.byref(p), dummy, 16, 128, dummy, None, None, None, None, None)
+    assert st == fm.FM_ERR_UNSUPPORTED
+    assert b"row tiles" in fm._lib.flashmask_last_error()
