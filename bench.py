@@ -757,7 +757,7 @@ def run_e2e(fm, run, dev, stream, steps, barrier, max_over_ranks, world):
     e0.record(stream)
     s_in.wait_event(e0)
     s_out.wait_event(e0)
-    n_e2e = max(1, min(steps, 5))
+    n_e2e = max(1, min(steps, 10))
     for _ in range(n_e2e):
         e2e_step()
     e2e_drain()

@@ -525,13 +525,15 @@ __global__ void __launch_bounds__(FM_K1_THREADS, FM_K1_MINB) k1_classify(const i
 // lane = 4 consecutive columns whose expanded intervals stay in registers while the warp walks
 // the column's row tiles; one ballot per row group turns the per-column tests into chunk bits.
 // Optional counts per (b, hm): PARTIAL tiles whose word is 0 (no masked cell at all), and dirty
-// sub-blocks over all PARTIAL tiles.  Grid (ceil(Tc / 4), B*Hm), 128 threads.
+// sub-blocks over all PARTIAL tiles.  Grid (ceil(Tc / 4), B*Hm, ceil(Tr / rows)), 128 threads: a
+// warp walks `rows` (8 or 32) row tiles, so small maps still spread over the SMs (one warp over all
+// 64 row tiles of an 8K map was 14.6 us, latency-bound).
 // ---------------------------------------------------------------------------------------
 __device__ __forceinline__ bool ivl_hits(int s, int e, int a, int b) { return s < e && s < b && e > a; }
 
 __global__ void __launch_bounds__(128) k1_refine(const int32_t* __restrict__ sri, const uint8_t* __restrict__ cmap,
                                                  int N, int C, int causal, int Tr, int Tc, uint32_t* __restrict__ words,
-                                                 unsigned long long* __restrict__ rcounts) {
+                                                 unsigned long long* __restrict__ rcounts, int rows) {
   pdl_wait();
   pdl_launch();
   const int lane = threadIdx.x & 31;
@@ -557,13 +559,14 @@ __global__ void __launch_bounds__(128) k1_refine(const int32_t* __restrict__ sri
   for (int c = 0; c < 8; ++c)
     if (j * 128 + c * 16 < N) colbits |= 1u << c;
   unsigned long long n_clean = 0, n_dirty = 0;
-  uint32_t cls32 = 0u;  // classes of row tiles [i & ~31, +32): lane l holds row (i & ~31) + l
-  for (int i = 0; i < Tr; ++i) {
-    if ((i & 31) == 0) {  // one strided load per lane instead of a dependent load per row tile
-      const int il = i + lane;
-      cls32 = il < Tr ? cmap[(static_cast<size_t>(bh) * Tr + il) * Tc + j] : 0u;
-    }
-    const uint32_t cls = __shfl_sync(0xffffffffu, cls32, i & 31);
+  // classes of this warp's row tiles [i0, i0 + rows), rows <= 32: lane l holds row i0 + l — one
+  // strided load per lane instead of a dependent load per row tile
+  // (grid-stride over row chunks: gridDim.z is capped at 65535 on the host)
+  for (int i0 = blockIdx.z * rows; i0 < Tr; i0 += gridDim.z * rows) {
+  const int i1 = min(Tr, i0 + rows);
+  const uint32_t cls32 = (lane < rows && i0 + lane < Tr) ? cmap[(static_cast<size_t>(bh) * Tr + i0 + lane) * Tc + j] : 0u;
+  for (int i = i0; i < i1; ++i) {
+    const uint32_t cls = __shfl_sync(0xffffffffu, cls32, i - i0);
     uint32_t w = 0u;
     if (cls == 0u) {
 #pragma unroll
@@ -589,6 +592,7 @@ __global__ void __launch_bounds__(128) k1_refine(const int32_t* __restrict__ sri
     }
     if (lane == 0) words[(static_cast<size_t>(bh) * Tr + i) * Tc + j] = w;
   }
+  }
   if (rcounts && lane == 0) {
     if (n_clean) atomicAdd(&rcounts[static_cast<size_t>(bh) * 2], n_clean);
     if (n_dirty) atomicAdd(&rcounts[static_cast<size_t>(bh) * 2 + 1], n_dirty);
@@ -601,9 +605,14 @@ cudaError_t launch_refine(const int32_t* sri, const uint8_t* cmap, const Dims& d
     cudaError_t e = cudaMemsetAsync(rcounts, 0, sizeof(int64_t) * 2 * d.B * d.Hm, st);
     if (e != cudaSuccess) return e;
   }
-  dim3 grid((d.Tc + 3) / 4, d.B * d.Hm);
+  // row tiles per warp: 8 for maps up to 2^20 tiles (several CTAs per SM), else 32 (fewer
+  // re-expansions of the column vectors)
+  const long tiles = static_cast<long>(d.Tr) * d.Tc * d.B * d.Hm;
+  const int rows = tiles <= (1L << 20) ? 8 : 32;
+  const long chunks = (d.Tr + rows - 1) / rows;
+  dim3 grid((d.Tc + 3) / 4, d.B * d.Hm, static_cast<unsigned>(chunks < 65535 ? chunks : 65535));
   return launch_pdl(k1_refine, grid, dim3(128), 0, st, sri, cmap, d.N, d.C, d.causal, d.Tr, d.Tc, words,
-                    reinterpret_cast<unsigned long long*>(rcounts));
+                    reinterpret_cast<unsigned long long*>(rcounts), rows);
 }
 
 // Sliding-window startend_row_indices (flashmask_sliding_window_indices): one thread per key.
@@ -701,21 +710,22 @@ __global__ void __launch_bounds__(1024) k1_order(const uint8_t* __restrict__ map
   const int units = FWD ? (Tr + 1) / 2 : Tc;
   int p2 = 1;
   while (p2 < units) p2 <<= 1;
-  for (int u = threadIdx.x; u < p2; u += blockDim.x) {
+  // one warp per unit: lanes read the unit's class bytes coalesced, a warp reduction sums them
+  const int lane = threadIdx.x & 31;
+  for (int u = threadIdx.x >> 5; u < p2; u += blockDim.x >> 5) {
     uint32_t w = 0;
     if (u < units) {
       if (FWD) {
         const uint8_t* r0 = map + (static_cast<size_t>(bh) * Tr + 2 * u) * Tc;
         const uint8_t* r1 = (2 * u + 1 < Tr) ? r0 + Tc : r0;
-        for (int j = 0; j < Tc; ++j) w += (r0[j] | r1[j]) != 0;
+        for (int j = lane; j < Tc; j += 32) w += (r0[j] | r1[j]) != 0;
       } else {
         const uint8_t* c = map + (static_cast<size_t>(bh) * Tc + u) * Trb;
-        for (int i = 0; i < Trb; ++i) w += c[i] != 0;
+        for (int i = lane; i < Trb; i += 32) w += c[i] != 0;
       }
-      key[u] = (w << 16) | (0xFFFFu - static_cast<uint32_t>(u));
-    } else {
-      key[u] = 0u;
+      w = __reduce_add_sync(0xffffffffu, w);
     }
+    if (lane == 0) key[u] = u < units ? (w << 16) | (0xFFFFu - static_cast<uint32_t>(u)) : 0u;
   }
   __syncthreads();
   for (int k = 2; k <= p2; k <<= 1) {

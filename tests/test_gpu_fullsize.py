@@ -183,3 +183,36 @@ def test_c3_generic_q_dk_dv_sampled_columns(fm):
         gk, gv = fo.backward_cols(q, k, v, do, vec, keys)
         assert_close(f"C3 b{b} h{h} dK cols", dk[b, keys, h].cpu().numpy(), gk)
         assert_close(f"C3 b{b} h{h} dV cols", dv[b, keys, h].cpu().numpy(), gv)
+
+
+@pytest.mark.parametrize("N,d,fam", [(262144, 128, "causal_document"), (262144 - 37, 64, "share_question"),
+                                     (262144 - 100, 128, "global_sliding_window")])
+def test_max_seqlen_sampled_rows_and_q_zero(fm, N, d, fam):
+    """The largest supported sequence (2048 column tiles: the forward visit list and the backward
+    row-tile list at capacity, include/flashmask.h), exact and ragged: sampled rows (O, lse, dQ) of
+    one head against the oracle and the Q = 0 closed forms (O, lse, dV) of both heads."""
+    from workloads import masks as wm
+    from workloads import tensors as wt
+    rng = np.random.default_rng(N + d)
+    m = wm.sample_family(fam, N, rng, (5, 9))
+    x = {k: t.cuda().to(torch.bfloat16) for k, t in wt.make_qkv(1, N, 2, d, base=11).items()}
+    x["sri"] = torch.from_numpy(wm.stack([m])).cuda()
+    c = {"causal": m.causal}
+    o, lse, dq, dk, dv = _run(fm, c, x, torch.float32)
+    vec = fo.expand(m.sri, m.causal, N)
+    rows = np.sort(np.concatenate([rng.choice(N, 30, replace=False), [0, N - 1]]))
+    q, k, v, do = (_head(x, n, 0, 1) for n in ("q", "k", "v", "do"))
+    O, L = fo.forward(q, k, v, vec, rows=rows, row_block=16)
+    gq, _, _ = fo.backward_rows(q, k, v, do, vec, rows)
+    assert_close(f"N{N} {fam} O rows", o[0, rows, 1].cpu().numpy(), O)
+    assert_lse(lse[0, 1, rows].cpu().numpy(), L)
+    assert_close(f"N{N} {fam} dQ rows", dq[0, rows, 1].cpu().numpy(), gq)
+    del o, lse, dq, dk, dv
+    xz = dict(x)
+    xz["q"] = torch.zeros_like(x["q"])
+    o, lse, dq, dk, dv = _run(fm, c, xz, torch.float32)
+    for h in (0, 1):
+        O, L = fo.forward_q_zero(_head(x, "v", 0, h), vec)
+        assert_close(f"N{N} Q=0 O h{h}", o[0, :, h].cpu().numpy(), O)
+        assert_lse(lse[0, h].cpu().numpy(), L)
+        assert_close(f"N{N} Q=0 dV h{h}", dv[0, :, h].cpu().numpy(), fo.dv_q_zero(_head(x, "do", 0, h), vec))
