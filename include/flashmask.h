@@ -102,7 +102,18 @@ enum {
    * Tiles are classified by Eq. 4 on the transposed problem (per-row-tile extrema against the
    * column range).  flashmask_classify then returns minmax per ROW tile ([B, Hm, Tr, 8], tile br).
    * Accepted by every entry point; FM_FLAG_FWD_PAIR is ignored with it (single-SM forward). */
-  FM_FLAG_ROWWISE = 16
+  FM_FLAG_ROWWISE = 16,
+  /* flashmask_fwd: always take each visited tile's row maximum before its exponentials (Alg. 1
+   * line 242).  By default, with bf16 operands and seqlen >= 16384, the single-SM
+   * forward instead computes every P of a row against one fixed reference
+   * m_r = ||q_r|| max_y ||k_y|| scale log2(e) - 64 (Cauchy-Schwarz bound of the row's logits; key
+   * norms from one extra pass over K): no row maximum, no rescaling, one pass per tile; rows whose sum ends below
+   * 2^-60 (bound too loose, or every key masked) are recomputed by the two-pass kernel
+   * (R33).  Same outputs to rounding (parity tolerances). */
+  FM_FLAG_NO_MAX_BOUND = 32,
+  /* Testing: use the bounded single pass of FM_FLAG_NO_MAX_BOUND's description at any seqlen (bf16
+   * operands).  Ignored together with FM_FLAG_NO_MAX_BOUND. */
+  FM_FLAG_MAX_BOUND = 64
 };
 
 typedef struct {

@@ -191,6 +191,12 @@ size_t carve(const fm::Dims& d, int pass, void* base, fm::Workspace* w) {
   }
   // LPT orders (>= ceil(Tr/2) pairs or Tc key tiles per (b, hm)) followed by one flag per (b, hm)
   w->order = reinterpret_cast<uint16_t*>(take(bhm * (d.Tc + 1) * sizeof(uint16_t)));
+  w->kmax = nullptr;
+  w->fix = nullptr;
+  if (pass == FM_PASS_FWD) {
+    w->kmax = reinterpret_cast<float*>(take(static_cast<size_t>(d.B) * d.Hkv * d.Tc * sizeof(float)));
+    w->fix = take(bh * ((d.Tr + 1) / 2));
+  }
   w->bytes = off;
   return off;
 }
@@ -399,14 +405,40 @@ fm_status flashmask_fwd(const fm_params* p, const void* q, const void* k, const 
   a.vec4 = w.vec4;
   a.o = o;
   a.lse = lse;
+  a.kmax = nullptr;
+  a.fix_out = nullptr;
+  a.fix = nullptr;
   if ((p->flags & FM_FLAG_FWD_PAIR) && d.D == 128 && !d.rowwise) {
     CUtensorMap tk64;
     if (!make_map(&tk64, k, d, d.Hkv, 64, &err)) return fail(FM_ERR_CUDA, err);
     e = timed(FM_KERNEL_FWD, st, [&] { return fm::launch_fwd2(d, tq, tk64, tv, to, a, st); });
-  } else {
-    e = timed(FM_KERNEL_FWD, st, [&] { return fm::launch_fwd(d, tq, tk, tv, to, a, st); });
+    if (e != cudaSuccess) return cuda_fail(e, "forward kernel");
+    return FM_OK;
   }
+  // R33 bounded single pass (bf16 operands): key norms per tile (K1e), the single-pass forward, then
+  // the two-pass forward over the units it flagged (CTAs of unflagged units exit at once).  Used from
+  // N = 16K: below, the fixup launch's waves of exiting CTAs (~1.5 us each, 215 KB of shared memory
+  // keep them one per SM) cost more than the single pass saves on the few tiles of a short unit
+  // (C2 -7..-9 %, R33)
+  const bool bounded = !d.in_f16 && (p->flags & FM_FLAG_NO_MAX_BOUND) == 0 &&
+                       (d.N >= 16384 || (p->flags & FM_FLAG_MAX_BOUND) != 0);
+  if (bounded) {
+    e = timed(FM_KERNEL_EXPAND, st, [&] { return fm::launch_key_norms(d, k, w.kmax, w.fix, st); });
+    if (e != cudaSuccess) return cuda_fail(e, "key norms");
+    a.kmax = w.kmax;
+    a.fix_out = w.fix;
+  }
+  e = timed(FM_KERNEL_FWD, st, [&] { return fm::launch_fwd(d, tq, tk, tv, to, a, st); });
   if (e != cudaSuccess) return cuda_fail(e, "forward kernel");
+  if (bounded) {
+    fm::FwdArgs f = a;
+    f.kmax = nullptr;
+    f.fix_out = nullptr;
+    f.fix = w.fix;
+    f.order = nullptr;
+    e = timed(FM_KERNEL_FWD, st, [&] { return fm::launch_fwd(d, tq, tk, tv, to, f, st); });
+    if (e != cudaSuccess) return cuda_fail(e, "forward fixup kernel");
+  }
   return FM_OK;
 }
 

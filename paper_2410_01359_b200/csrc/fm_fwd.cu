@@ -87,6 +87,7 @@ struct Smem {
   uint32_t tmem_base;
   int n_entries;
   int warp_cnt[NT / 32];
+  float warp_kmax[NT / 32];  // BND: largest key norm over each warp's visited column tiles
 };
 
 constexpr int PRODUCER_WARP = 16, MMA_WARP = 17;
@@ -106,7 +107,10 @@ __device__ __forceinline__ int ent_cls(uint32_t ent, int q) { return (ent >> (24
 // ROWW: row-wise representation (FM_FLAG_ROWWISE, R32) — a.vec4 holds each query
 // ROW's masked key intervals; a softmax thread (= one row) keeps its own in registers and no mask
 // slice is loaded per tile.
-template <int D, bool CAUSAL, bool OUT_F32, bool F16, bool ROWW>
+// BND: R33 bounded single pass (bf16 operands): P of every tile against the fixed per-row reference
+// ||q_r|| max_y ||k_y|| scale log2(e) - 64, no max pass, no rescaling; unfinished rows flag the
+// unit for the two-pass fixup launch (this kernel with BND = false and a.fix set).
+template <int D, bool CAUSAL, bool OUT_F32, bool F16, bool ROWW, bool BND>
 __global__ void __launch_bounds__(fwd::NT, 1)
     fm_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                   const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmO, const FwdArgs a) {
@@ -136,6 +140,13 @@ __global__ void __launch_bounds__(fwd::NT, 1)
   } else {
     pair = npairs - 1 - static_cast<int>(blockIdx.x);
     h = blockIdx.y;
+  }
+  // two-pass fixup launch (R33): only the units the bounded pass flagged (written by the stream
+  // predecessor); the others exit before touching any resource
+  const size_t unit = (static_cast<size_t>(b) * a.H + h) * npairs + pair;
+  if (!BND && a.fix != nullptr) {
+    pdl_wait();
+    if (a.fix[unit] == 0) return;
   }
   const int hk = h / a.G;                      // key/value head of this query head (GQA)
   const int hm = (a.Hm == 1) ? 0 : hk;
@@ -176,6 +187,10 @@ __global__ void __launch_bounds__(fwd::NT, 1)
     const uint8_t* row0 = a.fmap + (bhm * a.Tr + i0) * a.Tc;
     const uint8_t* row1 = row0 + a.Tc;
     int base = 0;
+    // BND: largest key norm of the head over ALL its column tiles — independent of which tiles are
+    // visited, so FM_FLAG_NO_SKIP (SKIP visited as PARTIAL) keeps the same reference bit for bit
+    float kv = 0.f;
+    const float* kmax_bh = BND ? a.kmax + (static_cast<size_t>(b) * (a.H / a.G) + hk) * a.Tc : nullptr;
     for (int j0 = 0; j0 < a.Tc; j0 += NT) {
       const int j = j0 + tid;
       uint32_t c0 = 0, c1 = 0;
@@ -196,10 +211,16 @@ __global__ void __launch_bounds__(fwd::NT, 1)
       }
       off += __popc(bal & ((1u << lane) - 1u));
       if (vis) sm.list[off] = static_cast<uint32_t>(j) | (c0 << 24) | (c1 << 26);
+      if (BND && j < a.Tc) kv = fmaxf(kv, __ldg(kmax_bh + j));
       base += tot;
       __syncthreads();
     }
     if (tid == 0) sm.n_entries = base;
+    if constexpr (BND) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) kv = fmaxf(kv, __shfl_xor_sync(0xffffffffu, kv, o));
+      if (lane == 0) sm.warp_kmax[warp] = kv;
+    }
   }
   tc_fence_before();
   __syncthreads();
@@ -360,6 +381,14 @@ __global__ void __launch_bounds__(fwd::NT, 1)
     // K1a's padding value: every key masked)
     if constexpr (ROWW)
       rmv = row < a.N ? a.vec4[bhm * static_cast<size_t>(a.Tc) * 128 + row] : make_int4(0, INT_MAX, 0, 0);
+    // R33 (BND): the row's fixed reference, ||q_r|| * max key norm of the head * scale * log2(e) - 64,
+    // so every P <= 2^64; set at the first visited tile (Q has landed once S has)
+    float m_ref = 0.f;
+    float kvis = 0.f;
+    if constexpr (BND) {
+#pragma unroll
+      for (int w = 0; w < NT / 32; ++w) kvis = fmaxf(kvis, sm.warp_kmax[w]);
+    }
     for (int e = 0; e < nE; ++e) {
       const uint32_t ent = sm.list[e];
       const int cls = ent_cls(ent, q);
@@ -370,14 +399,39 @@ __global__ void __launch_bounds__(fwd::NT, 1)
         mbar_wait(&sm.s_full[q], cnt & 1);
         if (row_t == 0 && hh == 0) FT(0 + q, e);
         tc_fence_after();
-        // Pass 1: max over this half's 64 columns, 32 at a time (S stays in TMEM for pass 2).
-        // On PARTIAL tiles the element mask (Alg. 1 lines 15-21) is applied here and the masked S
-        // written back to TMEM, so pass 2 is identical for PARTIAL and UNMASKED tiles.
-        float mx0 = -INFINITY, mx1 = -INFINITY, mx2 = -INFINITY, mx3 = -INFINITY;
         uint32_t sr[2][16];
         // f3: the 16-column chunks of this warp's 32 rows x 64 columns that hold a masked cell
         const uint32_t pm =
             (cls != 1) ? 0u : ((kRefine<CAUSAL> && !ROWW) ? (sm.cw[ms][q] >> (wl * 8 + hh * 4)) & 0xFu : 0xFu);
+        if constexpr (BND) {
+          if (cnt == 0) {
+            // ||q_r|| from the Q tile in shared memory: granule g ^ (row & 7) of the 128-byte
+            // swizzled row, so the 8 rows of a bank group read 8 different 16-byte columns
+            float ss = 0.f;
+#pragma unroll
+            for (int c = 0; c < D / 64; ++c) {
+#pragma unroll
+              for (int g = 0; g < 8; ++g) {
+                const uint4 u = *reinterpret_cast<const uint4*>(sm.q[q] + c * 16384 + row_t * 128 + ((g ^ (row_t & 7)) << 4));
+                const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                  const float lo = __uint_as_float(w4[t] << 16), hi = __uint_as_float(w4[t] & 0xFFFF0000u);
+                  ss = fmaf(lo, lo, fmaf(hi, hi, ss));
+                }
+              }
+            }
+            m_ref = sqrtf(ss) * (1.0f + 1.0f / 65536.0f) * kvis * sl2 - 64.0f;
+          }
+          if (Layout<D>::SEP_P && cnt > 0) {  // PV_q(e-1) done with the P buffer
+            mbar_wait(&sm.pv_done[q], (cnt - 1) & 1);
+            tc_fence_after();
+          }
+        } else {
+        // Pass 1: max over this half's 64 columns, 32 at a time (S stays in TMEM for pass 2).
+        // On PARTIAL tiles the element mask (Alg. 1 lines 15-21) is applied here and the masked S
+        // written back to TMEM, so pass 2 is identical for PARTIAL and UNMASKED tiles.
+        float mx0 = -INFINITY, mx1 = -INFINITY, mx2 = -INFINITY, mx3 = -INFINITY;
         tmem_ld16(tSh, sr[0]);
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
@@ -463,7 +517,8 @@ __global__ void __launch_bounds__(fwd::NT, 1)
             tmem_st32(tOh + c * 32, ov);
           }
         }
-        const float m_use = (m_used == -INFINITY) ? 0.f : m_used;
+        }  // two-pass (!BND)
+        const float m_use = BND ? m_ref : ((m_used == -INFINITY) ? 0.f : m_used);
         // Pass 2: P = exp2(S*scale*log2e - m) over this half's columns; packed FFMA2 for the
         // argument, MUFU ex2 for most pairs and the FMA-pipe polynomial for kPolyPairs of 8;
         // row sums with packed FADD2; packed bf16 P written back over consumed S columns.
@@ -478,7 +533,39 @@ __global__ void __launch_bounds__(fwd::NT, 1)
             tc_fence_before();
             mbar_arrive(&sm.s_read[q]);
           }
-          const float* sv = reinterpret_cast<const float*>(sr[ch & 1]);
+          float* sv = reinterpret_cast<float*>(sr[ch & 1]);
+          if (BND && (pm & (1u << ch))) {
+            // element mask of Alg. 1 lines 15-21 in registers (no max pass to carry it to TMEM)
+            const int4* mk = sm.mask[ms] + hh * 64 + ch * 16;
+            const int rmy = row - (j * 128 + hh * 64 + ch * 16);
+            if constexpr (ROWW) {
+#pragma unroll
+              for (int t = 0; t < 16; ++t) {
+                const int y = row - rmy + t;
+                bool msk = (static_cast<unsigned>(y - rmv.x) < static_cast<unsigned>(rmv.y)) ||
+                           (static_cast<unsigned>(y - rmv.z) < static_cast<unsigned>(rmv.w)) || y >= a.N;
+                if constexpr (CAUSAL) msk |= rmy < t;
+                sv[t] = msk ? -INFINITY : sv[t];
+              }
+            } else if (CAUSAL && j < (q == 0 ? i0 : i1)) {
+#pragma unroll
+              for (int t = 0; t < 16; ++t) {
+                const int4 mv = mk[t];
+                sv[t] = static_cast<unsigned>(row - mv.x) < static_cast<unsigned>(mv.y) ? -INFINITY : sv[t];
+              }
+            } else {
+#pragma unroll
+              for (int t = 0; t < 16; ++t) {
+                const int4 mv = mk[t];
+                bool msk = static_cast<unsigned>(row - mv.x) < static_cast<unsigned>(mv.y);
+                if constexpr (CAUSAL)
+                  msk |= rmy < t;
+                else
+                  msk |= static_cast<unsigned>(row - mv.z) < static_cast<unsigned>(mv.w);
+                sv[t] = msk ? -INFINITY : sv[t];
+              }
+            }
+          }
           uint32_t pk[8];
 #pragma unroll
           for (int kk = 0; kk < 8; ++kk) {
@@ -525,7 +612,10 @@ __global__ void __launch_bounds__(fwd::NT, 1)
     sm.xsum[q][hh][row_t] = l;
     named_bar_sync(bar_id, 64);
     l += sm.xsum[q][hh ^ 1][row_t];
-    const bool live = (cnt > 0) && (l > 0.f);
+    // BND: a row whose sum ends below 2^-60 (its logits far below the Cauchy-Schwarz bound, or every
+    // key masked) flags the unit; the two-pass fixup launch recomputes it (O and lse overwritten)
+    const bool live = (cnt > 0) && (BND ? (l >= 0x1p-60f) : (l > 0.f));
+    if (BND && row < a.N && !live) a.fix_out[unit] = 1;
     if (cnt > 0) {
       mbar_wait(&sm.o_full[q], 0);
       tc_fence_after();
@@ -594,7 +684,7 @@ __global__ void __launch_bounds__(fwd::NT, 1)
     }
     if (row < a.N && hh == 0)
       a.lse[(static_cast<size_t>(b) * a.H + h) * a.N + row] =
-          live ? (m_used + __log2f(l)) * 0.6931471805599453f : -INFINITY;
+          live ? ((BND ? m_ref : m_used) + __log2f(l)) * 0.6931471805599453f : -INFINITY;
     if (row_t == 0 && hh == 0) FTE(5 + q);
   }
 
@@ -612,10 +702,10 @@ __global__ void __launch_bounds__(fwd::NT, 1)
 #endif
 }
 
-template <int D, bool CAUSAL, bool OUT_F32, bool F16, bool ROWW>
+template <int D, bool CAUSAL, bool OUT_F32, bool F16, bool ROWW, bool BND>
 static cudaError_t launch_fwd_t(const Dims& d, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
                                 const CUtensorMap& to, const FwdArgs& a, cudaStream_t st) {
-  auto kern = fm_fwd_kernel<D, CAUSAL, OUT_F32, F16, ROWW>;
+  auto kern = fm_fwd_kernel<D, CAUSAL, OUT_F32, F16, ROWW, BND>;
   const size_t smem = sizeof(fwd::Smem<D>) + 1024;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (e != cudaSuccess) return e;
@@ -627,11 +717,14 @@ cudaError_t launch_fwd(const Dims& d, const CUtensorMap& tq, const CUtensorMap& 
                        const CUtensorMap& to, const FwdArgs& a, cudaStream_t st) {
 #define FM_F(DD, CC, FF)                                                                                    \
   do {                                                                                                      \
+    if (a.kmax != nullptr && !d.in_f16)  /* R33 bounded single pass: bf16 operands */                       \
+      return d.rowwise ? launch_fwd_t<DD, CC, FF, false, true, true>(d, tq, tk, tv, to, a, st)              \
+                       : launch_fwd_t<DD, CC, FF, false, false, true>(d, tq, tk, tv, to, a, st);            \
     if (d.rowwise)                                                                                          \
-      return d.in_f16 ? launch_fwd_t<DD, CC, FF, true, true>(d, tq, tk, tv, to, a, st)                      \
-                      : launch_fwd_t<DD, CC, FF, false, true>(d, tq, tk, tv, to, a, st);                    \
-    return d.in_f16 ? launch_fwd_t<DD, CC, FF, true, false>(d, tq, tk, tv, to, a, st)                       \
-                    : launch_fwd_t<DD, CC, FF, false, false>(d, tq, tk, tv, to, a, st);                     \
+      return d.in_f16 ? launch_fwd_t<DD, CC, FF, true, true, false>(d, tq, tk, tv, to, a, st)               \
+                      : launch_fwd_t<DD, CC, FF, false, true, false>(d, tq, tk, tv, to, a, st);             \
+    return d.in_f16 ? launch_fwd_t<DD, CC, FF, true, false, false>(d, tq, tk, tv, to, a, st)                \
+                    : launch_fwd_t<DD, CC, FF, false, false, false>(d, tq, tk, tv, to, a, st);              \
   } while (0)
   if (d.D == 128) {
     if (d.causal) { if (d.out_f32) FM_F(128, true, true); else FM_F(128, true, false); }

@@ -46,6 +46,8 @@ struct Workspace {
   float* dkv_part;  // split-G backward: [gsplit][2][B, N, Hkv, d] fp32 dV / dK partials
   uint16_t* order;  // LPT unit order (K1d): forward [B, Hm, ceil(Tr/2)] pairs, backward [B, Hm, Tc] key
                     // tiles, then one flag per (b, hm) (0: near-uniform work, keep the default order)
+  float* kmax;      // forward: [B, Hkv, Tc] largest key norm per 128-key tile (K1e, R33)
+  uint8_t* fix;     // forward: [B, H, ceil(Tr/2)] units the bounded single pass could not finish (R33)
   size_t bytes;
 };
 
@@ -73,6 +75,12 @@ struct FwdArgs {
   // CTA -> (head, pair) map taking `hgrp` heads at a time; nullptr: last pairs first per head
   const uint16_t* order;
   int hgrp;
+  // R33 bounded single pass: [B, Hkv, Tc] largest key norm per key tile (K1e) and the per-unit
+  // flags it raises for rows it cannot finish (fix_out); the two-pass fixup launch runs only the
+  // flagged units (fix != nullptr)
+  const float* kmax;
+  uint8_t* fix_out;
+  const uint8_t* fix;
 };
 
 struct BwdArgs {
@@ -137,6 +145,7 @@ cudaError_t launch_bwd(const Dims& d, const CUtensorMap& tq, const CUtensorMap& 
                        const CUtensorMap& tdo, const CUtensorMap& tdq, const CUtensorMap& tdk, const CUtensorMap& tdv,
                        const BwdArgs& a, cudaStream_t st);
 cudaError_t launch_dq_convert(const Dims& d, const float* dqacc, void* dq, cudaStream_t st);
+cudaError_t launch_key_norms(const Dims& d, const void* k, float* kmax, uint8_t* fix, cudaStream_t st);
 // K7: dK = scale * sum_s dK_s, dV = sum_s dV_s over the split-G partials, converted to the out dtype
 cudaError_t launch_dkv_reduce(const Dims& d, int gsplit, const float* part, void* dk, void* dv, cudaStream_t st);
 cudaError_t launch_dq(const Dims& d, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,

@@ -908,6 +908,61 @@ cudaError_t launch_dkv_reduce(const Dims& d, int gsplit, const float* part, void
   return launch_pdl(k7_dkv_reduce<false, false>, dim3(blocks), dim3(256), 0, st, part, gsplit, total8, d.scale, dk, dv);
 }
 
+// ---------------------------------------------------------------------------------------
+// K1e (bounded single-pass forward, R33): largest key norm of every 128-key tile,
+// kmax[b, hk, j] = max_y ||k_y||_2 in fp32, rounded up by a relative 2^-16 for the bf16 -> fp32
+// sums; by Cauchy-Schwarz |q_r . k_y| <= ||q_r|| kmax.  Also zeroes the forward's fixup flags
+// (n_fix bytes).  One warp per 32 keys, D/8 lanes per key row (16-byte loads, coalesced).
+// Grid (Tc, Hkv, B), 128 threads.
+// ---------------------------------------------------------------------------------------
+template <int D>
+__global__ void __launch_bounds__(128) k1e_key_norms(const uint16_t* __restrict__ k, int N, int Hkv, int Tc,
+                                                     float* __restrict__ kmax, uint8_t* __restrict__ fix,
+                                                     long n_fix) {
+  pdl_wait();  // kmax / fix may still be read by an earlier forward sharing the workspace
+  pdl_launch();
+  constexpr int G = D / 8;     // 16-byte granules per key row
+  constexpr int KPI = 32 / G;  // keys per warp iteration
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int j = blockIdx.x, hk = blockIdx.y, b = blockIdx.z;
+  const long cta = (static_cast<long>(b) * Hkv + hk) * Tc + j;
+  for (long t = cta * 128 + threadIdx.x; t < n_fix; t += static_cast<long>(gridDim.x) * gridDim.y * gridDim.z * 128)
+    fix[t] = 0;
+  float best = 0.f;
+#pragma unroll 4
+  for (int it = 0; it < 32 / KPI; ++it) {
+    const int y = j * 128 + warp * 32 + it * KPI + lane / G;
+    float ss = 0.f;
+    if (y < N) {
+      const uint4 u = reinterpret_cast<const uint4*>(k + ((static_cast<size_t>(b) * N + y) * Hkv + hk) * D)[lane % G];
+      const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const float lo = __uint_as_float(w[t] << 16), hi = __uint_as_float(w[t] & 0xFFFF0000u);
+        ss = fmaf(lo, lo, fmaf(hi, hi, ss));
+      }
+    }
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    best = fmaxf(best, ss);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) best = fmaxf(best, __shfl_xor_sync(0xffffffffu, best, o));
+  __shared__ float wmax[4];
+  if (lane == 0) wmax[warp] = best;
+  __syncthreads();
+  if (threadIdx.x == 0)
+    kmax[cta] = sqrtf(fmaxf(fmaxf(wmax[0], wmax[1]), fmaxf(wmax[2], wmax[3]))) * (1.0f + 1.0f / 65536.0f);
+}
+
+cudaError_t launch_key_norms(const Dims& d, const void* k, float* kmax, uint8_t* fix, cudaStream_t st) {
+  dim3 grid(d.Tc, d.Hkv, d.B);
+  const long n_fix = static_cast<long>(d.B) * d.H * ((d.Tr + 1) / 2);
+  const uint16_t* kp = static_cast<const uint16_t*>(k);
+  if (d.D == 128) return launch_pdl(k1e_key_norms<128>, grid, dim3(128), 0, st, kp, d.N, d.Hkv, d.Tc, kmax, fix, n_fix);
+  return launch_pdl(k1e_key_norms<64>, grid, dim3(128), 0, st, kp, d.N, d.Hkv, d.Tc, kmax, fix, n_fix);
+}
+
 cudaError_t launch_dq_convert(const Dims& d, const float* dqacc, void* dq, cudaStream_t st) {
   const long total8 = static_cast<long>(d.B) * d.N * d.H * d.D / 8;
   const long blocks = (total8 + 255) / 256;

@@ -23,6 +23,8 @@ FM_FLAG_DETERMINISTIC = 2
 FM_FLAG_NO_REFINE = 4
 FM_FLAG_FWD_PAIR = 8
 FM_FLAG_ROWWISE = 16
+FM_FLAG_NO_MAX_BOUND = 32
+FM_FLAG_MAX_BOUND = 64
 FM_PASS_FWD, FM_PASS_BWD = 0, 1
 
 EXPORTED = ["flashmask_workspace_size", "flashmask_classify", "flashmask_refine", "flashmask_fwd", "flashmask_bwd",

@@ -46,6 +46,12 @@ cases = [
                                                     flags=fm.FM_FLAG_DETERMINISTIC)),
     ("pair forward causal_document", lambda: run(wm.sample_family("causal_document", 900, rng, (2, 5)), 2, 128,
                                                  flags=fm.FM_FLAG_FWD_PAIR)),
+    # R33 bounded single pass (K1e + single-pass K2a + two-pass fixup launch); qk_sparse has fully
+    # masked rows, so its units go through the fixup
+    ("bounded causal_document d128", lambda: run(wm.sample_family("causal_document", 1000, rng, (2, 5)), 2, 128,
+                                                 flags=fm.FM_FLAG_MAX_BOUND)),
+    ("bounded qk_sparse d64 fixup", lambda: run(wm.sample_family("qk_sparse", 640, rng, (2, 5)), 2, 64,
+                                                flags=fm.FM_FLAG_MAX_BOUND)),
     # 256 forward / 512 backward CTAs: the LPT order (K1d) is used
     ("lpt causal_document 4K x 16 heads", lambda: run(wm.sample_family("causal_document", 4096, rng, (3, 7)), 16, 128)),
 ]
@@ -57,7 +63,7 @@ for name, f in cases:
 if which in ("all", "chain"):
     ws = torch.empty(64 << 20, dtype=torch.uint8, device="cuda")
     ms = [wm.sample_family(f, 768, rng, (2, 5)) for f in ("causal_document", "sliding_window", "document")]
-    for m in ms + ms:
-        run(m, 2, 128, ws=ws)
+    for i, m in enumerate(ms + ms):
+        run(m, 2, 128, ws=ws, flags=fm.FM_FLAG_MAX_BOUND if i % 2 else 0)
     torch.cuda.synchronize()
     print("ok chain", flush=True)

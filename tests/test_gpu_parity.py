@@ -11,6 +11,7 @@ import torch
 
 from oracle import flashmask_oracle as fo
 from workloads import masks as wm
+from workloads import tensors as wt
 
 from gpu_util import assert_close, assert_lse, build_case, oracle_head, to_cuda
 
@@ -164,10 +165,13 @@ def test_fwd_bwd_parity(fmlib, fam, N, d, B, H):
 
 @pytest.mark.parametrize("fam,N,d", [("causal_document", 1000, 128), ("global_sliding_window", 768, 128),
                                      ("document", 640, 64), ("random_eviction", 512, 128)])
-def test_skip_equivalence_bitwise(fmlib, fam, N, d):
-    """§4.4: skipping fully masked tiles changes nothing, bit for bit."""
-    _, _, _, r0 = _run(fmlib, fam, N, d, 1, 2, seed=3)
-    _, _, _, r1 = _run(fmlib, fam, N, d, 1, 2, seed=3, flags=fmlib.FM_FLAG_NO_SKIP)
+@pytest.mark.parametrize("bounded", [False, True])
+def test_skip_equivalence_bitwise(fmlib, fam, N, d, bounded):
+    """§4.4: skipping fully masked tiles changes nothing, bit for bit — for the two-pass
+    forward and for the bounded single pass (R33, whose reference does not depend on the visit list)."""
+    extra = fmlib.FM_FLAG_MAX_BOUND if bounded else 0
+    _, _, _, r0 = _run(fmlib, fam, N, d, 1, 2, seed=3, flags=extra)
+    _, _, _, r1 = _run(fmlib, fam, N, d, 1, 2, seed=3, flags=fmlib.FM_FLAG_NO_SKIP | extra)
     for name, a, b in zip(("O", "lse", "dK", "dV"), (r0[0], r0[1], r0[3], r0[4]), (r1[0], r1[1], r1[3], r1[4])):
         assert torch.equal(a, b), name
 
@@ -765,3 +769,62 @@ def test_refine_forward_bitwise(fmlib, fam, N, d):
         O, L, _ = oracle_head(t, masks, sri.numpy(), 0, h, 1, masks[0].causal, with_grad=False)
         assert_close(f"O[{h}]", r0[0][0, :, h].cpu().numpy(), O)
         assert_lse(r0[1][0, h].cpu().numpy(), L)
+
+
+# ------------------------------------------------ R33 bounded single pass (K1e + K2a BND + fixup)
+def _aligned(N, H, d, seed):
+    """Q rows and keys along one direction with small noise: Cauchy-Schwarz is nearly tight, so
+    the fixed reference sits ~64 above the true row maximum (P up to ~2^64 before normalising)."""
+    g = torch.Generator().manual_seed(seed)
+    q = 0.05 * torch.randn(1, N, H, d, generator=g)
+    q[..., 0] = 12.0
+    k = 0.05 * torch.randn(1, N, H, d, generator=g)
+    k[..., 0] = 1.0 + torch.rand(1, N, H, generator=g)
+    v = torch.randn(1, N, H, d, generator=g)
+    do = torch.randn(1, N, H, d, generator=g)
+    return {n: x.to(torch.bfloat16) for n, x in (("q", q), ("k", k), ("v", v), ("do", do))}
+
+
+@pytest.mark.parametrize("fam,N,d", [("full", 1024, 128), ("full", 1000, 64), ("causal_document", 1024, 128),
+                                     ("document", 896, 64), ("qk_sparse", 1024, 128), ("random_eviction", 640, 128)])
+@pytest.mark.parametrize("inputs", ["unit", "aligned", "large_norm"])
+def test_bounded_single_pass(fmlib, fam, N, d, inputs):
+    """R33 (forced at small N with FM_FLAG_MAX_BOUND; the default from N = 16K, covered by
+    test_gpu_fullsize): with bf16 operands the forward computes every P of a row against one fixed reference
+    (the Cauchy-Schwarz bound of its logits minus 64) in a single pass per tile, and rows whose sum
+    ends below 2^-60 are recomputed by the two-pass kernel.  Against the oracle and against
+    FM_FLAG_NO_MAX_BOUND: unit-normal inputs (single pass), Q and K aligned (tight bound, P near
+    2^64), large norms (bound far too loose: every unit recomputed, so the result equals the
+    two-pass run bit for bit); qk_sparse has fully masked rows (recomputed: O = 0, lse = -inf)."""
+    rng = np.random.default_rng(N + d)
+    m = wm.sample_family(fam, N, rng, (2, 5))
+    H = 2
+    if inputs == "aligned":
+        t = _aligned(N, H, d, seed=d)
+    else:
+        t = wt.make_qkv(1, N, H, d, base=7)
+        if inputs == "large_norm":
+            t = {n: (x.float() * (4.0 if n in ("q", "k") else 1.0)).to(torch.bfloat16) for n, x in t.items()}
+    sri = torch.from_numpy(wm.stack([m]))
+    sri_c, tc = to_cuda(sri, t)
+    res = {}
+    for flags in (fmlib.FM_FLAG_MAX_BOUND, fmlib.FM_FLAG_NO_MAX_BOUND):
+        o, lse = fmlib.flashmask_fwd(tc["q"], tc["k"], tc["v"], sri_c, m.causal, out_dtype=torch.float32, flags=flags)
+        dq, dk, dv = fmlib.flashmask_bwd(tc["q"], tc["k"], tc["v"], o, tc["do"], lse, sri_c, m.causal,
+                                         out_dtype=torch.float32)
+        torch.cuda.synchronize()
+        res[flags] = (o, lse, dq, dk, dv)
+    vec = fo.expand(m.sri, m.causal, N)
+    for h in range(H):
+        f = lambda n: t[n][0, :, h, :].double().numpy()
+        O, L = fo.forward(f("q"), f("k"), f("v"), vec)
+        _, _, gv = fo.backward(f("q"), f("k"), f("v"), f("do"), vec)
+        for flags, (o, lse, dq, dk, dv) in res.items():
+            assert_close(f"{inputs} O[h{h}] flags={flags}", o[0, :, h].cpu().numpy(), O)
+            assert_lse(lse[0, h].cpu().numpy(), L)
+            assert_close(f"{inputs} dV[h{h}] flags={flags}", dv[0, :, h].cpu().numpy(), gv)
+    a, b = res[fmlib.FM_FLAG_MAX_BOUND], res[fmlib.FM_FLAG_NO_MAX_BOUND]
+    if inputs == "large_norm":
+        assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1])  # every unit went through the fixup
+    elif fam != "qk_sparse":
+        assert not torch.equal(a[0], b[0])  # the single pass ran (another reference, other rounding)
