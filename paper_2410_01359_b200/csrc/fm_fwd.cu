@@ -57,6 +57,9 @@ constexpr int MST = 4;
 // of every 8 column pairs, how many take the FMA-pipe polynomial exp2 (the rest MUFU ex2):
 // 1-3 of 8 change the forward by < 2 %
 constexpr int kPolyPairs = 3;
+// the bounded single pass (BND, R33) issues fewer instructions per tile: 2 of 8 measured best there
+// (in-process A/B vs 3: C3 +0.2 %, 32K causal +1.1 %, random eviction +1.8 %, d = 64 +1.5..2 %)
+constexpr int kPolyPairsBnd = 2;
 // f3: mask only the dirty 32 x 16 sub-blocks of PARTIAL tiles (K1c words).  Compiled into the
 // causal kernels only: in-process A/B measured +2..+6 % on causal families
 // (+24 % QK-sparse) but -1.3 % on the non-causal C3 kernel (code generation) and +-1.5 % elsewhere.
@@ -572,7 +575,7 @@ __global__ void __launch_bounds__(fwd::NT, 1)
             const int k = ch * 8 + kk;
             const uint64_t x2 = f2fma(f2pack(sv[2 * kk], sv[2 * kk + 1]), sl2x2, negm2);
             float p0, p1;
-            if ((k & 7) >= 8 - kPolyPairs) {
+            if ((k & 7) >= 8 - (BND ? kPolyPairsBnd : kPolyPairs)) {
               exp2_poly2(x2, p0, p1);
             } else {
               float x0, x1;
