@@ -129,7 +129,8 @@ __global__ void __launch_bounds__(fwd::NT, 1)
   const int npairs = (a.Tr + 1) >> 1;
   // ---------------- one unit of work: the query-tile pair `pair` of head h, batch entry b ----------------
   // first: this CTA's first unit (TMEM allocation and the grid-dependency wait happen here)
-  auto unit_body = [&](const int b, const int h, const int pair, const bool first) {
+  // reinit: an earlier unit of this CTA initialised the mbarriers (invalidate before re-initialising)
+  auto unit_body = [&](const int b, const int h, const int pair, const bool first, const bool reinit) {
     const size_t unit = (static_cast<size_t>(b) * a.H + h) * npairs + pair;
     const int hk = h / a.G;                      // key/value head of this query head (GQA)
     const int hm = (a.Hm == 1) ? 0 : hk;
@@ -140,7 +141,7 @@ __global__ void __launch_bounds__(fwd::NT, 1)
     if (tid == 0) FTE(0);
     // ---- setup: barriers (warp 8), TMEM (warp 9) ----
     if (warp == PRODUCER_WARP && lane == 0) {
-      if (!first) {  // persistent fixup: the previous unit's barriers are quiescent (end-of-unit sync)
+      if (reinit) {  // persistent fixup: the previous unit's barriers are quiescent (end-of-unit sync)
         mbar_inval(&sm.bar_q);
         for (int s = 0; s < KST; ++s) { mbar_inval(&sm.k_full[s]); mbar_inval(&sm.k_empty[s]); }
         for (int s = 0; s < VST; ++s) { mbar_inval(&sm.v_full[s]); mbar_inval(&sm.v_empty[s]); }
@@ -711,13 +712,12 @@ __global__ void __launch_bounds__(fwd::NT, 1)
           const int uu = static_cast<int>(blockIdx.x + static_cast<long>(gridDim.x) * (base + w * 32 + l));
           const int pr = uu % npairs, hb = uu / npairs;
           tc_fence_after();
-          unit_body(hb / a.H, hb % a.H, pr, false);
+          unit_body(hb / a.H, hb % a.H, pr, false, any);
           any = true;
         }
       }
       __syncthreads();  // fixbits is rewritten by the next chunk
     }
-    (void)any;
     tc_fence_after();
     if (warp == MMA_WARP) tmem_dealloc<512>(sm.tmem_base);
   } else {
@@ -740,7 +740,7 @@ __global__ void __launch_bounds__(fwd::NT, 1)
       pair = npairs - 1 - static_cast<int>(blockIdx.x);
       h = blockIdx.y;
     }
-    unit_body(b, h, pair, true);
+    unit_body(b, h, pair, true, false);
     if (warp == MMA_WARP) {
       tc_fence_after();
       tmem_dealloc<512>(sm.tmem_base);

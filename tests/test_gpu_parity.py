@@ -828,3 +828,47 @@ def test_bounded_single_pass(fmlib, fam, N, d, inputs):
         assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1])  # every unit went through the fixup
     elif fam != "qk_sparse":
         assert not torch.equal(a[0], b[0])  # the single pass ran (another reference, other rounding)
+
+
+def test_bounded_fixup_many_units_bitwise(fmlib):
+    """R33 persistent fixup: with norms far too large for the bound every unit is flagged, and the
+    one-wave fixup launch (one CTA per SM) runs 512 units, several per CTA with its mbarriers
+    re-initialised between units — O and lse equal the two-pass forward bit for bit."""
+    rng = np.random.default_rng(11)
+    N, H, d = 4096, 32, 128
+    m = wm.sample_family("causal_document", N, rng, (3, 7))
+    t = wt.make_qkv(1, N, H, d, base=13, with_do=False)
+    t = {n: (x.float() * 4.0 if n in ("q", "k") else x.float()).to(torch.bfloat16) for n, x in t.items()}
+    sri_c, tc = to_cuda(torch.from_numpy(wm.stack([m])), t)
+    res = []
+    for flags in (fmlib.FM_FLAG_MAX_BOUND, fmlib.FM_FLAG_NO_MAX_BOUND):
+        for out_dtype in (torch.float32, torch.bfloat16):
+            res.append(fmlib.flashmask_fwd(tc["q"], tc["k"], tc["v"], sri_c, m.causal, out_dtype=out_dtype, flags=flags))
+    torch.cuda.synchronize()
+    for a, b in ((res[0], res[2]), (res[1], res[3])):
+        assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1])
+
+
+@pytest.mark.parametrize("d,H,Hkv", [(128, 8, 2), (64, 4, 1)])
+def test_bounded_gqa_bf16_out(fmlib, d, H, Hkv):
+    """R33 with GQA (the key-norm bound of the shared kv head) and bf16 outputs, against the oracle
+    (bf16 output rounding added to the bar, R27)."""
+    rng = np.random.default_rng(d + H)
+    N = 1000
+    m = wm.sample_family("causal_document", N, rng, (2, 5))
+    q = wt.make_tensor("q", 1, N, H, d, base=3)
+    k = wt.make_tensor("k", 1, N, Hkv, d, base=3)
+    v = wt.make_tensor("v", 1, N, Hkv, d, base=3)
+    sri_c = torch.from_numpy(wm.stack([m])).cuda()
+    o, lse = fmlib.flashmask_fwd(q.cuda(), k.cuda(), v.cuda(), sri_c, m.causal, out_dtype=torch.bfloat16,
+                                 flags=fmlib.FM_FLAG_MAX_BOUND)
+    torch.cuda.synchronize()
+    vec = fo.expand(m.sri, m.causal, N)
+    G = H // Hkv
+    for h in range(H):
+        O, L = fo.forward(q[0, :, h].double().numpy(), k[0, :, h // G].double().numpy(),
+                          v[0, :, h // G].double().numpy(), vec)
+        got = o[0, :, h].float().cpu().double().numpy()
+        err = np.abs(got - O)
+        assert (err <= 2e-2 + np.abs(O) * 2.0 ** -8).all() and err.mean() <= 2e-3, (h, err.max(), err.mean())
+        assert_lse(lse[0, h].cpu().numpy(), L)
