@@ -91,7 +91,8 @@ enum {
   /* flashmask_fwd, head_dim 128: run the forward on CTA pairs (K2b, tcgen05 cta_group::2: each
    * SM holds one query tile and half of every K/V tile, three S accumulators in TMEM) instead of
    * the single-SM kernel K2a.  Same results to rounding order (every output within the parity
-   * tolerances of the single-SM kernel). */
+   * tolerances of the single-SM kernel); with bf16 operands it takes the bounded single pass of
+   * FM_FLAG_NO_MAX_BOUND's description under the same conditions as K2a. */
   FM_FLAG_FWD_PAIR = 8,
   /* Row-wise representation ("by transposing the attention matrix, we can obtain a row-wise
    * representation using column index intervals"; R32): startend_row_indices[b, hm, r, .]

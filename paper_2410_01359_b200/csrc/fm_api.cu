@@ -408,18 +408,10 @@ fm_status flashmask_fwd(const fm_params* p, const void* q, const void* k, const 
   a.kmax = nullptr;
   a.fix_out = nullptr;
   a.fix = nullptr;
-  if ((p->flags & FM_FLAG_FWD_PAIR) && d.D == 128 && !d.rowwise) {
-    CUtensorMap tk64;
-    if (!make_map(&tk64, k, d, d.Hkv, 64, &err)) return fail(FM_ERR_CUDA, err);
-    e = timed(FM_KERNEL_FWD, st, [&] { return fm::launch_fwd2(d, tq, tk64, tv, to, a, st); });
-    if (e != cudaSuccess) return cuda_fail(e, "forward kernel");
-    return FM_OK;
-  }
+  a.q = q;
   // R33 bounded single pass (bf16 operands): key norms per tile (K1e), the single-pass forward, then
-  // the two-pass forward over the units it flagged (CTAs of unflagged units exit at once).  Used from
-  // N = 16K: below, the fixup launch's waves of exiting CTAs (~1.5 us each, 215 KB of shared memory
-  // keep them one per SM) cost more than the single pass saves on the few tiles of a short unit
-  // (C2 -7..-9 %, R33)
+  // the persistent two-pass fixup over the units it flagged.  Used from N = 16K: on the few tiles of
+  // a short unit its per-CTA bound set-up does not pay (C2 -4..-6 % when forced)
   const bool bounded = !d.in_f16 && (p->flags & FM_FLAG_NO_MAX_BOUND) == 0 &&
                        (d.N >= 16384 || (p->flags & FM_FLAG_MAX_BOUND) != 0);
   if (bounded) {
@@ -428,7 +420,13 @@ fm_status flashmask_fwd(const fm_params* p, const void* q, const void* k, const 
     a.kmax = w.kmax;
     a.fix_out = w.fix;
   }
-  e = timed(FM_KERNEL_FWD, st, [&] { return fm::launch_fwd(d, tq, tk, tv, to, a, st); });
+  if ((p->flags & FM_FLAG_FWD_PAIR) && d.D == 128 && !d.rowwise) {
+    CUtensorMap tk64;
+    if (!make_map(&tk64, k, d, d.Hkv, 64, &err)) return fail(FM_ERR_CUDA, err);
+    e = timed(FM_KERNEL_FWD, st, [&] { return fm::launch_fwd2(d, tq, tk64, tv, to, a, st); });
+  } else {
+    e = timed(FM_KERNEL_FWD, st, [&] { return fm::launch_fwd(d, tq, tk, tv, to, a, st); });
+  }
   if (e != cudaSuccess) return cuda_fail(e, "forward kernel");
   if (bounded) {
     fm::FwdArgs f = a;

@@ -166,7 +166,7 @@ __global__ void __launch_bounds__(fwd::NT, 1)
       // Q does not depend on the visit list: start its load before the list is built
       tma_prefetch_desc(&tmQ);
       mbar_expect_tx(&sm.bar_q, has_q1 ? 2 * S::TILE : S::TILE);
-  #pragma unroll
+#pragma unroll
       for (int c = 0; c < D / 64; ++c) {
         tma_load_4d(sm.q[0] + c * 16384, &tmQ, &sm.bar_q, c * 64, h, i0 * 128, b);
         if (has_q1) tma_load_4d(sm.q[1] + c * 16384, &tmQ, &sm.bar_q, c * 64, h, i1 * 128, b);
@@ -213,7 +213,7 @@ __global__ void __launch_bounds__(fwd::NT, 1)
       }
       if (tid == 0) sm.n_entries = base;
       if constexpr (BND) {
-  #pragma unroll
+#pragma unroll
         for (int o = 16; o > 0; o >>= 1) kv = fmaxf(kv, __shfl_xor_sync(0xffffffffu, kv, o));
         if (lane == 0) sm.warp_kmax[warp] = kv;
       }
@@ -239,14 +239,14 @@ __global__ void __launch_bounds__(fwd::NT, 1)
           const int ks = e % KST, vs = e % VST, ms = e % MST;
           mbar_wait(&sm.k_empty[ks], ((e / KST) & 1) ^ 1);
           mbar_expect_tx(&sm.k_full[ks], TB);
-  #pragma unroll
+#pragma unroll
           for (int c = 0; c < D / 64; ++c) tma_load_4d(sm.k[ks] + c * 16384, &tmK, &sm.k_full[ks], c * 64, hk, j * 128, b);
           FT(11, e);
           mbar_wait(&sm.m_empty[ms], ((e / MST) & 1) ^ 1);
           if (!ROWW && (ent_cls(ent, 0) == 1 || ent_cls(ent, 1) == 1)) {
             // f3: which 32-row x 16-column sub-blocks hold a masked cell (K1c); the ragged last
             // column tile keeps every sub-block masked (its padded keys need the bounds mask)
-  #pragma unroll
+#pragma unroll
             for (int qq = 0; qq < 2; ++qq) {
               uint32_t wq = 0xFFFFFFFFu;
               if (kRefine<CAUSAL> && a.cw != nullptr && ent_cls(ent, qq) == 1 && !(j == a.Tc - 1 && (a.N & 127) != 0))
@@ -260,7 +260,7 @@ __global__ void __launch_bounds__(fwd::NT, 1)
           }
           mbar_wait(&sm.v_empty[vs], ((e / VST) & 1) ^ 1);
           mbar_expect_tx(&sm.v_full[vs], TB);
-  #pragma unroll
+#pragma unroll
           for (int c = 0; c < D / 64; ++c) tma_load_4d(sm.v[vs] + c * 16384, &tmV, &sm.v_full[vs], c * 64, hk, j * 128, b);
           FT(14, e);
         }
@@ -287,7 +287,7 @@ __global__ void __launch_bounds__(fwd::NT, 1)
           if (lane == 0 && q == 0) FT(15, pe);
           tc_fence_after();
           const uint32_t v_addr = smem_u32(sm.v[vs]);
-  #pragma unroll
+#pragma unroll
           for (int kk = 0; kk < 8; ++kk) {
             const uint64_t bd = sdesc_sw128(v_addr + kk * 2048, 16384, 1024);
             // P of keys [0,64) sits in S columns [0,32), of keys [64,128) in S columns [64,96);
@@ -315,14 +315,14 @@ __global__ void __launch_bounds__(fwd::NT, 1)
           if (lane == 0) FT(8, e);
           tc_fence_after();
           const uint32_t k_addr = smem_u32(sm.k[ks]);
-  #pragma unroll
+#pragma unroll
           for (int q = 0; q < 2; ++q) {
             if (!Layout<D>::SEP_P && pend[q] >= 0) issue_pv(q);
             if (ent_cls(ent, q) != 0) {
               // SEP_P: S_q(e) overwrites S_q(pend) once the softmax has read it (s_read)
               if (Layout<D>::SEP_P && pend[q] >= 0) mbar_wait(&sm.s_read[q], pv_cnt[q] & 1);
               tc_fence_after();
-  #pragma unroll
+#pragma unroll
               for (int kk = 0; kk < D / 16; ++kk) {
                 const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
                 mma_ss_w(tS[q], sdesc_sw128(q_addr[q] + off, 16, 1024), sdesc_sw128(k_addr + off, 16, 1024), ID_S,
@@ -340,7 +340,7 @@ __global__ void __launch_bounds__(fwd::NT, 1)
           }
           mma_commit_w(&sm.k_empty[ks]);
         }
-  #pragma unroll
+#pragma unroll
         for (int q = 0; q < 2; ++q) {  // O_q complete: its epilogue need not wait for the other tile
           // SEP_P: consume the last s_read phase too (already complete: P follows the read), so
           // every mbarrier phase is observed
@@ -382,7 +382,7 @@ __global__ void __launch_bounds__(fwd::NT, 1)
       float m_ref = 0.f;
       float kvis = 0.f;
       if constexpr (BND) {
-  #pragma unroll
+#pragma unroll
         for (int w = 0; w < NT / 32; ++w) kvis = fmaxf(kvis, sm.warp_kmax[w]);
       }
       for (int e = 0; e < nE; ++e) {
@@ -403,14 +403,15 @@ __global__ void __launch_bounds__(fwd::NT, 1)
             if (cnt == 0) {
               // ||q_r|| from the Q tile in shared memory: granule g ^ (row & 7) of the 128-byte
               // swizzled row, so the 8 rows of a bank group read 8 different 16-byte columns
+              mbar_wait(&sm.bar_q, 0);  // observe the TMA write of Q (complete long since: S used it)
               float ss = 0.f;
-  #pragma unroll
+#pragma unroll
               for (int c = 0; c < D / 64; ++c) {
-  #pragma unroll
+#pragma unroll
                 for (int g = 0; g < 8; ++g) {
                   const uint4 u = *reinterpret_cast<const uint4*>(sm.q[q] + c * 16384 + row_t * 128 + ((g ^ (row_t & 7)) << 4));
                   const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
-  #pragma unroll
+#pragma unroll
                   for (int t = 0; t < 4; ++t) {
                     const float lo = __uint_as_float(w4[t] << 16), hi = __uint_as_float(w4[t] & 0xFFFF0000u);
                     ss = fmaf(lo, lo, fmaf(hi, hi, ss));
@@ -429,7 +430,7 @@ __global__ void __launch_bounds__(fwd::NT, 1)
           // written back to TMEM, so pass 2 is identical for PARTIAL and UNMASKED tiles.
           float mx0 = -INFINITY, mx1 = -INFINITY, mx2 = -INFINITY, mx3 = -INFINITY;
           tmem_ld16(tSh, sr[0]);
-  #pragma unroll
+#pragma unroll
           for (int c = 0; c < 4; ++c) {
             tmem_wait_ld();
             if (c + 1 < 4) tmem_ld16(tSh + (c + 1) * 16, sr[(c + 1) & 1]);
@@ -442,7 +443,7 @@ __global__ void __launch_bounds__(fwd::NT, 1)
               if constexpr (ROWW) {
                 // key y = row - rmy + t is masked for this row iff it lies in one of the row's key
                 // intervals, after the row (causal), or past N (the ragged last column tile)
-  #pragma unroll
+#pragma unroll
                 for (int t = 0; t < 16; ++t) {
                   const int y = row - rmy + t;
                   bool msk = (static_cast<unsigned>(y - rmv.x) < static_cast<unsigned>(rmv.y)) ||
@@ -453,14 +454,14 @@ __global__ void __launch_bounds__(fwd::NT, 1)
               } else if (CAUSAL && j < (q == 0 ? i0 : i1)) {
                 // causal: below the diagonal tile (j < i) no key of the tile lies after any of its
                 // rows, so the r < y test is dropped there (warp-uniform choice)
-  #pragma unroll
+#pragma unroll
                 for (int t = 0; t < 16; ++t) {
                   const int4 mv = mk[t];
                   const bool msk = static_cast<unsigned>(row - mv.x) < static_cast<unsigned>(mv.y);
                   sv[t] = msk ? -INFINITY : sv[t];
                 }
               } else {
-  #pragma unroll
+#pragma unroll
                 for (int t = 0; t < 16; ++t) {
                   const int4 mv = mk[t];
                   bool msk = static_cast<unsigned>(row - mv.x) < static_cast<unsigned>(mv.y);
@@ -473,7 +474,7 @@ __global__ void __launch_bounds__(fwd::NT, 1)
               }
               tmem_st16(tSh + c * 16, sr[c & 1]);  // masked S back to TMEM: pass 2 needs no mask work
             }
-  #pragma unroll
+#pragma unroll
             for (int t = 0; t < 16; t += 8) {
               mx0 = fmax3(mx0, sv[t], sv[t + 1]);
               mx1 = fmax3(mx1, sv[t + 2], sv[t + 3]);
@@ -503,12 +504,12 @@ __global__ void __launch_bounds__(fwd::NT, 1)
             tc_fence_after();
           }
           if (__any_sync(0xffffffffu, need) && cnt > 0) {
-  #pragma unroll 1
+#pragma unroll 1
             for (int c = 0; c < D / 64; ++c) {
               uint32_t ov[32];
               tmem_ld32(tOh + c * 32, ov);
               tmem_wait_ld();
-  #pragma unroll
+#pragma unroll
               for (int t = 0; t < 32; ++t) ov[t] = __float_as_uint(__uint_as_float(ov[t]) * alpha);
               tmem_st32(tOh + c * 32, ov);
             }
@@ -521,7 +522,7 @@ __global__ void __launch_bounds__(fwd::NT, 1)
           const uint64_t sl2x2 = f2pack(sl2, sl2), negm2 = f2pack(-m_use, -m_use);
           uint64_t acc[4] = {0ull, 0ull, 0ull, 0ull};
           tmem_ld16(tSh, sr[0]);
-  #pragma unroll
+#pragma unroll
           for (int ch = 0; ch < 4; ++ch) {
             tmem_wait_ld();
             if (ch + 1 < 4) tmem_ld16(tSh + (ch + 1) * 16, sr[(ch + 1) & 1]);
@@ -535,7 +536,7 @@ __global__ void __launch_bounds__(fwd::NT, 1)
               const int4* mk = sm.mask[ms] + hh * 64 + ch * 16;
               const int rmy = row - (j * 128 + hh * 64 + ch * 16);
               if constexpr (ROWW) {
-  #pragma unroll
+#pragma unroll
                 for (int t = 0; t < 16; ++t) {
                   const int y = row - rmy + t;
                   bool msk = (static_cast<unsigned>(y - rmv.x) < static_cast<unsigned>(rmv.y)) ||
@@ -544,13 +545,13 @@ __global__ void __launch_bounds__(fwd::NT, 1)
                   sv[t] = msk ? -INFINITY : sv[t];
                 }
               } else if (CAUSAL && j < (q == 0 ? i0 : i1)) {
-  #pragma unroll
+#pragma unroll
                 for (int t = 0; t < 16; ++t) {
                   const int4 mv = mk[t];
                   sv[t] = static_cast<unsigned>(row - mv.x) < static_cast<unsigned>(mv.y) ? -INFINITY : sv[t];
                 }
               } else {
-  #pragma unroll
+#pragma unroll
                 for (int t = 0; t < 16; ++t) {
                   const int4 mv = mk[t];
                   bool msk = static_cast<unsigned>(row - mv.x) < static_cast<unsigned>(mv.y);
@@ -563,7 +564,7 @@ __global__ void __launch_bounds__(fwd::NT, 1)
               }
             }
             uint32_t pk[8];
-  #pragma unroll
+#pragma unroll
             for (int kk = 0; kk < 8; ++kk) {
               const int k = ch * 8 + kk;
               const uint64_t x2 = f2fma(f2pack(sv[2 * kk], sv[2 * kk + 1]), sl2x2, negm2);
@@ -625,7 +626,7 @@ __global__ void __launch_bounds__(fwd::NT, 1)
         // S MMAs completed before o_full.  Rows >= N are clipped by the TMA unit.
         uint8_t* stg = sm.q[q];
         mbar_wait(&sm.bar_q, 0);  // the Q load into this buffer has landed (even if no tile used it)
-  #pragma unroll
+#pragma unroll
         for (int c = 0; c < D / 64; ++c) {
           uint32_t ov[32];
           if (cnt > 0) {
@@ -634,10 +635,10 @@ __global__ void __launch_bounds__(fwd::NT, 1)
           }
           const int col = hh * (D / 2) + c * 32;  // first of these 32 columns
           uint8_t* blk = stg + (col / 64) * 16384 + row_t * 128;
-  #pragma unroll
+#pragma unroll
           for (int t = 0; t < 4; ++t) {
             float f[8];
-  #pragma unroll
+#pragma unroll
             for (int u = 0; u < 8; ++u) f[u] = live ? __uint_as_float(ov[8 * t + u]) * inv : 0.f;
             const int chunk = (col % 64) / 8 + t;
             *reinterpret_cast<uint4*>(blk + ((chunk ^ (row_t & 7)) << 4)) =
@@ -648,13 +649,13 @@ __global__ void __launch_bounds__(fwd::NT, 1)
         named_bar_sync(9 + q, 256);
         const int row0 = (q == 0 ? i0 : i1) * 128;
         if (warp == q * 8 && lane == 0 && row0 < a.N) {
-  #pragma unroll
+#pragma unroll
           for (int c = 0; c < D / 64; ++c) tma_store_4d(&tmO, stg + c * 16384, c * 64, h, row0, b);
           bulk_commit();
           bulk_wait_read0();  // the staging buffer must outlive the TMA reads
         }
       }
-  #pragma unroll 1
+#pragma unroll 1
       for (int c = 0; c < (OUT_F32 ? D / 64 : 0); ++c) {
         uint32_t ov[32];
         if (cnt > 0) {  // WG-uniform: the tcgen05.ld stays warp-collective
@@ -662,16 +663,16 @@ __global__ void __launch_bounds__(fwd::NT, 1)
           tmem_wait_ld();
         }
         float f[32];
-  #pragma unroll
+#pragma unroll
         for (int t = 0; t < 32; ++t) f[t] = live ? __uint_as_float(ov[t]) * inv : 0.f;
         if (row < a.N) {
           if constexpr (OUT_F32) {
             float4* dst = reinterpret_cast<float4*>(static_cast<float*>(a.o) + orow + c * 32);
-  #pragma unroll
+#pragma unroll
             for (int t = 0; t < 8; ++t) dst[t] = make_float4(f[4 * t], f[4 * t + 1], f[4 * t + 2], f[4 * t + 3]);
           } else {
             uint4* dst = reinterpret_cast<uint4*>(static_cast<uint16_t*>(a.o) + orow + c * 32);
-  #pragma unroll
+#pragma unroll
             for (int t = 0; t < 4; ++t)
               dst[t] = make_uint4(pack16<F16>(f[8 * t], f[8 * t + 1]), pack16<F16>(f[8 * t + 2], f[8 * t + 3]),
                                   pack16<F16>(f[8 * t + 4], f[8 * t + 5]), pack16<F16>(f[8 * t + 6], f[8 * t + 7]));

@@ -106,13 +106,17 @@ struct Smem {
   uint32_t tmem_base;
   int n_entries;
   int warp_cnt[NT / 32];
+  float warp_kmax[NT / 32];  // BND: largest key norm of the head, per warp's share of the column tiles
 };
 
 __device__ __forceinline__ int ent_cls(uint32_t ent, int q) { return (ent >> (24 + 2 * q)) & 3; }
 
 }  // namespace fwd2
 
-template <bool CAUSAL, bool OUT_F32, bool F16>
+// BND (R33): the bounded single pass of K2a on the CTA pair — every P of a row against the fixed
+// reference ||q_r|| max||k|| scale log2(e) - 64: no max pass, no max chain between the warpsets, no O
+// rescale; rows whose sum ends below 2^-60 flag the unit for K2a's two-pass fixup launch.
+template <bool CAUSAL, bool OUT_F32, bool F16, bool BND>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fwd2::NT, 1)
     fm_fwd2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK64,
                    const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmO, const FwdArgs a) {
@@ -168,6 +172,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fwd2::NT, 1)
     const uint8_t* row1 = row0 + a.Tc;
     const bool has_q1 = i1 < a.Tr;
     int base = 0;
+    float kv = 0.f;  // BND: largest key norm of the kv head over all its column tiles
+    const float* kmax_bh = BND ? a.kmax + (static_cast<size_t>(b) * (a.H / a.G) + hk) * a.Tc : nullptr;
     for (int j0 = 0; j0 < a.Tc; j0 += NT) {
       const int j = j0 + tid;
       uint32_t c0 = 0, c1 = 0;
@@ -187,10 +193,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fwd2::NT, 1)
       }
       off += __popc(bal & ((1u << lane) - 1u));
       if (vis) sm.list[off] = static_cast<uint32_t>(j) | (c0 << 24) | (c1 << 26);
+      if (BND && j < a.Tc) kv = fmaxf(kv, __ldg(kmax_bh + j));
       base += tot;
       __syncthreads();
     }
     if (tid == 0) sm.n_entries = base;
+    if constexpr (BND) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) kv = fmaxf(kv, __shfl_xor_sync(0xffffffffu, kv, o));
+      if (lane == 0) sm.warp_kmax[warp] = kv;
+    }
   }
   tc_fence_before();
   __syncthreads();
@@ -315,6 +327,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fwd2::NT, 1)
     const uint32_t p_full_lead = mapa_shared(&sm.p_full[0], 0);
     float m_ref = -INFINITY;  // the running max this thread's row-sum share is relative to
     float l = 0.f;
+    if constexpr (BND) {
+      // R33 fixed reference: ||q_r|| (this row of Q, read from global memory: L2-resident, once per
+      // CTA) * the head's largest key norm * scale * log2(e) - 64
+      float kvis = 0.f;
+#pragma unroll
+      for (int w = 0; w < NT / 32; ++w) kvis = fmaxf(kvis, sm.warp_kmax[w]);
+      float ss = 0.f;
+      if (row < a.N) {
+        const uint4* qr = reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(a.q) +
+                                                         ((static_cast<size_t>(b) * a.N + row) * a.H + h) * D);
+#pragma unroll 4
+        for (int g = 0; g < D / 8; ++g) {
+          const uint4 u4 = __ldg(qr + g);
+          const uint32_t w4[4] = {u4.x, u4.y, u4.z, u4.w};
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            const float lo = __uint_as_float(w4[t] << 16), hi = __uint_as_float(w4[t] & 0xFFFF0000u);
+            ss = fmaf(lo, lo, fmaf(hi, hi, ss));
+          }
+        }
+      }
+      m_ref = sqrtf(ss) * (1.0f + 1.0f / 65536.0f) * kvis * sl2 - 64.0f;
+    }
     for (int e = W, u = 0; e < nE; e += 2, ++u) {
       const uint32_t ent = sm.list[e];
       const int cls = ent_cls(ent, rank);
@@ -327,10 +362,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fwd2::NT, 1)
       if (tr0) FT2P(14, e);
       if (tr0) FT2G(9, e);
       tc_fence_after();
+      uint32_t sr[2][16];
+      float m_cur = m_ref;
+      if constexpr (!BND) {
       // Pass 1: max over this half's 64 columns (Alg. 1 line 22), element mask of lines 15-21 on
       // PARTIAL tiles written back to TMEM, 16 columns at a time
       float mx0 = -INFINITY, mx1 = -INFINITY, mx2 = -INFINITY, mx3 = -INFINITY;
-      uint32_t sr[2][16];
       if (cls != 0) {
         const int j = static_cast<int>(ent & 0xFFFFFFu);
         const uint32_t pm = (cls != 1) ? 0u : (kRefine<CAUSAL> ? (sm.cw[ms] >> (wl * 8 + hh * 4)) & 0xFu : 0xFu);
@@ -390,7 +427,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fwd2::NT, 1)
       }
       if (tr0) FT2(7, e);
       const bool need = m_tile > m_prev + 8.0f;
-      const float m_cur = need ? m_tile : m_prev;
+      m_cur = need ? m_tile : m_prev;
       if (e + 1 < nE) {
         // each thread publishes (hh = 0) / releases (hh = 1) its own row: its arrive orders its own
         // accesses (also for compute-sanitizer racecheck, which does not follow warp-sync chains)
@@ -419,9 +456,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fwd2::NT, 1)
         l = (l == 0.f) ? 0.f : l * ex2(m_ref - m_cur);
         m_ref = m_cur;
       }
+      }  // two-pass (!BND)
       // Pass 2: P = exp2(S*scale*log2e - m) (Alg. 1 line 24), packed into the first 32 of this
       // half's S columns; row-sum share (line 25)
       if (cls != 0) {
+        const int j = static_cast<int>(ent & 0xFFFFFFu);
+        const uint32_t pm =
+            (!BND || cls != 1) ? 0u : (kRefine<CAUSAL> ? (sm.cw[ms] >> (wl * 8 + hh * 4)) & 0xFu : 0xFu);
         const float m_use = (m_cur == -INFINITY) ? 0.f : m_cur;
         const uint64_t sl2x2 = f2pack(sl2, sl2), negm2 = f2pack(-m_use, -m_use);
         uint64_t acc[4] = {0ull, 0ull, 0ull, 0ull};
@@ -430,14 +471,37 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fwd2::NT, 1)
         for (int ch = 0; ch < 4; ++ch) {
           tmem_wait_ld();
           if (ch + 1 < 4) tmem_ld16(tSh + (ch + 1) * 16, sr[(ch + 1) & 1]);
-          const float* sv = reinterpret_cast<const float*>(sr[ch & 1]);
+          float* sv = reinterpret_cast<float*>(sr[ch & 1]);
+          if (BND && (pm & (1u << ch))) {
+            // element mask of Alg. 1 lines 15-21 in registers (no max pass to carry it to TMEM)
+            const int4* mk = sm.mask[ms] + hh * 64 + ch * 16;
+            const int rmy = row - (j * 128 + hh * 64 + ch * 16);
+            if (CAUSAL && j < my_i) {
+#pragma unroll
+              for (int t = 0; t < 16; ++t) {
+                const int4 mv = mk[t];
+                sv[t] = static_cast<unsigned>(row - mv.x) < static_cast<unsigned>(mv.y) ? -INFINITY : sv[t];
+              }
+            } else {
+#pragma unroll
+              for (int t = 0; t < 16; ++t) {
+                const int4 mv = mk[t];
+                bool msk = static_cast<unsigned>(row - mv.x) < static_cast<unsigned>(mv.y);
+                if constexpr (CAUSAL)
+                  msk |= rmy < t;
+                else
+                  msk |= static_cast<unsigned>(row - mv.z) < static_cast<unsigned>(mv.w);
+                sv[t] = msk ? -INFINITY : sv[t];
+              }
+            }
+          }
           uint32_t pk[8];
 #pragma unroll
           for (int kk = 0; kk < 8; ++kk) {
             const int k = ch * 8 + kk;
             const uint64_t x2 = f2fma(f2pack(sv[2 * kk], sv[2 * kk + 1]), sl2x2, negm2);
             float p0, p1;
-            if ((k & 7) >= 8 - kPolyPairs) {
+            if ((k & 7) >= 8 - (BND ? 2 : kPolyPairs)) {
               exp2_poly2(x2, p0, p1);
             } else {
               float x0, x1;
@@ -463,6 +527,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fwd2::NT, 1)
         tmem_st16(tSh + 16, z);
       }
       tmem_wait_st();
+      if constexpr (BND) {  // the mask slice of stage ms was read by this pass
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sm.m_empty[ms]);
+      }
       if (tr0) FT2(8, e);
       if (tr0) FT2P(15, e);
       if (tr0) FT2G(10, e);
@@ -481,15 +549,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fwd2::NT, 1)
     sm.xm[W][hh][row_t] = m_ref;
     named_bar_sync(9, 512);
     float m_fin = -INFINITY;
-#pragma unroll
-    for (int x = 0; x < 4; ++x) m_fin = fmaxf(m_fin, sm.xm[x >> 1][x & 1][row_t]);
     float lt = 0.f;
+    if constexpr (BND) {  // one reference for the whole row
+      m_fin = m_ref;
 #pragma unroll
-    for (int x = 0; x < 4; ++x) {
-      const float lx = sm.xl[x >> 1][x & 1][row_t];
-      if (lx > 0.f) lt += lx * ex2(sm.xm[x >> 1][x & 1][row_t] - m_fin);
+      for (int x = 0; x < 4; ++x) lt += sm.xl[x >> 1][x & 1][row_t];
+    } else {
+#pragma unroll
+      for (int x = 0; x < 4; ++x) m_fin = fmaxf(m_fin, sm.xm[x >> 1][x & 1][row_t]);
+#pragma unroll
+      for (int x = 0; x < 4; ++x) {
+        const float lx = sm.xl[x >> 1][x & 1][row_t];
+        if (lx > 0.f) lt += lx * ex2(sm.xm[x >> 1][x & 1][row_t] - m_fin);
+      }
     }
-    const bool live = lt > 0.f;
+    // BND: a row whose sum ends below 2^-60 flags the unit for the two-pass fixup launch
+    const bool live = BND ? (nE > 0 && lt >= 0x1p-60f) : lt > 0.f;
+    if (BND && row < a.N && !live) a.fix_out[(static_cast<size_t>(b) * a.H + h) * npairs + pair] = 1;
     const float inv = live ? 1.0f / lt : 0.f;
     mbar_wait(&sm.o_full, 0);  // every MMA of the pair done (or, with no MMA, both Q tiles landed)
     tc_fence_after();
@@ -542,10 +618,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fwd2::NT, 1)
   if (tid == 0) FTE2(5);
 }
 
-template <bool CAUSAL, bool OUT_F32, bool F16>
+template <bool CAUSAL, bool OUT_F32, bool F16, bool BND>
 static cudaError_t launch_fwd2_t(const Dims& d, const CUtensorMap& tq, const CUtensorMap& tk64, const CUtensorMap& tv,
                                  const CUtensorMap& to, const FwdArgs& a, cudaStream_t st) {
-  auto kern = fm_fwd2_kernel<CAUSAL, OUT_F32, F16>;
+  auto kern = fm_fwd2_kernel<CAUSAL, OUT_F32, F16, BND>;
   const size_t smem = sizeof(fwd2::Smem) + 1024;
   static_assert(sizeof(fwd2::Smem) + 1024 <= 232448, "shared memory budget");
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
@@ -557,8 +633,12 @@ static cudaError_t launch_fwd2_t(const Dims& d, const CUtensorMap& tq, const CUt
 cudaError_t launch_fwd2(const Dims& d, const CUtensorMap& tq, const CUtensorMap& tk64, const CUtensorMap& tv,
                         const CUtensorMap& to, const FwdArgs& a, cudaStream_t st) {
   if (d.D != 128) return cudaErrorInvalidValue;
-#define FM_F2(CC, FF) \
-  return d.in_f16 ? launch_fwd2_t<CC, FF, true>(d, tq, tk64, tv, to, a, st) : launch_fwd2_t<CC, FF, false>(d, tq, tk64, tv, to, a, st)
+#define FM_F2(CC, FF)                                                                                    \
+  do {                                                                                                   \
+    if (a.kmax != nullptr && !d.in_f16) return launch_fwd2_t<CC, FF, false, true>(d, tq, tk64, tv, to, a, st); \
+    return d.in_f16 ? launch_fwd2_t<CC, FF, true, false>(d, tq, tk64, tv, to, a, st)                       \
+                    : launch_fwd2_t<CC, FF, false, false>(d, tq, tk64, tv, to, a, st);                     \
+  } while (0)
   if (d.causal) {
     if (d.out_f32) FM_F2(true, true); else FM_F2(true, false);
   } else {

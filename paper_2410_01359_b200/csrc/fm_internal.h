@@ -81,6 +81,7 @@ struct FwdArgs {
   const float* kmax;
   uint8_t* fix_out;
   const uint8_t* fix;
+  const void* q;  // Q itself (K2b's bounded pass reads ||q_r|| from it)
 };
 
 struct BwdArgs {

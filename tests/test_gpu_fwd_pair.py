@@ -117,3 +117,32 @@ def test_pair_forward_gqa(fmlib, fam, N, H, Hkv, per_kv):
         O, L = fo.forward(f(t["q"], h), f(t["k"], hk), f(t["v"], hk), vec)
         assert_close(f"O {fam} [{h}]", o2[0, :, h].cpu().numpy(), O)
         assert_lse(l2[0, h].cpu().numpy(), L)
+
+
+@pytest.mark.parametrize("fam,N", [("causal_document", 1000), ("document", 700), ("random_eviction", 1000),
+                                   ("qk_sparse", 1536), ("full", 129)])
+@pytest.mark.parametrize("scale_qk", [1.0, 4.0])
+def test_pair_bounded_single_pass(fmlib, fam, N, scale_qk):
+    """R33 on the CTA pair (FM_FLAG_FWD_PAIR | FM_FLAG_MAX_BOUND): against the oracle; with Q, K
+    scaled by 4 the bound is far too loose, every unit goes through K2a's two-pass fixup and the
+    result equals the single-SM two-pass forward bit for bit."""
+    masks, sri, t = _inputs(fam, N, 2, 2, 2, seed=5)
+    if scale_qk != 1.0:
+        t = {n: (x.float() * (scale_qk if n in ("q", "k") else 1.0)).to(torch.bfloat16) for n, x in t.items()}
+    sri_c, tc = to_cuda(sri, t)
+    causal = masks[0].causal
+    flags = fmlib.FM_FLAG_FWD_PAIR | fmlib.FM_FLAG_MAX_BOUND
+    o, lse = fmlib.flashmask_fwd(tc["q"], tc["k"], tc["v"], sri_c, causal, out_dtype=torch.float32, flags=flags)
+    o2, lse2 = fmlib.flashmask_fwd(tc["q"], tc["k"], tc["v"], sri_c, causal, out_dtype=torch.float32,
+                                   flags=fmlib.FM_FLAG_NO_MAX_BOUND)
+    torch.cuda.synchronize()
+    if scale_qk != 1.0:
+        assert torch.equal(o, o2) and torch.equal(lse, lse2)
+    sri_np = sri.numpy()
+    for b in range(2):
+        vec = fo.expand(sri_np[b, 0], causal, N)
+        for h in range(2):
+            f = lambda n: t[n][b, :, h, :].double().numpy()
+            O, L = fo.forward(f("q"), f("k"), f("v"), vec)
+            assert_close(f"O[{b},{h}]", o[b, :, h].cpu().numpy(), O)
+            assert_lse(lse[b, h].cpu().numpy(), L)
