@@ -207,3 +207,14 @@ def test_rowwise_full_size_sampled(fmlib, fam):
         gk, gv = fo.backward_cols(f(x["q"], h), f(x["k"], h), f(x["v"], h), f(x["do"], h), vec, keys)
         assert_close(f"dK {fam}[{h}]", dk[0, keys, h].cpu().numpy(), gk)
         assert_close(f"dV {fam}[{h}]", dv[0, keys, h].cpu().numpy(), gv)
+
+
+@pytest.mark.parametrize("fam,N,d", [(fam, 700, 128) for fam in wm.ROWWISE_FAMILIES] + [("causal_document", 515, 64),
+                                                                                      ("key_window", 700, 64)])
+def test_rowwise_bounded_single_pass(fmlib, fam, N, d):
+    """R33 bounded single pass (forced with FM_FLAG_MAX_BOUND at small N) on row-wise masks: the
+    element mask of PARTIAL tiles comes from the thread's own row vector inside the single pass."""
+    rng = np.random.default_rng(N + d + len(fam) + 1)
+    masks = [wm.rw_sample_family(fam, N, rng, (1, 5)) for _ in range(2)]
+    _check(fmlib, masks, 2, 2, d, flags=fmlib.FM_FLAG_MAX_BOUND, seed=N + 3)
+    _check(fmlib, masks[:1], 4, 2, d, flags=fmlib.FM_FLAG_MAX_BOUND, seed=N + 4)  # GQA
