@@ -105,7 +105,7 @@ enum {
    * Accepted by every entry point; FM_FLAG_FWD_PAIR is ignored with it (single-SM forward). */
   FM_FLAG_ROWWISE = 16,
   /* flashmask_fwd: always take each visited tile's row maximum before its exponentials (Alg. 1
-   * line 242).  By default, with bf16 operands and seqlen >= 16384, the single-SM
+   * line 242).  By default, with bf16 operands, column-wise masks and seqlen >= 16384, the single-SM
    * forward instead computes every P of a row against one fixed reference
    * m_r = ||q_r|| max_y ||k_y|| scale log2(e) - 64 (Cauchy-Schwarz bound of the row's logits; key
    * norms from one extra pass over K): no row maximum, no rescaling, one pass per tile; rows whose sum ends below

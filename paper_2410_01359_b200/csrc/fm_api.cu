@@ -412,8 +412,10 @@ fm_status flashmask_fwd(const fm_params* p, const void* q, const void* k, const 
   // R33 bounded single pass (bf16 operands): key norms per tile (K1e), the single-pass forward, then
   // the persistent two-pass fixup over the units it flagged.  Used from N = 16K: on the few tiles of
   // a short unit its per-CTA bound set-up does not pay (C2 -4..-6 % when forced)
+  // (column-wise masks only by default: row-wise ones keep the two-pass forward unless forced, see R33
+  // on the precision of rows dominated by one key)
   const bool bounded = !d.in_f16 && (p->flags & FM_FLAG_NO_MAX_BOUND) == 0 &&
-                       (d.N >= 16384 || (p->flags & FM_FLAG_MAX_BOUND) != 0);
+                       ((d.N >= 16384 && !d.rowwise) || (p->flags & FM_FLAG_MAX_BOUND) != 0);
   if (bounded) {
     e = timed(FM_KERNEL_EXPAND, st, [&] { return fm::launch_key_norms(d, k, w.kmax, w.fix, st); });
     if (e != cudaSuccess) return cuda_fail(e, "key norms");
