@@ -107,9 +107,9 @@ enum {
   /* flashmask_fwd: always take each visited tile's row maximum before its exponentials (Alg. 1
    * line 242).  By default, with bf16 operands, column-wise masks and seqlen >= 16384, the single-SM
    * forward instead computes every P of a row against one fixed reference
-   * m_r = ||q_r|| max_y ||k_y|| scale log2(e) - 64 (Cauchy-Schwarz bound of the row's logits; key
+   * m_r = ||q_r|| max_y ||k_y|| scale log2(e) - 96 (Cauchy-Schwarz bound of the row's logits; key
    * norms from one extra pass over K): no row maximum, no rescaling, one pass per tile; rows whose sum ends below
-   * 2^-60 (bound too loose, or every key masked) are recomputed by the two-pass kernel
+   * 2^-90 (bound too loose, or every key masked) are recomputed by the two-pass kernel
    * (R33).  Same outputs to rounding (parity tolerances). */
   FM_FLAG_NO_MAX_BOUND = 32,
   /* Testing: use the bounded single pass of FM_FLAG_NO_MAX_BOUND's description at any seqlen (bf16

@@ -112,7 +112,7 @@ __device__ __forceinline__ int ent_cls(uint32_t ent, int q) { return (ent >> (24
 // ROW's masked key intervals; a softmax thread (= one row) keeps its own in registers and no mask
 // slice is loaded per tile.
 // BND: R33 bounded single pass (bf16 operands): P of every tile against the fixed per-row reference
-// ||q_r|| max_y ||k_y|| scale log2(e) - 64, no max pass, no rescaling; unfinished rows flag the
+// ||q_r|| max_y ||k_y|| scale log2(e) - 96, no max pass, no rescaling; unfinished rows flag the
 // unit for the two-pass fixup launch (this kernel with BND = false and a.fix set).
 // FIX: the persistent two-pass fixup launch over the units a bounded pass flagged (BND = false).
 template <int D, bool CAUSAL, bool OUT_F32, bool F16, bool ROWW, bool BND, bool FIX>
@@ -377,8 +377,8 @@ __global__ void __launch_bounds__(fwd::NT, 1)
       // K1a's padding value: every key masked)
       if constexpr (ROWW)
         rmv = row < a.N ? a.vec4[bhm * static_cast<size_t>(a.Tc) * 128 + row] : make_int4(0, INT_MAX, 0, 0);
-      // R33 (BND): the row's fixed reference, ||q_r|| * max key norm of the head * scale * log2(e) - 64,
-      // so every P <= 2^64; set at the first visited tile (Q has landed once S has)
+      // R33 (BND): the row's fixed reference, ||q_r|| * max key norm of the head * scale * log2(e) - 96,
+      // so every P <= 2^96; set at the first visited tile (Q has landed once S has)
       float m_ref = 0.f;
       float kvis = 0.f;
       if constexpr (BND) {
@@ -418,7 +418,7 @@ __global__ void __launch_bounds__(fwd::NT, 1)
                   }
                 }
               }
-              m_ref = sqrtf(ss) * (1.0f + 1.0f / 65536.0f) * kvis * sl2 - 64.0f;
+              m_ref = sqrtf(ss) * (1.0f + 1.0f / 65536.0f) * kvis * sl2 - kBndHeadroom;
             }
             if (Layout<D>::SEP_P && cnt > 0) {  // PV_q(e-1) done with the P buffer
               mbar_wait(&sm.pv_done[q], (cnt - 1) & 1);
@@ -609,9 +609,9 @@ __global__ void __launch_bounds__(fwd::NT, 1)
       sm.xsum[q][hh][row_t] = l;
       named_bar_sync(bar_id, 64);
       l += sm.xsum[q][hh ^ 1][row_t];
-      // BND: a row whose sum ends below 2^-60 (its logits far below the Cauchy-Schwarz bound, or every
+      // BND: a row whose sum ends below 2^-90 (its logits far below the Cauchy-Schwarz bound, or every
       // key masked) flags the unit; the two-pass fixup launch recomputes it (O and lse overwritten)
-      const bool live = (cnt > 0) && (BND ? (l >= 0x1p-60f) : (l > 0.f));
+      const bool live = (cnt > 0) && (BND ? (l >= kBndMinSum) : (l > 0.f));
       if (BND && row < a.N && !live) a.fix_out[unit] = 1;
       if (cnt > 0) {
         mbar_wait(&sm.o_full[q], 0);

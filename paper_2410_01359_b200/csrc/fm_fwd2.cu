@@ -114,8 +114,8 @@ __device__ __forceinline__ int ent_cls(uint32_t ent, int q) { return (ent >> (24
 }  // namespace fwd2
 
 // BND (R33): the bounded single pass of K2a on the CTA pair — every P of a row against the fixed
-// reference ||q_r|| max||k|| scale log2(e) - 64: no max pass, no max chain between the warpsets, no O
-// rescale; rows whose sum ends below 2^-60 flag the unit for K2a's two-pass fixup launch.
+// reference ||q_r|| max||k|| scale log2(e) - 96: no max pass, no max chain between the warpsets, no O
+// rescale; rows whose sum ends below 2^-90 flag the unit for K2a's two-pass fixup launch.
 template <bool CAUSAL, bool OUT_F32, bool F16, bool BND>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fwd2::NT, 1)
     fm_fwd2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK64,
@@ -329,7 +329,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fwd2::NT, 1)
     float l = 0.f;
     if constexpr (BND) {
       // R33 fixed reference: ||q_r|| (this row of Q, read from global memory: L2-resident, once per
-      // CTA) * the head's largest key norm * scale * log2(e) - 64
+      // CTA) * the head's largest key norm * scale * log2(e) - 96
       float kvis = 0.f;
 #pragma unroll
       for (int w = 0; w < NT / 32; ++w) kvis = fmaxf(kvis, sm.warp_kmax[w]);
@@ -348,7 +348,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fwd2::NT, 1)
           }
         }
       }
-      m_ref = sqrtf(ss) * (1.0f + 1.0f / 65536.0f) * kvis * sl2 - 64.0f;
+      m_ref = sqrtf(ss) * (1.0f + 1.0f / 65536.0f) * kvis * sl2 - kBndHeadroom;
     }
     for (int e = W, u = 0; e < nE; e += 2, ++u) {
       const uint32_t ent = sm.list[e];
@@ -563,8 +563,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fwd2::NT, 1)
         if (lx > 0.f) lt += lx * ex2(sm.xm[x >> 1][x & 1][row_t] - m_fin);
       }
     }
-    // BND: a row whose sum ends below 2^-60 flags the unit for the two-pass fixup launch
-    const bool live = BND ? (nE > 0 && lt >= 0x1p-60f) : lt > 0.f;
+    // BND: a row whose sum ends below 2^-90 flags the unit for the two-pass fixup launch
+    const bool live = BND ? (nE > 0 && lt >= kBndMinSum) : lt > 0.f;
     if (BND && row < a.N && !live) a.fix_out[(static_cast<size_t>(b) * a.H + h) * npairs + pair] = 1;
     const float inv = live ? 1.0f / lt : 0.f;
     mbar_wait(&sm.o_full, 0);  // every MMA of the pair done (or, with no MMA, both Q tiles landed)

@@ -63,6 +63,14 @@ struct Dims {
   int rowwise;      // FM_FLAG_ROWWISE: vectors indexed by query row, values = key intervals (R32)
 };
 
+// R33 bounded single pass: the fixed reference sits kBndHeadroom (log2 units) below the
+// Cauchy-Schwarz bound, so every P <= 2^96 (bf16 / fp32 sums of <= 2^18 terms of |v| < 2^13 stay
+// finite); a row whose sum ends below kBndMinSum (its largest P < 2^-90, still 2^36 above the fp32
+// normal range) is recomputed by the two-pass fixup.  A row fails only when the bound exceeds its
+// true maximum by more than ~186 log2 units.
+constexpr float kBndHeadroom = 96.0f;
+constexpr float kBndMinSum = 0x1p-90f;
+
 struct FwdArgs {
   int B, N, H, Hm, Tr, Tc, G;
   float scale_log2;
