@@ -120,18 +120,30 @@ struct Smem {
 // Branch-free per template so the compiler can overlap the shared loads, FMAs and MUFU ops.
 // Rows [r0, r0 + 32) masked for this thread's key, as a bit set (bit u = row r0 + u): the
 // interval test of Alg. 2 lines 20-23 evaluated once per 32 rows instead of per element.
+// lo in (-N, N], 0 <= len <= INT_MAX.  W32: 32-bit only — lo + len is formed only when it stays below
+// 32 (at d = 64 the 64-bit form kept a sign word live across the compute loop, spilled to local
+// memory: in-process A/B +4 % on PARTIAL-heavy d = 64 backwards; at d = 128 the 64-bit form measured
+// 1-3 % faster, code generation)
+template <bool W32>
 __device__ __forceinline__ uint32_t range_bits(int lo, int len) {
   const int a = min(max(lo, 0), 32);
-  const int b = static_cast<int>(min(max(static_cast<long long>(lo) + len, 0ll), 32ll));
-  return b > a ? static_cast<uint32_t>(((1ull << b) - 1ull) & ~((1ull << a) - 1ull)) : 0u;
+  if constexpr (W32) {
+    const int b = (len >= 32 - lo) ? 32 : max(lo + len, 0);
+    const uint32_t mb = (b >= 32) ? 0xFFFFFFFFu : ((1u << b) - 1u);
+    const uint32_t ma = (a >= 32) ? 0xFFFFFFFFu : ((1u << a) - 1u);
+    return mb & ~ma;  // bits [a, b); empty when b <= a
+  } else {
+    const int b = static_cast<int>(min(max(static_cast<long long>(lo) + len, 0ll), 32ll));
+    return b > a ? static_cast<uint32_t>(((1ull << b) - 1ull) & ~((1ull << a) - 1ull)) : 0u;
+  }
 }
-template <bool CAUSAL>
+template <bool CAUSAL, bool W32>
 __device__ __forceinline__ uint32_t row_mask_bits(int r0, int key, int4 mv) {
-  uint32_t m = range_bits(mv.x - r0, mv.y);
+  uint32_t m = range_bits<W32>(mv.x - r0, mv.y);
   if constexpr (CAUSAL)
-    m |= range_bits(0, key - r0);  // rows r < key
+    m |= range_bits<W32>(0, key - r0);  // rows r < key
   else
-    m |= range_bits(mv.z - r0, mv.w);
+    m |= range_bits<W32>(mv.z - r0, mv.w);
   return m;
 }
 
@@ -467,7 +479,7 @@ __global__ void __launch_bounds__(bwd::NT, 1)
         }
         if (partial) {
           const uint32_t mb = ROWW ? row_mask_bits_rw<CAUSAL>(i * BR + q0, key, sm.rvec[st] + (ROWW ? q0 : 0), a.N)
-                                   : row_mask_bits<CAUSAL>(i * BR + q0, key, mv);
+                                   : row_mask_bits<CAUSAL, D == 64>(i * BR + q0, key, mv);
           pds_chunk<true, CAUSAL, F16, D == 64>(sr, dr, lv + q0, dv + q0, sl2, mb, pp[ch], dp[ch]);
         } else {
           pds_chunk<false, CAUSAL, F16, D == 64>(sr, dr, lv + q0, dv + q0, sl2, 0u, pp[ch], dp[ch]);
