@@ -641,6 +641,7 @@ def main():
         d = c0["d"]
         k3_bytes = rows_rank * (2 * 2 * d + 4 + 4 + 4 * d + 4)     # read O, dO, lse; write D, lse2, zero dQacc
         k5_bytes = rows_rank * (4 * d + 2 * d)                     # read dQacc, write bf16 dQ
+        k1e_bytes = rows_rank * 2 * d                               # K1e: read K (one kv head per head here)
         rooflines = [
             {"kernel": "fm_bwd_kernel (K4)", "bound": "tensor", "achieved": round(bwd_tf, 2) if bwd_tf else None,
              "peak": peak_sust, "unit": "TFLOP/s", "frac": round(bwd_tf / peak_sust, 4) if bwd_tf else None,
@@ -655,6 +656,10 @@ def main():
             {"kernel": "k5_dq_convert (K5)", "bound": "hbm", "achieved_TB/s": tb_s(k5_bytes, ksplit["dq_convert"][0]),
              "peak_TB/s": round(peak_hbm / 1e3, 3), "algorithmic_bytes": k5_bytes},
         ]
+        if ksplit.get("keynorm", (0, 0))[1]:  # the bounded forward ran (R33)
+            rooflines.append({"kernel": "k1e_key_norms (K1e)", "bound": "hbm",
+                              "achieved_TB/s": tb_s(k1e_bytes, ksplit["keynorm"][0]),
+                              "peak_TB/s": round(peak_hbm / 1e3, 3), "algorithmic_bytes": k1e_bytes})
         line = {
             "metric": METRIC,
             "value": round(value, 2), "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,

@@ -217,7 +217,8 @@ enum {
   FM_KERNEL_DQ_CONVERT = 5,  /* K5   dQ = scale * dQacc -> out dtype                         */
   FM_KERNEL_DQ = 6,          /* K6   deterministic dQ (FM_FLAG_DETERMINISTIC)                */
   FM_KERNEL_REFINE = 7,      /* K1c  f3 refinement words of PARTIAL tiles                    */
-  FM_NUM_KERNELS = 8
+  FM_KERNEL_KEYNORM = 8,     /* K1e  key norms per key tile for the bounded forward (R33)    */
+  FM_NUM_KERNELS = 9
 };
 
 /* Optional per-kernel timing for roofline reporting (off by default).  enable = 0: off;

@@ -417,7 +417,7 @@ fm_status flashmask_fwd(const fm_params* p, const void* q, const void* k, const 
   const bool bounded = !d.in_f16 && (p->flags & FM_FLAG_NO_MAX_BOUND) == 0 &&
                        ((d.N >= 16384 && !d.rowwise) || (p->flags & FM_FLAG_MAX_BOUND) != 0);
   if (bounded) {
-    e = timed(FM_KERNEL_EXPAND, st, [&] { return fm::launch_key_norms(d, k, w.kmax, w.fix, st); });
+    e = timed(FM_KERNEL_KEYNORM, st, [&] { return fm::launch_key_norms(d, k, w.kmax, w.fix, st); });
     if (e != cudaSuccess) return cuda_fail(e, "key norms");
     a.kmax = w.kmax;
     a.fix_out = w.fix;

@@ -30,7 +30,7 @@ FM_PASS_FWD, FM_PASS_BWD = 0, 1
 EXPORTED = ["flashmask_workspace_size", "flashmask_classify", "flashmask_refine", "flashmask_fwd", "flashmask_bwd",
             "flashmask_status_string", "flashmask_last_error", "flashmask_timing_enable", "flashmask_timing_collect",
             "flashmask_sliding_window_indices"]
-KERNEL_NAMES = ["expand", "classify", "fwd", "bwd_pre", "bwd", "dq_convert", "dq", "refine"]
+KERNEL_NAMES = ["expand", "classify", "fwd", "bwd_pre", "bwd", "dq_convert", "dq", "refine", "keynorm"]
 (FM_KERNEL_EXPAND, FM_KERNEL_CLASSIFY, FM_KERNEL_FWD, FM_KERNEL_BWD_PRE, FM_KERNEL_BWD, FM_KERNEL_DQ_CONVERT,
  FM_KERNEL_DQ, FM_KERNEL_REFINE) = range(8)
 
